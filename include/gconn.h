@@ -1,0 +1,219 @@
+/*
+ * gconn.h — C ABI of libgconn.so, the sm_100a implementation of the GConn
+ * connectivity design space (arXiv 2008.11839).
+ *
+ * The reference (`connlab`, /root/reference/pkg/src/connlab) is a pure
+ * Python package with no FFI; its drop-in surface is the Python driver API
+ * (driver.py:99-725).  This header is the seam *under* that surface: the
+ * Python package `paper_2008_11839_b200` mirrors the connlab names and binds
+ * these entry points with ctypes (see INTEGRATION.md for the binding a
+ * connlab maintainer would add).  Every entry point below names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers unless the parameter name ends
+ *     in `_host`.  Vertex ids are int32 (graphs.py:11, VERTEX_LIMIT = 2^31),
+ *     CSR offsets are int64 (graphs.py:47-51).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *     Calls are asynchronous with respect to the host unless documented
+ *     otherwise; stats are written when the call returns (entry points that
+ *     produce stats synchronize the stream once at the end).
+ *   - Scratch memory is caller-owned: query gc_workspace_size() and pass a
+ *     device buffer of at least that many bytes (the Python layer allocates
+ *     it from the PyTorch caching allocator).
+ *   - Return value: GC_OK or a GC_ERR_* status.  No C++ exception ever
+ *     crosses the ABI; gc_last_error() returns a thread-local message.
+ *     The Python layer maps GC_ERR_CONFIG -> connlab ConfigError and
+ *     GC_ERR_MALFORMED -> MalformedInputError (errors.py:4-13).
+ */
+#ifndef GCONN_H_
+#define GCONN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------*/
+enum {
+  GC_OK = 0,
+  GC_ERR_CONFIG = 2,     /* invalid spec / combination (ConfigError)        */
+  GC_ERR_MALFORMED = 3,  /* bad graph / endpoint out of range               */
+  GC_ERR_CUDA = 4,       /* a CUDA runtime error                             */
+  GC_ERR_OOM = 5,        /* workspace too small / allocation failed          */
+  GC_ERR_ARG = 6         /* null pointer or negative size                    */
+};
+
+/* ---- spec enums (driver.py:65-82, dset.py:29-50, minbased.py:24-37) ------*/
+enum gc_sample_kind { GC_SAMPLE_NONE = 0, GC_SAMPLE_KOUT = 1, GC_SAMPLE_HB = 2,
+                      GC_SAMPLE_BFS = 3, GC_SAMPLE_LDD = 4 };
+enum gc_finish_kind { GC_FINISH_ASYNC = 0, GC_FINISH_HOOKS = 1,
+                      GC_FINISH_EARLY = 2, GC_FINISH_REM_LOCK = 3,
+                      GC_FINISH_REM_CAS = 4, GC_FINISH_JTB = 5,
+                      GC_FINISH_SV = 6, GC_FINISH_LT = 7,
+                      GC_FINISH_STERGIOU = 8, GC_FINISH_LP = 9 };
+enum gc_find_kind { GC_FIND_NAIVE = 0, GC_FIND_SPLIT = 1, GC_FIND_HALVE = 2,
+                    GC_FIND_COMPRESS = 3, GC_FIND_TWO_TRY = 4 };
+enum gc_splice_kind { GC_SPLICE_NONE = 0, GC_SPLICE_SPLIT_ONE = 1,
+                      GC_SPLICE_HALVE_ONE = 2, GC_SPLICE_ATOMIC = 3 };
+enum gc_lt_connect { GC_LT_CONNECT = 0, GC_LT_PARENT = 1, GC_LT_EXTENDED = 2 };
+enum gc_lt_update { GC_LT_UPDATE_ALL = 0, GC_LT_UPDATE_ROOTS = 1 };
+enum gc_lt_shortcut { GC_LT_SHORTCUT_ONE = 0, GC_LT_SHORTCUT_FULL = 1 };
+enum gc_kout_mode { GC_KOUT_FIRST_K = 0, GC_KOUT_FIRST_PLUS_RANDOM = 1 };
+
+/* A symmetrized CSR graph in device memory (graphs.py:43-87 `Graph`):
+ * offsets[n+1] int64, targets[m] int32, rows sorted ascending, no
+ * self-loops, no duplicates; m counts directed entries. */
+typedef struct gc_csr {
+  int64_t n;
+  int64_t m;
+  const int64_t* offsets;
+  const int32_t* targets;
+} gc_csr;
+
+/* AlgorithmSpec (driver.py:99-110) flattened.  Host-side RNG-derived inputs
+ * (BFS source, JTB ranks, k-out random offsets) are computed by the Python
+ * layer with the reference's own generators and passed in, so runs are
+ * reproducible against the oracle. */
+typedef struct gc_spec {
+  int32_t sample;        /* gc_sample_kind                                   */
+  int32_t finish;        /* gc_finish_kind                                   */
+  int32_t find;          /* gc_find_kind   (union-find finishes)             */
+  int32_t splice;        /* gc_splice_kind (Rem finishes)                    */
+  int32_t lt_connect;    /* gc_lt_connect  (LT finish)                       */
+  int32_t lt_update;     /* gc_lt_update                                     */
+  int32_t lt_shortcut;   /* gc_lt_shortcut                                   */
+  int32_t lt_alter;      /* 0/1                                              */
+  int32_t kout_k;        /* sampling.py:19 default 2                         */
+  int32_t kout_mode;     /* gc_kout_mode                                     */
+  int32_t hb_edges;      /* sampling.py:20 default 4                         */
+  int32_t reserved0;
+  int64_t bfs_source;    /* BFS sampler source vertex (sampling.py:130-132)  */
+  uint64_t seed;         /* spec seed (driver.py:109)                        */
+  double ldd_beta;       /* LDD sampler: exponential shift rate              */
+  const uint32_t* jtb_ranks;          /* device, n entries, or NULL (dset.py:372-374) */
+  const int32_t* kout_rand_offsets;   /* device, (#deg>0 vertices) x (k-1) row offsets */
+} gc_spec;
+
+/* RunStats (validate.py:20-43) as produced on device.  Times are CUDA-event
+ * milliseconds per phase; inspection counts are computed analytically on
+ * device with the reference's definitions. */
+typedef struct gc_stats {
+  double t_sample_ms;
+  double t_finish_ms;
+  double t_finalize_ms;
+  int64_t insp_sample;
+  int64_t insp_finish;
+  int64_t rounds;
+  int64_t components;
+  int64_t l_max;          /* most frequent post-sample label (n for NONE)    */
+  int64_t lmax_count;     /* its multiplicity (cov = lmax_count / n)         */
+  int64_t n_active;       /* vertices the finish phase saw                   */
+  int64_t ic_count;       /* directed edges with differing post-sample labels */
+} gc_stats;
+
+/* ---- library ------------------------------------------------------------*/
+const char* gc_last_error(void);
+const char* gc_version(void);
+/* Scratch bytes needed by gc_static_cc / gc_spanning_forest / gc_finish_phase. */
+size_t gc_workspace_size(int64_t n, int64_t m, const gc_spec* spec);
+
+/* ---- static connectivity (driver.py:454-507 `_pipeline`,
+ *      `static_connectivity`) -------------------------------------------------
+ * labels_out[n] receives the finalized labels: each component's minimum
+ * vertex id (driver.py:420-429 + validate.py:251-259).  If
+ * `post_sample_out` is non-NULL it receives a copy of the post-sampling
+ * labels (the `post_sample` array of driver.py:466) for the cov/ic census;
+ * `want_ic` != 0 additionally counts label-crossing edges outside the timed
+ * phases (driver.py:406-417). */
+int gc_static_cc(const gc_csr* g, const gc_spec* spec, int32_t* labels_out,
+                 int32_t* post_sample_out, int want_ic, gc_stats* stats,
+                 void* ws, size_t ws_bytes, void* stream);
+
+/* ---- spanning forest (driver.py:510-536) --------------------------------
+ * Slot r of (fu, fv) holds the original edge recorded when r lost root
+ * status; empty slots hold -1 (ForestEdges.edges None). */
+int gc_spanning_forest(const gc_csr* g, const gc_spec* spec, int32_t* fu,
+                       int32_t* fv, gc_stats* stats, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* ---- finish phase only (driver.py:432-446) -------------------------------
+ * labels_io[n] holds the (possibly partial) input labels and receives the
+ * unfinalized finish output. */
+int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io,
+                    int64_t l_max, gc_stats* stats, void* ws, size_t ws_bytes,
+                    void* stream);
+
+/* ---- label finalization (driver.py:420-429) ------------------------------
+ * In place: chase to the root, then relabel each class by its minimum
+ * member (validate.py:251-259).  ws needs 4*n bytes. */
+int gc_label_finalization(int32_t* labels, int64_t n, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/* ---- batch union seam (dset.py:402-416 `union_edge_list`) ----------------
+ * Applies the spec's union rule to k edge pairs over parent[n] (in place).
+ * aux: 4*n bytes of zeroed scratch for HOOKS / REM_LOCK (else may be NULL). */
+int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us,
+                   const int32_t* vs, int64_t k, const gc_spec* spec,
+                   int32_t* aux, int32_t* fu, int32_t* fv, void* stream);
+
+/* ---- incremental (driver.py:567-725) -------------------------------------*/
+typedef struct gc_incr gc_incr;
+/* capacity = number of vertex slots; sentinel = capacity (driver.py:603). */
+int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream,
+                   gc_incr** out);
+/* One batch: ops[i] = (us[i], vs[i]) is an insert if is_query[i]==0, else a
+ * query.  Insert sub-phase, barrier, query sub-phase (driver.py:695-708);
+ * racy != 0 interleaves them (driver.py:674-694).  bits_out receives one
+ * byte per op (1 = query answered connected).  Times are accumulated into
+ * stats->t_sample_ms (insert) and stats->t_finish_ms (query). */
+int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs,
+                  const uint8_t* is_query, int64_t len, uint8_t* bits_out,
+                  int racy, gc_stats* stats);
+/* Columnar insert-only / query-only fast paths (no per-op flag array). */
+int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs,
+                   int64_t len, gc_stats* stats);
+int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs,
+                  int64_t len, uint8_t* bits_out, gc_stats* stats);
+/* Copy of the live state with the sentinel convention (driver.py:656,710). */
+int gc_incr_state(gc_incr* h, int32_t* state_out);
+/* Final labels (driver.py:715-725); returns the component count of the
+ * initialized vertices in *components. */
+int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components);
+int64_t gc_incr_capacity(gc_incr* h);
+void gc_incr_destroy(gc_incr* h);
+
+/* ---- graph generators + CSR build (graphs.py:90-121, 210-245, 297-308) ----
+ * gc_gen_rmat reproduces numpy's PCG64 stream bit-for-bit: (state_hi,
+ * state_lo, inc_hi, inc_lo) is `default_rng(seed).bit_generator.state`, and
+ * base[4] = (a, b, c, d) exactly as the reference computes them.  Output:
+ * src[ef*n], dst[ef*n] int64 pairs in the reference order. */
+int gc_gen_rmat(int32_t scale, int64_t num_pairs, const double* base_host,
+                uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                uint64_t inc_lo, int64_t* src, int64_t* dst, void* stream);
+/* numpy Generator.integers(0, n, size=(k, 2), dtype=int64) for n = 2^log2n
+ * (Lemire path without rejection). */
+int gc_gen_uniform_pow2(int32_t log2n, int64_t num_pairs, uint64_t state_hi,
+                        uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        int64_t* src, int64_t* dst, void* stream);
+/* Symmetrize, drop self-loops, dedupe, sort (build_csr semantics,
+ * graphs.py:90-121).  targets must have capacity 2*k; *m_out (host) receives
+ * the directed entry count.  An endpoint outside [0, n) -> GC_ERR_MALFORMED.
+ * ws needs gc_build_csr_workspace(n, k) bytes. */
+size_t gc_build_csr_workspace(int64_t n, int64_t k);
+int gc_build_csr(int64_t n, const int64_t* src, const int64_t* dst, int64_t k,
+                 int64_t* offsets, int32_t* targets, int64_t* m_out, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* Host helper: MT19937 continuing from Python random.Random().getstate()
+ * (624 words + index): out[i] = getrandbits(32).  Used for the JTB ranks of
+ * DisjointSets (dset.py:372-374). */
+int gc_mt19937_fill(const uint32_t* state624, int32_t index, uint32_t* out,
+                    int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCONN_H_ */

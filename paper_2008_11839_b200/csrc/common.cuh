@@ -1,0 +1,74 @@
+// common.cuh — shared device helpers for libgconn (sm_100a).
+//
+// Memory-model note.  The parent array P is shared by every thread of a
+// kernel and mutated with atomicCAS while other threads walk it.  All reads
+// of P therefore go through ld.relaxed.gpu (LDG.E.STRONG.GPU: served by L2,
+// never a stale L1 line), the GPU analogue of the reference's "single list
+// reads are atomic under the GIL" (parallel.py:3-8).  Read-only graph data
+// (offsets / targets) uses the non-coherent path (ld.global.nc).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gconn.h"
+
+namespace gc {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ int32_t ld_acq(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_rlx(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool cas(int32_t* p, int32_t expect, int32_t desired) {
+  return atomicCAS(p, expect, desired) == expect;
+}
+
+// fire-and-forget min (RED.MIN): the result is not needed by the caller
+__device__ __forceinline__ void red_min(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int64_t ldg64(const int64_t* p) { return __ldg(p); }
+__device__ __forceinline__ int32_t ldg32(const int32_t* p) { return __ldg(p); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of a 64-bit counter, one atomicAdd per block.
+template <int BLOCK>
+__device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
+  __shared__ unsigned long long part[BLOCK / kWarp];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) part[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long s = lane < BLOCK / kWarp ? part[lane] : 0ull;
+    s = warp_sum(s);
+    if (lane == 0 && s) atomicAdd(dst, s);
+  }
+}
+
+// Grid size for an elementwise kernel: enough CTAs to cover `work` items
+// but capped at a whole number of waves over the 148 SMs.
+inline int grid_for(int64_t work, int block, int max_waves = 32) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = int64_t(148) * (2048 / block) * max_waves;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+}  // namespace gc

@@ -1,0 +1,382 @@
+// incremental.cu — batch-incremental connectivity (driver.py:567-725).
+//
+// A handle owns the live state: a parent array with the sentinel
+// convention (slot value `cap` = uninitialised, driver.py:603-614) for the
+// union-find rules, or a cap+1 label array for SV / root-based LT
+// (driver.py:615-618).  Each batch runs the insert sub-phase (lazy init by
+// CAS sentinel->v, then the union kernel), a stream-ordered barrier, and the
+// read-only query sub-phase (driver.py:695-708); racy mode interleaves them
+// in one launch (driver.py:674-694).
+#include <climits>
+#include <cstring>
+
+#include "pipeline.cuh"
+#include "rounds.h"
+
+struct gc_incr {
+  gc_spec spec;
+  int64_t cap;
+  bool uf;
+  int32_t* state = nullptr;   // cap (UF) or cap+1 (rounds) entries
+  int32_t* aux = nullptr;     // hooks / locks
+  unsigned long long* ctr = nullptr;
+  // rounds scratch
+  gc::RoundsWs rw;
+  int64_t coo_cap = 0;
+  cudaStream_t st;
+  cudaEvent_t ev[4];
+};
+
+namespace gc {
+namespace {
+
+constexpr int kIB = 256;
+
+// ensure_init over the insert endpoints (driver.py:620-625): CAS sentinel -> v
+__global__ void k_incr_init(int32_t* P, const int32_t* us, const int32_t* vs, const uint8_t* isq,
+                            int64_t len, int32_t sentinel) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
+    if (isq && isq[i]) continue;
+    const int32_t u = us[i], v = vs[i];
+    if (P[u] == sentinel) atomicCAS(P + u, sentinel, u);
+    if (P[v] == sentinel) atomicCAS(P + v, sentinel, v);
+  }
+}
+
+__global__ void k_incr_query(const int32_t* P, const int32_t* us, const int32_t* vs,
+                             const uint8_t* isq, int64_t len, int32_t sentinel, uint8_t* bits) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
+    if (isq && !isq[i]) {
+      bits[i] = 0;
+      continue;
+    }
+    int32_t x = us[i], y = vs[i];
+    int32_t px = P[x];
+    if (px != sentinel)
+      while (px != x) { x = px; px = P[x]; }
+    int32_t py = P[y];
+    if (py != sentinel)
+      while (py != y) { y = py; py = P[y]; }
+    bits[i] = x == y;
+  }
+}
+
+// insert COO for the round finishes; LT maps endpoints through the labels
+// once up front (minbased.py:176-177)
+__global__ void __launch_bounds__(kIB)
+k_incr_coo(const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len,
+           const int32_t* labels, int map, Coo out, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < len; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool ins = i < len && !(isq && isq[i]);
+    const unsigned bal = __ballot_sync(0xffffffffu, ins);
+    if (!bal) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(cnt, static_cast<unsigned long long>(__popc(bal)));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (ins) {
+      const unsigned long long p = pos + __popc(bal & ((1u << lane) - 1u));
+      const int32_t u = us[i], v = vs[i];
+      out.u[p] = map ? labels[u] : u;
+      out.v[p] = map ? labels[v] : v;
+      out.w[p] = 1;
+    }
+  }
+}
+
+// lazily initialise fresh endpoints of a label array (driver.py:639-641)
+__global__ void k_label_init(int32_t* L, const int32_t* us, const int32_t* vs, const uint8_t* isq,
+                             int64_t len, int32_t sentinel) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
+    if (isq && isq[i]) continue;
+    const int32_t u = us[i], v = vs[i];
+    if (L[u] == sentinel) L[u] = u;
+    if (L[v] == sentinel) L[v] = v;
+  }
+}
+
+__global__ void k_incr_export(const int32_t* S, int64_t cap, int32_t sentinel, int32_t* out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < cap; v += stride) {
+    const int32_t s = S[v];
+    out[v] = s == sentinel ? int32_t(v) : s;
+  }
+}
+
+__global__ void k_incr_count(const int32_t* S, const int32_t* fin, int64_t cap, int32_t sentinel,
+                             unsigned long long* out) {
+  unsigned long long c = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < cap; v += stride)
+    c += S[v] != sentinel && fin[v] == v;
+  block_add<kIB>(out, c);
+}
+
+int g1(int64_t work) { return grid_for(work, kIB, 8); }
+
+__global__ void k_count_bytes(const uint8_t* a, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) c += a[i] != 0;
+  block_add<kIB>(out, c);
+}
+
+void ensure_coo(gc_incr* h, int64_t len) {
+  if (len <= h->coo_cap) return;
+  int64_t cap = len < 1024 ? 1024 : len;
+  for (Coo* c : {&h->rw.work, &h->rw.spare}) {
+    cudaFree(c->u);
+    cudaFree(c->v);
+    cudaFree(c->w);
+    c->u = c->v = nullptr;
+    c->w = nullptr;
+    GC_CUDA(cudaMalloc(&c->u, cap * 4));
+    GC_CUDA(cudaMalloc(&c->v, cap * 4));
+    GC_CUDA(cudaMalloc(&c->w, cap));
+    c->idx = nullptr;
+  }
+  h->coo_cap = cap;
+}
+
+double elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float t = 0;
+  GC_CUDA(cudaEventElapsedTime(&t, a, b));
+  return t;
+}
+
+CooUnionArgs uf_args(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len,
+                     const uint8_t* skip) {
+  CooUnionArgs a{};
+  a.P = h->state;
+  a.H = h->spec.finish == GC_FINISH_HOOKS ? h->aux : nullptr;
+  a.L = h->spec.finish == GC_FINISH_REM_LOCK ? h->aux : nullptr;
+  a.R = h->spec.jtb_ranks;
+  a.n = int32_t(h->cap);
+  a.us = us;
+  a.vs = vs;
+  a.k = len;
+  a.skip = skip;
+  return a;
+}
+
+// insert sub-phase; returns added inspections (driver.py:627-649)
+void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len,
+                  int64_t n_ins, gc_stats* stats) {
+  cudaStream_t st = h->st;
+  const int32_t sentinel = int32_t(h->cap);
+  if (h->uf) {
+    k_incr_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel);
+    GC_CHECK_LAUNCH();
+    launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false,
+                     uf_args(h, us, vs, len, isq), st);
+    if (stats) stats->insp_finish += n_ins;
+    return;
+  }
+  ensure_coo(h, len);
+  k_label_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel);
+  unsigned long long* cnt = h->ctr + C_SCRATCH0;
+  GC_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+  Coo w = h->rw.work;
+  k_incr_coo<<<g1(len), kIB, 0, st>>>(us, vs, isq, len, h->state, h->spec.finish == GC_FINISH_LT,
+                                      w, cnt);
+  GC_CHECK_LAUNCH();
+  h->rw.work.len = n_ins;
+  h->rw.work.weight = n_ins;
+  GC_CUDA(cudaMemsetAsync(h->ctr + C_INSP_FINISH, 0, 8, st));
+  const int64_t r = run_rounds_coo(h->spec, h->state, h->cap + 1, h->rw.work, h->rw, h->ctr,
+                                   C_INSP_FINISH, st);
+  unsigned long long* hw = pinned_words();
+  GC_CUDA(cudaMemcpyAsync(hw, h->ctr + C_INSP_FINISH, 8, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->rounds += r;
+    stats->insp_finish += n_ins + int64_t(hw[0]);
+  }
+}
+
+int64_t count_inserts(const uint8_t* isq, int64_t len, cudaStream_t st, unsigned long long* ctr) {
+  if (!isq) return len;
+  unsigned long long* c = ctr + C_SCRATCH1;
+  GC_CUDA(cudaMemsetAsync(c, 0, 8, st));
+  k_count_bytes<<<g1(len), kIB, 0, st>>>(isq, len, c);
+  GC_CHECK_LAUNCH();
+  unsigned long long* hw = pinned_words();
+  GC_CUDA(cudaMemcpyAsync(hw, c, 8, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  return len - int64_t(hw[0]);
+}
+
+}  // namespace
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream, gc_incr** out) {
+  return guarded([&] {
+    require(spec && out, GC_ERR_ARG, "null argument");
+    require(capacity >= 0 && capacity < (int64_t(1) << 31) - 1, GC_ERR_MALFORMED,
+            "capacity outside [0, 2^31 - 1)");
+    const bool uf = spec->finish >= GC_FINISH_ASYNC && spec->finish <= GC_FINISH_JTB;
+    const bool ok = uf || spec->finish == GC_FINISH_SV ||
+                    (spec->finish == GC_FINISH_LT && spec->lt_update == GC_LT_UPDATE_ROOTS);
+    require(ok, GC_ERR_CONFIG, "incremental needs a root-based finish");
+    if (uf) require(valid_uf(UFConfig{spec->finish, spec->find, spec->splice}), GC_ERR_CONFIG,
+                    "unsupported union-find combination");
+    require(spec->finish != GC_FINISH_JTB || spec->jtb_ranks, GC_ERR_ARG, "JTB needs ranks");
+    gc_incr* h = new gc_incr();
+    h->spec = *spec;
+    h->cap = capacity;
+    h->uf = uf;
+    h->st = static_cast<cudaStream_t>(stream);
+    try {
+      const int64_t slots = uf ? capacity : capacity + 1;
+      GC_CUDA(cudaMalloc(&h->state, (slots > 0 ? slots : 1) * 4));
+      GC_CUDA(cudaMalloc(&h->ctr, sizeof(unsigned long long) * C_COUNT_));
+      GC_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long) * C_COUNT_, h->st));
+      fill(h->state, slots, int32_t(capacity), h->st);  // every slot = sentinel
+      if (spec->finish == GC_FINISH_HOOKS || spec->finish == GC_FINISH_REM_LOCK) {
+        GC_CUDA(cudaMalloc(&h->aux, (capacity > 0 ? capacity : 1) * 4));
+        fill(h->aux, capacity, spec->finish == GC_FINISH_HOOKS ? int32_t(capacity) : 0, h->st);
+      }
+      if (!uf) {
+        GC_CUDA(cudaMalloc(&h->rw.a, (capacity + 1) * 4));
+        GC_CUDA(cudaMalloc(&h->rw.b, (capacity + 1) * 4));
+      }
+      for (auto& e : h->ev) GC_CUDA(cudaEventCreate(&e));
+      GC_CUDA(cudaStreamSynchronize(h->st));
+    } catch (...) {
+      gc_incr_destroy(h);
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void gc_incr_destroy(gc_incr* h) {
+  if (!h) return;
+  cudaFree(h->state);
+  cudaFree(h->aux);
+  cudaFree(h->ctr);
+  cudaFree(h->rw.a);
+  cudaFree(h->rw.b);
+  for (Coo* c : {&h->rw.work, &h->rw.spare}) {
+    cudaFree(c->u);
+    cudaFree(c->v);
+    cudaFree(c->w);
+  }
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  delete h;
+}
+
+int64_t gc_incr_capacity(gc_incr* h) { return h ? h->cap : -1; }
+
+int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* is_query,
+                  int64_t len, uint8_t* bits_out, int racy, gc_stats* stats) {
+  return guarded([&] {
+    require(h && len >= 0, GC_ERR_ARG, "bad arguments");
+    if (len == 0) return;
+    require(us && vs && bits_out, GC_ERR_ARG, "null batch arrays");
+    cudaStream_t st = h->st;
+    const int32_t sentinel = int32_t(h->cap);
+    if (racy) {
+      require(h->uf, GC_ERR_CONFIG, "racy mode interleaves single ops and only works with union-find finishes");
+      require(h->spec.splice != GC_SPLICE_ATOMIC, GC_ERR_CONFIG,
+              "the splice rule moves non-roots across trees mid-union: use batched mode");
+      const int64_t n_ins = count_inserts(is_query, len, st, h->ctr);
+      GC_CUDA(cudaEventRecord(h->ev[0], st));
+      launch_incr_racy(UFConfig{h->spec.finish, h->spec.find, h->spec.splice},
+                       uf_args(h, us, vs, len, nullptr), is_query, sentinel, bits_out, st);
+      GC_CUDA(cudaEventRecord(h->ev[1], st));
+      GC_CUDA(cudaEventSynchronize(h->ev[1]));
+      if (stats) {
+        stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
+        stats->insp_finish += n_ins;
+      }
+      return;
+    }
+    const int64_t n_ins = count_inserts(is_query, len, st, h->ctr);
+    GC_CUDA(cudaEventRecord(h->ev[0], st));
+    if (n_ins) insert_phase(h, us, vs, is_query, len, n_ins, stats);
+    GC_CUDA(cudaEventRecord(h->ev[1], st));
+    k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out);
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaEventRecord(h->ev[2], st));
+    GC_CUDA(cudaEventSynchronize(h->ev[2]));
+    if (stats) {
+      stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
+      stats->t_finish_ms += elapsed(h->ev[1], h->ev[2]);
+    }
+  });
+}
+
+int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, gc_stats* stats) {
+  return guarded([&] {
+    require(h && len >= 0, GC_ERR_ARG, "bad arguments");
+    if (len == 0) return;
+    GC_CUDA(cudaEventRecord(h->ev[0], h->st));
+    insert_phase(h, us, vs, nullptr, len, len, stats);
+    GC_CUDA(cudaEventRecord(h->ev[1], h->st));
+    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    if (stats) stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
+  });
+}
+
+int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, uint8_t* bits_out,
+                  gc_stats* stats) {
+  return guarded([&] {
+    require(h && len >= 0, GC_ERR_ARG, "bad arguments");
+    if (len == 0) return;
+    GC_CUDA(cudaEventRecord(h->ev[0], h->st));
+    k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap),
+                                             bits_out);
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaEventRecord(h->ev[1], h->st));
+    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    if (stats) stats->t_finish_ms += elapsed(h->ev[0], h->ev[1]);
+  });
+}
+
+int gc_incr_state(gc_incr* h, int32_t* state_out) {
+  return guarded([&] {
+    require(h && state_out, GC_ERR_ARG, "bad arguments");
+    const int64_t slots = h->uf ? h->cap : h->cap + 1;
+    if (slots > 0)
+      GC_CUDA(cudaMemcpyAsync(state_out, h->state, slots * 4, cudaMemcpyDeviceToDevice, h->st));
+    GC_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components) {
+  return guarded([&] {
+    require(h && components, GC_ERR_ARG, "bad arguments");
+    *components = 0;
+    const int64_t cap = h->cap;
+    if (cap == 0) return;
+    require(labels_out, GC_ERR_ARG, "null labels");
+    cudaStream_t st = h->st;
+    int32_t* mins = nullptr;
+    GC_CUDA(cudaMallocAsync(&mins, cap * 4, st));
+    GC_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
+    k_incr_export<<<g1(cap), kIB, 0, st>>>(h->state, cap, int32_t(cap), labels_out);
+    run_finalize(labels_out, int32_t(cap), mins, h->ctr, st);
+    GC_CUDA(cudaMemsetAsync(h->ctr + C_SCRATCH0, 0, 8, st));
+    k_incr_count<<<g1(cap), kIB, 0, st>>>(h->state, labels_out, cap, int32_t(cap), h->ctr + C_SCRATCH0);
+    GC_CHECK_LAUNCH();
+    unsigned long long* hw = pinned_words();
+    GC_CUDA(cudaMemcpyAsync(hw, h->ctr + C_SCRATCH0, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaFreeAsync(mins, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    *components = int64_t(hw[0]);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// pipeline.cuh — elementwise kernels shared by the static, forest and
+// incremental drivers (initialisation, compression, most-frequent label,
+// active gather, finalisation, canonicalisation).
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace gc {
+
+constexpr int kEwBlock = 256;
+
+// P[v] = v; optional hook / lock arrays (DisjointSets.__init__, dset.py:353-379)
+__global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n);
+
+// Full compression to the fixpoint (sampling.py:38-47 compress_all).
+__global__ void k_compress(int32_t* P, int32_t n);
+
+// Most-frequent label (sampling.py:29-35): probe a strided sample for the
+// candidate, count it exactly; a strict majority is provably the argmax,
+// otherwise an exact histogram decides (ties -> smaller label).
+__global__ void k_mode_probe(const int32_t* P, int32_t n, unsigned long long* ctr);
+__global__ void k_count_eq(const int32_t* P, int32_t n, unsigned long long* ctr);
+__global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr);
+__global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr);
+__global__ void k_hist_argmax(const int32_t* hist, int32_t n, unsigned long long* ctr);
+
+// Active vertices: label != l_max (driver.py:473), plus sum of their degrees
+// (the finish inspection count, driver.py:335-336).
+__global__ void k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
+                                unsigned long long* ctr);
+
+// Pointer jump to the root in place; counts roots and flags labels that are
+// not their class minimum (label_finalization, driver.py:420-429).
+__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr);
+// canonical_labels (validate.py:251-259), skipped on device when the
+// finalize pass proved labels already canonical.
+__global__ void k_canon_init(int32_t* mins, int32_t n, const unsigned long long* ctr);
+__global__ void k_canon_min(const int32_t* P, int32_t* mins, int32_t n, const unsigned long long* ctr);
+__global__ void k_canon_apply(int32_t* P, const int32_t* mins, int32_t n, const unsigned long long* ctr);
+
+// Label-crossing directed edges over the active rows (driver.py:406-417 ic),
+// computed outside the timed phases.
+__global__ void k_ic_census(const int32_t* P, int32_t n, const int64_t* off, const int32_t* tgt,
+                            const int32_t* list, unsigned long long* ctr);
+
+__global__ void k_fill(int32_t* a, int64_t n, int32_t v);
+__global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long long* out);
+
+// Host helpers
+void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cudaStream_t st);
+void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st);
+void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
+
+}  // namespace gc

@@ -1,0 +1,45 @@
+// samplers.h — sampling-phase launchers (sampling.py:61-172 + the new LDD
+// sampler).  Each leaves P holding labels that refine the true partition.
+#pragma once
+
+#include "internal.h"
+
+namespace gc {
+
+struct SamplerWs {
+  int32_t* coo_u = nullptr;   // k-out random mode pairs
+  int32_t* coo_v = nullptr;
+  int32_t* lvl = nullptr;     // BFS / LDD level or cluster claim
+  int32_t* par = nullptr;     // BFS discovery parent
+  int32_t* q0 = nullptr;      // frontier queues
+  int32_t* q1 = nullptr;
+  uint16_t* start = nullptr;  // LDD start round per vertex
+};
+
+template <class A>
+void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
+  (void)m;
+  if (s.sample == GC_SAMPLE_KOUT && s.kout_mode == GC_KOUT_FIRST_PLUS_RANDOM) {
+    w.coo_u = a.template take<int32_t>(n * int64_t(s.kout_k));
+    w.coo_v = a.template take<int32_t>(n * int64_t(s.kout_k));
+  }
+  if (s.sample == GC_SAMPLE_HB) w.q0 = a.template take<int32_t>(n);  // phase-2 roots
+  if (s.sample == GC_SAMPLE_BFS || s.sample == GC_SAMPLE_LDD) {
+    w.lvl = a.template take<int32_t>(n);
+    w.par = a.template take<int32_t>(n);
+    w.q0 = a.template take<int32_t>(n);
+    w.q1 = a.template take<int32_t>(n);
+  }
+  if (s.sample == GC_SAMPLE_LDD) w.start = a.template take<uint16_t>(n);
+}
+
+void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a, bool forest,
+              SamplerWs& w, unsigned long long* ctr, cudaStream_t st);
+void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a, bool forest,
+            SamplerWs& w, unsigned long long* ctr, cudaStream_t st);
+void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t* fv, SamplerWs& w,
+             unsigned long long* ctr, cudaStream_t st);
+void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
+             cudaStream_t st);
+
+}  // namespace gc

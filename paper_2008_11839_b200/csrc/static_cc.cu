@@ -1,0 +1,423 @@
+// static_cc.cu — the two-phase static pipeline (driver.py:454-507) and its
+// spanning-forest / finish-only / finalisation entry points.
+//
+//   sample  : init sets -> sampler (k-out / HB / BFS / LDD) -> compress
+//             -> most-frequent label L_max                 (driver.py:465-471)
+//   census  : optional post-sample copy + ic count, untimed (driver.py:495)
+//   finish  : active gather -> union-find rows or min-label rounds
+//                                                           (driver.py:473-481)
+//   finalize: pointer jump + canonical labels              (driver.py:483-490)
+//
+// Every phase is a fixed kernel sequence on one stream with no host
+// round-trip, except the round-based finishes which read a change flag per
+// round (the reference's own fixpoint loop, minbased.py:124-304).
+#include <climits>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+#include "pipeline.cuh"
+#include "rounds.h"
+#include "samplers.h"
+
+namespace gc {
+
+namespace {
+
+struct EventSet {
+  cudaEvent_t e[6];
+  EventSet() {
+    for (auto& x : e) GC_CUDA(cudaEventCreate(&x));
+  }
+  ~EventSet() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+};
+
+bool is_union_finish(int f) { return f >= GC_FINISH_ASYNC && f <= GC_FINISH_JTB; }
+
+UFConfig finish_cfg(const gc_spec& s) { return UFConfig{s.finish, s.find, s.splice}; }
+
+// driver.py:96 — samplers use Async+Halve when the finish is not union-find
+UFConfig sampler_cfg(const gc_spec& s) {
+  if (is_union_finish(s.finish)) return finish_cfg(s);
+  return UFConfig{GC_FINISH_ASYNC, GC_FIND_HALVE, GC_SPLICE_NONE};
+}
+
+void validate_spec(const gc_spec& s) {
+  require(s.sample >= GC_SAMPLE_NONE && s.sample <= GC_SAMPLE_LDD, GC_ERR_CONFIG, "unknown sampler");
+  require(s.finish >= GC_FINISH_ASYNC && s.finish <= GC_FINISH_LP, GC_ERR_CONFIG, "unknown finish");
+  if (is_union_finish(s.finish))
+    require(valid_uf(finish_cfg(s)), GC_ERR_CONFIG, "unsupported union-find combination");
+  if (s.finish == GC_FINISH_LT) {
+    require(s.lt_connect >= 0 && s.lt_connect <= 2 && s.lt_update >= 0 && s.lt_update <= 1 &&
+                s.lt_shortcut >= 0 && s.lt_shortcut <= 1,
+            GC_ERR_CONFIG, "invalid LT variant");
+    require(!(s.lt_connect == GC_LT_CONNECT && !s.lt_alter), GC_ERR_CONFIG,
+            "Connect requires the alter phase");
+  }
+  require(s.kout_k >= 1 || s.sample != GC_SAMPLE_KOUT, GC_ERR_CONFIG, "kout_k must be >= 1");
+  if (s.finish == GC_FINISH_JTB || (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB))
+    require(sampler_cfg(s).unite != GC_FINISH_JTB || s.jtb_ranks != nullptr, GC_ERR_ARG,
+            "JTB needs ranks");
+}
+
+void validate_csr(const gc_csr* g) {
+  require(g != nullptr, GC_ERR_ARG, "null graph");
+  require(g->n >= 0 && g->n < (int64_t(1) << 31), GC_ERR_MALFORMED, "vertex count outside [0, 2^31)");
+  require(g->m >= 0, GC_ERR_MALFORMED, "negative edge count");
+  require(g->n == 0 || g->offsets != nullptr, GC_ERR_ARG, "null offsets");
+  require(g->m == 0 || g->targets != nullptr, GC_ERR_ARG, "null targets");
+}
+
+// Workspace layout shared by every static entry point.
+template <class A>
+struct Layout {
+  unsigned long long* ctr = nullptr;
+  int32_t* H = nullptr;
+  int32_t* L = nullptr;
+  int32_t* list = nullptr;
+  int32_t* hist = nullptr;
+  RoundsWs rounds;
+  SamplerWs samp;
+
+  void carve(A& a, int64_t n, int64_t m, const gc_spec& s, bool forest) {
+    ctr = a.template take<unsigned long long>(C_COUNT_);
+    const UFConfig sc = sampler_cfg(s);
+    const bool any_uf = is_union_finish(s.finish) || s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB;
+    if (any_uf && sc.unite == GC_FINISH_HOOKS) H = a.template take<int32_t>(n);
+    if (any_uf && sc.unite == GC_FINISH_REM_LOCK) L = a.template take<int32_t>(n);
+    list = a.template take<int32_t>(n);
+    hist = a.template take<int32_t>(n);
+    if (!is_union_finish(s.finish)) rounds_carve(a, rounds, n, m, s, forest);
+    sampler_carve(a, samp, n, m, s);
+  }
+};
+
+struct Pipeline {
+  const gc_csr& g;
+  const gc_spec& s;
+  int32_t* P;
+  int32_t* fu;
+  int32_t* fv;
+  cudaStream_t st;
+  Layout<Arena> ws;
+  int32_t n;
+
+  Pipeline(const gc_csr& g_, const gc_spec& s_, int32_t* P_, int32_t* fu_, int32_t* fv_,
+           void* wsp, size_t wsb, cudaStream_t st_)
+      : g(g_), s(s_), P(P_), fu(fu_), fv(fv_), st(st_), n(int32_t(g_.n)) {
+    Arena a(wsp, wsb);
+    ws.carve(a, g.n, g.m, s, fu != nullptr);
+    GC_CUDA(cudaMemsetAsync(ws.ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
+  }
+
+  RowUnionArgs rows(const UFConfig& c) const {
+    RowUnionArgs a{};
+    a.P = P;
+    a.H = c.unite == GC_FINISH_HOOKS ? ws.H : nullptr;
+    a.L = c.unite == GC_FINISH_REM_LOCK ? ws.L : nullptr;
+    a.R = s.jtb_ranks;
+    a.fu = fu;
+    a.fv = fv;
+    a.n = n;
+    a.off = g.offsets;
+    a.tgt = g.targets;
+    return a;
+  }
+
+  void init_sets(const UFConfig& c) {
+    if (n == 0) return;
+    int32_t* H = c.unite == GC_FINISH_HOOKS ? ws.H : nullptr;
+    int32_t* L = c.unite == GC_FINISH_REM_LOCK ? ws.L : nullptr;
+    k_init_sets<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, H, L, n);
+    GC_CHECK_LAUNCH();
+  }
+
+  // ---- sampling phase (driver.py:378-403) -------------------------------
+  void sample() {
+    const UFConfig sc = sampler_cfg(s);
+    if (s.sample == GC_SAMPLE_NONE) {
+      init_sets(sc);
+      return;  // l_max = n sentinel, set on host
+    }
+    if (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB) {
+      init_sets(sc);
+      if (s.sample == GC_SAMPLE_KOUT) {
+        run_kout(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
+      } else {
+        run_hb(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
+      }
+      if (n) {
+        k_compress<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n);
+        GC_CHECK_LAUNCH();
+      }
+    } else if (s.sample == GC_SAMPLE_BFS) {
+      init_sets(sc);
+      run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
+    } else {
+      init_sets(sc);
+      run_ldd(g, s, P, ws.samp, ws.ctr, st);
+    }
+    run_mode(P, n, ws.hist, ws.ctr, st);
+  }
+
+  void set_lmax_sentinel() {
+    // driver.py:467-468: the sentinel n matches no vertex
+    unsigned long long v[2] = {static_cast<unsigned long long>(n), 0ull};
+    GC_CUDA(cudaMemcpyAsync(ws.ctr + C_LMAX, v, sizeof(v), cudaMemcpyHostToDevice, st));
+    // keep the host array alive until the copy is done
+    GC_CUDA(cudaStreamSynchronize(st));
+  }
+
+  // ---- finish phase (driver.py:473-481) ----------------------------------
+  // Returns the number of rounds (round-based finishes) and fills the active
+  // list when the sampler left a dominant label.
+  int64_t finish() {
+    const bool all_active = s.sample == GC_SAMPLE_NONE;
+    if (!all_active && n) {
+      k_gather_active<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n, g.offsets, ws.list,
+                                                                     ws.ctr);
+      GC_CHECK_LAUNCH();
+    }
+    if (is_union_finish(s.finish)) {
+      RowUnionArgs a = rows(finish_cfg(s));
+      if (all_active) {
+        // every vertex is active: each undirected edge is presented once
+        // (t < u, a prefix of the sorted row); the reference inspection
+        // count Σdeg is added analytically
+        a.list = nullptr;
+        a.count_dev = nullptr;
+        a.count_host = n;
+        a.take_max = INT_MAX;
+        a.lower_only = 1;
+        a.insp = nullptr;
+        unsigned long long m = static_cast<unsigned long long>(g.m);
+        GC_CUDA(cudaMemcpyAsync(ws.ctr + C_INSP_FINISH, &m, sizeof(m), cudaMemcpyHostToDevice, st));
+        GC_CUDA(cudaStreamSynchronize(st));
+      } else {
+        a.list = ws.list;
+        a.count_dev = ws.ctr + C_N_ACTIVE;
+        a.count_host = n;
+        a.take_max = INT_MAX;
+        a.lower_only = 0;
+        a.insp = nullptr;  // counted by the gather
+      }
+      launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
+      return 0;
+    }
+    return run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
+  }
+};
+
+double ms(cudaEvent_t a, cudaEvent_t b) {
+  float t = 0.f;
+  GC_CUDA(cudaEventElapsedTime(&t, a, b));
+  return double(t);
+}
+
+void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* post, int want_ic,
+                int32_t* fu, int32_t* fv, gc_stats* stats, void* ws, size_t wsb, void* stream) {
+  validate_csr(g);
+  require(spec != nullptr, GC_ERR_ARG, "null spec");
+  validate_spec(*spec);
+  require(g->n == 0 || labels != nullptr, GC_ERR_ARG, "null labels");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool forest = fu != nullptr;
+  if (forest) {
+    require(fv != nullptr, GC_ERR_ARG, "null forest array");
+    fill(fu, g->n, -1, st);
+    fill(fv, g->n, -1, st);
+  }
+  Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
+  static thread_local EventSet ev;
+  const int32_t n = pl.n;
+
+  GC_CUDA(cudaEventRecord(ev.e[0], st));
+  pl.sample();
+  GC_CUDA(cudaEventRecord(ev.e[1], st));
+  if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
+  if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+  if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
+    k_ic_census<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, g->offsets, g->targets,
+                                                               nullptr, pl.ws.ctr);
+    GC_CHECK_LAUNCH();
+  }
+  GC_CUDA(cudaEventRecord(ev.e[2], st));
+  const int64_t rounds = pl.finish();
+  GC_CUDA(cudaEventRecord(ev.e[3], st));
+  if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st);
+  GC_CUDA(cudaEventRecord(ev.e[4], st));
+  unsigned long long c[C_COUNT_];
+  GC_CUDA(cudaMemcpyAsync(c, pl.ws.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  if (forest) {
+    // spanning_forest: component_count = n - |forest| (driver.py:535)
+    unsigned long long* cnt = pl.ws.ctr + C_SCRATCH1;
+    GC_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+    if (n) k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, cnt);
+    unsigned long long pop = 0;
+    GC_CUDA(cudaMemcpyAsync(&pop, cnt, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    c[C_COMPONENTS] = static_cast<unsigned long long>(n) - pop;
+  }
+  GC_CUDA(cudaStreamSynchronize(st));
+  require(c[C_SCRATCH1] == 0 || forest, GC_ERR_MALFORMED, "label array contains a cycle");
+  if (stats) {
+    stats->t_sample_ms = ms(ev.e[0], ev.e[1]);
+    stats->t_finish_ms = ms(ev.e[2], ev.e[3]);
+    stats->t_finalize_ms = forest ? 0.0 : ms(ev.e[3], ev.e[4]);
+    stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
+    stats->insp_finish = int64_t(c[C_INSP_FINISH]);
+    stats->rounds = rounds;
+    stats->components = int64_t(c[C_COMPONENTS]);
+    if (spec->sample == GC_SAMPLE_NONE) {
+      stats->l_max = n;
+      stats->lmax_count = n ? 1 : 0;  // identity labels: every count is 1
+      stats->n_active = n;
+      stats->ic_count = g->m;  // every directed edge crosses identity labels
+    } else {
+      stats->l_max = int64_t(c[C_LMAX]);
+      stats->lmax_count = int64_t(c[C_LMAX_COUNT]);
+      stats->n_active = int64_t(c[C_N_ACTIVE]);
+      stats->ic_count = want_ic ? int64_t(c[C_IC]) : -1;
+    }
+  }
+}
+
+}  // namespace
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_last_error(const char* msg) { g_err = msg; }
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+const char* gc_last_error(void) { return g_err.c_str(); }
+
+const char* gc_version(void) { return "gconn-b200 0.1.0 (sm_100a)"; }
+
+size_t gc_workspace_size(int64_t n, int64_t m, const gc_spec* spec) {
+  if (!spec || n < 0 || m < 0) return 0;
+  Sizer sz;
+  Layout<Sizer> l;
+  l.carve(sz, n, m, *spec, true);
+  return sz.used + 4096;
+}
+
+int gc_static_cc(const gc_csr* g, const gc_spec* spec, int32_t* labels_out, int32_t* post_sample_out,
+                 int want_ic, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    run_static(g, spec, labels_out, post_sample_out, want_ic, nullptr, nullptr, stats, ws, ws_bytes,
+               stream);
+  });
+}
+
+int gc_spanning_forest(const gc_csr* g, const gc_spec* spec, int32_t* fu, int32_t* fv,
+                       gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(spec != nullptr, GC_ERR_ARG, "null spec");
+    require(fu != nullptr && fv != nullptr, GC_ERR_ARG, "null forest arrays");
+    const bool root_based =
+        is_union_finish(spec->finish) ? spec->splice != GC_SPLICE_ATOMIC
+        : spec->finish == GC_FINISH_SV ? true
+        : spec->finish == GC_FINISH_LT ? spec->lt_update == GC_LT_UPDATE_ROOTS
+                                       : false;
+    require(root_based, GC_ERR_CONFIG, "spanning forest needs a root-based finish");
+    // the labels buffer lives in the workspace tail for the forest driver
+    Arena a(ws, ws_bytes);
+    const int64_t n = g ? g->n : 0;
+    int32_t* labels = a.take<int32_t>(n);
+    run_static(g, spec, labels, nullptr, 0, fu, fv, stats, static_cast<char*>(ws) + a.used,
+               ws_bytes - a.used, stream);
+  });
+}
+
+int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io, int64_t l_max,
+                    gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    validate_csr(g);
+    require(spec != nullptr, GC_ERR_ARG, "null spec");
+    validate_spec(*spec);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    gc_spec s2 = *spec;
+    s2.sample = GC_SAMPLE_KOUT;  // force the gather path (labels are given)
+    Pipeline pl(*g, s2, labels_io, nullptr, nullptr, ws, ws_bytes, st);
+    const int32_t n = pl.n;
+    unsigned long long lm = static_cast<unsigned long long>(l_max);
+    GC_CUDA(cudaMemcpyAsync(pl.ws.ctr + C_LMAX, &lm, 8, cudaMemcpyHostToDevice, st));
+    if (is_union_finish(spec->finish)) {
+      UFConfig c = finish_cfg(*spec);
+      if (n && (c.unite == GC_FINISH_HOOKS || c.unite == GC_FINISH_REM_LOCK)) {
+        int32_t* buf = c.unite == GC_FINISH_HOOKS ? pl.ws.H : pl.ws.L;
+        fill(buf, n, c.unite == GC_FINISH_HOOKS ? n : 0, st);
+      }
+    }
+    static thread_local EventSet ev;
+    GC_CUDA(cudaEventRecord(ev.e[0], st));
+    const int64_t rounds = pl.finish();
+    GC_CUDA(cudaEventRecord(ev.e[1], st));
+    unsigned long long c[C_COUNT_];
+    GC_CUDA(cudaMemcpyAsync(c, pl.ws.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->t_finish_ms = ms(ev.e[0], ev.e[1]);
+      stats->insp_finish = int64_t(c[C_INSP_FINISH]);
+      stats->rounds = rounds;
+      stats->n_active = int64_t(c[C_N_ACTIVE]);
+      stats->l_max = l_max;
+    }
+  });
+}
+
+int gc_label_finalization(int32_t* labels, int64_t n, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && n < (int64_t(1) << 31), GC_ERR_MALFORMED, "bad length");
+    if (n == 0) return;
+    Arena a(ws, ws_bytes);
+    unsigned long long* ctr = a.take<unsigned long long>(C_COUNT_);
+    int32_t* mins = a.take<int32_t>(n);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
+    run_finalize(labels, int32_t(n), mins, ctr, st);
+    unsigned long long cyc = 0;
+    GC_CUDA(cudaMemcpyAsync(&cyc, ctr + C_SCRATCH1, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    require(cyc == 0, GC_ERR_MALFORMED, "label array contains a cycle");
+  });
+}
+
+int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us, const int32_t* vs, int64_t k,
+                   const gc_spec* spec, int32_t* aux, int32_t* fu, int32_t* fv, void* stream) {
+  return guarded([&] {
+    require(spec != nullptr, GC_ERR_ARG, "null spec");
+    require(is_union_finish(spec->finish), GC_ERR_CONFIG, "union_edges needs a union-find rule");
+    UFConfig c = finish_cfg(*spec);
+    require(valid_uf(c), GC_ERR_CONFIG, "unsupported union-find combination");
+    require(c.unite != GC_FINISH_JTB || spec->jtb_ranks, GC_ERR_ARG, "JTB needs ranks");
+    require((c.unite != GC_FINISH_HOOKS && c.unite != GC_FINISH_REM_LOCK) || aux, GC_ERR_ARG,
+            "hooks / rem_lock need aux scratch");
+    CooUnionArgs a{};
+    a.P = parent;
+    a.H = c.unite == GC_FINISH_HOOKS ? aux : nullptr;
+    a.L = c.unite == GC_FINISH_REM_LOCK ? aux : nullptr;
+    a.R = spec->jtb_ranks;
+    a.fu = fu;
+    a.fv = fv;
+    a.n = int32_t(n);
+    a.us = us;
+    a.vs = vs;
+    a.k = k;
+    a.skip = nullptr;
+    launch_union_coo(c, fu != nullptr, a, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

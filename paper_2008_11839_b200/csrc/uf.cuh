@@ -1,0 +1,296 @@
+// uf.cuh — the concurrent union / find / splice menu on sm_100a.
+//
+// Device restatement of dset.py (reference /root/reference/pkg/src/connlab):
+//   finds   dset.py:109-172   (naive, compress, split, halve, two-try)
+//   splices dset.py:180-214   (split-one, halve-one, atomic splice)
+//   unions  dset.py:222-331   (async, hooks, early, rem-lock, rem-cas, jtb)
+// The Python reference serializes CAS through 64 striped locks
+// (parallel.py:17-36); here every CAS is a native 32-bit atomicCAS on the
+// L2-resident parent array and every read is ld.relaxed.gpu.
+//
+// Conventions kept from the reference (dset.py:9-15): links go from the
+// larger root id to the smaller (except JTB), failed compression CASes are
+// dropped, and a root loses root status exactly once, so forest recording
+// at the winning hook is single-shot.
+#pragma once
+
+#include "common.cuh"
+
+namespace gc {
+
+struct UFState {
+  int32_t* P;           // parent[n]
+  int32_t* H;           // hooks[n] (HOOKS), initialised to n
+  int32_t* L;           // locks[n] (REM_LOCK), initialised to 0
+  const uint32_t* R;    // ranks[n] (JTB)
+  int32_t* fu;          // forest slot u (nullable)
+  int32_t* fv;          // forest slot v
+  int32_t n;
+};
+
+template <bool FOREST>
+__device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u, int32_t v) {
+  if constexpr (FOREST) {
+    s.fu[slot] = u;
+    s.fv[slot] = v;
+  }
+}
+
+// ---------------------------------------------------------------- finds ---
+
+template <int FIND>
+__device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
+  if constexpr (FIND == GC_FIND_NAIVE) {
+    // dset.py:109-112
+    while (true) {
+      int32_t pu = ld_acq(P + u);
+      if (pu == u) return u;
+      u = pu;
+    }
+  } else if constexpr (FIND == GC_FIND_COMPRESS) {
+    // dset.py:115-123: locate the root, then swing the path onto it
+    int32_t r = u;
+    while (true) {
+      int32_t pr = ld_acq(P + r);
+      if (pr == r) break;
+      r = pr;
+    }
+    while (true) {
+      int32_t j = ld_acq(P + u);
+      if (j <= r) break;
+      atomicCAS(P + u, j, r);
+      u = j;
+    }
+    return r;
+  } else if constexpr (FIND == GC_FIND_SPLIT) {
+    // dset.py:126-135
+    int32_t v = ld_acq(P + u);
+    int32_t w = ld_acq(P + v);
+    while (v != w) {
+      atomicCAS(P + u, v, w);
+      u = v;
+      v = ld_acq(P + u);
+      w = ld_acq(P + v);
+    }
+    return v;
+  } else if constexpr (FIND == GC_FIND_HALVE) {
+    // dset.py:138-147
+    int32_t v = ld_acq(P + u);
+    int32_t w = ld_acq(P + v);
+    while (v != w) {
+      atomicCAS(P + u, v, w);
+      u = ld_acq(P + u);
+      v = ld_acq(P + u);
+      w = ld_acq(P + v);
+    }
+    return v;
+  } else {  // GC_FIND_TWO_TRY, dset.py:150-163
+    int32_t v = ld_acq(P + u);
+    int32_t w = ld_acq(P + v);
+    while (v != w) {
+      if (!cas(P + u, v, w)) {
+        int32_t v2 = ld_acq(P + u);
+        int32_t w2 = ld_acq(P + v2);
+        if (v2 != w2) atomicCAS(P + u, v2, w2);
+      }
+      u = v;
+      v = ld_acq(P + u);
+      w = ld_acq(P + v);
+    }
+    return v;
+  }
+}
+
+// -------------------------------------------------------------- splices ---
+
+template <int SPLICE>
+__device__ __forceinline__ int32_t splice(int32_t u, int32_t v, int32_t* P) {
+  if constexpr (SPLICE == GC_SPLICE_SPLIT_ONE) {
+    // dset.py:180-186: returns u's old parent
+    int32_t pu = ld_acq(P + u);
+    int32_t w = ld_acq(P + pu);
+    if (pu != w) atomicCAS(P + u, pu, w);
+    return pu;
+  } else if constexpr (SPLICE == GC_SPLICE_HALVE_ONE) {
+    // dset.py:189-195: returns u's old grandparent
+    int32_t pu = ld_acq(P + u);
+    int32_t w = ld_acq(P + pu);
+    if (pu != w) atomicCAS(P + u, pu, w);
+    return w;
+  } else {
+    // dset.py:198-207: Rem's splice swings P[u] onto P[v]
+    int32_t pu = ld_acq(P + u);
+    int32_t pv = ld_acq(P + v);
+    atomicCAS(P + u, pu, pv);
+    return pu;
+  }
+}
+
+// --------------------------------------------------------------- unions ---
+// All return true iff this call merged two trees.
+
+template <int FIND, bool FOREST>
+__device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:222-234
+  int32_t* P = s.P;
+  int32_t pu = find<FIND>(u, P);
+  int32_t pv = find<FIND>(v, P);
+  while (pu != pv) {
+    if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
+    if (ld_acq(P + pu) == pu && cas(P + pu, pu, pv)) {
+      record<FOREST>(s, pu, u, v);
+      return true;
+    }
+    pu = find<FIND>(u, P);
+    pv = find<FIND>(v, P);
+  }
+  return false;
+}
+
+template <int FIND, bool FOREST>
+__device__ __forceinline__ bool union_hooks(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:237-252: claim the hook slot, then an uncontended parent write.
+  int32_t* P = s.P;
+  const int32_t unhooked = s.n;
+  int32_t pu = find<FIND>(u, P);
+  int32_t pv = find<FIND>(v, P);
+  while (pu != pv) {
+    if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
+    if (ld_acq(P + pu) == pu && cas(s.H + pu, unhooked, pv)) {
+      record<FOREST>(s, pu, u, v);
+      // release: the forest slot is visible before the parent write
+      __threadfence();
+      st_rlx(P + pu, pv);
+      return true;
+    }
+    pu = find<FIND>(u, P);
+    pv = find<FIND>(v, P);
+  }
+  return false;
+}
+
+template <int FIND, bool FOREST>
+__device__ __forceinline__ bool union_early(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:255-274
+  int32_t* P = s.P;
+  int32_t pu = u, pv = v;
+  bool merged = false;
+  while (pu != pv) {
+    if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
+    if (ld_acq(P + pu) == pu && cas(P + pu, pu, pv)) {
+      record<FOREST>(s, pu, u, v);
+      merged = true;
+      break;
+    }
+    int32_t z = ld_acq(P + pu);
+    int32_t w = ld_acq(P + z);
+    if (z != w) atomicCAS(P + pu, z, w);
+    pu = w;
+  }
+  if constexpr (FIND != GC_FIND_NAIVE) {
+    find<FIND>(u, P);
+    find<FIND>(v, P);
+  }
+  return merged;
+}
+
+template <int FIND, int SPLICE, bool FOREST>
+__device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:277-300.  A failed re-validation re-derives and loops, as the
+  // reference does (the paper's pseudocode returns instead).
+  int32_t* P = s.P;
+  int32_t ru = u, rv = v;
+  while (true) {
+    int32_t pru = ld_acq(P + ru);
+    int32_t prv = ld_acq(P + rv);
+    if (pru == prv) break;
+    if (pru < prv) {
+      int32_t t = ru; ru = rv; rv = t;
+      t = pru; pru = prv; prv = t;
+    }
+    if (ru == pru) {
+      // per-vertex spin lock; independent thread scheduling guarantees the
+      // holder makes progress even when it shares a warp with waiters
+      while (atomicCAS(s.L + ru, 0, 1) != 0) __nanosleep(32);
+      __threadfence();
+      int32_t pv = ld_acq(P + rv);
+      bool linked = (ru == ld_acq(P + ru)) && ru > pv;
+      if (linked) {
+        st_rlx(P + ru, pv);
+        record<FOREST>(s, ru, u, v);
+      }
+      __threadfence();
+      atomicExch(s.L + ru, 0);
+      if (linked) return true;
+    } else {
+      ru = splice<SPLICE>(ru, rv, P);
+    }
+  }
+  if constexpr (FIND != GC_FIND_NAIVE) {
+    find<FIND>(u, P);
+    find<FIND>(v, P);
+  }
+  return false;
+}
+
+template <int FIND, int SPLICE, bool FOREST>
+__device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:303-316
+  int32_t* P = s.P;
+  int32_t ru = u, rv = v;
+  while (true) {
+    int32_t pru = ld_acq(P + ru);
+    int32_t prv = ld_acq(P + rv);
+    if (pru == prv) return false;
+    if (pru < prv) {
+      int32_t t = ru; ru = rv; rv = t;
+      t = pru; pru = prv; prv = t;
+    }
+    if (ru == pru && cas(P + ru, ru, prv)) {
+      record<FOREST>(s, ru, u, v);
+      if constexpr (FIND != GC_FIND_NAIVE) {
+        find<FIND>(u, P);
+        find<FIND>(v, P);
+      }
+      return true;
+    }
+    ru = splice<SPLICE>(ru, rv, P);
+  }
+}
+
+template <int FIND, bool FOREST>
+__device__ __forceinline__ bool union_jtb(const UFState& s, int32_t u, int32_t v) {
+  // dset.py:319-331: link the lower (rank, id) root under the higher one
+  int32_t* P = s.P;
+  while (true) {
+    int32_t ru = find<FIND>(u, P);
+    int32_t rv = find<FIND>(v, P);
+    if (ru == rv) return false;
+    uint32_t kru = s.R[ru], krv = s.R[rv];
+    if (kru > krv || (kru == krv && ru > rv)) { int32_t t = ru; ru = rv; rv = t; }
+    if (cas(P + ru, ru, rv)) {
+      record<FOREST>(s, ru, u, v);
+      return true;
+    }
+  }
+}
+
+// Compile-time (union, find, splice) triple.  Only the 32 combinations of
+// dset.py:60-76 are ever instantiated (see dispatch.cuh).
+template <int UNION, int FIND, int SPLICE, bool FOREST>
+struct Rule {
+  static constexpr int kUnion = UNION;
+  static constexpr int kFind = FIND;
+  static constexpr int kSplice = SPLICE;
+  static constexpr bool kForest = FOREST;
+  __device__ __forceinline__ static bool unite(const UFState& s, int32_t u, int32_t v) {
+    if constexpr (UNION == GC_FINISH_ASYNC) return union_async<FIND, FOREST>(s, u, v);
+    else if constexpr (UNION == GC_FINISH_HOOKS) return union_hooks<FIND, FOREST>(s, u, v);
+    else if constexpr (UNION == GC_FINISH_EARLY) return union_early<FIND, FOREST>(s, u, v);
+    else if constexpr (UNION == GC_FINISH_REM_LOCK) return union_rem_lock<FIND, SPLICE, FOREST>(s, u, v);
+    else if constexpr (UNION == GC_FINISH_REM_CAS) return union_rem_cas<FIND, SPLICE, FOREST>(s, u, v);
+    else return union_jtb<FIND, FOREST>(s, u, v);
+  }
+};
+
+}  // namespace gc

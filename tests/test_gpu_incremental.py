@@ -1,0 +1,87 @@
+"""Incremental parity (driver.py:567-725) against reference goldens and the
+SequentialUF oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2008_11839_b200 import ConfigError, Insert, Query, incremental, parse_spec, path_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_bits(golden):
+    g = golden.incr["golden"]
+    batches = [[Insert(0, 1), Query(0, 1), Query(0, 2)], [Insert(1, 2), Query(0, 2)]]
+    labels, results, st = incremental(None, parse_spec("none+async+halve"), batches, capacity=5)
+    assert [b.tolist() for b in results] == g["bits"]
+    assert labels.tolist() == g["labels"]
+    assert st.component_count == g["components"]
+    assert set(st.phase_times) == {"insert", "query"}
+
+
+def test_random_stream_all_incremental_specs(golden):
+    r = golden.incr["random"]
+    ops = [Insert(u, v) if k == "i" else Query(u, v) for k, u, v in r["ops"]]
+    batches = [ops[i:i + r["batch"]] for i in range(0, len(ops), r["batch"])]
+    for text, exp in r["results"].items():
+        labels, results, st = incremental(None, parse_spec(text), batches, capacity=r["capacity"])
+        assert [b.tolist() for b in results] == exp["bits"], text
+        assert labels.tolist() == exp["labels"], text
+        assert st.component_count == exp["components"], text
+        assert st.rounds == exp["rounds"], text
+        assert st.edge_inspections.get("insert", 0) == exp["insp"], text
+
+
+def test_every_incremental_spec_vs_sequential_oracle():
+    rng = np.random.default_rng(4)
+    cap = 300
+    ops = []
+    for _ in range(3000):
+        u, v = int(rng.integers(0, cap)), int(rng.integers(0, cap))
+        ops.append(Insert(u, v) if rng.random() < 0.3 else Query(u, v))
+    batches = [ops[i:i + 128] for i in range(0, len(ops), 128)]
+    us = np.array([o.u for o in ops]); vs = np.array([o.v for o in ops])
+    isq = np.array([isinstance(o, Query) for o in ops], dtype=np.uint8)
+    bits, lab = oracle.incremental_replay(cap, us, vs, isq, 128)
+    from paper_2008_11839_b200 import enumerate_specs, format_spec
+    for spec in enumerate_specs():
+        if spec.sample.value != "none" or not spec.incremental_capable():
+            continue
+        labels, results, _ = incremental(None, spec, batches, capacity=cap)
+        assert np.concatenate(results).tolist() == bits.tolist(), format_spec(spec)
+        assert labels.tolist() == lab.tolist(), format_spec(spec)
+
+
+def test_starts_from_graph():
+    g = path_graph(6)
+    batches = [[Query(0, 5), Insert(6, 0), Query(6, 5)]]
+    labels, results, _ = incremental(g, parse_spec("none+sv"), batches, capacity=7)
+    assert results[0].tolist() == [True, False, True]
+    assert labels.tolist() == [0] * 7
+
+
+def test_racy_mode_soundness():
+    g = path_graph(50)
+    ops = [Insert(i + 50, i + 51) for i in range(30)] + [Query(i, i + 1) for i in range(40)]
+    labels, results, _ = incremental(g, parse_spec("none+async+halve"), [ops], capacity=81, racy=True)
+    bits, lab = oracle.incremental_replay(81, np.r_[np.arange(49), [o.u for o in ops]],
+                                          np.r_[np.arange(1, 50), [o.v for o in ops]],
+                                          np.r_[np.zeros(49), [isinstance(o, Query) for o in ops]].astype(np.uint8),
+                                          10 ** 6)
+    assert labels.tolist() == lab.tolist()
+    for pos, op in enumerate(ops):
+        if results[0][pos]:
+            assert isinstance(op, Query)
+
+
+@pytest.mark.parametrize("text,racy", [("none+lp", False), ("none+lt_pusa", False), ("none+sv", True),
+                                       ("none+rem_cas+naive+splice", True)])
+def test_rejections(text, racy):
+    with pytest.raises(ConfigError):
+        incremental(None, parse_spec(text), [[Insert(0, 1)]], capacity=4, racy=racy)
+
+
+def test_lazy_capacity():
+    labels, _, st = incremental(None, parse_spec("none+async+naive"), [[Insert(97, 99)]])
+    assert len(labels) == 100 and labels[97] == labels[99] == 97 and labels[98] == 98
+    assert st.component_count == 1
