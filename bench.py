@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: GConn static connectivity on B200 (BASELINE.json configs[1]).
+
+Workload (one "step"): static connectivity with k-out sampling + union-find
+Rem-CAS + path halving + splice (`kout+rem_cas+halve+splice`) on the RMAT
+scale-24 average-degree-16 graph (edge_factor 8, seed 1, the reference's
+gen_rmat distribution reproduced bit-for-bit on the GPU), inputs resident in
+HBM.  metric = undirected edges / second = (m_dir / 2) / step time, the
+reference's throughput definition (bench.py:167).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): every rank runs its own replica of the
+workload (weak scaling, no collective on the data path); value = all ranks'
+edges / max-over-ranks time.
+
+--impl reference times the reference algorithm's CPU restatement (oracle/,
+a C port of connlab's _pipeline with OpenMP on all host threads) on the same
+config; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SPEC = "kout+rem_cas+halve+splice"
+METRIC = "connectivity edges/sec (static & incremental) on RMAT at 1/2/4/8 B200"
+UNIT = "edges/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_graph(scale: int, ef: int, seed: int):
+    from paper_2008_11839_b200 import build_csr, gen_rmat
+    el = gen_rmat(scale, ef, seed=seed, device=True)
+    g = build_csr(el, keep_host=False)
+    del el
+    return g
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2008_11839_b200 import Graph, parse_spec, static_connectivity, static_connectivity_device
+    from paper_2008_11839_b200 import _native as N
+
+    spec = parse_spec(SPEC)
+    g = make_graph(args.scale, args.edge_factor, args.seed)
+    n, m = g.n, g.m
+    torch.cuda.synchronize()
+
+    # ---- untimed parity check against the CPU oracle (rank 0)
+    parity = None
+    labels, st0 = static_connectivity_device(g, spec, metrics=True)
+    if rank == 0 and not args.skip_check:
+        import oracle
+        off_h = g._d_off.cpu().numpy()
+        tgt_h = g._d_tgt.cpu().numpy()
+        ref, comps = oracle.components(n, off_h, tgt_h)
+        ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref)) and st0.component_count == comps
+        parity = {"labels_bit_exact": ok, "components": comps, "cov": st0.cov, "ic": st0.ic,
+                  "insp_sample": st0.edge_inspections.get("sample", 0),
+                  "insp_finish": st0.edge_inspections.get("finish", 0)}
+        if not ok:
+            print(json.dumps({"error": "parity failure", "parity": parity}), file=sys.stderr)
+            sys.exit(3)
+    del labels
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        _, st = static_connectivity_device(g, spec, metrics=False)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    lib = N.lib()
+    l0 = lib.gc_launch_count()
+    times, ksamp, kfin, kstats = [], [], [], None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            ksamp.append(st.kernel_ms_sample)
+            kfin.append(st.kernel_ms_finish)
+            kstats = st
+    torch.cuda.synchronize()
+    launches = lib.gc_launch_count() - l0
+    if ws > 1:
+        dist.barrier()
+    total_ms = sum(times)
+    tmax = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms = float(tmax.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * (m / 2) * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end: public API with host (pinned) buffers, H2D + D2H inside
+    e2e = None
+    if args.e2e_steps > 0:
+        off_h = g._d_off.cpu().pin_memory()
+        tgt_h = g._d_tgt.cpu().pin_memory()
+        host_g = Graph(n, off_h, tgt_h)
+        static_connectivity(host_g, spec)  # warm the path
+        torch.cuda.synchronize()
+        et = []
+        for _ in range(args.e2e_steps):
+            hg = Graph(n, off_h, tgt_h)  # fresh container: no cached device copy
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            lab, _ = static_connectivity(hg, spec)
+            torch.cuda.synchronize()
+            et.append(time.perf_counter() - t0)
+        e2e_t = statistics.median(et)
+        e2e = {"value": ws * (m / 2) / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 8 * (n + 1) + 4 * m,
+               "d2h_bytes_per_step": 4 * n, "seconds_per_step": e2e_t,
+               "timing": "wall clock around static_connectivity(host Graph) incl. pinned H2D, D2H, int64 labels"}
+
+    # ---- roofline of the dominant kernel (k-out union over the sampled rows)
+    peak, peak_kind = peaks()
+    e_s = kstats.edge_inspections.get("sample", 0)
+    e_f = kstats.edge_inspections.get("finish", 0)
+    kout_bytes = 8 * (n + 1) + 4 * e_s + 8 * n  # offsets + sampled targets + parent read/write
+    kms = statistics.mean(ksamp)
+    achieved = kout_bytes / (kms / 1e3) / 1e9
+    step_bytes = 4 * (e_s + e_f) + 8 * (n + 1) + 4 * n * 7  # SURVEY 8(d), P = 7 with sampling
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": args.traffic,
+                "kernel": "k_union_rows<Rule<REM_CAS,HALVE,SPLICE>> (k-out sampling)",
+                "kernel_ms": kms, "kernel_bytes": kout_bytes, "peak_source": peak_kind,
+                "step_alg_bytes": step_bytes,
+                "step_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+                "kernel_share_of_step": kms / ms_per_step}
+
+    cpu = None
+    if rank == 0 and args.cpu_baseline:
+        cpu = cpu_baseline(g)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": {"workload": f"static CC {SPEC} on RMAT scale-{args.scale} ef{args.edge_factor} "
+                                       f"(avg degree 16) seed {args.seed}",
+                           "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2,
+                           "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
+                           "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+                "e2e": e2e, "gpu_launches": launches, "launches_per_step": launches / args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(g):
+    """The reference algorithm's C port (oracle/) on this box's host cores."""
+    import oracle
+    off = g._d_off.cpu().numpy()
+    tgt = g._d_tgt.cpu().numpy()
+    threads = oracle.max_threads()
+    _, st, tm = oracle.static_uf(g.n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
+    t = sum(tm)
+    return {"value": (g.m / 2) / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"one full run of the same workload (n={g.n}, m={g.m}) — "
+                      f"sample {tm[0]:.3f}s finish {tm[1]:.3f}s finalize {tm[2]:.3f}s",
+            "seconds": t}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    n, e = oracle.gen_rmat(args.scale, args.edge_factor, seed=args.seed)
+    off, tgt = oracle.build_csr(n, e)
+    del e
+    m = len(tgt)
+    threads = oracle.max_threads()
+    for _ in range(args.warmup):
+        oracle.static_uf(n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
+    times = []
+    for _ in range(args.steps):
+        _, st, tm = oracle.static_uf(n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
+        times.append(sum(tm))
+    t = sum(times)
+    value = (m / 2) * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": f"static CC {SPEC} on RMAT scale-{args.scale} ef{args.edge_factor} "
+                                   f"(avg degree 16) seed {args.seed}", "spec": SPEC, "n": n,
+                       "m_directed": m},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": "the full workload per step: C/OpenMP restatement of connlab "
+                                       "_pipeline (oracle/gconn_oracle.c or_static_uf); the reference "
+                                       "itself is pure Python and takes ~45 s per run at this size"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--skip-check", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

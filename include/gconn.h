@@ -112,11 +112,16 @@ typedef struct gc_stats {
   int64_t lmax_count;     /* its multiplicity (cov = lmax_count / n)         */
   int64_t n_active;       /* vertices the finish phase saw                   */
   int64_t ic_count;       /* directed edges with differing post-sample labels */
+  double t_sample_kernel_ms; /* the sampler's union / traversal kernel alone */
+  double t_finish_kernel_ms; /* the finish union kernel (or all rounds) alone */
 } gc_stats;
 
 /* ---- library ------------------------------------------------------------*/
 const char* gc_last_error(void);
 const char* gc_version(void);
+/* Cumulative number of CUDA kernels libgconn has launched in this process
+ * (bench.py reports the delta over its timed region as gpu_launches). */
+long long gc_launch_count(void);
 /* Scratch bytes needed by gc_static_cc / gc_spanning_forest / gc_finish_phase. */
 size_t gc_workspace_size(int64_t n, int64_t m, const gc_spec* spec);
 

@@ -113,3 +113,32 @@ def incremental_replay(cap, us, vs, isq, batch):
     lib().or_incremental_replay(cap, _p(us), _p(vs), _p(isq), len(us), batch, bits.ctypes.data,
                                 lab.ctypes.data)
     return bits[:len(us)].astype(bool), lab[:cap].astype(np.int64)
+
+
+_UNION = {"async": 0, "rem_cas": 4}
+_FIND = {"naive": 0, "split": 1, "halve": 2, "compress": 3}
+_SPLICE = {"none": 0, "split": 1, "halve": 2, "splice": 3}
+
+
+def max_threads() -> int:
+    h = lib()
+    h.or_max_threads.restype = C.c_int
+    return int(h.or_max_threads())
+
+
+def static_uf(n, off, tgt, sample="kout", k=2, union="rem_cas", find="halve", splice="splice",
+              threads=0):
+    """CPU port of the union-find static pipeline (driver.py:454-500) — the
+    bench.py CPU baseline.  Returns (labels int32, stats dict, (t_sample, t_finish, t_finalize))."""
+    h = lib()
+    h.or_static_uf.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    tgt = np.ascontiguousarray(tgt, dtype=np.int32)
+    P = np.empty(max(n, 1), dtype=np.int32)
+    st = np.zeros(8, dtype=np.int64)
+    tm = np.zeros(3, dtype=np.float64)
+    h.or_static_uf(n, _p(off), _p(tgt), {"none": 0, "kout": 1}[sample], k, _UNION[union], _FIND[find],
+                   _SPLICE[splice], threads, P.ctypes.data, st.ctypes.data, tm.ctypes.data)
+    return P[:n], {"insp_sample": int(st[0]), "insp_finish": int(st[1]), "l_max": int(st[2]),
+                   "components": int(st[3]), "active": int(st[4])}, tuple(tm.tolist())

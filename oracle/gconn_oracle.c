@@ -240,3 +240,162 @@ void or_incremental_replay(int64_t cap, const int32_t* us, const int32_t* vs, co
   for (int64_t v = 0; v < cap; ++v) labels[v] = uf_find(p, (int32_t)v);
   free(p);
 }
+
+/* ===================================================================== *
+ * Static pipeline port (the CPU baseline arm of bench.py).               *
+ * driver.py:454-500 `_pipeline` for union-find finishes with the none /  *
+ * k-out (FIRST_K) samplers, over the dset.py union / find / splice menu, *
+ * multi-threaded with OpenMP; CAS = __atomic compare-exchange (the       *
+ * reference's striped-lock CAS, parallel.py:17-36).                      *
+ * ===================================================================== */
+enum { OR_ASYNC = 0, OR_REM_CAS = 4 };
+enum { OR_NAIVE = 0, OR_SPLIT = 1, OR_HALVE = 2, OR_COMPRESS = 3 };
+enum { OR_SPLIT_ONE = 1, OR_HALVE_ONE = 2, OR_SPLICE = 3 };
+
+static inline int32_t ld(int32_t* p) { return __atomic_load_n(p, __ATOMIC_RELAXED); }
+static inline int casw(int32_t* p, int32_t e, int32_t d) {
+  return __atomic_compare_exchange_n(p, &e, d, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED);
+}
+
+/* dset.py:109-147 */
+static int32_t or_find(int find, int32_t u, int32_t* P) {
+  if (find == OR_NAIVE) {
+    int32_t pu;
+    while ((pu = ld(P + u)) != u) u = pu;
+    return u;
+  }
+  if (find == OR_COMPRESS) {
+    int32_t r = u, pr, j;
+    while ((pr = ld(P + r)) != r) r = pr;
+    while ((j = ld(P + u)) > r) { casw(P + u, j, r); u = j; }
+    return r;
+  }
+  int32_t v = ld(P + u), w = ld(P + v);
+  while (v != w) {
+    casw(P + u, v, w);
+    u = find == OR_SPLIT ? v : ld(P + u);
+    v = ld(P + u);
+    w = ld(P + v);
+  }
+  return v;
+}
+
+/* dset.py:222-234 */
+static void or_union_async(int find, int32_t u, int32_t v, int32_t* P) {
+  int32_t pu = or_find(find, u, P), pv = or_find(find, v, P);
+  while (pu != pv) {
+    if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
+    if (ld(P + pu) == pu && casw(P + pu, pu, pv)) return;
+    pu = or_find(find, u, P);
+    pv = or_find(find, v, P);
+  }
+}
+
+/* dset.py:303-316 with the splices of dset.py:180-207 */
+static void or_union_rem(int find, int splice, int32_t u, int32_t v, int32_t* P) {
+  int32_t ru = u, rv = v;
+  for (;;) {
+    int32_t pru = ld(P + ru), prv = ld(P + rv);
+    if (pru == prv) return;
+    if (pru < prv) { int32_t t = ru; ru = rv; rv = t; t = pru; pru = prv; prv = t; }
+    if (ru == pru && casw(P + ru, ru, prv)) {
+      if (find != OR_NAIVE) { or_find(find, u, P); or_find(find, v, P); }
+      return;
+    }
+    if (splice == OR_SPLICE) {
+      casw(P + ru, pru, prv);
+      ru = pru;
+    } else {
+      int32_t pu = ld(P + ru), w = ld(P + pu);
+      if (pu != w) casw(P + ru, pu, w);
+      ru = splice == OR_SPLIT_ONE ? pu : w;
+    }
+  }
+}
+
+static inline void or_unite(int uni, int find, int splice, int32_t u, int32_t v, int32_t* P) {
+  if (uni == OR_REM_CAS) or_union_rem(find, splice, u, v, P);
+  else or_union_async(find, u, v, P);
+}
+
+static double wall(void) {
+#ifdef _OPENMP
+  return omp_get_wtime();
+#else
+  return 0.0;
+#endif
+}
+
+/* stats[0] insp_sample, [1] insp_finish, [2] l_max, [3] components,
+ * [4] active vertices; times[0..2] sample / finish / finalize seconds. */
+int or_static_uf(int64_t n, const int64_t* off, const int32_t* tgt, int sample, int k, int uni,
+                 int find, int splice, int threads, int32_t* P, int64_t* stats, double* times) {
+  if (threads > 0) {
+#ifdef _OPENMP
+    omp_set_num_threads(threads);
+#endif
+  }
+  int64_t insp_s = 0, insp_f = 0;
+  double t0 = wall();
+  /* DisjointSets.__init__ (dset.py:359) */
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) P[v] = (int32_t)v;
+  int32_t lmax = (int32_t)n;
+  if (sample == 1) {
+    /* kout_sample FIRST_K (sampling.py:61-86) */
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : insp_s)
+    for (int64_t v = 0; v < n; ++v) {
+      int64_t b = off[v], d = off[v + 1] - b, take = d < k ? d : k;
+      insp_s += take;
+      for (int64_t j = 0; j < take; ++j) or_unite(uni, find, splice, (int32_t)v, tgt[b + j], P);
+    }
+    /* compress_all (sampling.py:38-47) */
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v) {
+      int32_t r = P[v];
+      while (P[r] != r) r = P[r];
+      P[v] = r;
+    }
+    /* most_frequent_label (sampling.py:29-35): exact histogram, ties low */
+    int32_t* cnt = calloc((size_t)(n ? n : 1), sizeof(int32_t));
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v) __atomic_fetch_add(cnt + P[v], 1, __ATOMIC_RELAXED);
+    int64_t best = -1;
+    lmax = 0;
+    for (int64_t v = 0; v < n; ++v)
+      if (cnt[v] > best) { best = cnt[v]; lmax = (int32_t)v; }
+    free(cnt);
+  }
+  double t1 = wall();
+  /* _union_finish over the active vertices (driver.py:333-348, :473) */
+  int64_t active = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : insp_f, active)
+  for (int64_t u = 0; u < n; ++u) {
+    if (P[u] == lmax) continue;
+    ++active;
+    insp_f += off[u + 1] - off[u];
+    for (int64_t j = off[u]; j < off[u + 1]; ++j) or_unite(uni, find, splice, (int32_t)u, tgt[j], P);
+  }
+  double t2 = wall();
+  /* label_finalization (driver.py:420-429): roots are component minima */
+  int64_t comps = 0;
+#pragma omp parallel for schedule(static) reduction(+ : comps)
+  for (int64_t v = 0; v < n; ++v) {
+    int32_t r = ld(P + v);
+    while (ld(P + r) != r) r = ld(P + r);
+    P[v] = r;
+    comps += r == v;
+  }
+  double t3 = wall();
+  stats[0] = insp_s; stats[1] = insp_f; stats[2] = lmax; stats[3] = comps; stats[4] = active;
+  times[0] = t1 - t0; times[1] = t2 - t1; times[2] = t3 - t2;
+  return 0;
+}
+
+int or_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

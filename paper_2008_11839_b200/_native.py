@@ -48,13 +48,15 @@ class Stats(C.Structure):
                 ("t_finalize_ms", C.c_double), ("insp_sample", C.c_int64),
                 ("insp_finish", C.c_int64), ("rounds", C.c_int64), ("components", C.c_int64),
                 ("l_max", C.c_int64), ("lmax_count", C.c_int64), ("n_active", C.c_int64),
-                ("ic_count", C.c_int64)]
+                ("ic_count", C.c_int64), ("t_sample_kernel_ms", C.c_double),
+                ("t_finish_kernel_ms", C.c_double)]
 
 
 _VP, _I64, _I32, _SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
 _SIGNATURES = {
     "gc_last_error": (C.c_char_p, []),
     "gc_version": (C.c_char_p, []),
+    "gc_launch_count": (C.c_longlong, []),
     "gc_workspace_size": (_SZ, [_I64, _I64, C.POINTER(Spec)]),
     "gc_static_cc": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, C.c_int,
                                C.POINTER(Stats), _VP, _SZ, _VP]),

@@ -242,7 +242,7 @@ int gc_gen_rmat(int32_t scale, int64_t num_pairs, const double* base_host, uint6
     a.jlev_c_hi = uint64_t(jl.c >> 64);
     a.jlev_c_lo = uint64_t(jl.c);
     const int64_t chunks = (num_pairs + kGenChunk - 1) / kGenChunk;
-    k_rmat<<<grid_for(chunks, 128, 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(a, src, dst);
+    (k_rmat<<<grid_for(chunks, 128, 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(a, src, dst), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   });
 }
@@ -253,8 +253,8 @@ int gc_gen_uniform_pow2(int32_t log2n, int64_t num_pairs, uint64_t state_hi, uin
     require(log2n >= 1 && log2n <= 31, GC_ERR_CONFIG, "log2n must be in [1, 31]");
     if (num_pairs <= 0) return;
     const int64_t chunks = (num_pairs + kGenChunk - 1) / kGenChunk;
-    k_uniform_pow2<<<grid_for(chunks, 128, 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        log2n, num_pairs, state_hi, state_lo, inc_hi, inc_lo, src, dst);
+    (k_uniform_pow2<<<grid_for(chunks, 128, 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        log2n, num_pairs, state_hi, state_lo, inc_hi, inc_lo, src, dst), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   });
 }
@@ -283,7 +283,7 @@ int gc_build_csr(int64_t n, const int64_t* src, const int64_t* dst, int64_t k, i
     GC_CUDA(cudaMemcpyAsync(w.ctr, &sentinel, 8, cudaMemcpyHostToDevice, st));
     int64_t m = 0;
     if (k > 0) {
-      k_sym_keys<<<grid_for(k, 256, 16), 256, 0, st>>>(src, dst, k, n, bits, w.keys, w.ctr);
+      (k_sym_keys<<<grid_for(k, 256, 16), 256, 0, st>>>(src, dst, k, n, bits, w.keys, w.ctr), ::gc::count_launch());
       GC_CHECK_LAUNCH();
       unsigned long long bad = 0;
       GC_CUDA(cudaMemcpyAsync(&bad, w.ctr, 8, cudaMemcpyDeviceToHost, st));
@@ -304,7 +304,7 @@ int gc_build_csr(int64_t n, const int64_t* src, const int64_t* dst, int64_t k, i
       }
       m = int64_t(nu) - (nu > 0 && last == sentinel ? 1 : 0);
     }
-    k_csr_fill<<<grid_for(m + 1, 256, 16), 256, 0, st>>>(w.keys, m, n, bits, offsets, targets);
+    (k_csr_fill<<<grid_for(m + 1, 256, 16), 256, 0, st>>>(w.keys, m, n, bits, offsets, targets), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaStreamSynchronize(st));
     *m_out = m;

@@ -170,7 +170,7 @@ void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
   cudaStream_t st = h->st;
   const int32_t sentinel = int32_t(h->cap);
   if (h->uf) {
-    k_incr_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel);
+    (k_incr_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false,
                      uf_args(h, us, vs, len, isq), st);
@@ -178,12 +178,12 @@ void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     return;
   }
   ensure_coo(h, len);
-  k_label_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel);
+  (k_label_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel), ::gc::count_launch());
   unsigned long long* cnt = h->ctr + C_SCRATCH0;
   GC_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
   Coo w = h->rw.work;
-  k_incr_coo<<<g1(len), kIB, 0, st>>>(us, vs, isq, len, h->state, h->spec.finish == GC_FINISH_LT,
-                                      w, cnt);
+  (k_incr_coo<<<g1(len), kIB, 0, st>>>(us, vs, isq, len, h->state, h->spec.finish == GC_FINISH_LT,
+                                      w, cnt), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   h->rw.work.len = n_ins;
   h->rw.work.weight = n_ins;
@@ -203,7 +203,7 @@ int64_t count_inserts(const uint8_t* isq, int64_t len, cudaStream_t st, unsigned
   if (!isq) return len;
   unsigned long long* c = ctr + C_SCRATCH1;
   GC_CUDA(cudaMemsetAsync(c, 0, 8, st));
-  k_count_bytes<<<g1(len), kIB, 0, st>>>(isq, len, c);
+  (k_count_bytes<<<g1(len), kIB, 0, st>>>(isq, len, c), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   unsigned long long* hw = pinned_words();
   GC_CUDA(cudaMemcpyAsync(hw, c, 8, cudaMemcpyDeviceToHost, st));
@@ -307,7 +307,7 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     GC_CUDA(cudaEventRecord(h->ev[0], st));
     if (n_ins) insert_phase(h, us, vs, is_query, len, n_ins, stats);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
-    k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out);
+    (k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[2], st));
     GC_CUDA(cudaEventSynchronize(h->ev[2]));
@@ -336,8 +336,8 @@ int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len,
     require(h && len >= 0, GC_ERR_ARG, "bad arguments");
     if (len == 0) return;
     GC_CUDA(cudaEventRecord(h->ev[0], h->st));
-    k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap),
-                                             bits_out);
+    (k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap),
+                                             bits_out), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[1], h->st));
     GC_CUDA(cudaEventSynchronize(h->ev[1]));
@@ -366,10 +366,10 @@ int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components) {
     int32_t* mins = nullptr;
     GC_CUDA(cudaMallocAsync(&mins, cap * 4, st));
     GC_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
-    k_incr_export<<<g1(cap), kIB, 0, st>>>(h->state, cap, int32_t(cap), labels_out);
+    (k_incr_export<<<g1(cap), kIB, 0, st>>>(h->state, cap, int32_t(cap), labels_out), ::gc::count_launch());
     run_finalize(labels_out, int32_t(cap), mins, h->ctr, st);
     GC_CUDA(cudaMemsetAsync(h->ctr + C_SCRATCH0, 0, 8, st));
-    k_incr_count<<<g1(cap), kIB, 0, st>>>(h->state, labels_out, cap, int32_t(cap), h->ctr + C_SCRATCH0);
+    (k_incr_count<<<g1(cap), kIB, 0, st>>>(h->state, labels_out, cap, int32_t(cap), h->ctr + C_SCRATCH0), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     unsigned long long* hw = pinned_words();
     GC_CUDA(cudaMemcpyAsync(hw, h->ctr + C_SCRATCH0, 8, cudaMemcpyDeviceToHost, st));

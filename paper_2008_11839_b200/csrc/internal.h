@@ -82,6 +82,7 @@ enum Counter : int {
   C_NEXT,          // frontier size (BFS/LDD)
   C_SCRATCH0,
   C_SCRATCH1,
+  C_CYCLE,         // finalize walk exceeded n steps (cyclic input labels)
   C_COUNT_ = 32
 };
 
@@ -141,6 +142,10 @@ void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t*
                       int32_t sentinel, uint8_t* bits, cudaStream_t st);
 
 int num_sms();
+
+// Kernel launches issued by libgconn (process-wide, exported through
+// gc_launch_count for the bench's gpu_launches claim).
+void count_launch();
 
 // Thread-local last-error string behind gc_last_error().
 void set_last_error(const char* msg);

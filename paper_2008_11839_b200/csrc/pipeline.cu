@@ -1,6 +1,8 @@
 // pipeline.cu — elementwise phases of the two-phase pipeline
 // (driver.py:454-500): set initialisation, compression, most-frequent label,
 // active gather, finalisation and canonical relabelling.
+#include <atomic>
+
 #include "pipeline.cuh"
 
 namespace gc {
@@ -168,7 +170,7 @@ __global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
   }
   block_add<kEwBlock>(ctr + C_COMPONENTS, roots);
   if (__syncthreads_or(noncanon) && threadIdx.x == 0) ctr[C_NONCANON] = 1;
-  if (cyc) ctr[C_SCRATCH1] = 1;
+  if (cyc) ctr[C_CYCLE] = 1;
 }
 
 __global__ void k_canon_init(int32_t* mins, int32_t n, const unsigned long long* ctr) {
@@ -205,7 +207,9 @@ __global__ void k_ic_census(const int32_t* P, int32_t n, const int64_t* off, con
     const int32_t pu = P[u];
     for (int64_t j = off[u]; j < off[u + 1]; ++j) {
       const int32_t pt = P[tgt[j]];
-      ic += (pu != pt) + (pt == lmax);
+      // over all rows: count crossing entries; over the active rows only,
+      // the reverse entries from L_max-labelled rows are added back
+      ic += list ? (pu != pt) + (pt == lmax) : (pu != pt);
     }
   }
   block_add<kEwBlock>(ctr + C_IC, ic);
@@ -224,39 +228,56 @@ __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long
   block_add<kEwBlock>(out, c);
 }
 
+namespace {
+std::atomic<long long> g_launches{0};
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+long long launch_total() { return g_launches.load(); }
+
 unsigned long long* pinned_words() {
   static thread_local unsigned long long* p = nullptr;
   if (!p) GC_CUDA(cudaMallocHost(&p, 64 * sizeof(unsigned long long)));
   return p;
 }
 
+__global__ void k_set_ctr(unsigned long long* ctr, int idx, unsigned long long v) { ctr[idx] = v; }
+
+void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
+  (k_set_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st) {
   if (n <= 0) return;
-  k_fill<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(a, n, v);
+  (k_fill<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(a, n, v), ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
 void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cudaStream_t st) {
   if (n > 0) {
     const int g = grid_for(n, kEwBlock, 8);
-    k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr);
-    k_count_eq<<<g, kEwBlock, 0, st>>>(P, n, ctr);
-    k_hist_zero<<<g, kEwBlock, 0, st>>>(hist, n, ctr);
-    k_hist_add<<<g, kEwBlock, 0, st>>>(P, hist, n, ctr);
-    k_hist_argmax<<<g, kEwBlock, 0, st>>>(hist, n, ctr);
+    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr), ::gc::count_launch());
+    (k_count_eq<<<g, kEwBlock, 0, st>>>(P, n, ctr), ::gc::count_launch());
+    (k_hist_zero<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
+    (k_hist_add<<<g, kEwBlock, 0, st>>>(P, hist, n, ctr), ::gc::count_launch());
+    (k_hist_argmax<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
   }
-  k_mode_finish<<<1, 1, 0, st>>>(n, ctr);
+  (k_mode_finish<<<1, 1, 0, st>>>(n, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
 void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st) {
   if (n <= 0) return;
   const int g = grid_for(n, kEwBlock, 8);
-  k_finalize<<<g, kEwBlock, 0, st>>>(P, n, ctr);
-  k_canon_init<<<g, kEwBlock, 0, st>>>(mins, n, ctr);
-  k_canon_min<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr);
-  k_canon_apply<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr);
+  (k_finalize<<<g, kEwBlock, 0, st>>>(P, n, ctr), ::gc::count_launch());
+  (k_canon_init<<<g, kEwBlock, 0, st>>>(mins, n, ctr), ::gc::count_launch());
+  (k_canon_min<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr), ::gc::count_launch());
+  (k_canon_apply<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
 }  // namespace gc
+
+extern "C" long long gc_launch_count(void) { return gc::launch_total(); }

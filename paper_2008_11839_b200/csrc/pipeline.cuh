@@ -53,5 +53,6 @@ __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long
 void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cudaStream_t st);
 void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st);
 void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
+void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 
 }  // namespace gc

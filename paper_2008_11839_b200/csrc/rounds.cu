@@ -329,7 +329,7 @@ int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsW
   int64_t rounds = 0;
   const int gv = grid_e(nl);
   if (fo.on()) {
-    k_fill_u64<<<gv, kRB, 0, st>>>(w.win, nl, kNoWin);
+    (k_fill_u64<<<gv, kRB, 0, st>>>(w.win, nl, kNoWin), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
   if (s.finish == GC_FINISH_SV) {
@@ -339,13 +339,13 @@ int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsW
       ++rounds;
       insp += work.weight;
       GC_CUDA(cudaMemcpyAsync(B, A, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-      k_set<<<1, 1, 0, st>>>(flag, 0);
-      if (work.len) k_sv_hook<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win, flag);
+      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
+      if (work.len) (k_sv_hook<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win, flag), ::gc::count_launch());
       if (fo.on() && work.len) {
-        k_sv_win<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win);
-        k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv);
+        (k_sv_win<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win), ::gc::count_launch());
+        (k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv), ::gc::count_launch());
       }
-      k_full_shortcut<<<gv, kRB, 0, st>>>(B, nl);
+      (k_full_shortcut<<<gv, kRB, 0, st>>>(B, nl), ::gc::count_launch());
       GC_CHECK_LAUNCH();
       const bool changed = read_flag(flag, st);
       int32_t* t = A; A = B; B = t;
@@ -362,19 +362,19 @@ int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsW
       ++rounds;
       insp += cur->weight;
       GC_CUDA(cudaMemcpyAsync(msg, P, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-      k_set<<<1, 1, 0, st>>>(flag, 0);
-      if (cur->len) k_lt_connect<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect);
+      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
+      if (cur->len) (k_lt_connect<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect), ::gc::count_launch());
       if (fo.on() && cur->len) {
-        k_lt_win<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect, w.win);
-        k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv);
+        (k_lt_win<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect, w.win), ::gc::count_launch());
+        (k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv), ::gc::count_launch());
       }
-      if (s.lt_update == GC_LT_UPDATE_ROOTS) k_lt_update<<<gv, kRB, 0, st>>>(P, msg, nl);
-      k_lt_shortcut<<<gv, kRB, 0, st>>>(P, msg, nl, s.lt_shortcut == GC_LT_SHORTCUT_FULL, flag);
+      if (s.lt_update == GC_LT_UPDATE_ROOTS) (k_lt_update<<<gv, kRB, 0, st>>>(P, msg, nl), ::gc::count_launch());
+      (k_lt_shortcut<<<gv, kRB, 0, st>>>(P, msg, nl, s.lt_shortcut == GC_LT_SHORTCUT_FULL, flag), ::gc::count_launch());
       GC_CHECK_LAUNCH();
       if (s.lt_alter && cur->len) {
-        k_set<<<1, 1, 0, st>>>(ctr + C_WORK, 0);
-        k_set<<<1, 1, 0, st>>>(ctr + C_WORK_W, 0);
-        k_lt_alter<<<grid_e(cur->len), kRB, 0, st>>>(*cur, *nxt, P, ctr);
+        (k_set<<<1, 1, 0, st>>>(ctr + C_WORK, 0), ::gc::count_launch());
+        (k_set<<<1, 1, 0, st>>>(ctr + C_WORK_W, 0), ::gc::count_launch());
+        (k_lt_alter<<<grid_e(cur->len), kRB, 0, st>>>(*cur, *nxt, P, ctr), ::gc::count_launch());
         GC_CHECK_LAUNCH();
         unsigned long long* h = host_words();
         GC_CUDA(cudaMemcpyAsync(h + 8, ctr + C_CHANGED, 8, cudaMemcpyDeviceToHost, st));
@@ -397,10 +397,10 @@ int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsW
     while (true) {
       ++rounds;
       insp += work.weight;
-      k_set<<<1, 1, 0, st>>>(flag, 0);
-      k_st_init<<<gv, kRB, 0, st>>>(A, B, nl);
-      if (work.len) k_st_edges<<<grid_e(work.len), kRB, 0, st>>>(work, A, B);
-      k_differ<<<gv, kRB, 0, st>>>(A, B, nl, flag);
+      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
+      (k_st_init<<<gv, kRB, 0, st>>>(A, B, nl), ::gc::count_launch());
+      if (work.len) (k_st_edges<<<grid_e(work.len), kRB, 0, st>>>(work, A, B), ::gc::count_launch());
+      (k_differ<<<gv, kRB, 0, st>>>(A, B, nl, flag), ::gc::count_launch());
       GC_CHECK_LAUNCH();
       const bool changed = read_flag(flag, st);
       int32_t* t = A; A = B; B = t;
@@ -415,8 +415,8 @@ int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsW
     ++rounds;
     insp += work.weight;
     GC_CUDA(cudaMemcpyAsync(snap, P, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-    k_set<<<1, 1, 0, st>>>(flag, 0);
-    if (work.len) k_lp<<<grid_e(work.len), kRB, 0, st>>>(work, snap, P, flag);
+    (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
+    if (work.len) (k_lp<<<grid_e(work.len), kRB, 0, st>>>(work, snap, P, flag), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     if (!read_flag(flag, st)) break;
   }
@@ -439,15 +439,15 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
   const int32_t lmax = all_active ? n : int32_t(h[C_LMAX]);
   const int64_t degsum = all_active ? g.m : int64_t(h[C_INSP_FINISH]);
   if (count == 0) {
-    k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, 0);
+    (k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, 0), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     return 0;
   }
   // gather the working COO (driver.py:325-330), twin-deduplicated:
   // per-row kept counts, exclusive scan, then a write pass
   const bool map_labels = s.finish == GC_FINISH_LT || s.finish == GC_FINISH_LP;
-  k_coo_count<<<grid_e(count + 1), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax,
-                                                 all_active, w.cnt);
+  (k_coo_count<<<grid_e(count + 1), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax,
+                                                 all_active, w.cnt), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   size_t tb = w.cub_bytes;
   GC_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt, w.pos, int(count + 1), st));
@@ -458,8 +458,8 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
   work.weight = degsum;
   Coo out = work;
   if (!fu) out.idx = nullptr;
-  k_coo_write<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
-                                             map_labels, w.pos, out);
+  (k_coo_write<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
+                                             map_labels, w.pos, out), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   work.idx = out.idx;
   if (!fu) w.spare.idx = nullptr;
@@ -467,7 +467,7 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
   ForestOut fo;
   if (fu) fo = ForestOut{g.offsets, g.targets, fu, fv};
   const int64_t rounds = loop_rounds(s, P, n, work, w, ctr, insp, fo, st);
-  k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, static_cast<unsigned long long>(insp));
+  (k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, static_cast<unsigned long long>(insp)), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   return rounds;
 }
@@ -483,7 +483,7 @@ int64_t run_rounds_coo(const gc_spec& s, int32_t* labels, int64_t nl, Coo& work,
                        unsigned long long* ctr, int counter_slot, cudaStream_t st) {
   int64_t insp = 0;
   const int64_t r = loop_rounds(s, labels, nl, work, w, ctr, insp, ForestOut{}, st);
-  k_add<<<1, 1, 0, st>>>(ctr + counter_slot, static_cast<unsigned long long>(insp));
+  (k_add<<<1, 1, 0, st>>>(ctr + counter_slot, static_cast<unsigned long long>(insp)), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   return r;
 }

@@ -51,8 +51,8 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
   }
   require(s.kout_k == 1 || s.kout_rand_offsets != nullptr, GC_ERR_ARG,
           "FIRST_PLUS_RANDOM needs host-drawn row offsets");
-  k_kout_random_pairs<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(
-      g.offsets, g.targets, n, s.kout_k, s.kout_rand_offsets, w.coo_u, w.coo_v, ctr);
+  (k_kout_random_pairs<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(
+      g.offsets, g.targets, n, s.kout_k, s.kout_rand_offsets, w.coo_u, w.coo_v, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   CooUnionArgs ca{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, w.coo_u, w.coo_v, int64_t(n) * s.kout_k,
                   nullptr};
@@ -103,8 +103,8 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:95-96
   GC_CUDA(cudaMemsetAsync(ctr + C_SCRATCH0, 0, 8, st));
-  k_hb_phase1<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, n, a.P, a.fu,
-                                                             a.fv, w.q0, ctr);
+  (k_hb_phase1<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, n, a.P, a.fu,
+                                                             a.fv, w.q0, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   // Phase 2 (sampling.py:110-116): union the first N edges of each root
   a.list = w.q0;
@@ -239,7 +239,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   int32_t* minv = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
   unsigned long long* qc[2] = {ctr + C_NEXT, ctr + C_SCRATCH0};
   int32_t* q[2] = {w.q0, w.q1};
-  k_bfs_seed<<<1, 1, 0, st>>>(w.lvl, q[0], qc[0], int32_t(s.bfs_source), minv);
+  (k_bfs_seed<<<1, 1, 0, st>>>(w.lvl, q[0], qc[0], int32_t(s.bfs_source), minv), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   unsigned long long* pinned = pinned_words();
   unsigned long long cur = 1;
@@ -248,9 +248,9 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     GC_CUDA(cudaMemsetAsync(qc[cur_i ^ 1], 0, 8, st));
     const int64_t blocks64 = (int64_t(cur) * 32 + kBfsBlock - 1) / kBfsBlock / 32 + 1;
     int blocks = int(blocks64 < int64_t(num_sms()) * 8 ? blocks64 : int64_t(num_sms()) * 8);
-    k_bfs_expand<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[cur_i], qc[cur_i], w.lvl,
+    (k_bfs_expand<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[cur_i], qc[cur_i], w.lvl,
                                                 fu ? w.par : nullptr, q[cur_i ^ 1], qc[cur_i ^ 1],
-                                                level, ctr + C_INSP_SAMPLE, minv);
+                                                level, ctr + C_INSP_SAMPLE, minv), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(pinned, qc[cur_i ^ 1], 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
@@ -258,10 +258,10 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     cur_i ^= 1;
   }
   if (fu) {
-    k_bfs_reroot<<<1, 1, 0, st>>>(w.par, minv);
+    (k_bfs_reroot<<<1, 1, 0, st>>>(w.par, minv), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  k_bfs_label<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(w.lvl, w.par, minv, n, P, fu, fv);
+  (k_bfs_label<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(w.lvl, w.par, minv, n, P, fu, fv), ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
@@ -410,8 +410,8 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   int32_t* dmax = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
   GC_CUDA(cudaMemsetAsync(dmax, 0, 4, st));
   const int ge = grid_for(n, kEwBlock, 8);
-  k_ldd_delta_max<<<ge, kEwBlock, 0, st>>>(n, s.seed, beta, dmax);
-  k_ldd_start<<<ge, kEwBlock, 0, st>>>(n, s.seed, beta, dmax, w.start, w.lvl, w.par);
+  (k_ldd_delta_max<<<ge, kEwBlock, 0, st>>>(n, s.seed, beta, dmax), ::gc::count_launch());
+  (k_ldd_start<<<ge, kEwBlock, 0, st>>>(n, s.seed, beta, dmax, w.start, w.lvl, w.par), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   unsigned long long* hq = pinned_words();
   GC_CUDA(cudaMemcpyAsync(hq + 1, dmax, 4, cudaMemcpyDeviceToHost, st));
@@ -429,11 +429,11 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     if (cur) {
       const int64_t blocks64 = (int64_t(cur) * 32 + kBfsBlock - 1) / kBfsBlock / 32 + 1;
       const int blocks = int(blocks64 < int64_t(num_sms()) * 8 ? blocks64 : int64_t(num_sms()) * 8);
-      k_ldd_grow<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[ci], qc[ci], w.lvl, w.par,
-                                               q[ci ^ 1], qc[ci ^ 1], r, ctr + C_INSP_SAMPLE);
+      (k_ldd_grow<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[ci], qc[ci], w.lvl, w.par,
+                                               q[ci ^ 1], qc[ci ^ 1], r, ctr + C_INSP_SAMPLE), ::gc::count_launch());
     }
     if (r <= last_start)
-      k_ldd_centres<<<ge, kEwBlock, 0, st>>>(n, r, w.start, w.lvl, w.par, q[ci ^ 1], qc[ci ^ 1]);
+      (k_ldd_centres<<<ge, kEwBlock, 0, st>>>(n, r, w.start, w.lvl, w.par, q[ci ^ 1], qc[ci ^ 1]), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(hq, qc[ci ^ 1], 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
@@ -444,8 +444,8 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   // labels: minimum member id per cluster (q0 is free again: reuse as mins)
   int32_t* mins = w.q0;
   fill(mins, n, INT_MAX, st);
-  k_ldd_mins<<<ge, kEwBlock, 0, st>>>(w.par, mins, n);
-  k_ldd_label<<<ge, kEwBlock, 0, st>>>(w.par, mins, P, n);
+  (k_ldd_mins<<<ge, kEwBlock, 0, st>>>(w.par, mins, n), ::gc::count_launch());
+  (k_ldd_label<<<ge, kEwBlock, 0, st>>>(w.par, mins, P, n), ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 

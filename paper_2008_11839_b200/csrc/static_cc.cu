@@ -26,7 +26,7 @@ namespace gc {
 namespace {
 
 struct EventSet {
-  cudaEvent_t e[6];
+  cudaEvent_t e[10];
   EventSet() {
     for (auto& x : e) GC_CUDA(cudaEventCreate(&x));
   }
@@ -104,6 +104,8 @@ struct Pipeline {
   cudaStream_t st;
   Layout<Arena> ws;
   int32_t n;
+  cudaEvent_t* kev = nullptr;  // [0,1] sampler kernel, [2,3] finish kernel
+  bool timed_sample = false;
 
   Pipeline(const gc_csr& g_, const gc_spec& s_, int32_t* P_, int32_t* fu_, int32_t* fv_,
            void* wsp, size_t wsb, cudaStream_t st_)
@@ -131,7 +133,7 @@ struct Pipeline {
     if (n == 0) return;
     int32_t* H = c.unite == GC_FINISH_HOOKS ? ws.H : nullptr;
     int32_t* L = c.unite == GC_FINISH_REM_LOCK ? ws.L : nullptr;
-    k_init_sets<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, H, L, n);
+    (k_init_sets<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, H, L, n), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 
@@ -144,31 +146,37 @@ struct Pipeline {
     }
     if (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB) {
       init_sets(sc);
+      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
       if (s.sample == GC_SAMPLE_KOUT) {
         run_kout(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       } else {
         run_hb(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       }
+      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      timed_sample = true;
       if (n) {
-        k_compress<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n);
+        (k_compress<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n), ::gc::count_launch());
         GC_CHECK_LAUNCH();
       }
     } else if (s.sample == GC_SAMPLE_BFS) {
       init_sets(sc);
+      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
       run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
+      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      timed_sample = true;
     } else {
       init_sets(sc);
+      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
       run_ldd(g, s, P, ws.samp, ws.ctr, st);
+      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      timed_sample = true;
     }
     run_mode(P, n, ws.hist, ws.ctr, st);
   }
 
   void set_lmax_sentinel() {
     // driver.py:467-468: the sentinel n matches no vertex
-    unsigned long long v[2] = {static_cast<unsigned long long>(n), 0ull};
-    GC_CUDA(cudaMemcpyAsync(ws.ctr + C_LMAX, v, sizeof(v), cudaMemcpyHostToDevice, st));
-    // keep the host array alive until the copy is done
-    GC_CUDA(cudaStreamSynchronize(st));
+    set_ctr(ws.ctr, C_LMAX, static_cast<unsigned long long>(n), st);
   }
 
   // ---- finish phase (driver.py:473-481) ----------------------------------
@@ -177,8 +185,8 @@ struct Pipeline {
   int64_t finish() {
     const bool all_active = s.sample == GC_SAMPLE_NONE;
     if (!all_active && n) {
-      k_gather_active<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n, g.offsets, ws.list,
-                                                                     ws.ctr);
+      (k_gather_active<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n, g.offsets, ws.list,
+                                                                     ws.ctr), ::gc::count_launch());
       GC_CHECK_LAUNCH();
     }
     if (is_union_finish(s.finish)) {
@@ -193,9 +201,7 @@ struct Pipeline {
         a.take_max = INT_MAX;
         a.lower_only = 1;
         a.insp = nullptr;
-        unsigned long long m = static_cast<unsigned long long>(g.m);
-        GC_CUDA(cudaMemcpyAsync(ws.ctr + C_INSP_FINISH, &m, sizeof(m), cudaMemcpyHostToDevice, st));
-        GC_CUDA(cudaStreamSynchronize(st));
+        set_ctr(ws.ctr, C_INSP_FINISH, static_cast<unsigned long long>(g.m), st);
       } else {
         a.list = ws.list;
         a.count_dev = ws.ctr + C_N_ACTIVE;
@@ -204,10 +210,16 @@ struct Pipeline {
         a.lower_only = 0;
         a.insp = nullptr;  // counted by the gather
       }
+      if (kev) GC_CUDA(cudaEventRecord(kev[2], st));
       launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
+      if (kev) GC_CUDA(cudaEventRecord(kev[3], st));
       return 0;
     }
-    return run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
+    if (kev) GC_CUDA(cudaEventRecord(kev[2], st));
+    const int64_t r =
+        run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
+    if (kev) GC_CUDA(cudaEventRecord(kev[3], st));
+    return r;
   }
 };
 
@@ -232,6 +244,7 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
   }
   Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
   static thread_local EventSet ev;
+  pl.kev = ev.e + 5;
   const int32_t n = pl.n;
 
   GC_CUDA(cudaEventRecord(ev.e[0], st));
@@ -240,8 +253,8 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
   if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
   if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
-    k_ic_census<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, g->offsets, g->targets,
-                                                               nullptr, pl.ws.ctr);
+    (k_ic_census<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, g->offsets, g->targets,
+                                                               nullptr, pl.ws.ctr), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
   GC_CUDA(cudaEventRecord(ev.e[2], st));
@@ -255,18 +268,20 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
     // spanning_forest: component_count = n - |forest| (driver.py:535)
     unsigned long long* cnt = pl.ws.ctr + C_SCRATCH1;
     GC_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-    if (n) k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, cnt);
+    if (n) (k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, cnt), ::gc::count_launch());
     unsigned long long pop = 0;
     GC_CUDA(cudaMemcpyAsync(&pop, cnt, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
     c[C_COMPONENTS] = static_cast<unsigned long long>(n) - pop;
   }
   GC_CUDA(cudaStreamSynchronize(st));
-  require(c[C_SCRATCH1] == 0 || forest, GC_ERR_MALFORMED, "label array contains a cycle");
+  require(c[C_CYCLE] == 0, GC_ERR_MALFORMED, "label array contains a cycle");
   if (stats) {
     stats->t_sample_ms = ms(ev.e[0], ev.e[1]);
     stats->t_finish_ms = ms(ev.e[2], ev.e[3]);
     stats->t_finalize_ms = forest ? 0.0 : ms(ev.e[3], ev.e[4]);
+    stats->t_sample_kernel_ms = pl.timed_sample ? ms(ev.e[5], ev.e[6]) : 0.0;
+    stats->t_finish_kernel_ms = ms(ev.e[7], ev.e[8]);
     stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
     stats->insp_finish = int64_t(c[C_INSP_FINISH]);
     stats->rounds = rounds;
@@ -350,8 +365,7 @@ int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io, in
     s2.sample = GC_SAMPLE_KOUT;  // force the gather path (labels are given)
     Pipeline pl(*g, s2, labels_io, nullptr, nullptr, ws, ws_bytes, st);
     const int32_t n = pl.n;
-    unsigned long long lm = static_cast<unsigned long long>(l_max);
-    GC_CUDA(cudaMemcpyAsync(pl.ws.ctr + C_LMAX, &lm, 8, cudaMemcpyHostToDevice, st));
+    set_ctr(pl.ws.ctr, C_LMAX, static_cast<unsigned long long>(l_max), st);
     if (is_union_finish(spec->finish)) {
       UFConfig c = finish_cfg(*spec);
       if (n && (c.unite == GC_FINISH_HOOKS || c.unite == GC_FINISH_REM_LOCK)) {
@@ -388,7 +402,7 @@ int gc_label_finalization(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
     GC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
     run_finalize(labels, int32_t(n), mins, ctr, st);
     unsigned long long cyc = 0;
-    GC_CUDA(cudaMemcpyAsync(&cyc, ctr + C_SCRATCH1, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaMemcpyAsync(&cyc, ctr + C_CYCLE, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
     require(cyc == 0, GC_ERR_MALFORMED, "label array contains a cycle");
   });

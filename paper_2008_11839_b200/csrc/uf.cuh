@@ -104,25 +104,26 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
 // -------------------------------------------------------------- splices ---
 
 template <int SPLICE>
-__device__ __forceinline__ int32_t splice(int32_t u, int32_t v, int32_t* P) {
+__device__ __forceinline__ int32_t splice(int32_t u, int32_t pu_seen, int32_t pv_seen, int32_t* P) {
+  // Rem walks call this with P[u] = pu_seen > pv_seen = P[v] as observed at
+  // the loop head; every write below replaces a parent by a smaller id, so
+  // concurrent splices can never close a cycle.
   if constexpr (SPLICE == GC_SPLICE_SPLIT_ONE) {
     // dset.py:180-186: returns u's old parent
-    int32_t pu = ld_acq(P + u);
-    int32_t w = ld_acq(P + pu);
+    const int32_t pu = ld_acq(P + u);
+    const int32_t w = ld_acq(P + pu);
     if (pu != w) atomicCAS(P + u, pu, w);
     return pu;
   } else if constexpr (SPLICE == GC_SPLICE_HALVE_ONE) {
     // dset.py:189-195: returns u's old grandparent
-    int32_t pu = ld_acq(P + u);
-    int32_t w = ld_acq(P + pu);
+    const int32_t pu = ld_acq(P + u);
+    const int32_t w = ld_acq(P + pu);
     if (pu != w) atomicCAS(P + u, pu, w);
     return w;
   } else {
     // dset.py:198-207: Rem's splice swings P[u] onto P[v]
-    int32_t pu = ld_acq(P + u);
-    int32_t pv = ld_acq(P + v);
-    atomicCAS(P + u, pu, pv);
-    return pu;
+    atomicCAS(P + u, pu_seen, pv_seen);
+    return pu_seen;
   }
 }
 
@@ -223,7 +224,7 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
       atomicExch(s.L + ru, 0);
       if (linked) return true;
     } else {
-      ru = splice<SPLICE>(ru, rv, P);
+      ru = splice<SPLICE>(ru, pru, prv, P);
     }
   }
   if constexpr (FIND != GC_FIND_NAIVE) {
@@ -254,7 +255,7 @@ __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32
       }
       return true;
     }
-    ru = splice<SPLICE>(ru, rv, P);
+    ru = splice<SPLICE>(ru, pru, prv, P);
   }
 }
 

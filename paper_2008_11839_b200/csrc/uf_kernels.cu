@@ -152,9 +152,9 @@ struct RowsLaunch {
     const int64_t cap = int64_t(num_sms()) * (2048 / kRowBlock) * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_union_rows<R><<<int(blocks), kRowBlock, 0, st>>>(s, a.off, a.tgt, a.list, a.count_dev,
+    (k_union_rows<R><<<int(blocks), kRowBlock, 0, st>>>(s, a.off, a.tgt, a.list, a.count_dev,
                                                         a.count_host, a.take_max, a.lower_only,
-                                                        a.insp);
+                                                        a.insp), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
@@ -169,7 +169,7 @@ struct CooLaunch {
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip);
+    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
@@ -187,7 +187,7 @@ struct RacyLaunch {
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    k_incr_racy<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, is_query, sentinel, bits);
+    (k_incr_racy<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, is_query, sentinel, bits), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
