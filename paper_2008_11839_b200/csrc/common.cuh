@@ -23,6 +23,13 @@ __device__ __forceinline__ int32_t ld_acq(const int32_t* p) {
   return v;
 }
 
+// plain global load (L1-cacheable), never hoisted across other memory ops
+__device__ __forceinline__ int32_t ld_weak(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_rlx(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -3,6 +3,8 @@
 // active gather, finalisation and canonical relabelling.
 #include <atomic>
 
+#include <cub/cub.cuh>
+
 #include "pipeline.cuh"
 
 namespace gc {
@@ -16,20 +18,91 @@ __global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n) {
   }
 }
 
+__device__ __forceinline__ int32_t root_weak(const int32_t* P, int32_t x) {
+  int32_t y;
+  while ((y = ld_weak(P + x)) != x) x = y;
+  return x;
+}
+
 __global__ void k_compress(int32_t* P, int32_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t v = int32_t(i);
-    int32_t p = ld_acq(P + v);
+    const int32_t p = ld_weak(P + v);
     if (p == v) continue;
-    int32_t r = p;
-    while (true) {
-      const int32_t q = ld_acq(P + r);
-      if (q == r) break;
-      r = q;
-    }
-    if (r != p) st_rlx(P + v, r);
+    const int32_t r = root_weak(P, p);
+    if (r != p) P[v] = r;
   }
+}
+
+// Fused post-sampling pass (sampling.py:38-47 compress_all, :29-35 count of
+// the probe's candidate, driver.py:473 active gather): each thread owns 4
+// consecutive vertices (one 16-byte load), resolves their roots with
+// L1-cacheable loads (the union kernel has finished: parents only shrink
+// toward roots from here), writes them back, counts the candidate label and
+// appends the vertices not carrying it to the active list with one global
+// atomic per block.  If the candidate turns out not to be the mode, the
+// histogram fallback re-gathers (k_gather_active).
+template <bool COMPRESS>
+__global__ void __launch_bounds__(kEwBlock)
+k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr) {
+  using Scan = cub::BlockScan<int, kEwBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long base;
+  const int32_t cand = int32_t(ctr[C_CAND]);
+  unsigned long long ccount = 0, degsum = 0;
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  for (int64_t q0 = int64_t(blockIdx.x) * kEwBlock; q0 < nq; q0 += int64_t(gridDim.x) * kEwBlock) {
+    const int64_t q = q0 + threadIdx.x;
+    int32_t lab[4] = {cand, cand, cand, cand};
+    const int64_t v0 = q * 4;
+    if (q < nq) {
+      if (v0 + 3 < n) {
+        const int4 p4 = *reinterpret_cast<const int4*>(P + v0);
+        lab[0] = p4.x; lab[1] = p4.y; lab[2] = p4.z; lab[3] = p4.w;
+      } else {
+        for (int j = 0; j < 4; ++j) if (v0 + j < n) lab[j] = P[v0 + j];
+      }
+      if (COMPRESS) {
+        bool dirty = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (v0 + j >= n) continue;
+          const int32_t r = root_weak(P, lab[j]);
+          dirty |= r != lab[j];
+          lab[j] = r;
+        }
+        if (dirty) {
+          if (v0 + 3 < n) *reinterpret_cast<int4*>(P + v0) = make_int4(lab[0], lab[1], lab[2], lab[3]);
+          else for (int j = 0; j < 4; ++j) if (v0 + j < n) P[v0 + j] = lab[j];
+        }
+      }
+    }
+    int act = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (v0 + j >= n || q >= nq) continue;
+      ccount += lab[j] == cand;
+      act += lab[j] != cand;
+    }
+    int rank, total;
+    Scan(tmp).ExclusiveSum(act, rank, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(ctr + C_N_ACTIVE, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    if (act) {
+      unsigned long long pos = base + rank;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (v0 + j < n && lab[j] != cand) {
+          list[pos++] = int32_t(v0 + j);
+          degsum += static_cast<unsigned long long>(off[v0 + j + 1] - off[v0 + j]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  block_add<kEwBlock>(ctr + C_CAND_COUNT, ccount);
+  block_add<kEwBlock>(ctr + C_INSP_FINISH, degsum);
 }
 
 constexpr int kProbe = 1024;
@@ -41,7 +114,12 @@ __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t
   const int s = n < kProbe ? n : kProbe;
   const int i = threadIdx.x;
   if (i == 0) best = 0ull;
-  if (i < s) lab[i] = ld_acq(P + (int64_t(i) * n) / s);
+  if (i < s) {
+    // walk to the root so the probe can run before compression
+    int32_t x = ld_weak(P + (int64_t(i) * n) / s), y;
+    while ((y = ld_weak(P + x)) != x) x = y;
+    lab[i] = x;
+  }
   __syncthreads();
   if (i < s) {
     const int32_t me = lab[i];
@@ -75,7 +153,11 @@ __global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr) {
   if (majority(ctr, n)) return;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) hist[v] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[C_SCRATCH0] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctr[C_SCRATCH0] = 0;
+    ctr[C_N_ACTIVE] = 0;      // the optimistic gather used a non-mode candidate
+    ctr[C_INSP_FINISH] = 0;
+  }
 }
 
 __global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr) {
@@ -125,24 +207,27 @@ __global__ void k_mode_finish(int32_t n, unsigned long long* ctr) {
   }
 }
 
-__global__ void k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
-                                unsigned long long* ctr) {
+__global__ void __launch_bounds__(kEwBlock)
+k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
+                unsigned long long* ctr, int only_fallback) {
+  if (only_fallback && majority(ctr, n)) return;
+  using Scan = cub::BlockScan<int, kEwBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long base;
   const int32_t lmax = int32_t(ctr[C_LMAX]);
   unsigned long long degsum = 0;
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t v = base + threadIdx.x;
-    const bool act = v < n && P[v] != lmax;
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
-    if (bal == 0) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(ctr + C_N_ACTIVE, static_cast<unsigned long long>(__popc(bal)));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
+  for (int64_t b0 = int64_t(blockIdx.x) * kEwBlock; b0 < n; b0 += int64_t(gridDim.x) * kEwBlock) {
+    const int64_t v = b0 + threadIdx.x;
+    const int act = v < n && P[v] != lmax;
+    int rank, total;
+    Scan(tmp).ExclusiveSum(act, rank, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(ctr + C_N_ACTIVE, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
     if (act) {
-      list[pos + __popc(bal & ((1u << lane) - 1u))] = int32_t(v);
+      list[base + rank] = int32_t(v);
       degsum += static_cast<unsigned long long>(off[v + 1] - off[v]);
     }
+    __syncthreads();
   }
   block_add<kEwBlock>(ctr + C_INSP_FINISH, degsum);
 }
@@ -150,23 +235,42 @@ __global__ void k_gather_active(const int32_t* P, int32_t n, const int64_t* off,
 __global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
   unsigned long long roots = 0;
   bool noncanon = false, cyc = false;
+  const int64_t nq = (int64_t(n) + 3) / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int32_t v = int32_t(i);
-    int32_t r = ld_acq(P + v);
-    if (r == v) {
-      ++roots;
-      continue;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int64_t v0 = q * 4;
+    int32_t lab[4];
+    const bool full = v0 + 3 < n;
+    if (full) {
+      const int4 p4 = *reinterpret_cast<const int4*>(P + v0);
+      lab[0] = p4.x; lab[1] = p4.y; lab[2] = p4.z; lab[3] = p4.w;
+    } else {
+      for (int j = 0; j < 4; ++j) lab[j] = v0 + j < n ? P[v0 + j] : int32_t(v0 + j);
     }
-    int64_t steps = 0;
-    while (true) {
-      const int32_t q = ld_acq(P + r);
-      if (q == r) break;
-      r = q;
-      if (++steps > n) { cyc = true; break; }
+    bool dirty = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int32_t v = int32_t(v0 + j);
+      if (v >= n) continue;
+      int32_t r = lab[j];
+      if (r == v) {
+        ++roots;
+        continue;
+      }
+      int64_t steps = 0;
+      int32_t y;
+      while ((y = ld_weak(P + r)) != r) {
+        r = y;
+        if (++steps > n) { cyc = true; break; }
+      }
+      dirty |= r != lab[j];
+      lab[j] = r;
+      noncanon |= r > v;
     }
-    st_rlx(P + v, r);
-    noncanon |= r > v;
+    if (dirty) {
+      if (full) *reinterpret_cast<int4*>(P + v0) = make_int4(lab[0], lab[1], lab[2], lab[3]);
+      else for (int j = 0; j < 4; ++j) if (v0 + j < n) P[v0 + j] = lab[j];
+    }
   }
   block_add<kEwBlock>(ctr + C_COMPONENTS, roots);
   if (__syncthreads_or(noncanon) && threadIdx.x == 0) ctr[C_NONCANON] = 1;
@@ -268,10 +372,45 @@ void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cud
   GC_CHECK_LAUNCH();
 }
 
-void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st) {
+void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, int32_t* hist,
+                     unsigned long long* ctr, bool compress, cudaStream_t st) {
+  if (n > 0) {
+    const int64_t nq = (int64_t(n) + 3) / 4;
+    const int gq = grid_for(nq, kEwBlock, 4);
+    const int g = grid_for(n, kEwBlock, 4);
+    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr), ::gc::count_launch());
+    if (compress) (k_post_sample<true><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
+    else (k_post_sample<false><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
+    // exact-mode fallback: every kernel below exits at once on a strict majority
+    (k_hist_zero<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
+    (k_hist_add<<<g, kEwBlock, 0, st>>>(P, hist, n, ctr), ::gc::count_launch());
+    (k_hist_argmax<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
+  }
+  (k_mode_finish<<<1, 1, 0, st>>>(n, ctr), ::gc::count_launch());
+  if (n > 0)
+    (k_gather_active<<<grid_for(n, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, off, list, ctr, 1),
+     ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
+void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr,
+                cudaStream_t st) {
+  if (n <= 0) return;
+  (k_gather_active<<<grid_for(n, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, off, list, ctr, 0),
+   ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
+void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st,
+                  bool maybe_noncanon) {
   if (n <= 0) return;
   const int g = grid_for(n, kEwBlock, 8);
-  (k_finalize<<<g, kEwBlock, 0, st>>>(P, n, ctr), ::gc::count_launch());
+  (k_finalize<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, ctr),
+   ::gc::count_launch());
+  if (!maybe_noncanon) {
+    GC_CHECK_LAUNCH();
+    return;
+  }
   (k_canon_init<<<g, kEwBlock, 0, st>>>(mins, n, ctr), ::gc::count_launch());
   (k_canon_min<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr), ::gc::count_launch());
   (k_canon_apply<<<g, kEwBlock, 0, st>>>(P, mins, n, ctr), ::gc::count_launch());

@@ -30,7 +30,7 @@ __global__ void k_hist_argmax(const int32_t* hist, int32_t n, unsigned long long
 // Active vertices: label != l_max (driver.py:473), plus sum of their degrees
 // (the finish inspection count, driver.py:335-336).
 __global__ void k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
-                                unsigned long long* ctr);
+                                unsigned long long* ctr, int only_fallback);
 
 // Pointer jump to the root in place; counts roots and flags labels that are
 // not their class minimum (label_finalization, driver.py:420-429).
@@ -51,7 +51,17 @@ __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long
 
 // Host helpers
 void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cudaStream_t st);
-void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st);
+// Post-sampling: candidate probe, (compress +) candidate count + optimistic
+// active gather in one pass, exact-mode fallback.  Leaves L_max, the active
+// list, its size and degree sum in the counters.
+void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, int32_t* hist,
+                     unsigned long long* ctr, bool compress, cudaStream_t st);
+// Active gather for a known L_max (finish_phase).
+void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr,
+                cudaStream_t st);
+// Pointer jump (+ canonical relabel when labels may not be class minima).
+void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st,
+                  bool maybe_noncanon = true);
 void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 

@@ -154,24 +154,22 @@ struct Pipeline {
       }
       if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
       timed_sample = true;
-      if (n) {
-        (k_compress<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n), ::gc::count_launch());
-        GC_CHECK_LAUNCH();
-      }
+      run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, true, st);
     } else if (s.sample == GC_SAMPLE_BFS) {
       init_sets(sc);
       if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
       run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
       if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
       timed_sample = true;
+      run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     } else {
       init_sets(sc);
       if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
       run_ldd(g, s, P, ws.samp, ws.ctr, st);
       if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
       timed_sample = true;
+      run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     }
-    run_mode(P, n, ws.hist, ws.ctr, st);
   }
 
   void set_lmax_sentinel() {
@@ -183,12 +181,9 @@ struct Pipeline {
   // Returns the number of rounds (round-based finishes) and fills the active
   // list when the sampler left a dominant label.
   int64_t finish() {
+    // the active list was gathered by the post-sampling pass (or by
+    // run_gather for finish_phase)
     const bool all_active = s.sample == GC_SAMPLE_NONE;
-    if (!all_active && n) {
-      (k_gather_active<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, n, g.offsets, ws.list,
-                                                                     ws.ctr), ::gc::count_launch());
-      GC_CHECK_LAUNCH();
-    }
     if (is_union_finish(s.finish)) {
       RowUnionArgs a = rows(finish_cfg(s));
       if (all_active) {
@@ -235,6 +230,7 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
   require(spec != nullptr, GC_ERR_ARG, "null spec");
   validate_spec(*spec);
   require(g->n == 0 || labels != nullptr, GC_ERR_ARG, "null labels");
+  require(reinterpret_cast<uintptr_t>(labels) % 16 == 0, GC_ERR_ARG, "labels must be 16-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool forest = fu != nullptr;
   if (forest) {
@@ -260,7 +256,7 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
   GC_CUDA(cudaEventRecord(ev.e[2], st));
   const int64_t rounds = pl.finish();
   GC_CUDA(cudaEventRecord(ev.e[3], st));
-  if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st);
+  if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
   GC_CUDA(cudaEventRecord(ev.e[4], st));
   unsigned long long c[C_COUNT_];
   GC_CUDA(cudaMemcpyAsync(c, pl.ws.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
@@ -375,6 +371,7 @@ int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io, in
     }
     static thread_local EventSet ev;
     GC_CUDA(cudaEventRecord(ev.e[0], st));
+    run_gather(labels_io, n, g->offsets, pl.ws.list, pl.ws.ctr, st);
     const int64_t rounds = pl.finish();
     GC_CUDA(cudaEventRecord(ev.e[1], st));
     unsigned long long c[C_COUNT_];
@@ -395,6 +392,7 @@ int gc_label_finalization(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
   return guarded([&] {
     require(n >= 0 && n < (int64_t(1) << 31), GC_ERR_MALFORMED, "bad length");
     if (n == 0) return;
+    require(reinterpret_cast<uintptr_t>(labels) % 16 == 0, GC_ERR_ARG, "labels must be 16-byte aligned");
     Arena a(ws, ws_bytes);
     unsigned long long* ctr = a.take<unsigned long long>(C_COUNT_);
     int32_t* mins = a.take<int32_t>(n);

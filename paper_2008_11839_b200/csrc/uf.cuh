@@ -36,14 +36,36 @@ __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u
   }
 }
 
+// Parent reads.  The first kWeakReads loads of a union call are plain
+// (L1-cacheable) loads: the hub vertices near the roots of large trees are
+// read by millions of threads and an L1 hit avoids an L2 round trip to one
+// hot line.  Any value read, however stale, is an ancestor of the vertex it
+// was read from (parents only move up and decrease), so stale reads can
+// cost retries but never merge the wrong sets; every link is still decided
+// by a CAS at L2.  After the budget is spent all further reads are
+// ld.relaxed.gpu, so each retry loop observes fresh values and terminates
+// exactly as the all-strong algorithm does.
+constexpr int kWeakReads = 48;
+
+struct Reader {
+  int budget = kWeakReads;
+  __device__ __forceinline__ int32_t operator()(const int32_t* p) {
+    if (budget > 0) {
+      --budget;
+      return ld_weak(p);
+    }
+    return ld_acq(p);
+  }
+};
+
 // ---------------------------------------------------------------- finds ---
 
 template <int FIND>
-__device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
+__device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd) {
   if constexpr (FIND == GC_FIND_NAIVE) {
     // dset.py:109-112
     while (true) {
-      int32_t pu = ld_acq(P + u);
+      int32_t pu = rd(P + u);
       if (pu == u) return u;
       u = pu;
     }
@@ -51,12 +73,12 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
     // dset.py:115-123: locate the root, then swing the path onto it
     int32_t r = u;
     while (true) {
-      int32_t pr = ld_acq(P + r);
+      int32_t pr = rd(P + r);
       if (pr == r) break;
       r = pr;
     }
     while (true) {
-      int32_t j = ld_acq(P + u);
+      int32_t j = rd(P + u);
       if (j <= r) break;
       atomicCAS(P + u, j, r);
       u = j;
@@ -64,38 +86,38 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
     return r;
   } else if constexpr (FIND == GC_FIND_SPLIT) {
     // dset.py:126-135
-    int32_t v = ld_acq(P + u);
-    int32_t w = ld_acq(P + v);
+    int32_t v = rd(P + u);
+    int32_t w = rd(P + v);
     while (v != w) {
       atomicCAS(P + u, v, w);
       u = v;
-      v = ld_acq(P + u);
-      w = ld_acq(P + v);
+      v = rd(P + u);
+      w = rd(P + v);
     }
     return v;
   } else if constexpr (FIND == GC_FIND_HALVE) {
     // dset.py:138-147
-    int32_t v = ld_acq(P + u);
-    int32_t w = ld_acq(P + v);
+    int32_t v = rd(P + u);
+    int32_t w = rd(P + v);
     while (v != w) {
       atomicCAS(P + u, v, w);
-      u = ld_acq(P + u);
-      v = ld_acq(P + u);
-      w = ld_acq(P + v);
+      u = rd(P + u);
+      v = rd(P + u);
+      w = rd(P + v);
     }
     return v;
   } else {  // GC_FIND_TWO_TRY, dset.py:150-163
-    int32_t v = ld_acq(P + u);
-    int32_t w = ld_acq(P + v);
+    int32_t v = rd(P + u);
+    int32_t w = rd(P + v);
     while (v != w) {
       if (!cas(P + u, v, w)) {
-        int32_t v2 = ld_acq(P + u);
-        int32_t w2 = ld_acq(P + v2);
+        int32_t v2 = rd(P + u);
+        int32_t w2 = rd(P + v2);
         if (v2 != w2) atomicCAS(P + u, v2, w2);
       }
       u = v;
-      v = ld_acq(P + u);
-      w = ld_acq(P + v);
+      v = rd(P + u);
+      w = rd(P + v);
     }
     return v;
   }
@@ -104,20 +126,20 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P) {
 // -------------------------------------------------------------- splices ---
 
 template <int SPLICE>
-__device__ __forceinline__ int32_t splice(int32_t u, int32_t pu_seen, int32_t pv_seen, int32_t* P) {
+__device__ __forceinline__ int32_t splice(int32_t u, int32_t pu_seen, int32_t pv_seen, int32_t* P, Reader& rd) {
   // Rem walks call this with P[u] = pu_seen > pv_seen = P[v] as observed at
   // the loop head; every write below replaces a parent by a smaller id, so
   // concurrent splices can never close a cycle.
   if constexpr (SPLICE == GC_SPLICE_SPLIT_ONE) {
     // dset.py:180-186: returns u's old parent
-    const int32_t pu = ld_acq(P + u);
-    const int32_t w = ld_acq(P + pu);
+    const int32_t pu = rd(P + u);
+    const int32_t w = rd(P + pu);
     if (pu != w) atomicCAS(P + u, pu, w);
     return pu;
   } else if constexpr (SPLICE == GC_SPLICE_HALVE_ONE) {
     // dset.py:189-195: returns u's old grandparent
-    const int32_t pu = ld_acq(P + u);
-    const int32_t w = ld_acq(P + pu);
+    const int32_t pu = rd(P + u);
+    const int32_t w = rd(P + pu);
     if (pu != w) atomicCAS(P + u, pu, w);
     return w;
   } else {
@@ -134,16 +156,17 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t v) {
   // dset.py:222-234
   int32_t* P = s.P;
-  int32_t pu = find<FIND>(u, P);
-  int32_t pv = find<FIND>(v, P);
+  Reader rd;
+  int32_t pu = find<FIND>(u, P, rd);
+  int32_t pv = find<FIND>(v, P, rd);
   while (pu != pv) {
     if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
-    if (ld_acq(P + pu) == pu && cas(P + pu, pu, pv)) {
+    if (rd(P + pu) == pu && cas(P + pu, pu, pv)) {
       record<FOREST>(s, pu, u, v);
       return true;
     }
-    pu = find<FIND>(u, P);
-    pv = find<FIND>(v, P);
+    pu = find<FIND>(u, P, rd);
+    pv = find<FIND>(v, P, rd);
   }
   return false;
 }
@@ -152,20 +175,21 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_hooks(const UFState& s, int32_t u, int32_t v) {
   // dset.py:237-252: claim the hook slot, then an uncontended parent write.
   int32_t* P = s.P;
+  Reader rd;
   const int32_t unhooked = s.n;
-  int32_t pu = find<FIND>(u, P);
-  int32_t pv = find<FIND>(v, P);
+  int32_t pu = find<FIND>(u, P, rd);
+  int32_t pv = find<FIND>(v, P, rd);
   while (pu != pv) {
     if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
-    if (ld_acq(P + pu) == pu && cas(s.H + pu, unhooked, pv)) {
+    if (rd(P + pu) == pu && cas(s.H + pu, unhooked, pv)) {
       record<FOREST>(s, pu, u, v);
       // release: the forest slot is visible before the parent write
       __threadfence();
       st_rlx(P + pu, pv);
       return true;
     }
-    pu = find<FIND>(u, P);
-    pv = find<FIND>(v, P);
+    pu = find<FIND>(u, P, rd);
+    pv = find<FIND>(v, P, rd);
   }
   return false;
 }
@@ -174,23 +198,24 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_early(const UFState& s, int32_t u, int32_t v) {
   // dset.py:255-274
   int32_t* P = s.P;
+  Reader rd;
   int32_t pu = u, pv = v;
   bool merged = false;
   while (pu != pv) {
     if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
-    if (ld_acq(P + pu) == pu && cas(P + pu, pu, pv)) {
+    if (rd(P + pu) == pu && cas(P + pu, pu, pv)) {
       record<FOREST>(s, pu, u, v);
       merged = true;
       break;
     }
-    int32_t z = ld_acq(P + pu);
-    int32_t w = ld_acq(P + z);
+    int32_t z = rd(P + pu);
+    int32_t w = rd(P + z);
     if (z != w) atomicCAS(P + pu, z, w);
     pu = w;
   }
   if constexpr (FIND != GC_FIND_NAIVE) {
-    find<FIND>(u, P);
-    find<FIND>(v, P);
+    find<FIND>(u, P, rd);
+    find<FIND>(v, P, rd);
   }
   return merged;
 }
@@ -200,10 +225,11 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
   // dset.py:277-300.  A failed re-validation re-derives and loops, as the
   // reference does (the paper's pseudocode returns instead).
   int32_t* P = s.P;
+  Reader rd;
   int32_t ru = u, rv = v;
   while (true) {
-    int32_t pru = ld_acq(P + ru);
-    int32_t prv = ld_acq(P + rv);
+    int32_t pru = rd(P + ru);
+    int32_t prv = rd(P + rv);
     if (pru == prv) break;
     if (pru < prv) {
       int32_t t = ru; ru = rv; rv = t;
@@ -214,6 +240,7 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
       // holder makes progress even when it shares a warp with waiters
       while (atomicCAS(s.L + ru, 0, 1) != 0) __nanosleep(32);
       __threadfence();
+      // re-validate with fresh (L2) reads while holding ru's lock
       int32_t pv = ld_acq(P + rv);
       bool linked = (ru == ld_acq(P + ru)) && ru > pv;
       if (linked) {
@@ -224,12 +251,12 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
       atomicExch(s.L + ru, 0);
       if (linked) return true;
     } else {
-      ru = splice<SPLICE>(ru, pru, prv, P);
+      ru = splice<SPLICE>(ru, pru, prv, P, rd);
     }
   }
   if constexpr (FIND != GC_FIND_NAIVE) {
-    find<FIND>(u, P);
-    find<FIND>(v, P);
+    find<FIND>(u, P, rd);
+    find<FIND>(v, P, rd);
   }
   return false;
 }
@@ -238,10 +265,11 @@ template <int FIND, int SPLICE, bool FOREST>
 __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32_t v) {
   // dset.py:303-316
   int32_t* P = s.P;
+  Reader rd;
   int32_t ru = u, rv = v;
   while (true) {
-    int32_t pru = ld_acq(P + ru);
-    int32_t prv = ld_acq(P + rv);
+    int32_t pru = rd(P + ru);
+    int32_t prv = rd(P + rv);
     if (pru == prv) return false;
     if (pru < prv) {
       int32_t t = ru; ru = rv; rv = t;
@@ -250,12 +278,12 @@ __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32
     if (ru == pru && cas(P + ru, ru, prv)) {
       record<FOREST>(s, ru, u, v);
       if constexpr (FIND != GC_FIND_NAIVE) {
-        find<FIND>(u, P);
-        find<FIND>(v, P);
+        find<FIND>(u, P, rd);
+        find<FIND>(v, P, rd);
       }
       return true;
     }
-    ru = splice<SPLICE>(ru, pru, prv, P);
+    ru = splice<SPLICE>(ru, pru, prv, P, rd);
   }
 }
 
@@ -263,9 +291,10 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_jtb(const UFState& s, int32_t u, int32_t v) {
   // dset.py:319-331: link the lower (rank, id) root under the higher one
   int32_t* P = s.P;
+  Reader rd;
   while (true) {
-    int32_t ru = find<FIND>(u, P);
-    int32_t rv = find<FIND>(v, P);
+    int32_t ru = find<FIND>(u, P, rd);
+    int32_t rv = find<FIND>(v, P, rd);
     if (ru == rv) return false;
     uint32_t kru = s.R[ru], krv = s.R[rv];
     if (kru > krv || (kru == krv && ru > rv)) { int32_t t = ru; ru = rv; rv = t; }

@@ -149,7 +149,8 @@ struct RowsLaunch {
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n};
     int64_t warps = (a.count_host + 31) / 32;
     int64_t blocks = (warps * 32 + kRowBlock - 1) / kRowBlock;
-    const int64_t cap = int64_t(num_sms()) * (2048 / kRowBlock) * 8;
+    // one resident wave, grid-stride over 32-row groups
+    const int64_t cap = int64_t(num_sms()) * (2048 / kRowBlock);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     (k_union_rows<R><<<int(blocks), kRowBlock, 0, st>>>(s, a.off, a.tgt, a.list, a.count_dev,
