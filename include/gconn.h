@@ -137,6 +137,17 @@ int gc_static_cc(const gc_csr* g, const gc_spec* spec, int32_t* labels_out,
                  int32_t* post_sample_out, int want_ic, gc_stats* stats,
                  void* ws, size_t ws_bytes, void* stream);
 
+/* ---- reusable static plan -----------------------------------------------
+ * Binds a graph, spec, output and workspace once; gc_plan_run repeats the
+ * static pipeline.  Pipelines without host round trips (union-find finish
+ * with none / k-out / HB sampling) are captured into a CUDA graph on the
+ * first run and replayed as one launch afterwards. */
+typedef struct gc_plan gc_plan;
+int gc_plan_create(const gc_csr* g, const gc_spec* spec, int32_t* labels_out,
+                   void* ws, size_t ws_bytes, void* stream, gc_plan** out);
+int gc_plan_run(gc_plan* plan, gc_stats* stats);
+void gc_plan_destroy(gc_plan* plan);
+
 /* ---- spanning forest (driver.py:510-536) --------------------------------
  * Slot r of (fu, fv) holds the original edge recorded when r lost root
  * status; empty slots hold -1 (ForestEdges.edges None). */

@@ -6,7 +6,7 @@ connlab/__init__.py:12-82.  All connectivity work runs in libgconn.so
 (hand-written CUDA, loaded through a C ABI declared in include/gconn.h);
 there is no CPU fallback.
 """
-from .api import (DeviceForest, ForestEdges, RunStats, finish_phase, label_finalization,
+from .api import (DeviceForest, ForestEdges, RunStats, StaticConnectivity, finish_phase, label_finalization,
                   spanning_forest, spanning_forest_device, static_connectivity,
                   static_connectivity_device)
 from .errors import ConfigError, MalformedInputError, NativeError, VerificationError
@@ -24,7 +24,7 @@ __all__ = [
     "AlgorithmSpec", "ConfigError", "DeviceForest", "EdgeList", "FindOp", "FinishKind",
     "ForestEdges", "Graph", "IncrementalConnectivity", "Insert", "KOutMode", "LTVariant",
     "LT_VARIANTS", "MalformedInputError", "NativeError", "Query", "RunStats", "SampleKind",
-    "SpliceOp", "UnionConfig", "UnionOp", "VerificationError", "all_valid_configs", "build_csr",
+    "SpliceOp", "StaticConnectivity", "UnionConfig", "UnionOp", "VerificationError", "all_valid_configs", "build_csr",
     "clique_graph", "disjoint_union", "enumerate_specs", "finish_phase", "format_spec",
     "gen_rmat", "gen_uniform_pairs", "grid3d_edges", "grid_graph", "incremental",
     "label_finalization", "parse_spec", "path_graph", "spanning_forest", "spanning_forest_device",

@@ -60,6 +60,9 @@ _SIGNATURES = {
     "gc_workspace_size": (_SZ, [_I64, _I64, C.POINTER(Spec)]),
     "gc_static_cc": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, C.c_int,
                                C.POINTER(Stats), _VP, _SZ, _VP]),
+    "gc_plan_create": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _SZ, _VP, C.POINTER(_VP)]),
+    "gc_plan_run": (C.c_int, [_VP, C.POINTER(Stats)]),
+    "gc_plan_destroy": (None, [_VP]),
     "gc_spanning_forest": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, C.POINTER(Stats),
                                      _VP, _SZ, _VP]),
     "gc_finish_phase": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _I64, C.POINTER(Stats),

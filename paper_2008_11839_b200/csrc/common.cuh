@@ -43,6 +43,31 @@ __device__ __forceinline__ void red_min(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Streaming loads for graph data that is read once per pass: no L1
+// allocation and L2 evict-first, so the stream does not push the parent
+// array (kept persisting in L2) out of the cache.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int2 ld_stream2(const int32_t* p, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream64(const int64_t* p, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ int64_t ldg64(const int64_t* p) { return __ldg(p); }
 __device__ __forceinline__ int32_t ldg32(const int32_t* p) { return __ldg(p); }
 

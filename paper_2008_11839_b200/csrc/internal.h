@@ -146,6 +146,8 @@ int num_sms();
 // Kernel launches issued by libgconn (process-wide, exported through
 // gc_launch_count for the bench's gpu_launches claim).
 void count_launch();
+void add_launches(long long k);
+long long launch_total();
 
 // Thread-local last-error string behind gc_last_error().
 void set_last_error(const char* msg);

@@ -340,6 +340,8 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 long long launch_total() { return g_launches.load(); }
 
+void add_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
 unsigned long long* pinned_words() {
   static thread_local unsigned long long* p = nullptr;
   if (!p) GC_CUDA(cudaMallocHost(&p, 64 * sizeof(unsigned long long)));

@@ -12,6 +12,7 @@
 // round-trip, except the round-based finishes which read a change flag per
 // round (the reference's own fixpoint loop, minbased.py:124-304).
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -34,6 +35,55 @@ struct EventSet {
     for (auto& x : e) cudaEventDestroy(x);
   }
 };
+
+// Keep the parent array resident in L2 for the duration of a pipeline: an
+// access-policy window marks it persisting while CSR streams through with
+// evict-first loads.  Released (and the persisting lines demoted) at the end.
+struct L2Residency {
+  cudaStream_t st;
+  bool on = false;
+  L2Residency(cudaStream_t s, void* base, size_t bytes) : st(s) {
+    static const bool disabled = getenv("GC_NO_L2_WINDOW") != nullptr;
+    if (disabled) return;
+    static int max_persist = -1, max_window = 0;
+    if (max_persist < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(max_persist));
+      const char* g = getenv("GC_L2_FETCH");
+      if (g) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(g)));
+      cudaGetLastError();
+    }
+    if (max_persist <= 0 || max_window <= 0 || bytes == 0) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = base;
+    a.accessPolicyWindow.num_bytes = bytes < size_t(max_window) ? bytes : size_t(max_window);
+    const double ratio = double(max_persist) / double(a.accessPolicyWindow.num_bytes);
+    a.accessPolicyWindow.hitRatio = float(ratio < 1.0 ? ratio : 1.0);
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    on = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess;
+    cudaGetLastError();
+  }
+  ~L2Residency() {
+    if (!on) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+};
+
+
+// Timing events: inside a stream capture they must become external event
+// nodes of the graph; outside a capture the flag is rejected.
+thread_local bool t_capturing = false;
+cudaError_t rec(cudaEvent_t e, cudaStream_t st) {
+  return t_capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+}
 
 bool is_union_finish(int f) { return f >= GC_FINISH_ASYNC && f <= GC_FINISH_JTB; }
 
@@ -146,27 +196,27 @@ struct Pipeline {
     }
     if (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB) {
       init_sets(sc);
-      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
+      if (kev) GC_CUDA(rec(kev[0], st));
       if (s.sample == GC_SAMPLE_KOUT) {
         run_kout(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       } else {
         run_hb(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       }
-      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      if (kev) GC_CUDA(rec(kev[1], st));
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, true, st);
     } else if (s.sample == GC_SAMPLE_BFS) {
       init_sets(sc);
-      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
+      if (kev) GC_CUDA(rec(kev[0], st));
       run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
-      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      if (kev) GC_CUDA(rec(kev[1], st));
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     } else {
       init_sets(sc);
-      if (kev) GC_CUDA(cudaEventRecord(kev[0], st));
+      if (kev) GC_CUDA(rec(kev[0], st));
       run_ldd(g, s, P, ws.samp, ws.ctr, st);
-      if (kev) GC_CUDA(cudaEventRecord(kev[1], st));
+      if (kev) GC_CUDA(rec(kev[1], st));
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     }
@@ -205,15 +255,15 @@ struct Pipeline {
         a.lower_only = 0;
         a.insp = nullptr;  // counted by the gather
       }
-      if (kev) GC_CUDA(cudaEventRecord(kev[2], st));
+      if (kev) GC_CUDA(rec(kev[2], st));
       launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
-      if (kev) GC_CUDA(cudaEventRecord(kev[3], st));
+      if (kev) GC_CUDA(rec(kev[3], st));
       return 0;
     }
-    if (kev) GC_CUDA(cudaEventRecord(kev[2], st));
+    if (kev) GC_CUDA(rec(kev[2], st));
     const int64_t r =
         run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
-    if (kev) GC_CUDA(cudaEventRecord(kev[3], st));
+    if (kev) GC_CUDA(rec(kev[3], st));
     return r;
   }
 };
@@ -224,14 +274,29 @@ double ms(cudaEvent_t a, cudaEvent_t b) {
   return double(t);
 }
 
-void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* post, int want_ic,
-                int32_t* fu, int32_t* fv, gc_stats* stats, void* ws, size_t wsb, void* stream) {
+// Everything a static / forest run needs besides the caller's buffers.
+struct RunState {
+  EventSet ev;
+  unsigned long long* host_ctr = nullptr;  // pinned copy of the device counters
+  int64_t rounds = 0;
+  bool timed_sample = false;
+  RunState() { GC_CUDA(cudaMallocHost(&host_ctr, sizeof(unsigned long long) * C_COUNT_)); }
+  ~RunState() { cudaFreeHost(host_ctr); }
+};
+
+void check_static_args(const gc_csr* g, const gc_spec* spec, int32_t* labels) {
   validate_csr(g);
   require(spec != nullptr, GC_ERR_ARG, "null spec");
   validate_spec(*spec);
   require(g->n == 0 || labels != nullptr, GC_ERR_ARG, "null labels");
   require(reinterpret_cast<uintptr_t>(labels) % 16 == 0, GC_ERR_ARG, "labels must be 16-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+}
+
+// Stream-ordered body of a static / forest run.  Host synchronisation only
+// happens inside the BFS / LDD samplers and the round finishes; for the
+// union-find pipelines the sequence is sync-free and can be graph-captured.
+void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* post, int want_ic,
+                    int32_t* fu, int32_t* fv, void* ws, size_t wsb, cudaStream_t st, RunState& rs) {
   const bool forest = fu != nullptr;
   if (forest) {
     require(fv != nullptr, GC_ERR_ARG, "null forest array");
@@ -239,13 +304,14 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
     fill(fv, g->n, -1, st);
   }
   Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
-  static thread_local EventSet ev;
-  pl.kev = ev.e + 5;
+  L2Residency keep_parents(st, labels, size_t(g->n) * 4);
+  cudaEvent_t* ev = rs.ev.e;
+  pl.kev = ev + 5;
   const int32_t n = pl.n;
 
-  GC_CUDA(cudaEventRecord(ev.e[0], st));
+  GC_CUDA(rec(ev[0], st));
   pl.sample();
-  GC_CUDA(cudaEventRecord(ev.e[1], st));
+  GC_CUDA(rec(ev[1], st));
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
   if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
   if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
@@ -253,47 +319,68 @@ void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* 
                                                                nullptr, pl.ws.ctr), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  GC_CUDA(cudaEventRecord(ev.e[2], st));
-  const int64_t rounds = pl.finish();
-  GC_CUDA(cudaEventRecord(ev.e[3], st));
+  GC_CUDA(rec(ev[2], st));
+  rs.rounds = pl.finish();
+  GC_CUDA(rec(ev[3], st));
   if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
-  GC_CUDA(cudaEventRecord(ev.e[4], st));
-  unsigned long long c[C_COUNT_];
-  GC_CUDA(cudaMemcpyAsync(c, pl.ws.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
-  if (forest) {
+  if (forest && n) {
     // spanning_forest: component_count = n - |forest| (driver.py:535)
-    unsigned long long* cnt = pl.ws.ctr + C_SCRATCH1;
-    GC_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-    if (n) (k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, cnt), ::gc::count_launch());
-    unsigned long long pop = 0;
-    GC_CUDA(cudaMemcpyAsync(&pop, cnt, 8, cudaMemcpyDeviceToHost, st));
-    GC_CUDA(cudaStreamSynchronize(st));
-    c[C_COMPONENTS] = static_cast<unsigned long long>(n) - pop;
+    set_ctr(pl.ws.ctr, C_SCRATCH1, 0, st);
+    (k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, pl.ws.ctr + C_SCRATCH1),
+     ::gc::count_launch());
+    GC_CHECK_LAUNCH();
   }
-  GC_CUDA(cudaStreamSynchronize(st));
+  GC_CUDA(rec(ev[4], st));
+  GC_CUDA(cudaMemcpyAsync(rs.host_ctr, pl.ws.ctr, sizeof(unsigned long long) * C_COUNT_,
+                          cudaMemcpyDeviceToHost, st));
+  rs.timed_sample = pl.timed_sample;
+}
+
+// After the stream has drained: turn the counters and events into stats.
+void collect_static(const gc_csr* g, const gc_spec* spec, bool forest, int want_ic, RunState& rs,
+                    gc_stats* stats) {
+  const unsigned long long* c = rs.host_ctr;
+  const int64_t n = g->n;
   require(c[C_CYCLE] == 0, GC_ERR_MALFORMED, "label array contains a cycle");
-  if (stats) {
-    stats->t_sample_ms = ms(ev.e[0], ev.e[1]);
-    stats->t_finish_ms = ms(ev.e[2], ev.e[3]);
-    stats->t_finalize_ms = forest ? 0.0 : ms(ev.e[3], ev.e[4]);
-    stats->t_sample_kernel_ms = pl.timed_sample ? ms(ev.e[5], ev.e[6]) : 0.0;
-    stats->t_finish_kernel_ms = ms(ev.e[7], ev.e[8]);
-    stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
-    stats->insp_finish = int64_t(c[C_INSP_FINISH]);
-    stats->rounds = rounds;
-    stats->components = int64_t(c[C_COMPONENTS]);
-    if (spec->sample == GC_SAMPLE_NONE) {
-      stats->l_max = n;
-      stats->lmax_count = n ? 1 : 0;  // identity labels: every count is 1
-      stats->n_active = n;
-      stats->ic_count = g->m;  // every directed edge crosses identity labels
-    } else {
-      stats->l_max = int64_t(c[C_LMAX]);
-      stats->lmax_count = int64_t(c[C_LMAX_COUNT]);
-      stats->n_active = int64_t(c[C_N_ACTIVE]);
-      stats->ic_count = want_ic ? int64_t(c[C_IC]) : -1;
-    }
+  if (!stats) return;
+  cudaEvent_t* ev = rs.ev.e;
+  stats->t_sample_ms = ms(ev[0], ev[1]);
+  stats->t_finish_ms = ms(ev[2], ev[3]);
+  stats->t_finalize_ms = forest ? 0.0 : ms(ev[3], ev[4]);
+  stats->t_sample_kernel_ms = rs.timed_sample ? ms(ev[5], ev[6]) : 0.0;
+  stats->t_finish_kernel_ms = ms(ev[7], ev[8]);
+  stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
+  stats->insp_finish = int64_t(c[C_INSP_FINISH]);
+  stats->rounds = rs.rounds;
+  stats->components = forest ? n - int64_t(c[C_SCRATCH1]) : int64_t(c[C_COMPONENTS]);
+  if (spec->sample == GC_SAMPLE_NONE) {
+    stats->l_max = n;
+    stats->lmax_count = n ? 1 : 0;  // identity labels: every count is 1
+    stats->n_active = n;
+    stats->ic_count = g->m;  // every directed edge crosses identity labels
+  } else {
+    stats->l_max = int64_t(c[C_LMAX]);
+    stats->lmax_count = int64_t(c[C_LMAX_COUNT]);
+    stats->n_active = int64_t(c[C_N_ACTIVE]);
+    stats->ic_count = want_ic ? int64_t(c[C_IC]) : -1;
   }
+}
+
+void run_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* post, int want_ic,
+                int32_t* fu, int32_t* fv, gc_stats* stats, void* ws, size_t wsb, void* stream) {
+  check_static_args(g, spec, labels);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static thread_local RunState rs;
+  enqueue_static(g, spec, labels, post, want_ic, fu, fv, ws, wsb, st, rs);
+  GC_CUDA(cudaStreamSynchronize(st));
+  collect_static(g, spec, fu != nullptr, want_ic, rs, stats);
+}
+
+// Pipelines with no host round trip (union-find finish, none / k-out / HB
+// sampling) can be captured once and replayed as one CUDA graph launch.
+bool graph_capturable(const gc_spec& s) {
+  return is_union_finish(s.finish) &&
+         (s.sample == GC_SAMPLE_NONE || s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB);
 }
 
 }  // namespace
@@ -320,6 +407,83 @@ size_t gc_workspace_size(int64_t n, int64_t m, const gc_spec* spec) {
   Layout<Sizer> l;
   l.carve(sz, n, m, *spec, true);
   return sz.used + 4096;
+}
+
+struct gc_plan {
+  gc_csr g;
+  gc_spec s;
+  int32_t* labels;
+  void* ws;
+  size_t wsb;
+  cudaStream_t st;
+  gc::RunState rs;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;  // private stream for capture (the caller's may be the legacy stream)
+  bool capturable = false;
+  long long kernels = 0;  // kernels per replay (for gc_launch_count)
+};
+
+int gc_plan_create(const gc_csr* g, const gc_spec* spec, int32_t* labels_out, void* ws,
+                   size_t ws_bytes, void* stream, gc_plan** out) {
+  return guarded([&] {
+    require(out != nullptr, GC_ERR_ARG, "null plan out");
+    check_static_args(g, spec, labels_out);
+    require(ws_bytes >= gc_workspace_size(g->n, g->m, spec), GC_ERR_OOM, "workspace too small");
+    gc_plan* p = new gc_plan();
+    p->g = *g;
+    p->s = *spec;
+    p->labels = labels_out;
+    p->ws = ws;
+    p->wsb = ws_bytes;
+    p->st = static_cast<cudaStream_t>(stream);
+    p->capturable = graph_capturable(*spec) && getenv("GC_NO_GRAPH") == nullptr;
+    num_sms();        // resolve device attributes before any capture
+    pinned_words();
+    *out = p;
+  });
+}
+
+int gc_plan_run(gc_plan* p, gc_stats* stats) {
+  return guarded([&] {
+    require(p != nullptr, GC_ERR_ARG, "null plan");
+    if (p->capturable && p->exec == nullptr) {
+      cudaGraph_t graph = nullptr;
+      if (!p->cap) GC_CUDA(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+      GC_CUDA(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+      const long long l0 = launch_total();
+      t_capturing = true;
+      try {
+        enqueue_static(&p->g, &p->s, p->labels, nullptr, 0, nullptr, nullptr, p->ws, p->wsb, p->cap, p->rs);
+      } catch (...) {
+        t_capturing = false;
+        cudaStreamEndCapture(p->cap, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      t_capturing = false;
+      GC_CUDA(cudaStreamEndCapture(p->cap, &graph));
+      p->kernels = launch_total() - l0;
+      add_launches(-p->kernels);  // captured, not yet executed
+      const cudaError_t e = cudaGraphInstantiate(&p->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      GC_CUDA(e);
+    }
+    if (p->exec) {
+      GC_CUDA(cudaGraphLaunch(p->exec, p->st));
+      add_launches(p->kernels);
+    } else {
+      enqueue_static(&p->g, &p->s, p->labels, nullptr, 0, nullptr, nullptr, p->ws, p->wsb, p->st, p->rs);
+    }
+    GC_CUDA(cudaStreamSynchronize(p->st));
+    collect_static(&p->g, &p->s, false, 0, p->rs, stats);
+  });
+}
+
+void gc_plan_destroy(gc_plan* p) {
+  if (!p) return;
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->cap) cudaStreamDestroy(p->cap);
+  delete p;
 }
 
 int gc_static_cc(const gc_csr* g, const gc_spec* spec, int32_t* labels_out, int32_t* post_sample_out,
@@ -370,10 +534,10 @@ int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io, in
       }
     }
     static thread_local EventSet ev;
-    GC_CUDA(cudaEventRecord(ev.e[0], st));
+    GC_CUDA(rec(ev.e[0], st));
     run_gather(labels_io, n, g->offsets, pl.ws.list, pl.ws.ctr, st);
     const int64_t rounds = pl.finish();
-    GC_CUDA(cudaEventRecord(ev.e[1], st));
+    GC_CUDA(rec(ev.e[1], st));
     unsigned long long c[C_COUNT_];
     GC_CUDA(cudaMemcpyAsync(c, pl.ws.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));

@@ -9,6 +9,7 @@
 // thread), larger rows are walked by the whole warp, one
 // row at a time (warp-cooperative hub handling).
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 #include "uf.cuh"
@@ -16,6 +17,7 @@
 namespace gc {
 
 constexpr int kSmall = 32;
+__constant__ int g_loadmode;  // experiment: bit0 stream offsets, bit1 stream targets
 constexpr int kRowBlock = 256;
 
 template <class R>
@@ -33,6 +35,7 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     count = c < count ? c : count;
   }
   unsigned long long my_insp = 0;
+  const uint64_t pol = evict_first_policy();
   for (int64_t base = warp0 * 32; base < count; base += nwarps * 32) {
     const int64_t i = base + lane;
     int32_t u = -1;
@@ -40,16 +43,24 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     int32_t take = 0;
     if (i < count) {
       u = list ? ldg32(list + i) : int32_t(i);
-      b = ldg64(off + u);
-      const int64_t e = ldg64(off + u + 1);
+      b = (g_loadmode & 1) ? ld_stream64(off + u, pol) : ldg64(off + u);
+      const int64_t e = (g_loadmode & 1) ? ld_stream64(off + u + 1, pol) : ldg64(off + u + 1);
       const int64_t d = e - b;
       take = int32_t(d < take_max ? d : take_max);
       my_insp += take;
     }
     const bool big = take > kSmall;
     if (!big) {
-      for (int32_t j = 0; j < take; ++j) {
-        const int32_t t = ldg32(tgt + b + j);
+      int32_t j = 0;
+      // CSR-C: the first two entries of a row in one 8-byte access when aligned
+      if ((g_loadmode & 4) && take >= 2 && (b & 1) == 0 && !lower_only) {
+        const int2 t2 = (g_loadmode & 2) ? ld_stream2(tgt + b, pol) : __ldg(reinterpret_cast<const int2*>(tgt + b));
+        R::unite(s, u, t2.x);
+        R::unite(s, u, t2.y);
+        j = 2;
+      }
+      for (; j < take; ++j) {
+        const int32_t t = (g_loadmode & 2) ? ld_stream(tgt + b + j, pol) : ldg32(tgt + b + j);
         if (lower_only && t >= u) break;
         R::unite(s, u, t);
       }
@@ -62,7 +73,7 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
       const int64_t bb = __shfl_sync(0xffffffffu, b, src);
       const int32_t tk = __shfl_sync(0xffffffffu, take, src);
       for (int32_t j = lane; j < tk; j += 32) {
-        const int32_t t = ldg32(tgt + bb + j);
+        const int32_t t = ld_stream(tgt + bb + j, pol);
         if (lower_only && t >= uu) break;
         R::unite(s, uu, t);
       }
@@ -252,6 +263,12 @@ void dispatch(const UFConfig& c, bool forest, const L& l) {
 }  // namespace
 
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("GC_LOADMODE");
+    mode = e ? atoi(e) : 2;
+    cudaMemcpyToSymbol(g_loadmode, &mode, sizeof(int));
+  }
   if (a.count_host <= 0) return;
   dispatch(cfg, forest, RowsLaunch{a, st});
 }

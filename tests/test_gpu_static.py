@@ -15,7 +15,7 @@ from paper_2008_11839_b200 import (ConfigError, Graph, enumerate_specs, finish_p
 pytestmark = pytest.mark.gpu
 
 
-def _check(golden, name, spec, labels, st):
+def _check(golden, name, spec, labels, st, check_ic=True):
     ref = golden.spec_stats[name][format_spec(spec)]
     n, off, tgt, oracle = golden.graphs[name]
     assert np.array_equal(labels, oracle), (name, format_spec(spec))
@@ -25,7 +25,8 @@ def _check(golden, name, spec, labels, st):
     exp = {k: ref[k] for k in got}
     assert got == exp, (name, format_spec(spec))
     assert st.cov == pytest.approx(ref["cov"], abs=0, rel=1e-12), (name, format_spec(spec))
-    assert st.ic == pytest.approx(ref["ic"], abs=0, rel=1e-12), (name, format_spec(spec))
+    if check_ic:
+        assert st.ic == pytest.approx(ref["ic"], abs=0, rel=1e-12), (name, format_spec(spec))
 
 
 @pytest.mark.parametrize("sample", ["none", "kout", "hb", "bfs"])
@@ -88,3 +89,16 @@ def test_config1_rmat_s16_stats(golden):
                "insp_finish": st.edge_inspections.get("finish", 0), "components": st.component_count}
         assert got == {k: ref[k] for k in got}, text
         assert st.cov == pytest.approx(ref["cov"], rel=1e-12) and st.ic == pytest.approx(ref["ic"], rel=1e-12)
+
+
+def test_plan_replay_matches_direct(golden):
+    from paper_2008_11839_b200 import StaticConnectivity
+    for name in ["rmat_s10_ef8", "ba_120_a3", "comps_30", "edgeless4", "star64"]:
+        g = graph_of(golden, name)
+        for text in ["kout+rem_cas+halve+splice", "none+async+halve", "hb+jtb+twotry", "none+lt_prs",
+                     "bfs+sv"]:
+            plan = StaticConnectivity(g, parse_spec(text))
+            for _ in range(3):  # first run captures, later runs replay the CUDA graph
+                labels, st = plan.run()
+                # plans skip the untimed ic census (metrics are off on the replay path)
+                _check(golden, name, parse_spec(text), labels.cpu().numpy(), st, check_ic=False)
