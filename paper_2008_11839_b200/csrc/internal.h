@@ -83,6 +83,13 @@ enum Counter : int {
   C_SCRATCH0,
   C_SCRATCH1,
   C_CYCLE,         // finalize walk exceeded n steps (cyclic input labels)
+  C_DONE,          // round loops: fixpoint reached
+  C_ROUNDS,        // round loops: rounds executed
+  C_RINSP,         // round loops: accumulated per-round inspections
+  C_WLEN0,         // round loops: working length, parity 0 / 1
+  C_WLEN1,
+  C_WWT0,          // round loops: working weight, parity 0 / 1
+  C_WWT1,
   C_COUNT_ = 32
 };
 

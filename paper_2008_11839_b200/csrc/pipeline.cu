@@ -350,6 +350,13 @@ unsigned long long* pinned_words() {
 
 __global__ void k_set_ctr(unsigned long long* ctr, int idx, unsigned long long v) { ctr[idx] = v; }
 
+__global__ void k_add_ctr(unsigned long long* ctr, int idx, unsigned long long v) { ctr[idx] += v; }
+
+void set_ctr_add(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
+  (k_add_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
   (k_set_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
   GC_CHECK_LAUNCH();

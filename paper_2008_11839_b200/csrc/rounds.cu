@@ -1,9 +1,15 @@
 // rounds.cu — Jacobi min-label rounds (minbased.py:124-304) on sm_100a.
 //
 // Layout: the working edge set is a COO (u, v[, idx], w) built once from the
-// active CSR rows (driver.py:325-330 _gather_edges).  Every round is a short
-// fixed kernel sequence; the host reads one change flag per round through a
-// pinned word, mirroring the reference's per-round fixpoint test.
+// active CSR rows (driver.py:325-330 _gather_edges).
+//
+// Control: the fixpoint test of every family lives on the device.  Each
+// round is a fixed kernel sequence bracketed by a 1-thread prologue (count
+// the round and its inspections, clear the change flag) and epilogue (set
+// `done` when the round changed nothing — that round is counted, as in the
+// reference).  Every kernel returns at once when `done` is set, so the host
+// enqueues rounds in batches and reads `done` once per batch instead of once
+// per round.
 #include <climits>
 #include <cub/cub.cuh>
 
@@ -15,18 +21,70 @@ namespace gc {
 namespace {
 
 constexpr int kRB = 256;
+constexpr int kBatch = 4;  // rounds enqueued per host check
 constexpr unsigned long long kNoWin = ~0ull;
 
 unsigned long long* host_words() { return pinned_words(); }
 
+// device-side round control words (slots of the counter block)
+struct Ctl {
+  unsigned long long* done;
+  unsigned long long* changed;
+  unsigned long long* rounds;
+  unsigned long long* insp;
+  unsigned long long* len;  // [2] working length per parity
+  unsigned long long* wt;   // [2] working weight per parity
+};
+
+Ctl make_ctl(unsigned long long* ctr) {
+  return Ctl{ctr + C_DONE, ctr + C_CHANGED, ctr + C_ROUNDS, ctr + C_RINSP, ctr + C_WLEN0, ctr + C_WWT0};
+}
+
 __global__ void k_set(unsigned long long* p, unsigned long long v) { *p = v; }
-__global__ void k_add(unsigned long long* p, unsigned long long v) { *p += v; }
+
+__global__ void k_ctl_init(Ctl c, unsigned long long len, unsigned long long wt, int nonempty) {
+  *c.done = nonempty ? 0ull : 1ull;
+  *c.changed = 0;
+  *c.rounds = 0;
+  *c.insp = 0;
+  c.len[0] = c.len[1] = len;
+  c.wt[0] = c.wt[1] = wt;
+}
+
+// round prologue: count it (insp += len(work) of this round), clear flags;
+// with alter, the next parity's length / weight restart at zero
+__global__ void k_round_begin(Ctl c, int par, int alter) {
+  if (*c.done) return;
+  *c.rounds += 1;
+  *c.insp += c.wt[par];
+  *c.changed = 0;
+  if (alter) {
+    c.len[par ^ 1] = 0;
+    c.wt[par ^ 1] = 0;
+  }
+}
+
+__global__ void k_round_end(Ctl c) {
+  if (*c.done) return;
+  if (*c.changed == 0) *c.done = 1;
+}
+
+#define GC_SKIP_IF_DONE(ctl) \
+  if (*(ctl).done) return
+
+__global__ void k_copy(int32_t* dst, const int32_t* src, int64_t n, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
 
 // ---------------------------------------------------------------- gather ---
 __device__ __forceinline__ bool keep_entry(int32_t u, int32_t t, bool all_active, const int32_t* P,
                                            int32_t lmax, bool& twin) {
   twin = all_active || P[t] != lmax;
-  return !twin || t > u;
+  if (!twin) return true;
+  // label-equal twins never produce a message in any round rule: drop them
+  return t > u && (all_active || P[u] != P[t]);
 }
 
 __global__ void k_coo_count(const int64_t* off, const int32_t* tgt, const int32_t* P,
@@ -84,7 +142,8 @@ __global__ void k_coo_write(const int64_t* off, const int32_t* tgt, const int32_
 // edge index (minbased.py:95-116); the source row of CSR position j is found
 // by binary search over the offsets.
 __global__ void k_commit_win(unsigned long long* win, int64_t n, const int64_t* off,
-                             const int32_t* tgt, int32_t* fu, int32_t* fv) {
+                             const int32_t* tgt, int32_t* fu, int32_t* fv, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     const unsigned long long j = win[v];
@@ -108,11 +167,13 @@ __global__ void k_fill_u64(unsigned long long* a, int64_t n, unsigned long long 
 // ------------------------------------------------------ Shiloach-Vishkin ---
 // minbased.py:124-155: hook the larger endpoint label onto the smaller when
 // the larger is a root of the snapshot, then fully shortcut.
-__global__ void k_sv_hook(Coo c, const int32_t* __restrict__ prev, int32_t* cur,
-                          unsigned long long* win, unsigned long long* changed) {
+__global__ void k_sv_hook(Coo c, const unsigned long long* len, const int32_t* __restrict__ prev,
+                          int32_t* cur, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   bool any = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     const int32_t pu = prev[c.u[k]], pv = prev[c.v[k]];
     const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
     if (lo != hi && prev[hi] == hi) {
@@ -120,13 +181,15 @@ __global__ void k_sv_hook(Coo c, const int32_t* __restrict__ prev, int32_t* cur,
       any = true;
     }
   }
-  if (__syncthreads_or(any) && threadIdx.x == 0) *changed = 1;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
-__global__ void k_sv_win(Coo c, const int32_t* __restrict__ prev, const int32_t* cur,
-                         unsigned long long* win) {
+__global__ void k_sv_win(Coo c, const unsigned long long* len, const int32_t* __restrict__ prev,
+                         const int32_t* cur, unsigned long long* win, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     const int32_t pu = prev[c.u[k]], pv = prev[c.v[k]];
     const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
     if (lo != hi && prev[hi] == hi && cur[hi] == lo)
@@ -134,7 +197,8 @@ __global__ void k_sv_win(Coo c, const int32_t* __restrict__ prev, const int32_t*
   }
 }
 
-__global__ void k_full_shortcut(int32_t* a, int64_t n) {
+__global__ void k_full_shortcut(int32_t* a, int64_t n, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     int32_t r = ld_acq(a + v);
@@ -170,9 +234,12 @@ __device__ __forceinline__ void lt_messages(int connect, int32_t u, int32_t v, c
   }
 }
 
-__global__ void k_lt_connect(Coo c, const int32_t* __restrict__ L, int32_t* msg, int connect) {
+__global__ void k_lt_connect(Coo c, const unsigned long long* len, const int32_t* __restrict__ L,
+                             int32_t* msg, int connect, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     lt_messages(connect, c.u[k], c.v[k], L, [&](int32_t r, int32_t x) {
       if (x < ld_acq(msg + r)) red_min(msg + r, x);  // msg only decreases
     });
@@ -180,10 +247,12 @@ __global__ void k_lt_connect(Coo c, const int32_t* __restrict__ L, int32_t* msg,
 }
 
 // forest: a root lowered this round records its smallest winning edge index
-__global__ void k_lt_win(Coo c, const int32_t* __restrict__ L, const int32_t* msg, int connect,
-                         unsigned long long* win) {
+__global__ void k_lt_win(Coo c, const unsigned long long* len, const int32_t* __restrict__ L,
+                         const int32_t* msg, int connect, unsigned long long* win, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     const unsigned long long idx = static_cast<unsigned long long>(c.idx[k]);
     lt_messages(connect, c.u[k], c.v[k], L, [&](int32_t r, int32_t x) {
       if (L[r] == r && msg[r] < r && msg[r] == x) atomicMin(win + r, idx);
@@ -192,7 +261,8 @@ __global__ void k_lt_win(Coo c, const int32_t* __restrict__ L, const int32_t* ms
 }
 
 // update: roots take their message (ROOTS) or everyone does (ALL)
-__global__ void k_lt_update(const int32_t* L, int32_t* msg, int64_t n) {
+__global__ void k_lt_update(const int32_t* L, int32_t* msg, int64_t n, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     const int32_t l = L[v];
@@ -202,8 +272,8 @@ __global__ void k_lt_update(const int32_t* L, int32_t* msg, int64_t n) {
 
 // shortcut (one step: new[new[v]], full: root of new) + change test vs the
 // round's starting labels; writes the next labels into L
-__global__ void k_lt_shortcut(int32_t* L, const int32_t* msg, int64_t n, int full,
-                              unsigned long long* changed) {
+__global__ void k_lt_shortcut(int32_t* L, const int32_t* msg, int64_t n, int full, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   bool any = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
@@ -222,29 +292,32 @@ __global__ void k_lt_shortcut(int32_t* L, const int32_t* msg, int64_t n, int ful
       L[v] = x;
     }
   }
-  if (__syncthreads_or(any) && threadIdx.x == 0) *changed = 1;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
 // alter: rewrite working edges to the current labels, drop closed ones.
 // Block-aggregated compaction: one global atomic per block.
-__global__ void __launch_bounds__(kRB) k_lt_alter(Coo in, Coo out, const int32_t* L,
-                                                  unsigned long long* ctr) {
+__global__ void __launch_bounds__(kRB) k_lt_alter(Coo in, const unsigned long long* in_len, Coo out,
+                                                  unsigned long long* out_len, unsigned long long* out_wt,
+                                                  const int32_t* L, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   using Scan = cub::BlockScan<int, kRB>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
+  const int64_t m = int64_t(*in_len);
   unsigned long long wsum = 0;
-  for (int64_t t0 = int64_t(blockIdx.x) * kRB; t0 < in.len; t0 += int64_t(gridDim.x) * kRB) {
+  for (int64_t t0 = int64_t(blockIdx.x) * kRB; t0 < m; t0 += int64_t(gridDim.x) * kRB) {
     const int64_t k = t0 + threadIdx.x;
     int32_t a = 0, b = 0;
     int keep = 0;
-    if (k < in.len) {
+    if (k < m) {
       a = L[in.u[k]];
       b = L[in.v[k]];
       keep = a != b;
     }
     int rank, total;
     Scan(tmp).ExclusiveSum(keep, rank, total);
-    if (threadIdx.x == 0) base = total ? atomicAdd(ctr + C_WORK, static_cast<unsigned long long>(total)) : 0;
+    if (threadIdx.x == 0) base = total ? atomicAdd(out_len, static_cast<unsigned long long>(total)) : 0;
     __syncthreads();
     if (keep) {
       const unsigned long long p = base + rank;
@@ -256,12 +329,13 @@ __global__ void __launch_bounds__(kRB) k_lt_alter(Coo in, Coo out, const int32_t
     }
     __syncthreads();
   }
-  block_add<kRB>(ctr + C_WORK_W, wsum);
+  block_add<kRB>(out_wt, wsum);
 }
 
 // --------------------------------------------------------------- Stergiou ---
 // minbased.py:251-276: reads only the previous array
-__global__ void k_st_init(const int32_t* prev, int32_t* cur, int64_t n) {
+__global__ void k_st_init(const int32_t* prev, int32_t* cur, int64_t n, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     const int32_t p = prev[v];
@@ -270,9 +344,12 @@ __global__ void k_st_init(const int32_t* prev, int32_t* cur, int64_t n) {
   }
 }
 
-__global__ void k_st_edges(Coo c, const int32_t* __restrict__ prev, int32_t* cur) {
+__global__ void k_st_edges(Coo c, const unsigned long long* len, const int32_t* __restrict__ prev,
+                           int32_t* cur, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     const int32_t u = c.u[k], v = c.v[k];
     const int32_t pu = prev[u], pv = prev[v];
     red_min(cur + u, pv);
@@ -282,37 +359,34 @@ __global__ void k_st_edges(Coo c, const int32_t* __restrict__ prev, int32_t* cur
   }
 }
 
-__global__ void k_differ(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* changed) {
+__global__ void k_differ(const int32_t* a, const int32_t* b, int64_t n, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
   bool any = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
     any |= a[v] != b[v];
-  if (__syncthreads_or(any) && threadIdx.x == 0) *changed = 1;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
 // ------------------------------------------------------ label propagation ---
 // minbased.py:284-304: lower the larger endpoint label of every differing edge
-__global__ void k_lp(Coo c, const int32_t* __restrict__ snap, int32_t* L, unsigned long long* changed) {
+__global__ void k_lp(Coo c, const unsigned long long* len, const int32_t* __restrict__ snap,
+                     int32_t* L, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t m = int64_t(*len);
   bool any = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < c.len; k += stride) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     const int32_t u = c.u[k], v = c.v[k];
     const int32_t lu = snap[u], lv = snap[v];
     if (lu > lv) red_min(L + u, lv);
     if (lv > lu) red_min(L + v, lu);
     any |= lu != lv;
   }
-  if (__syncthreads_or(any) && threadIdx.x == 0) *changed = 1;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
 int grid_e(int64_t work) { return grid_for(work, kRB, 8); }
-
-bool read_flag(unsigned long long* dev, cudaStream_t st) {
-  unsigned long long* h = host_words();
-  GC_CUDA(cudaMemcpyAsync(h, dev, 8, cudaMemcpyDeviceToHost, st));
-  GC_CUDA(cudaStreamSynchronize(st));
-  return *h != 0;
-}
 
 struct ForestOut {
   const int64_t* off = nullptr;
@@ -322,105 +396,84 @@ struct ForestOut {
   bool on() const { return fu != nullptr; }
 };
 
-// The round loops.  `insp` accumulates the reference's per-round counts.
-int64_t loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsWs& w,
-                    unsigned long long* ctr, int64_t& insp, const ForestOut& fo, cudaStream_t st) {
-  unsigned long long* flag = ctr + C_CHANGED;
-  int64_t rounds = 0;
+#define L1(kernel, grid, ...) ((kernel<<<grid, kRB, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
+
+// Enqueue one round of the configured family (round `r`, parity r & 1).
+void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, RoundsWs& w, Ctl ctl,
+                   int64_t edge_cap, const ForestOut& fo, int32_t*& A, int32_t*& B, cudaStream_t st) {
+  const int par = r & 1;
   const int gv = grid_e(nl);
-  if (fo.on()) {
-    (k_fill_u64<<<gv, kRB, 0, st>>>(w.win, nl, kNoWin), ::gc::count_launch());
-    GC_CHECK_LAUNCH();
-  }
+  const int ge = grid_e(edge_cap > 0 ? edge_cap : 1);
+  const bool alter = s.finish == GC_FINISH_LT && s.lt_alter;
+  Coo& cur = alter ? coo[par] : coo[0];
+  const unsigned long long* len = alter ? ctl.len + par : ctl.len;
+  ((k_round_begin<<<1, 1, 0, st>>>(ctl, alter ? par : 0, int(alter))), ::gc::count_launch());
   if (s.finish == GC_FINISH_SV) {
-    int32_t* A = P;
-    int32_t* B = w.b;
-    while (true) {
-      ++rounds;
-      insp += work.weight;
-      GC_CUDA(cudaMemcpyAsync(B, A, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
-      if (work.len) (k_sv_hook<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win, flag), ::gc::count_launch());
-      if (fo.on() && work.len) {
-        (k_sv_win<<<grid_e(work.len), kRB, 0, st>>>(work, A, B, w.win), ::gc::count_launch());
-        (k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv), ::gc::count_launch());
-      }
-      (k_full_shortcut<<<gv, kRB, 0, st>>>(B, nl), ::gc::count_launch());
-      GC_CHECK_LAUNCH();
-      const bool changed = read_flag(flag, st);
-      int32_t* t = A; A = B; B = t;
-      if (!changed) break;
+    L1(k_copy, gv, B, A, nl, ctl);
+    L1(k_sv_hook, ge, cur, len, A, B, ctl);
+    if (fo.on()) {
+      L1(k_sv_win, ge, cur, len, A, B, w.win, ctl);
+      L1(k_commit_win, gv, w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv, ctl);
     }
-    if (A != P) GC_CUDA(cudaMemcpyAsync(P, A, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-    return rounds;
-  }
-  if (s.finish == GC_FINISH_LT) {
+    L1(k_full_shortcut, gv, B, nl, ctl);
+    std::swap(A, B);
+  } else if (s.finish == GC_FINISH_LT) {
     int32_t* msg = w.b;
-    Coo* cur = &work;
-    Coo* nxt = &w.spare;
-    while (true) {
-      ++rounds;
-      insp += cur->weight;
-      GC_CUDA(cudaMemcpyAsync(msg, P, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
-      if (cur->len) (k_lt_connect<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect), ::gc::count_launch());
-      if (fo.on() && cur->len) {
-        (k_lt_win<<<grid_e(cur->len), kRB, 0, st>>>(*cur, P, msg, s.lt_connect, w.win), ::gc::count_launch());
-        (k_commit_win<<<gv, kRB, 0, st>>>(w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv), ::gc::count_launch());
-      }
-      if (s.lt_update == GC_LT_UPDATE_ROOTS) (k_lt_update<<<gv, kRB, 0, st>>>(P, msg, nl), ::gc::count_launch());
-      (k_lt_shortcut<<<gv, kRB, 0, st>>>(P, msg, nl, s.lt_shortcut == GC_LT_SHORTCUT_FULL, flag), ::gc::count_launch());
-      GC_CHECK_LAUNCH();
-      if (s.lt_alter && cur->len) {
-        (k_set<<<1, 1, 0, st>>>(ctr + C_WORK, 0), ::gc::count_launch());
-        (k_set<<<1, 1, 0, st>>>(ctr + C_WORK_W, 0), ::gc::count_launch());
-        (k_lt_alter<<<grid_e(cur->len), kRB, 0, st>>>(*cur, *nxt, P, ctr), ::gc::count_launch());
-        GC_CHECK_LAUNCH();
-        unsigned long long* h = host_words();
-        GC_CUDA(cudaMemcpyAsync(h + 8, ctr + C_CHANGED, 8, cudaMemcpyDeviceToHost, st));
-        GC_CUDA(cudaMemcpyAsync(h + 9, ctr + C_WORK, 16, cudaMemcpyDeviceToHost, st));
-        GC_CUDA(cudaStreamSynchronize(st));
-        nxt->len = int64_t(h[9]);
-        nxt->weight = int64_t(h[10]);
-        Coo* t = cur; cur = nxt; nxt = t;
-        if (h[8] == 0) break;
-      } else {
-        if (!read_flag(flag, st)) break;
-      }
+    L1(k_copy, gv, msg, P, nl, ctl);
+    L1(k_lt_connect, ge, cur, len, P, msg, s.lt_connect, ctl);
+    if (fo.on()) {
+      L1(k_lt_win, ge, cur, len, P, msg, s.lt_connect, w.win, ctl);
+      L1(k_commit_win, gv, w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv, ctl);
     }
-    if (cur != &work) std::swap(work, w.spare);
-    return rounds;
+    if (s.lt_update == GC_LT_UPDATE_ROOTS) L1(k_lt_update, gv, P, msg, nl, ctl);
+    L1(k_lt_shortcut, gv, P, msg, nl, int(s.lt_shortcut == GC_LT_SHORTCUT_FULL), ctl);
+    if (alter)
+      ((k_lt_alter<<<ge, kRB, 0, st>>>(cur, len, coo[par ^ 1], ctl.len + (par ^ 1), ctl.wt + (par ^ 1), P,
+                                       ctl)), ::gc::count_launch());
+  } else if (s.finish == GC_FINISH_STERGIOU) {
+    L1(k_st_init, gv, A, B, nl, ctl);
+    L1(k_st_edges, ge, cur, len, A, B, ctl);
+    L1(k_differ, gv, A, B, nl, ctl);
+    std::swap(A, B);
+  } else {
+    int32_t* snap = w.a;
+    L1(k_copy, gv, snap, P, nl, ctl);
+    L1(k_lp, ge, cur, len, snap, P, ctl);
   }
-  if (s.finish == GC_FINISH_STERGIOU) {
-    int32_t* A = P;
-    int32_t* B = w.b;
-    while (true) {
-      ++rounds;
-      insp += work.weight;
-      (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
-      (k_st_init<<<gv, kRB, 0, st>>>(A, B, nl), ::gc::count_launch());
-      if (work.len) (k_st_edges<<<grid_e(work.len), kRB, 0, st>>>(work, A, B), ::gc::count_launch());
-      (k_differ<<<gv, kRB, 0, st>>>(A, B, nl, flag), ::gc::count_launch());
-      GC_CHECK_LAUNCH();
-      const bool changed = read_flag(flag, st);
-      int32_t* t = A; A = B; B = t;
-      if (!changed) break;
-    }
-    if (A != P) GC_CUDA(cudaMemcpyAsync(P, A, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-    return rounds;
+  ((k_round_end<<<1, 1, 0, st>>>(ctl)), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
+// The round loop: rounds are enqueued kBatch at a time; the host reads the
+// device `done` word once per batch.  Returns (rounds, inspections).
+void loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsWs& w, unsigned long long* ctr,
+                 int64_t len, int64_t weight, bool nonempty, const ForestOut& fo, cudaStream_t st,
+                 int64_t& rounds_out, int64_t& insp_out) {
+  const Ctl ctl = make_ctl(ctr);
+  ((k_ctl_init<<<1, 1, 0, st>>>(ctl, static_cast<unsigned long long>(len),
+                                static_cast<unsigned long long>(weight), int(nonempty))),
+   ::gc::count_launch());
+  if (fo.on()) {
+    (k_fill_u64<<<grid_e(nl), kRB, 0, st>>>(w.win, nl, kNoWin), ::gc::count_launch());
   }
-  // label propagation
-  int32_t* snap = w.a;
-  while (true) {
-    ++rounds;
-    insp += work.weight;
-    GC_CUDA(cudaMemcpyAsync(snap, P, size_t(nl) * 4, cudaMemcpyDeviceToDevice, st));
-    (k_set<<<1, 1, 0, st>>>(flag, 0), ::gc::count_launch());
-    if (work.len) (k_lp<<<grid_e(work.len), kRB, 0, st>>>(work, snap, P, flag), ::gc::count_launch());
-    GC_CHECK_LAUNCH();
-    if (!read_flag(flag, st)) break;
+  GC_CHECK_LAUNCH();
+  Coo coo[2] = {work, w.spare};
+  if (!fo.on()) coo[1].idx = nullptr;
+  int32_t* A = P;
+  int32_t* B = w.b;
+  unsigned long long* h = host_words();
+  for (int r = 0; nonempty;) {
+    for (int k = 0; k < kBatch; ++k, ++r) enqueue_round(s, r, P, nl, coo, w, ctl, len, fo, A, B, st);
+    GC_CUDA(cudaMemcpyAsync(h, ctl.done, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    if (h[0]) break;
   }
-  return rounds;
+  // SV / Stergiou ping-pong: at termination both buffers hold the fixpoint
+  // (the last executed round changed nothing), so P is already final
+  GC_CUDA(cudaMemcpyAsync(h, ctl.rounds, 16, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  rounds_out = int64_t(h[0]);
+  insp_out = int64_t(h[1]);
 }
 
 }  // namespace
@@ -462,12 +515,14 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
                                              map_labels, w.pos, out), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   work.idx = out.idx;
-  if (!fu) w.spare.idx = nullptr;
-  int64_t insp = s.finish == GC_FINISH_LP ? 0 : degsum;  // LP does not count the gather
   ForestOut fo;
   if (fu) fo = ForestOut{g.offsets, g.targets, fu, fv};
-  const int64_t rounds = loop_rounds(s, P, n, work, w, ctr, insp, fo, st);
-  (k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, static_cast<unsigned long long>(insp)), ::gc::count_launch());
+  int64_t rounds = 0, insp = 0;
+  loop_rounds(s, P, n, work, w, ctr, work.len, work.weight, true, fo, st, rounds, insp);
+  // LP does not count the gather (driver.py:355-364)
+  const int64_t total = (s.finish == GC_FINISH_LP ? 0 : degsum) + insp;
+  (k_set<<<1, 1, 0, st>>>(ctr + C_INSP_FINISH, static_cast<unsigned long long>(total)),
+   ::gc::count_launch());
   GC_CHECK_LAUNCH();
   return rounds;
 }
@@ -481,11 +536,11 @@ size_t rounds_cub_bytes(int64_t n) {
 
 int64_t run_rounds_coo(const gc_spec& s, int32_t* labels, int64_t nl, Coo& work, RoundsWs& w,
                        unsigned long long* ctr, int counter_slot, cudaStream_t st) {
-  int64_t insp = 0;
-  const int64_t r = loop_rounds(s, labels, nl, work, w, ctr, insp, ForestOut{}, st);
-  (k_add<<<1, 1, 0, st>>>(ctr + counter_slot, static_cast<unsigned long long>(insp)), ::gc::count_launch());
+  int64_t rounds = 0, insp = 0;
+  loop_rounds(s, labels, nl, work, w, ctr, work.len, work.weight, true, ForestOut{}, st, rounds, insp);
+  (k_set<<<1, 1, 0, st>>>(ctr + counter_slot, static_cast<unsigned long long>(insp)), ::gc::count_launch());
   GC_CHECK_LAUNCH();
-  return r;
+  return rounds;
 }
 
 }  // namespace gc

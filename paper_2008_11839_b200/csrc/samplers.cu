@@ -117,29 +117,53 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
 }
 
 // ------------------------------------------------------------------- BFS ---
-// Level-synchronous top-down BFS from the host-chosen probe source
-// (sampling.py:120-172).  The discovery parent is the smallest frontier
-// vertex adjacent to x — exactly the reference's "first occurrence in the
-// sorted frontier's concatenated rows" (np.unique return_index, :153-155) —
-// computed with atomicMin, so the BFS forest is bit-identical.
+// Level-synchronous BFS from the host-chosen probe source (sampling.py:
+// 120-172), direction-optimising: top-down over a frontier queue while the
+// frontier is small, bottom-up over a frontier bitmap (n/8 bytes, L2
+// resident) once its edges dominate.  The discovery parent of x is the
+// smallest frontier vertex adjacent to x — exactly the reference's "first
+// occurrence in the sorted frontier's concatenated rows" (np.unique
+// return_index, :153-155): top-down takes it with atomicMin, bottom-up by
+// scanning x's ascending row and stopping at the first frontier member.
+// Both give the same forest, bit for bit.  The sample inspection count is
+// the reference's per-level sum of frontier degrees, i.e. the degree sum of
+// every reached vertex (:141-144).
 constexpr int kBfsBlock = 256;
 
+__device__ __forceinline__ bool test_bit(const uint32_t* bits, int32_t x) {
+  return (__ldg(bits + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+// frontier statistics of the level being produced: [0] count, [1] degree sum
 __global__ void __launch_bounds__(kBfsBlock)
-k_bfs_expand(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
-             const int32_t* __restrict__ q, const unsigned long long* qcount, int32_t* lvl,
-             int32_t* par, int32_t* qn, unsigned long long* qncount, int32_t level,
-             unsigned long long* insp, int32_t* minv) {
+k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
+         const int32_t* __restrict__ q, const unsigned long long* qstat, int32_t* lvl, int32_t* par,
+         int32_t* qn, unsigned long long* nstat, uint32_t* nbits, int32_t level, int32_t* minv) {
   const int lane = threadIdx.x & 31;
-  const int64_t count = int64_t(*qcount);
+  const int64_t count = int64_t(qstat[0]);
   const int64_t warp0 = (int64_t(blockIdx.x) * kBfsBlock + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * kBfsBlock) >> 5;
-  unsigned long long my_insp = 0;
+  unsigned long long degs = 0;
   int32_t my_min = INT_MAX;
   auto visit = [&](int32_t f, int32_t x) {
     const int32_t lx = ld_acq(lvl + x);
     if (lx != -1 && lx != level + 1) return false;
     if (par) atomicMin(par + x, f);
     return lx == -1 && atomicCAS(lvl + x, -1, level + 1) == -1;
+  };
+  // warp-aggregated enqueue of newly claimed vertices
+  auto push = [&](bool fresh, int32_t x) {
+    const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+    if (!bal) return;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(nstat, static_cast<unsigned long long>(__popc(bal)));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (fresh) {
+      qn[pos + __popc(bal & ((1u << lane) - 1u))] = x;
+      atomicOr(nbits + (x >> 5), 1u << (x & 31));
+      degs += static_cast<unsigned long long>(off[x + 1] - off[x]);
+      my_min = x < my_min ? x : my_min;
+    }
   };
   for (int64_t base = warp0 * 32; base < count; base += nwarps * 32) {
     const int64_t i = base + lane;
@@ -149,18 +173,22 @@ k_bfs_expand(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
       f = q[i];
       b = off[f];
       d = off[f + 1] - b;
-      my_insp += d;
     }
     const bool big = d > 32;
-    if (!big) {
-      for (int64_t j = 0; j < d; ++j) {
-        const int32_t x = tgt[b + j];
-        if (visit(f, x)) {
-          const unsigned long long pos = atomicAdd(qncount, 1ull);
-          qn[pos] = x;
-          my_min = x < my_min ? x : my_min;
-        }
+    // small rows: lanes walk their own rows in lock-step
+    int64_t dm = big ? 0 : d;
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t t = __shfl_xor_sync(0xffffffffu, dm, o);
+      dm = t > dm ? t : dm;
+    }
+    for (int64_t j = 0; j < dm; ++j) {
+      int32_t x = 0;
+      bool fresh = false;
+      if (!big && j < d) {
+        x = tgt[b + j];
+        fresh = visit(f, x);
       }
+      push(fresh, x);
     }
     unsigned mask = __ballot_sync(0xffffffffu, big);
     while (mask) {
@@ -171,23 +199,17 @@ k_bfs_expand(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
       const int64_t dd = __shfl_sync(0xffffffffu, d, src);
       for (int64_t j0 = 0; j0 < dd; j0 += 32) {
         const int64_t j = j0 + lane;
-        const bool fresh = j < dd && visit(ff, tgt[bb + j]);
-        const unsigned bal = __ballot_sync(0xffffffffu, fresh);
-        if (bal) {
-          unsigned long long pos = 0;
-          if (lane == 0) pos = atomicAdd(qncount, static_cast<unsigned long long>(__popc(bal)));
-          pos = __shfl_sync(0xffffffffu, pos, 0);
-          if (fresh) {
-            const int32_t x = tgt[bb + j];
-            qn[pos + __popc(bal & ((1u << lane) - 1u))] = x;
-            my_min = x < my_min ? x : my_min;
-          }
+        int32_t x = 0;
+        bool fresh = false;
+        if (j < dd) {
+          x = tgt[bb + j];
+          fresh = visit(ff, x);
         }
+        push(fresh, x);
       }
     }
   }
-  block_add<kBfsBlock>(insp, my_insp);
-  // block-reduce the minimum discovered id
+  block_add<kBfsBlock>(nstat + 1, degs);
   for (int o = 16; o > 0; o >>= 1) {
     const int32_t t = __shfl_xor_sync(0xffffffffu, my_min, o);
     my_min = t < my_min ? t : my_min;
@@ -195,15 +217,76 @@ k_bfs_expand(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
 }
 
-__global__ void k_bfs_seed(int32_t* lvl, int32_t* q, unsigned long long* qc, int32_t s, int32_t* minv) {
+// bottom-up: every unreached vertex looks for its first frontier neighbour;
+// a warp owns 32 consecutive vertices and writes its next-bitmap word whole
+__global__ void __launch_bounds__(kBfsBlock)
+k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, int32_t* lvl,
+         int32_t* par, const uint32_t* __restrict__ cbits, uint32_t* nbits, unsigned long long* nstat,
+         int32_t level, int32_t* minv) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = 0, degs = 0;
+  int32_t my_min = INT_MAX;
+  const int64_t stride = int64_t(gridDim.x) * kBfsBlock;
+  for (int64_t base = int64_t(blockIdx.x) * kBfsBlock; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    bool found = false;
+    if (v < n && lvl[v] == -1) {
+      const int64_t b = off[v], e = off[v + 1];
+      for (int64_t j = b; j < e; ++j) {
+        const int32_t t = tgt[j];
+        if (test_bit(cbits, t)) {
+          found = true;
+          lvl[v] = level + 1;
+          if (par) par[v] = t;
+          degs += static_cast<unsigned long long>(e - b);
+          break;
+        }
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, found);
+    if (lane == 0 && word) nbits[(base + (threadIdx.x & ~31)) >> 5] = word;
+    if (found) {
+      ++cnt;
+      my_min = int32_t(v) < my_min ? int32_t(v) : my_min;
+    }
+  }
+  block_add<kBfsBlock>(nstat, cnt);
+  block_add<kBfsBlock>(nstat + 1, degs);
+  for (int o = 16; o > 0; o >>= 1) {
+    const int32_t t = __shfl_xor_sync(0xffffffffu, my_min, o);
+    my_min = t < my_min ? t : my_min;
+  }
+  if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+// bitmap -> queue (switching back to top-down)
+__global__ void k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    const bool in = v < n && ((bits[v >> 5] >> (v & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (!bal) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(qc, static_cast<unsigned long long>(__popc(bal)));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (in) q[pos + __popc(bal & ((1u << lane) - 1u))] = int32_t(v);
+  }
+}
+
+__global__ void k_bfs_seed(const int64_t* off, int32_t* lvl, int32_t* q, unsigned long long* qstat,
+                           uint32_t* bits, int32_t s, int32_t* minv, unsigned long long* insp) {
   lvl[s] = 0;
   q[0] = s;
-  *qc = 1;
+  qstat[0] = 1;
+  qstat[1] = static_cast<unsigned long long>(off[s + 1] - off[s]);
+  bits[s >> 5] |= 1u << (s & 31);
   *minv = s;
+  *insp += qstat[1];
 }
 
 // Re-root the discovery tree at the component minimum (sampling.py:161-168)
-// and label the component with it (:158-160).
 __global__ void k_bfs_reroot(int32_t* par, const int32_t* minv) {
   int32_t cur = *minv, prev = -1;
   while (cur != -1) {
@@ -215,6 +298,7 @@ __global__ void k_bfs_reroot(int32_t* par, const int32_t* minv) {
   }
 }
 
+// label the component with its minimum (:158-160) and emit forest slots
 __global__ void k_bfs_label(const int32_t* lvl, const int32_t* par, const int32_t* minv,
                             int32_t n, int32_t* P, int32_t* fu, int32_t* fv) {
   const int32_t mn = *minv;
@@ -234,28 +318,57 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:128-129
   require(s.bfs_source >= 0 && s.bfs_source < n, GC_ERR_ARG, "BFS source out of range");
+  const int64_t words = (int64_t(n) + 31) / 32;
   fill(w.lvl, n, -1, st);
   if (fu) fill(w.par, n, INT_MAX, st);
+  GC_CUDA(cudaMemsetAsync(w.fb0, 0, words * 4, st));
+  GC_CUDA(cudaMemsetAsync(w.fb1, 0, words * 4, st));
   int32_t* minv = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
-  unsigned long long* qc[2] = {ctr + C_NEXT, ctr + C_SCRATCH0};
+  // frontier stats [count, degree sum] for the two parities live in w.stat
+  unsigned long long* fs[2] = {w.stat, w.stat + 2};
   int32_t* q[2] = {w.q0, w.q1};
-  (k_bfs_seed<<<1, 1, 0, st>>>(w.lvl, q[0], qc[0], int32_t(s.bfs_source), minv), ::gc::count_launch());
+  uint32_t* fb[2] = {w.fb0, w.fb1};
+  GC_CUDA(cudaMemsetAsync(w.stat, 0, 4 * sizeof(unsigned long long), st));
+  (k_bfs_seed<<<1, 1, 0, st>>>(g.offsets, w.lvl, q[0], fs[0], fb[0], int32_t(s.bfs_source), minv,
+                               ctr + C_INSP_SAMPLE), ::gc::count_launch());
   GC_CHECK_LAUNCH();
-  unsigned long long* pinned = pinned_words();
-  unsigned long long cur = 1;
-  int cur_i = 0;
-  for (int32_t level = 0; cur > 0; ++level) {
-    GC_CUDA(cudaMemsetAsync(qc[cur_i ^ 1], 0, 8, st));
-    const int64_t blocks64 = (int64_t(cur) * 32 + kBfsBlock - 1) / kBfsBlock / 32 + 1;
-    int blocks = int(blocks64 < int64_t(num_sms()) * 8 ? blocks64 : int64_t(num_sms()) * 8);
-    (k_bfs_expand<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[cur_i], qc[cur_i], w.lvl,
-                                                fu ? w.par : nullptr, q[cur_i ^ 1], qc[cur_i ^ 1],
-                                                level, ctr + C_INSP_SAMPLE, minv), ::gc::count_launch());
+  unsigned long long* h = pinned_words();
+  GC_CUDA(cudaMemcpyAsync(h, fs[0], 16, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  unsigned long long nf = h[0], mf = h[1];
+  int64_t unexplored = g.m - int64_t(mf);
+  bool bottom_up = false;
+  const int bu_grid = grid_for(n, kBfsBlock, 4);
+  for (int32_t level = 0; nf > 0; ++level) {
+    const int c = level & 1, nx = c ^ 1;
+    // Beamer's heuristic: go bottom-up when the frontier's edges exceed
+    // 1/14 of the unexplored ones, back top-down when it shrinks below n/24
+    const bool want_bu = bottom_up ? (nf >= uint64_t(n) / 24) : (int64_t(mf) * 14 > unexplored);
+    if (!want_bu && bottom_up) {
+      // the current frontier only exists as a bitmap: build its queue
+      GC_CUDA(cudaMemsetAsync(fs[c], 0, 8, st));
+      (k_bits_to_queue<<<grid_for(n, kEwBlock, 4), kEwBlock, 0, st>>>(fb[c], n, q[c], fs[c]),
+       ::gc::count_launch());
+    }
+    bottom_up = want_bu;
+    GC_CUDA(cudaMemsetAsync(fs[nx], 0, 16, st));
+    GC_CUDA(cudaMemsetAsync(fb[nx], 0, words * 4, st));
+    if (bottom_up) {
+      (k_bfs_bu<<<bu_grid, kBfsBlock, 0, st>>>(g.offsets, g.targets, n, w.lvl, fu ? w.par : nullptr,
+                                               fb[c], fb[nx], fs[nx], level, minv), ::gc::count_launch());
+    } else {
+      const int64_t blocks64 = (int64_t(nf) * 32 + kBfsBlock - 1) / kBfsBlock / 32 + 1;
+      const int blocks = int(blocks64 < int64_t(num_sms()) * 8 ? blocks64 : int64_t(num_sms()) * 8);
+      (k_bfs_td<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[c], fs[c], w.lvl, fu ? w.par : nullptr,
+                                               q[nx], fs[nx], fb[nx], level, minv), ::gc::count_launch());
+    }
     GC_CHECK_LAUNCH();
-    GC_CUDA(cudaMemcpyAsync(pinned, qc[cur_i ^ 1], 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaMemcpyAsync(h, fs[nx], 16, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
-    cur = *pinned;
-    cur_i ^= 1;
+    nf = h[0];
+    mf = h[1];
+    unexplored -= int64_t(mf);
+    set_ctr_add(ctr, C_INSP_SAMPLE, mf, st);
   }
   if (fu) {
     (k_bfs_reroot<<<1, 1, 0, st>>>(w.par, minv), ::gc::count_launch());
@@ -422,24 +535,28 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   unsigned long long* qc[2] = {ctr + C_NEXT, ctr + C_SCRATCH0};
   int32_t* q[2] = {w.q0, w.q1};
   GC_CUDA(cudaMemsetAsync(qc[0], 0, 8, st));
-  unsigned long long cur = 0;
+  // Rounds are enqueued kLddBatch at a time with fixed grids (the kernels
+  // read the frontier size on the device); the host checks termination once
+  // per batch.  Rounds past the end are empty launches.
+  constexpr int kLddBatch = 8;
+  const int grow_grid = num_sms() * 8;
   int ci = 0;
-  for (int32_t r = 0;; ++r) {
-    GC_CUDA(cudaMemsetAsync(qc[ci ^ 1], 0, 8, st));
-    if (cur) {
-      const int64_t blocks64 = (int64_t(cur) * 32 + kBfsBlock - 1) / kBfsBlock / 32 + 1;
-      const int blocks = int(blocks64 < int64_t(num_sms()) * 8 ? blocks64 : int64_t(num_sms()) * 8);
-      (k_ldd_grow<<<blocks, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[ci], qc[ci], w.lvl, w.par,
-                                               q[ci ^ 1], qc[ci ^ 1], r, ctr + C_INSP_SAMPLE), ::gc::count_launch());
+  for (int32_t r = 0;;) {
+    for (int k = 0; k < kLddBatch; ++k, ++r) {
+      GC_CUDA(cudaMemsetAsync(qc[ci ^ 1], 0, 8, st));
+      if (r > 0)
+        (k_ldd_grow<<<grow_grid, kBfsBlock, 0, st>>>(g.offsets, g.targets, q[ci], qc[ci], w.lvl, w.par,
+                                                     q[ci ^ 1], qc[ci ^ 1], r, ctr + C_INSP_SAMPLE),
+         ::gc::count_launch());
+      if (r <= last_start)
+        (k_ldd_centres<<<ge, kEwBlock, 0, st>>>(n, r, w.start, w.lvl, w.par, q[ci ^ 1], qc[ci ^ 1]),
+         ::gc::count_launch());
+      ci ^= 1;
     }
-    if (r <= last_start)
-      (k_ldd_centres<<<ge, kEwBlock, 0, st>>>(n, r, w.start, w.lvl, w.par, q[ci ^ 1], qc[ci ^ 1]), ::gc::count_launch());
     GC_CHECK_LAUNCH();
-    GC_CUDA(cudaMemcpyAsync(hq, qc[ci ^ 1], 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaMemcpyAsync(hq, qc[ci], 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
-    cur = *hq;
-    ci ^= 1;
-    if (cur == 0 && r >= last_start) break;
+    if (*hq == 0 && r > last_start) break;
   }
   // labels: minimum member id per cluster (q0 is free again: reuse as mins)
   int32_t* mins = w.q0;

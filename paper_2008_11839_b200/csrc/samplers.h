@@ -14,6 +14,9 @@ struct SamplerWs {
   int32_t* q0 = nullptr;      // frontier queues
   int32_t* q1 = nullptr;
   uint16_t* start = nullptr;  // LDD start round per vertex
+  uint32_t* fb0 = nullptr;    // BFS frontier bitmaps
+  uint32_t* fb1 = nullptr;
+  unsigned long long* stat = nullptr;  // frontier [count, degree sum] x 2
 };
 
 template <class A>
@@ -29,6 +32,11 @@ void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
     w.par = a.template take<int32_t>(n);
     w.q0 = a.template take<int32_t>(n);
     w.q1 = a.template take<int32_t>(n);
+    w.stat = a.template take<unsigned long long>(8);
+  }
+  if (s.sample == GC_SAMPLE_BFS) {
+    w.fb0 = a.template take<uint32_t>((n + 31) / 32);
+    w.fb1 = a.template take<uint32_t>((n + 31) / 32);
   }
   if (s.sample == GC_SAMPLE_LDD) w.start = a.template take<uint16_t>(n);
 }

@@ -17,7 +17,6 @@
 namespace gc {
 
 constexpr int kSmall = 32;
-__constant__ int g_loadmode;  // experiment: bit0 stream offsets, bit1 stream targets
 constexpr int kRowBlock = 256;
 
 template <class R>
@@ -43,8 +42,11 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     int32_t take = 0;
     if (i < count) {
       u = list ? ldg32(list + i) : int32_t(i);
-      b = (g_loadmode & 1) ? ld_stream64(off + u, pol) : ldg64(off + u);
-      const int64_t e = (g_loadmode & 1) ? ld_stream64(off + u + 1, pol) : ldg64(off + u + 1);
+      // offsets stream through (no L1 allocation, L2 evict-first); targets
+      // keep the default L1 path, which measured faster for the
+      // neighbouring-row reuse within a warp
+      b = ld_stream64(off + u, pol);
+      const int64_t e = ld_stream64(off + u + 1, pol);
       const int64_t d = e - b;
       take = int32_t(d < take_max ? d : take_max);
       my_insp += take;
@@ -52,15 +54,8 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     const bool big = take > kSmall;
     if (!big) {
       int32_t j = 0;
-      // CSR-C: the first two entries of a row in one 8-byte access when aligned
-      if ((g_loadmode & 4) && take >= 2 && (b & 1) == 0 && !lower_only) {
-        const int2 t2 = (g_loadmode & 2) ? ld_stream2(tgt + b, pol) : __ldg(reinterpret_cast<const int2*>(tgt + b));
-        R::unite(s, u, t2.x);
-        R::unite(s, u, t2.y);
-        j = 2;
-      }
       for (; j < take; ++j) {
-        const int32_t t = (g_loadmode & 2) ? ld_stream(tgt + b + j, pol) : ldg32(tgt + b + j);
+        const int32_t t = ldg32(tgt + b + j);
         if (lower_only && t >= u) break;
         R::unite(s, u, t);
       }
@@ -73,7 +68,7 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
       const int64_t bb = __shfl_sync(0xffffffffu, b, src);
       const int32_t tk = __shfl_sync(0xffffffffu, take, src);
       for (int32_t j = lane; j < tk; j += 32) {
-        const int32_t t = ld_stream(tgt + bb + j, pol);
+        const int32_t t = ldg32(tgt + bb + j);
         if (lower_only && t >= uu) break;
         R::unite(s, uu, t);
       }
@@ -263,12 +258,6 @@ void dispatch(const UFConfig& c, bool forest, const L& l) {
 }  // namespace
 
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st) {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("GC_LOADMODE");
-    mode = e ? atoi(e) : 2;
-    cudaMemcpyToSymbol(g_loadmode, &mode, sizeof(int));
-  }
   if (a.count_host <= 0) return;
   dispatch(cfg, forest, RowsLaunch{a, st});
 }
