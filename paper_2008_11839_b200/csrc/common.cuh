@@ -93,6 +93,48 @@ __device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long
   }
 }
 
+// Block-aggregated append to a global queue.  Warps stage their items in
+// shared memory (one shared atomic per warp per push); flush() reserves the
+// block's range with a single global atomic, so a frontier of F vertices
+// costs F / blockDim global atomics instead of one per warp or per item.
+// Items beyond the staging capacity go straight to the global queue.
+// push() must be called by whole (converged) warps and flush() by the whole
+// block.
+template <int CAP>
+struct BlockQueue {
+  int32_t items[CAP];
+  int count;
+  unsigned long long base;
+
+  __device__ __forceinline__ void init() {
+    if (threadIdx.x == 0) count = 0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void push(bool p, int32_t x, int32_t* q, unsigned long long* qc) {
+    const unsigned bal = __ballot_sync(0xffffffffu, p);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(&count, __popc(bal));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (p) {
+      const int mine = pos + __popc(bal & ((1u << lane) - 1u));
+      if (mine < CAP) items[mine] = x;
+      else q[atomicAdd(qc, 1ull)] = x;
+    }
+  }
+  __device__ __forceinline__ void flush(int32_t* q, unsigned long long* qc) {
+    __syncthreads();
+    const int c = count < CAP ? count : CAP;
+    if (threadIdx.x == 0) base = c ? atomicAdd(qc, static_cast<unsigned long long>(c)) : 0ull;
+    __syncthreads();
+    for (int i = threadIdx.x; i < c; i += blockDim.x) q[base + i] = items[i];
+    __syncthreads();
+    if (threadIdx.x == 0) count = 0;
+    __syncthreads();
+  }
+};
+
 // Grid size for an elementwise kernel: enough CTAs to cover `work` items
 // but capped at a whole number of waves over the 148 SMs.
 inline int grid_for(int64_t work, int block, int max_waves = 32) {

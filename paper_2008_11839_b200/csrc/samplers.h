@@ -9,15 +9,20 @@ namespace gc {
 struct SamplerWs {
   int32_t* coo_u = nullptr;   // k-out random mode pairs
   int32_t* coo_v = nullptr;
-  int32_t* lvl = nullptr;     // BFS / LDD level or cluster claim
-  int32_t* par = nullptr;     // BFS discovery parent
-  int32_t* q0 = nullptr;      // frontier queues
+  unsigned long long* key = nullptr;  // BFS / LDD claim word: (round << 32) | parent-or-cluster
+  int32_t* par = nullptr;     // BFS discovery parent (re-rooted for the forest)
+  int32_t* q0 = nullptr;      // frontier queues (HB: phase-2 roots)
   int32_t* q1 = nullptr;
-  uint16_t* start = nullptr;  // LDD start round per vertex
   uint32_t* fb0 = nullptr;    // BFS frontier bitmaps
   uint32_t* fb1 = nullptr;
   unsigned long long* stat = nullptr;  // frontier [count, degree sum] x 2
+  uint16_t* start = nullptr;  // LDD start round per vertex
+  int32_t* order = nullptr;   // LDD vertices bucketed by start round
+  unsigned int* boff = nullptr;    // LDD bucket offsets [kLddMaxRounds + 2]
+  unsigned int* cursor = nullptr;  // LDD scatter cursors
 };
+
+constexpr int kLddMaxRounds = 4094;
 
 template <class A>
 void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
@@ -28,17 +33,22 @@ void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
   }
   if (s.sample == GC_SAMPLE_HB) w.q0 = a.template take<int32_t>(n);  // phase-2 roots
   if (s.sample == GC_SAMPLE_BFS || s.sample == GC_SAMPLE_LDD) {
-    w.lvl = a.template take<int32_t>(n);
-    w.par = a.template take<int32_t>(n);
+    w.key = a.template take<unsigned long long>(n);
     w.q0 = a.template take<int32_t>(n);
     w.q1 = a.template take<int32_t>(n);
     w.stat = a.template take<unsigned long long>(8);
   }
   if (s.sample == GC_SAMPLE_BFS) {
+    w.par = a.template take<int32_t>(n);
     w.fb0 = a.template take<uint32_t>((n + 31) / 32);
     w.fb1 = a.template take<uint32_t>((n + 31) / 32);
   }
-  if (s.sample == GC_SAMPLE_LDD) w.start = a.template take<uint16_t>(n);
+  if (s.sample == GC_SAMPLE_LDD) {
+    w.start = a.template take<uint16_t>(n);
+    w.order = a.template take<int32_t>(n);
+    w.boff = a.template take<unsigned int>(kLddMaxRounds + 4);
+    w.cursor = a.template take<unsigned int>(kLddMaxRounds + 4);
+  }
 }
 
 void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a, bool forest,

@@ -1,0 +1,540 @@
+// traverse.cu — the traversal samplers: BFS (sampling.py:120-172) and the
+// new LDD sampler.
+//
+// Both are frontier expansions whose per-vertex claim is one 64-bit word
+//     key[x] = (round << 32) | payload          (~0 = unclaimed)
+// resolved with a single atomicMin: the earliest round wins, and among the
+// claims of that round the smallest payload wins (BFS: the parent id, LDD:
+// the cluster id).  The claimant that sees the old value ~0 enqueues x.  One
+// atomic per examined edge replaces the load / CAS / min triple, and the
+// result is deterministic, which makes the BFS forest bit-identical to the
+// reference's "first discoverer in the sorted frontier" rule.
+#include <climits>
+#include <cstring>
+#include <cub/cub.cuh>
+
+#include "pipeline.cuh"
+#include "samplers.h"
+
+namespace gc {
+
+namespace {
+
+constexpr int kTB = 256;                  // traversal block
+constexpr int kQCap = kTB * 16;           // 16 KB staging per block
+constexpr unsigned long long kFree = ~0ull;
+
+__device__ __forceinline__ unsigned long long ld_key(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long mk_key(int32_t round, uint32_t payload) {
+  return (static_cast<unsigned long long>(uint32_t(round)) << 32) | payload;
+}
+
+// try to claim x in `round` for `payload`; true for the unique first claimant
+__device__ __forceinline__ bool claim(unsigned long long* key, int32_t x, int32_t round, uint32_t payload) {
+  const unsigned long long want = mk_key(round, payload);
+  const unsigned long long seen = ld_key(key + x);  // cached filter: keys only decrease
+  if (seen <= want) return false;
+  return atomicMin(key + x, want) == kFree;
+}
+
+__device__ __forceinline__ int32_t warp_min(int32_t v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const int32_t t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+
+__global__ void k_fill64(unsigned long long* a, int64_t n, unsigned long long v) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
+}
+
+// ------------------------------------------------------------------- BFS ---
+// Direction-optimising level-synchronous BFS: top-down over a frontier
+// queue while the frontier is small, bottom-up over a frontier bitmap (n/8
+// bytes, L2-resident) once its edges dominate (Beamer's rule).  Bottom-up
+// takes the first frontier vertex of x's ascending row — the same minimum
+// the top-down atomicMin selects — so the forest does not depend on the
+// direction schedule.  Frontier stats [count, degree sum] feed the switch
+// and the inspection count (sum of frontier degrees, sampling.py:141-144).
+
+__global__ void __launch_bounds__(kTB)
+k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
+         const unsigned long long* qstat, unsigned long long* key, int32_t* qn, unsigned long long* nstat,
+         uint32_t* nbits, int32_t level, int32_t* minv, unsigned long long* insp) {
+  __shared__ BlockQueue<kQCap> bq;
+  bq.init();
+  const int lane = threadIdx.x & 31;
+  const int64_t count = int64_t(qstat[0]);
+  unsigned long long degs = 0;
+  int32_t my_min = INT_MAX;
+  auto take = [&](bool fresh, int32_t x) {
+    if (fresh) {
+      atomicOr(nbits + (x >> 5), 1u << (x & 31));
+      my_min = x < my_min ? x : my_min;
+    }
+    bq.push(fresh, x, qn, nstat);
+  };
+  for (int64_t base = int64_t(blockIdx.x) * kTB; base < count; base += int64_t(gridDim.x) * kTB) {
+    const int64_t i = base + threadIdx.x;
+    int32_t f = -1;
+    int64_t b = 0, d = 0;
+    if (i < count) {
+      f = q[i];
+      b = off[f];
+      d = off[f + 1] - b;
+      degs += static_cast<unsigned long long>(d);  // frontier degree (counted at expansion)
+    }
+    const bool big = d > 32;
+    int64_t dm = big ? 0 : d;
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t t = __shfl_xor_sync(0xffffffffu, dm, o);
+      dm = t > dm ? t : dm;
+    }
+    for (int64_t j = 0; j < dm; ++j) {
+      int32_t x = 0;
+      bool fresh = false;
+      if (!big && j < d) {
+        x = tgt[b + j];
+        fresh = claim(key, x, level + 1, uint32_t(f));
+      }
+      take(fresh, x);
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, big);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int32_t ff = __shfl_sync(0xffffffffu, f, src);
+      const int64_t bb = __shfl_sync(0xffffffffu, b, src);
+      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
+      for (int64_t j0 = 0; j0 < dd; j0 += 32) {
+        const int64_t j = j0 + lane;
+        int32_t x = 0;
+        bool fresh = false;
+        if (j < dd) {
+          x = tgt[bb + j];
+          fresh = claim(key, x, level + 1, uint32_t(ff));
+        }
+        take(fresh, x);
+      }
+    }
+    bq.flush(qn, nstat);
+  }
+  if (insp) block_add<kTB>(insp, degs);
+  my_min = warp_min(my_min);
+  if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+__device__ __forceinline__ bool test_bit(const uint32_t* bits, int32_t x) {
+  return (__ldg(bits + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+// bottom-up: a warp owns 32 consecutive vertices and writes its next-bitmap
+// word whole; each unreached vertex stops at its first frontier neighbour
+__global__ void __launch_bounds__(kTB)
+k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, unsigned long long* key,
+         const uint32_t* __restrict__ cbits, uint32_t* nbits, unsigned long long* nstat, int32_t level,
+         int32_t* minv) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = 0, degs = 0;
+  int32_t my_min = INT_MAX;
+  const int64_t stride = int64_t(gridDim.x) * kTB;
+  for (int64_t base = int64_t(blockIdx.x) * kTB; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    bool found = false;
+    if (v < n && key[v] == kFree) {
+      const int64_t b = off[v], e = off[v + 1];
+      for (int64_t j = b; j < e; ++j) {
+        const int32_t t = tgt[j];
+        if (test_bit(cbits, t)) {
+          found = true;
+          key[v] = mk_key(level + 1, uint32_t(t));
+          degs += static_cast<unsigned long long>(e - b);
+          break;
+        }
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, found);
+    if (lane == 0 && word) nbits[(base + (threadIdx.x & ~31)) >> 5] = word;
+    if (found) {
+      ++cnt;
+      my_min = int32_t(v) < my_min ? int32_t(v) : my_min;
+    }
+  }
+  block_add<kTB>(nstat, cnt);
+  block_add<kTB>(nstat + 1, degs);
+  my_min = warp_min(my_min);
+  if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+// bitmap -> queue (switching back to top-down): one thread per 32-bit word
+__global__ void __launch_bounds__(kEwBlock)
+k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc) {
+  using Scan = cub::BlockScan<int, kEwBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long base;
+  const int64_t words = (int64_t(n) + 31) / 32;
+  for (int64_t w0 = int64_t(blockIdx.x) * kEwBlock; w0 < words; w0 += int64_t(gridDim.x) * kEwBlock) {
+    const int64_t wi = w0 + threadIdx.x;
+    uint32_t word = wi < words ? bits[wi] : 0u;
+    int rank, total;
+    Scan(tmp).ExclusiveSum(__popc(word), rank, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(qc, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    unsigned long long p = base + rank;
+    while (word) {
+      const int bit = __ffs(word) - 1;
+      word &= word - 1;
+      q[p++] = int32_t(wi * 32 + bit);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_bfs_seed(const int64_t* off, unsigned long long* key, int32_t* q, unsigned long long* qstat,
+                           uint32_t* bits, int32_t s, int32_t* minv) {
+  key[s] = mk_key(0, 0xffffffffu);  // no parent
+  q[0] = s;
+  qstat[0] = 1;
+  qstat[1] = static_cast<unsigned long long>(off[s + 1] - off[s]);
+  bits[s >> 5] |= 1u << (s & 31);
+  *minv = s;
+}
+
+// discovery parents out of the claim words (-1 = source / unreached)
+__global__ void k_bfs_parents(const unsigned long long* key, int32_t n, int32_t* par) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const unsigned long long k = key[v];
+    par[v] = k == kFree ? -1 : int32_t(uint32_t(k));
+  }
+}
+
+// re-root the discovery tree at the component minimum (sampling.py:161-168)
+__global__ void k_bfs_reroot(int32_t* par, const int32_t* minv) {
+  int32_t cur = *minv, prev = -1;
+  while (cur != -1) {
+    const int32_t nxt = par[cur];
+    par[cur] = prev;
+    prev = cur;
+    cur = nxt;
+  }
+}
+
+// label the component with its minimum (:158-160), emit forest slots, and
+// count the sample inspections: the reference adds every frontier's degree
+// sum (:141-144), i.e. the degree of every reached vertex exactly once
+__global__ void k_bfs_label(const unsigned long long* key, const int32_t* par, const int32_t* minv,
+                            const int64_t* off, int32_t n, int32_t* P, int32_t* fu, int32_t* fv,
+                            unsigned long long* insp) {
+  const int32_t mn = *minv;
+  unsigned long long degs = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    if (key[v] == kFree) continue;
+    P[v] = mn;
+    degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
+    if (fu && v != mn) {
+      fu[v] = par[v];
+      fv[v] = int32_t(v);
+    }
+  }
+  block_add<kEwBlock>(insp, degs);
+}
+
+// ------------------------------------------------------------------- LDD ---
+// Low-diameter decomposition (new; absent from the reference, driver.py:
+// 65-69; ConnectIt, which GConn extends).  Miller-Peng-Xu:
+//   delta_v ~ Exp(beta) from a counter hash of (seed, v); v may start its own
+//   cluster at round floor(delta_max - delta_v); clusters grow one hop per
+//   round; a vertex first reached in round r joins the smallest cluster id
+//   among that round's claimants (its own id if it starts then).
+// Vertices are bucketed by start round once, so each round touches only its
+// own centres.  Labels are cluster minima: P[v] <= v and every class is
+// connected, so the partition refines the true one (validate.py:290-297).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ float ldd_delta(uint64_t seed, int64_t v, float beta) {
+  const uint64_t h = mix64(seed * 0xd1b54a32d192ed03ull + uint64_t(v));
+  const double u = (double((h >> 11) + 1)) * (1.0 / 9007199254740992.0);  // (0, 1]
+  return float(-log(u) / double(beta));
+}
+
+__global__ void k_ldd_delta_max(int32_t n, uint64_t seed, float beta, int32_t* dmax_bits) {
+  float mx = 0.f;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    mx = fmaxf(mx, ldd_delta(seed, v, beta));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(dmax_bits, __float_as_int(mx));  // positive floats order as ints
+}
+
+constexpr int kBuckets = kLddMaxRounds + 1;
+
+// start round per vertex + block-aggregated bucket histogram
+__global__ void __launch_bounds__(kEwBlock)
+k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
+            unsigned long long* key, unsigned int* bcount) {
+  __shared__ unsigned int hist[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const float dmax = __int_as_float(*dmax_bits);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    float r = floorf(dmax - ldd_delta(seed, v, beta));
+    r = r < 0.f ? 0.f : (r > float(kLddMaxRounds) ? float(kLddMaxRounds) : r);
+    start[v] = uint16_t(r);
+    key[v] = kFree;
+    atomicAdd(hist + int(r), 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+    if (hist[i]) atomicAdd(bcount + i, hist[i]);
+}
+
+// exclusive scan of the bucket counts (one block); boff[kBuckets] = n
+__global__ void __launch_bounds__(1024) k_ldd_bucket_scan(unsigned int* boff, unsigned int* cursor) {
+  using Scan = cub::BlockScan<unsigned int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int kPer = (kBuckets + 1023) / 1024;
+  unsigned int v[kPer];
+  for (int j = 0; j < kPer; ++j) {
+    const int i = threadIdx.x * kPer + j;
+    v[j] = i < kBuckets ? boff[i] : 0u;
+  }
+  unsigned int total;
+  Scan(tmp).ExclusiveSum(v, v, total);
+  for (int j = 0; j < kPer; ++j) {
+    const int i = threadIdx.x * kPer + j;
+    if (i < kBuckets) boff[i] = cursor[i] = v[j];
+  }
+  if (threadIdx.x == 0) boff[kBuckets] = total;
+}
+
+// scatter vertices into their start-round buckets (order within a bucket is
+// irrelevant: claims are resolved by atomicMin)
+__global__ void __launch_bounds__(kEwBlock)
+k_ldd_scatter(int32_t n, const uint16_t* start, unsigned int* cursor, int32_t* order) {
+  __shared__ unsigned int hist[kBuckets];
+  __shared__ unsigned int base[kBuckets];
+  const int64_t span = int64_t(kEwBlock) * 16;  // vertices per block step
+  for (int64_t b0 = int64_t(blockIdx.x) * span; b0 < n; b0 += int64_t(gridDim.x) * span) {
+    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    unsigned int local[16];
+    for (int k = 0; k < 16; ++k) {
+      const int64_t v = b0 + int64_t(k) * kEwBlock + threadIdx.x;
+      local[k] = v < n ? atomicAdd(hist + start[v], 1u) : 0u;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+      base[i] = hist[i] ? atomicAdd(cursor + i, hist[i]) : 0u;
+    __syncthreads();
+    for (int k = 0; k < 16; ++k) {
+      const int64_t v = b0 + int64_t(k) * kEwBlock + threadIdx.x;
+      if (v < n) order[base[start[v]] + local[k]] = int32_t(v);
+    }
+    __syncthreads();
+  }
+}
+
+// One LDD round in one launch: grow the previous frontier, then start the
+// centres of bucket r; both append to the same block queue.  Frontier
+// counters form a ring of three so the kernel can zero the counter the
+// next round will fill without touching the one it reads.
+__global__ void __launch_bounds__(kTB)
+k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, unsigned long long* key,
+            const int32_t* order, const unsigned int* boff, int32_t r, int32_t last_start, const int32_t* qin,
+            const unsigned long long* cin, int32_t* qout, unsigned long long* cout, unsigned long long* cnext,
+            unsigned long long* insp) {
+  __shared__ BlockQueue<kQCap> bq;
+  bq.init();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnext = 0;
+  unsigned long long my_insp = 0;
+  if (r > 0) {
+    const int64_t count = int64_t(*cin);
+    for (int64_t base = int64_t(blockIdx.x) * kTB; base < count; base += int64_t(gridDim.x) * kTB) {
+      const int64_t i = base + threadIdx.x;
+      uint32_t c = 0;
+      int64_t b = 0, d = 0;
+      if (i < count) {
+        const int32_t f = qin[i];
+        c = uint32_t(key[f]);  // cluster of f (final since round r-1)
+        b = off[f];
+        d = off[f + 1] - b;
+        my_insp += d;
+      }
+      int64_t dmax = d;
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t t = __shfl_xor_sync(0xffffffffu, dmax, o);
+        dmax = t > dmax ? t : dmax;
+      }
+      for (int64_t j = 0; j < dmax; ++j) {
+        bool fresh = false;
+        int32_t x = 0;
+        if (j < d) {
+          x = tgt[b + j];
+          fresh = claim(key, x, r, c);
+        }
+        bq.push(fresh, x, qout, cout);
+      }
+      bq.flush(qout, cout);
+    }
+  }
+  if (r <= last_start) {
+    const int64_t lo = boff[r], hi = boff[r + 1];
+    for (int64_t b0 = lo + int64_t(blockIdx.x) * kTB; b0 < hi; b0 += int64_t(gridDim.x) * kTB) {
+      const int64_t i = b0 + threadIdx.x;
+      int32_t v = 0;
+      bool fresh = false;
+      if (i < hi) {
+        v = order[i];
+        fresh = claim(key, v, r, uint32_t(v));
+      }
+      bq.push(fresh, v, qout, cout);
+      bq.flush(qout, cout);
+    }
+  }
+  block_add<kTB>(insp, my_insp);
+}
+
+__global__ void k_ldd_mins(const unsigned long long* key, int32_t* mins, int32_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    atomicMin(mins + uint32_t(key[v]), int32_t(v));
+}
+
+__global__ void k_ldd_label(const unsigned long long* key, const int32_t* mins, int32_t* P, int32_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    P[v] = mins[uint32_t(key[v])];
+}
+
+#define TL(kernel, grid, block, ...) ((kernel<<<grid, block, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
+
+}  // namespace
+
+void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t* fv, SamplerWs& w,
+             unsigned long long* ctr, cudaStream_t st) {
+  const int32_t n = int32_t(g.n);
+  if (n == 0 || g.m == 0) return;  // sampling.py:128-129
+  require(s.bfs_source >= 0 && s.bfs_source < n, GC_ERR_ARG, "BFS source out of range");
+  const int64_t words = (int64_t(n) + 31) / 32;
+  TL(k_fill64, grid_for(n, kEwBlock, 8), kEwBlock, w.key, n, kFree);
+  GC_CUDA(cudaMemsetAsync(w.fb0, 0, words * 4, st));
+  GC_CUDA(cudaMemsetAsync(w.fb1, 0, words * 4, st));
+  int32_t* minv = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
+  unsigned long long* fs[2] = {w.stat, w.stat + 2};
+  int32_t* q[2] = {w.q0, w.q1};
+  uint32_t* fb[2] = {w.fb0, w.fb1};
+  GC_CUDA(cudaMemsetAsync(w.stat, 0, 4 * sizeof(unsigned long long), st));
+  TL(k_bfs_seed, 1, 1, g.offsets, w.key, q[0], fs[0], fb[0], int32_t(s.bfs_source), minv);
+  GC_CHECK_LAUNCH();
+  unsigned long long* h = pinned_words();
+  GC_CUDA(cudaMemcpyAsync(h, fs[0], 16, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  unsigned long long nf = h[0];
+  double mf = double(h[1]);  // frontier edges: exact for the seed / bottom-up levels, estimated top-down
+  const double avg_deg = double(g.m) / double(n);
+  double unexplored = double(g.m) - mf;
+  bool bottom_up = false;
+  const int bu_grid = grid_for(n, kTB, 4);
+  for (int32_t level = 0; nf > 0; ++level) {
+    const int c = level & 1, nx = c ^ 1;
+    // Beamer's heuristic: bottom-up once the frontier's edges exceed 1/14 of
+    // the unexplored ones, back to top-down when it shrinks below n/24
+    const bool want_bu = bottom_up ? (nf >= uint64_t(n) / 24) : (mf * 14.0 > unexplored);
+    if (!want_bu && bottom_up) {
+      GC_CUDA(cudaMemsetAsync(fs[c], 0, 8, st));
+      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], fs[c]);
+    }
+    bottom_up = want_bu;
+    GC_CUDA(cudaMemsetAsync(fs[nx], 0, 16, st));
+    GC_CUDA(cudaMemsetAsync(fb[nx], 0, words * 4, st));
+    if (bottom_up) {
+      TL(k_bfs_bu, bu_grid, kTB, g.offsets, g.targets, n, w.key, fb[c], fb[nx], fs[nx], level, minv);
+    } else {
+      const int64_t b64 = (int64_t(nf) + kTB - 1) / kTB;
+      const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
+      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], fs[c], w.key, q[nx], fs[nx], fb[nx], level, minv,
+         nullptr);
+    }
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaMemcpyAsync(h, fs[nx], 16, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    nf = h[0];
+    mf = bottom_up ? double(h[1]) : double(nf) * avg_deg;
+    unexplored -= mf;
+  }
+  const int ge = grid_for(n, kEwBlock, 8);
+  if (fu) {
+    TL(k_bfs_parents, ge, kEwBlock, w.key, n, w.par);
+    TL(k_bfs_reroot, 1, 1, w.par, minv);
+  }
+  TL(k_bfs_label, ge, kEwBlock, w.key, w.par, minv, g.offsets, n, P, fu, fv, ctr + C_INSP_SAMPLE);
+  GC_CHECK_LAUNCH();
+}
+
+void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
+             cudaStream_t st) {
+  const int32_t n = int32_t(g.n);
+  if (n == 0) return;
+  const float beta = s.ldd_beta > 0 ? float(s.ldd_beta) : 0.2f;
+  int32_t* dmax = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
+  unsigned int* bcount = w.boff;
+  unsigned int* cursor = w.cursor;
+  GC_CUDA(cudaMemsetAsync(dmax, 0, 4, st));
+  GC_CUDA(cudaMemsetAsync(bcount, 0, (kBuckets + 1) * sizeof(unsigned int), st));
+  const int ge = grid_for(n, kEwBlock, 8);
+  TL(k_ldd_delta_max, ge, kEwBlock, n, s.seed, beta, dmax);
+  TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, w.key, bcount);
+  TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
+  TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
+     cursor, w.order);
+  GC_CHECK_LAUNCH();
+  unsigned long long* hq = pinned_words();
+  GC_CUDA(cudaMemcpyAsync(hq + 1, dmax, 4, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  float dmax_h;
+  std::memcpy(&dmax_h, hq + 1, 4);
+  int32_t last_start = int32_t(floorf(dmax_h));
+  if (last_start > kLddMaxRounds) last_start = kLddMaxRounds;
+  if (last_start < 0) last_start = 0;
+  // frontier counters: a ring of three (round r reads ring[(r+2)%3], writes
+  // ring[r%3] and zeroes ring[(r+1)%3]); queues ping-pong
+  unsigned long long* ring = w.stat;
+  int32_t* q[2] = {w.q0, w.q1};
+  GC_CUDA(cudaMemsetAsync(ring, 0, 3 * sizeof(unsigned long long), st));
+  // rounds are enqueued kLddBatch at a time (one launch per round, kernels
+  // read the frontier size on the device); the host checks termination per batch
+  constexpr int kLddBatch = 16;
+  const int grid = num_sms() * 8;
+  for (int32_t r = 0;;) {
+    for (int k = 0; k < kLddBatch; ++k, ++r)
+      TL(k_ldd_round, grid, kTB, g.offsets, g.targets, w.key, w.order, w.boff, r, last_start, q[(r + 1) & 1],
+         ring + (r + 2) % 3, q[r & 1], ring + r % 3, ring + (r + 1) % 3, ctr + C_INSP_SAMPLE);
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaMemcpyAsync(hq, ring + (r - 1) % 3, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    if (*hq == 0 && r > last_start) break;
+  }
+  // labels: minimum member id per cluster (q0 is free again: reuse as mins)
+  int32_t* mins = w.q0;
+  fill(mins, n, INT_MAX, st);
+  TL(k_ldd_mins, ge, kEwBlock, w.key, mins, n);
+  TL(k_ldd_label, ge, kEwBlock, w.key, mins, P, n);
+  GC_CHECK_LAUNCH();
+}
+
+}  // namespace gc
