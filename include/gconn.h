@@ -152,8 +152,11 @@ void gc_plan_destroy(gc_plan* plan);
  * Slot r of (fu, fv) holds the original edge recorded when r lost root
  * status; empty slots hold -1 (ForestEdges.edges None). */
 int gc_spanning_forest(const gc_csr* g, const gc_spec* spec, int32_t* fu,
-                       int32_t* fv, gc_stats* stats, void* ws,
-                       size_t ws_bytes, void* stream);
+                       int32_t* fv, int32_t* parent_out, gc_stats* stats,
+                       void* ws, size_t ws_bytes, void* stream);
+/* parent_out (nullable) receives the unfinalised parent array — a valid
+ * union-find state (P[v] <= v, roots are class minima) that the sharded
+ * driver keeps merging into. */
 
 /* ---- finish phase only (driver.py:432-446) -------------------------------
  * labels_io[n] holds the (possibly partial) input labels and receives the
@@ -175,6 +178,15 @@ int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us,
                    const int32_t* vs, int64_t k, const gc_spec* spec,
                    int32_t* aux, int32_t* fu, int32_t* fv, void* stream);
 
+/* Like gc_union_edges, but appends every edge whose union merged two trees
+ * to (out_u, out_v) (capacity k) and counts them in *out_count (device).
+ * Root-based rules only.  This is the exchange unit of the sharded drivers
+ * (SURVEY 8e): the merging edges of a shard form a spanning forest of it. */
+int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
+                        const int32_t* vs, int64_t k, const gc_spec* spec,
+                        int32_t* aux, int32_t* out_u, int32_t* out_v,
+                        unsigned long long* out_count, void* stream);
+
 /* ---- incremental (driver.py:567-725) -------------------------------------*/
 typedef struct gc_incr gc_incr;
 /* capacity = number of vertex slots; sentinel = capacity (driver.py:603). */
@@ -191,6 +203,11 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs,
 /* Columnar insert-only / query-only fast paths (no per-op flag array). */
 int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs,
                    int64_t len, gc_stats* stats);
+/* Insert-only batch that also records the edges that merged two trees
+ * (capacity len) — the per-batch exchange of the sharded incremental driver. */
+int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs,
+                        int64_t len, int32_t* out_u, int32_t* out_v,
+                        unsigned long long* out_count, gc_stats* stats);
 int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs,
                   int64_t len, uint8_t* bits_out, gc_stats* stats);
 /* Copy of the live state with the sentinel convention (driver.py:656,710). */

@@ -63,8 +63,10 @@ _SIGNATURES = {
     "gc_plan_create": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _SZ, _VP, C.POINTER(_VP)]),
     "gc_plan_run": (C.c_int, [_VP, C.POINTER(Stats)]),
     "gc_plan_destroy": (None, [_VP]),
-    "gc_spanning_forest": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, C.POINTER(Stats),
+    "gc_spanning_forest": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _VP, C.POINTER(Stats),
                                      _VP, _SZ, _VP]),
+    "gc_union_edges_list": (C.c_int, [_VP, _I64, _VP, _VP, _I64, C.POINTER(Spec), _VP, _VP, _VP, _VP, _VP]),
+    "gc_incr_insert_list": (C.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _VP, C.POINTER(Stats)]),
     "gc_finish_phase": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _I64, C.POINTER(Stats),
                                   _VP, _SZ, _VP]),
     "gc_label_finalization": (C.c_int, [_VP, _I64, _VP, _SZ, _VP]),

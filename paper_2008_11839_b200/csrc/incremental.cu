@@ -330,6 +330,32 @@ int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len
   });
 }
 
+int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, int32_t* out_u,
+                        int32_t* out_v, unsigned long long* out_count, gc_stats* stats) {
+  return guarded([&] {
+    require(h && len >= 0 && out_u && out_v && out_count, GC_ERR_ARG, "bad arguments");
+    require(h->uf && h->spec.splice != GC_SPLICE_ATOMIC, GC_ERR_CONFIG,
+            "recording merging edges needs a root-based union-find rule");
+    if (len == 0) return;
+    cudaStream_t st = h->st;
+    GC_CUDA(cudaEventRecord(h->ev[0], st));
+    (k_incr_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap)),
+     ::gc::count_launch());
+    GC_CHECK_LAUNCH();
+    CooUnionArgs a = uf_args(h, us, vs, len, nullptr);
+    a.lu = out_u;
+    a.lv = out_v;
+    a.lcount = out_count;
+    launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
+    GC_CUDA(cudaEventRecord(h->ev[1], st));
+    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    if (stats) {
+      stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
+      stats->insp_finish += len;
+    }
+  });
+}
+
 int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, uint8_t* bits_out,
                   gc_stats* stats) {
   return guarded([&] {

@@ -139,6 +139,9 @@ struct CooUnionArgs {
   const int32_t* vs;
   int64_t k;
   const uint8_t* skip;   // optional: entries with skip[i] != 0 are not unions (queries)
+  int32_t* lu = nullptr;  // optional: compact list of the edges that merged two trees
+  int32_t* lv = nullptr;
+  unsigned long long* lcount = nullptr;
 };
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st);
 

@@ -497,7 +497,7 @@ int gc_static_cc(const gc_csr* g, const gc_spec* spec, int32_t* labels_out, int3
 }
 
 int gc_spanning_forest(const gc_csr* g, const gc_spec* spec, int32_t* fu, int32_t* fv,
-                       gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+                       int32_t* parent_out, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
   return guarded([&] {
     require(spec != nullptr, GC_ERR_ARG, "null spec");
     require(fu != nullptr && fv != nullptr, GC_ERR_ARG, "null forest arrays");
@@ -507,10 +507,10 @@ int gc_spanning_forest(const gc_csr* g, const gc_spec* spec, int32_t* fu, int32_
         : spec->finish == GC_FINISH_LT ? spec->lt_update == GC_LT_UPDATE_ROOTS
                                        : false;
     require(root_based, GC_ERR_CONFIG, "spanning forest needs a root-based finish");
-    // the labels buffer lives in the workspace tail for the forest driver
-    Arena a(ws, ws_bytes);
+    // the parent buffer is the caller's, or lives in the workspace head
     const int64_t n = g ? g->n : 0;
-    int32_t* labels = a.take<int32_t>(n);
+    Arena a(ws, ws_bytes);
+    int32_t* labels = parent_out ? parent_out : a.take<int32_t>(n);
     run_static(g, spec, labels, nullptr, 0, fu, fv, stats, static_cast<char*>(ws) + a.used,
                ws_bytes - a.used, stream);
   });
@@ -595,6 +595,36 @@ int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us, const int32_t*
     a.k = k;
     a.skip = nullptr;
     launch_union_coo(c, fu != nullptr, a, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us, const int32_t* vs, int64_t k,
+                        const gc_spec* spec, int32_t* aux, int32_t* out_u, int32_t* out_v,
+                        unsigned long long* out_count, void* stream) {
+  return guarded([&] {
+    require(spec != nullptr && out_u && out_v && out_count, GC_ERR_ARG, "null argument");
+    require(is_union_finish(spec->finish), GC_ERR_CONFIG, "union_edges needs a union-find rule");
+    UFConfig c = finish_cfg(*spec);
+    require(valid_uf(c), GC_ERR_CONFIG, "unsupported union-find combination");
+    require(c.splice != GC_SPLICE_ATOMIC, GC_ERR_CONFIG,
+            "atomic splice is not root-based: merging edges cannot be recorded");
+    require(c.unite != GC_FINISH_JTB || spec->jtb_ranks, GC_ERR_ARG, "JTB needs ranks");
+    require((c.unite != GC_FINISH_HOOKS && c.unite != GC_FINISH_REM_LOCK) || aux, GC_ERR_ARG,
+            "hooks / rem_lock need aux scratch");
+    CooUnionArgs a{};
+    a.P = parent;
+    a.H = c.unite == GC_FINISH_HOOKS ? aux : nullptr;
+    a.L = c.unite == GC_FINISH_REM_LOCK ? aux : nullptr;
+    a.R = spec->jtb_ranks;
+    a.n = int32_t(n);
+    a.us = us;
+    a.vs = vs;
+    a.k = k;
+    a.skip = nullptr;
+    a.lu = out_u;
+    a.lv = out_v;
+    a.lcount = out_count;
+    launch_union_coo(c, false, a, static_cast<cudaStream_t>(stream));
   });
 }
 

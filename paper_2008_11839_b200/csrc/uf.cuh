@@ -26,13 +26,23 @@ struct UFState {
   int32_t* fu;          // forest slot u (nullable)
   int32_t* fv;          // forest slot v
   int32_t n;
+  int32_t* lu = nullptr;  // optional compact list of merging edges (distributed exchange)
+  int32_t* lv = nullptr;
+  unsigned long long* lcount = nullptr;
 };
 
 template <bool FOREST>
 __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u, int32_t v) {
   if constexpr (FOREST) {
-    s.fu[slot] = u;
-    s.fv[slot] = v;
+    if (s.fu) {
+      s.fu[slot] = u;
+      s.fv[slot] = v;
+    }
+    if (s.lu) {
+      const unsigned long long i = atomicAdd(s.lcount, 1ull);
+      s.lu[i] = u;
+      s.lv[i] = v;
+    }
   }
 }
 

@@ -172,7 +172,7 @@ struct CooLaunch {
   template <class R>
   void go() const {
     if (a.k <= 0) return;
-    UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n};
+    UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
@@ -263,7 +263,7 @@ void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, 
 }
 
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st) {
-  dispatch(cfg, forest, CooLaunch{a, st});
+  dispatch(cfg, forest || a.lu != nullptr, CooLaunch{a, st});
 }
 
 void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t* is_query,

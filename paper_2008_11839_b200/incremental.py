@@ -78,6 +78,20 @@ class IncrementalConnectivity:
         N.check(N.lib().gc_incr_insert(self._h, us.data_ptr() if n else None,
                                        vs.data_ptr() if n else None, n, C.byref(self.stats)))
 
+    def insert_list(self, us, vs):
+        """Insert-only batch that also returns the edges that merged two trees
+        (the exchange unit of the sharded driver; root-based rules only)."""
+        torch = _torch()
+        n = int(us.numel())
+        ou = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        ov = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        if n:
+            N.check(N.lib().gc_incr_insert_list(self._h, us.data_ptr(), vs.data_ptr(), n, ou.data_ptr(),
+                                                ov.data_ptr(), cnt.data_ptr(), C.byref(self.stats)))
+        c = int(cnt.item())
+        return ou[:c], ov[:c]
+
     def query(self, us, vs):
         """Query-only batch; returns a uint8 CUDA tensor of connected bits."""
         torch = _torch()

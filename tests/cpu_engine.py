@@ -1,0 +1,96 @@
+"""CPU stand-in for distributed.GpuEngine — test infrastructure only.
+
+Lets the -m "not gpu" suite drive the sharded drivers' collective logic
+(gloo, world size 2-3) with a plain union-find that follows the same rules
+as the GPU engine: larger root under smaller, each undirected edge of a row
+shard processed only as (u, t) with t < u, merging edges recorded."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def _find(p, x):
+    r = x
+    while p[r] != r:
+        r = p[r]
+    while p[x] != r:
+        p[x], x = r, p[x]
+    return r
+
+
+def _union(p, u, v):
+    a, b = _find(p, u), _find(p, v)
+    if a == b:
+        return False
+    if a < b:
+        a, b = b, a
+    p[a] = b
+    return True
+
+
+class CpuEngine:
+    device = "cpu"
+
+    def local_forest(self, shard, spec):
+        n = shard.n
+        p = np.arange(n, dtype=np.int64)
+        off, tgt = shard.offsets, shard.targets
+        fu, fv = [], []
+        for u in range(n):
+            for j in range(off[u], off[u + 1]):
+                t = int(tgt[j])
+                if t < u and _union(p, u, t):
+                    fu.append(u)
+                    fv.append(t)
+        return (torch.from_numpy(p.astype(np.int32)), torch.tensor(fu, dtype=torch.int32),
+                torch.tensor(fv, dtype=torch.int32))
+
+    def union_list(self, parent, us, vs, spec):
+        p = parent.numpy().astype(np.int64)
+        mu, mv = [], []
+        for u, v in zip(us.tolist(), vs.tolist()):
+            if _union(p, u, v):
+                mu.append(u)
+                mv.append(v)
+        parent.copy_(torch.from_numpy(p.astype(np.int32)))
+        return torch.tensor(mu, dtype=torch.int32), torch.tensor(mv, dtype=torch.int32)
+
+    def finalize(self, parent):
+        p = parent.numpy().astype(np.int64)
+        return torch.from_numpy(np.array([_find(p, v) for v in range(len(p))], dtype=np.int32))
+
+    # incremental: parent with sentinel `cap` for uninitialised slots
+    def incr_create(self, spec, cap):
+        return {"p": np.full(cap, cap, dtype=np.int64), "cap": cap}
+
+    def _init(self, h, x):
+        if h["p"][x] == h["cap"]:
+            h["p"][x] = x
+
+    def incr_insert_list(self, h, us, vs):
+        mu, mv = [], []
+        for u, v in zip(us.tolist(), vs.tolist()):
+            self._init(h, u)
+            self._init(h, v)
+            if _union(h["p"], u, v):
+                mu.append(u)
+                mv.append(v)
+        return torch.tensor(mu, dtype=torch.int32), torch.tensor(mv, dtype=torch.int32)
+
+    def incr_insert(self, h, us, vs):
+        self.incr_insert_list(h, us, vs)
+
+    def incr_query(self, h, us, vs):
+        p, cap = h["p"], h["cap"]
+
+        def root(x):
+            return x if p[x] == cap else _find(p, x)
+        return torch.tensor([int(root(u) == root(v)) for u, v in zip(us.tolist(), vs.tolist())], dtype=torch.uint8)
+
+    def incr_labels(self, h):
+        p, cap = h["p"], h["cap"]
+        inited = p != cap
+        lab = np.array([_find(p, v) if inited[v] else v for v in range(cap)], dtype=np.int32)
+        comps = int(sum(1 for v in range(cap) if inited[v] and lab[v] == v))
+        return torch.from_numpy(lab), comps

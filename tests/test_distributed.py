@@ -1,0 +1,153 @@
+"""Multi-process (gloo, world size 2 and 3) tests of the sharded drivers'
+host logic — sharding, tree-wise forest merge, per-batch exchange — with a
+CPU engine standing in for libgconn, checked against the C oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from golden_data import Golden
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _forest_worker(rank, world, port, names, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_engine import CpuEngine
+        from paper_2008_11839_b200 import Graph, parse_spec
+        from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_spanning_forest
+        gold = Golden()
+        out = {}
+        for name in names:
+            n, off, tgt, orc = gold.graphs[name]
+            g = Graph(n, off, tgt)
+            lo, hi = shard_bounds(off, world)[rank]
+            res = sharded_spanning_forest(shard_graph(g, lo, hi), parse_spec("none+async+halve"),
+                                          engine=CpuEngine())
+            out[name] = (res.labels.numpy().astype(np.int64), res.forest_u.numpy(), res.forest_v.numpy(),
+                         res.components)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(fn, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port) + args + (q,)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    import queue as _q
+    import time as _t
+    deadline = _t.time() + 240
+    while len(res) < world:
+        try:
+            r, v = q.get(timeout=2)
+            res[r] = v
+        except _q.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs) or _t.time() > deadline:
+                for p in procs:
+                    p.kill()
+                raise AssertionError("a rank failed: " + str([p.exitcode for p in procs]))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_forest_and_labels(world):
+    gold = Golden()
+    names = ["rmat_s10_ef8", "comps_30", "two_comp", "star_150", "rand120_400", "edgeless4", "grid_12x12"]
+    res = _run(_forest_worker, world, names)
+    for name in names:
+        n, off, tgt, orc = gold.graphs[name]
+        comps = len(np.unique(orc)) if n else 0
+        for rank in range(world):
+            labels, fu, fv, c = res[rank][name]
+            assert np.array_equal(labels, orc), (name, rank)
+            assert c == comps
+            slot_u = np.full(n, -1, np.int32)
+            slot_v = np.full(n, -1, np.int32)
+            # forest edges as slots: any injective placement works for the clauses
+            slot_u[:len(fu)] = fu
+            slot_v[:len(fv)] = fv
+            rep = oracle.check_forest(n, off, tgt, slot_u, slot_v, orc)
+            assert rep["passed"], (name, rank, rep)
+            assert len(fu) == n - comps
+
+
+def test_shard_bounds_balance():
+    from paper_2008_11839_b200.distributed import shard_bounds
+    gold = Golden()
+    n, off, tgt, _ = gold.graphs["rmat_s10_ef8"]
+    for world in (1, 2, 4, 8):
+        b = shard_bounds(off, world)
+        assert b[0][0] == 0 and b[-1][1] == n
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+        sizes = [off[hi] - off[lo] for lo, hi in b]
+        assert max(sizes) - min(sizes) <= max(np.diff(off)) + len(tgt) // world // 4 + 1
+
+
+def _incr_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_engine import CpuEngine
+        from paper_2008_11839_b200 import parse_spec
+        from paper_2008_11839_b200.distributed import ShardedIncremental
+        rng = np.random.default_rng(7)
+        cap = 200
+        inc = ShardedIncremental(parse_spec("none+async+halve"), cap, engine=CpuEngine())
+        bits_all = []
+        for b in range(12):
+            us = torch.from_numpy(rng.integers(0, cap, 25).astype(np.int32))
+            vs = torch.from_numpy(rng.integers(0, cap, 25).astype(np.int32))
+            qu = torch.from_numpy(rng.integers(0, cap, 30).astype(np.int32))
+            qv = torch.from_numpy(rng.integers(0, cap, 30).astype(np.int32))
+            inc.insert(us, vs)
+            bits_all.append(inc.query(qu, qv).numpy().astype(bool))
+        lab, comps = inc.labels()
+        q.put((rank, (bits_all, lab.numpy().astype(np.int64), comps, inc.exchanged)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_incremental(world):
+    res = _run(_incr_worker, world)
+    rng = np.random.default_rng(7)
+    cap = 200
+    us_all, vs_all, isq_all = [], [], []
+    for b in range(12):
+        us = rng.integers(0, cap, 25); vs = rng.integers(0, cap, 25)
+        qu = rng.integers(0, cap, 30); qv = rng.integers(0, cap, 30)
+        us_all += [us, qu]; vs_all += [vs, qv]
+        isq_all += [np.zeros(25, np.uint8), np.ones(30, np.uint8)]
+    us = np.concatenate(us_all); vs = np.concatenate(vs_all); isq = np.concatenate(isq_all)
+    bits, lab = oracle.incremental_replay(cap, us, vs, isq, 55)
+    exp_bits = [bits[b * 55 + 25:(b + 1) * 55] for b in range(12)]
+    inited = np.zeros(cap, bool)
+    inited[us[isq == 0]] = True
+    inited[vs[isq == 0]] = True
+    for rank in range(world):
+        got_bits, got_lab, comps, exch = res[rank]
+        for b in range(12):
+            assert got_bits[b].tolist() == exp_bits[b].tolist(), (rank, b)
+        assert np.array_equal(got_lab, lab)
+        assert comps == int(sum(1 for v in range(cap) if inited[v] and lab[v] == v))

@@ -1,0 +1,112 @@
+"""The sharded drivers on the GPU engine (libgconn).  One GPU is visible, so
+(1) the P-rank tree merge is replayed in-process shard by shard, and (2) two
+real ranks share cuda:0 over gloo (collectives staged through host memory)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from golden_data import Golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _merge_in_process(g, spec, world):
+    from paper_2008_11839_b200.distributed import GpuEngine, shard_bounds, shard_graph
+    eng = GpuEngine()
+    states = []
+    for lo, hi in shard_bounds(g.offsets, world):
+        states.append(list(eng.local_forest(shard_graph(g, lo, hi), spec)))
+    step = 1
+    while step < world:
+        for r in range(0, world, 2 * step):
+            if r + step < world:
+                parent, fu, fv = states[r]
+                _, ou, ov = states[r + step]
+                mu, mv = eng.union_list(parent, ou, ov, spec)
+                states[r] = [parent, torch.cat([fu, mu]), torch.cat([fv, mv])]
+        step *= 2
+    parent, fu, fv = states[0]
+    return eng.finalize(parent), fu, fv
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_tree_merge_on_gpu(world):
+    from paper_2008_11839_b200 import Graph, build_csr, gen_rmat, parse_spec
+    gold = Golden()
+    graphs = [(name,) + gold.graphs[name] for name in ["rmat_s10_ef8", "comps_30", "two_comp", "grid_12x12"]]
+    g16 = build_csr(gen_rmat(16, 8, seed=1, device=True))
+    o16, _ = oracle.components(g16.n, g16.offsets, g16.targets)
+    graphs.append(("rmat_s16", g16.n, g16.offsets, g16.targets, o16))
+    for spec_text in ["none+async+halve", "none+rem_cas+split+halve", "none+hooks+compress", "none+jtb+naive"]:
+        spec = parse_spec(spec_text)
+        for name, n, off, tgt, orc in graphs:
+            labels, fu, fv = _merge_in_process(Graph(n, off, tgt), spec, world)
+            lab = labels.cpu().numpy().astype(np.int64)
+            from paper_2008_11839_b200 import label_finalization
+            assert np.array_equal(label_finalization(lab), orc), (name, spec_text, world)
+            su = np.full(n, -1, np.int32); sv = np.full(n, -1, np.int32)
+            su[:fu.numel()] = fu.cpu().numpy(); sv[:fv.numel()] = fv.cpu().numpy()
+            rep = oracle.check_forest(n, off, tgt, su, sv, orc)
+            assert rep["passed"], (name, spec_text, world, rep)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _two_rank_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec
+        from paper_2008_11839_b200.distributed import ShardedIncremental, shard_bounds, shard_graph, \
+            sharded_spanning_forest
+        g = build_csr(gen_rmat(14, 8, seed=3, device=True))
+        lo, hi = shard_bounds(g.offsets, world)[rank]
+        res = sharded_spanning_forest(shard_graph(g.cuda(), lo, hi), parse_spec("none+async+halve"))
+        # incremental: the graph's edges in 8 batches, then queries
+        ue = g.undirected_edges()
+        inc = ShardedIncremental(parse_spec("none+async+halve"), g.n)
+        for part in np.array_split(np.arange(len(ue)), 8):
+            inc.insert(torch.from_numpy(ue[part, 0].astype(np.int32)).cuda(),
+                       torch.from_numpy(ue[part, 1].astype(np.int32)).cuda())
+        lab, comps = inc.labels()
+        q.put((rank, (res.labels.cpu().numpy(), res.forest_u.cpu().numpy(), res.forest_v.cpu().numpy(),
+                      lab.cpu().numpy(), comps)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_share_one_gpu():
+    import torch.multiprocessing as mp
+    from paper_2008_11839_b200 import build_csr, gen_rmat
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    g = build_csr(gen_rmat(14, 8, seed=3, device=True))
+    orc, comps = oracle.components(g.n, g.offsets, g.targets)
+    iso = int((np.diff(g.offsets) == 0).sum())
+    for r in range(2):
+        labels, fu, fv, ilab, icomps = res[r]
+        assert np.array_equal(labels.astype(np.int64), orc)
+        su = np.full(g.n, -1, np.int32); sv = np.full(g.n, -1, np.int32)
+        su[:len(fu)] = fu; sv[:len(fv)] = fv
+        assert oracle.check_forest(g.n, g.offsets, g.targets, su, sv, orc)["passed"]
+        assert np.array_equal(ilab.astype(np.int64), orc)
+        assert icomps == comps - iso
