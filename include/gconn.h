@@ -187,6 +187,25 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
                         int32_t* aux, int32_t* out_u, int32_t* out_v,
                         unsigned long long* out_count, void* stream);
 
+/* ---- DisjointSets probes and validation (dset.py:381-399,
+ *      validate.py:178-259) -------------------------------------------------
+ * gc_find_batch: roots_out[i] = find(xs[i]) with the given gc_find_kind,
+ * applying its compaction writes to parent (DisjointSets.find_root); xs ==
+ * NULL means xs[i] = i (k <= n).  GC_FIND_NAIVE is the read-only probe of
+ * same_set / labels_array. */
+int gc_find_batch(int32_t* parent, int64_t n, const int32_t* xs, int64_t k,
+                  int32_t find_kind, int32_t* roots_out, void* stream);
+/* canonical_labels (validate.py:251-259) in place: each label value becomes
+ * the minimum index carrying it.  Values must lie in [0, n); ws needs
+ * 4*n + 512 bytes. */
+int gc_canonical_labels(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
+                        void* stream);
+/* check_forest clause (a) (validate.py:200-206): *first_missing (device)
+ * receives the smallest i whose (us[i], vs[i]) is not in the CSR, or
+ * UINT64_MAX when every edge exists. */
+int gc_edges_exist(const gc_csr* g, const int32_t* us, const int32_t* vs,
+                   int64_t k, unsigned long long* first_missing, void* stream);
+
 /* ---- incremental (driver.py:567-725) -------------------------------------*/
 typedef struct gc_incr gc_incr;
 /* capacity = number of vertex slots; sentinel = capacity (driver.py:603). */

@@ -68,6 +68,13 @@ __device__ __forceinline__ int64_t ld_stream64(const int64_t* p, uint64_t pol) {
   return v;
 }
 
+// L1-allocating read-only load with an L2 evict-first hint
+__device__ __forceinline__ int32_t ld_l1_evict_first(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ int64_t ldg64(const int64_t* p) { return __ldg(p); }
 __device__ __forceinline__ int32_t ldg32(const int32_t* p) { return __ldg(p); }
 

@@ -53,9 +53,12 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     }
     const bool big = take > kSmall;
     if (!big) {
-      int32_t j = 0;
-      for (; j < take; ++j) {
-        const int32_t t = ldg32(tgt + b + j);
+      // the first two targets are fetched together (one DRAM round trip for
+      // k-out's default k = 2); later ones on demand
+      const int32_t f0 = take > 0 ? ldg32(tgt + b) : 0;
+      const int32_t f1 = take > 1 ? ldg32(tgt + b + 1) : 0;
+      for (int32_t j = 0; j < take; ++j) {
+        const int32_t t = j == 0 ? f0 : j == 1 ? f1 : ldg32(tgt + b + j);
         if (lower_only && t >= u) break;
         R::unite(s, u, t);
       }

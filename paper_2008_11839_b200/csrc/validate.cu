@@ -1,0 +1,114 @@
+// validate.cu — device routes behind the reference's DisjointSets probes
+// (dset.py:381-399) and its validation helpers (validate.py:178-259): batched
+// finds with the configured compaction, canonical min-member relabelling of
+// an arbitrary labelling, and the "every recorded edge exists" clause of
+// check_forest.  None of these are on the timed path; they make the
+// drop-in API complete at BASELINE sizes, where the reference's per-edge
+// Python loops take minutes.
+#include <climits>
+
+#include "internal.h"
+#include "pipeline.cuh"
+#include "uf.cuh"
+
+namespace gc {
+
+namespace {
+
+template <int FIND>
+__global__ void k_find_batch(int32_t* P, const int32_t* __restrict__ xs, int64_t k, int32_t* roots) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
+    Reader rd;
+    roots[i] = find<FIND>(xs ? ldg32(xs + i) : int32_t(i), P, rd);
+  }
+}
+
+// (u, v) present in row u of the sorted CSR?  Records the smallest failing
+// index (the witness of validate.py:200-206 is the first missing edge).
+__global__ void k_edges_exist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int64_t n,
+                              const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
+                              unsigned long long* first_missing) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
+    const int32_t u = us[i], v = vs[i];
+    bool ok = u >= 0 && u < n && v >= 0 && v < n;
+    if (ok) {
+      int64_t lo = off[u], hi = off[u + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (tgt[mid] < v) lo = mid + 1;
+        else hi = mid;
+      }
+      ok = lo < off[u + 1] && tgt[lo] == v;
+    }
+    if (!ok) atomicMin(first_missing, static_cast<unsigned long long>(i));
+  }
+}
+
+__global__ void k_set_noncanon(unsigned long long* ctr) { ctr[C_NONCANON] = 1; }
+
+}  // namespace
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+int gc_find_batch(int32_t* parent, int64_t n, const int32_t* xs, int64_t k, int32_t find_kind,
+                  int32_t* roots_out, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && n < (int64_t(1) << 31) && k >= 0, GC_ERR_ARG, "bad size");
+    require(parent != nullptr || n == 0, GC_ERR_ARG, "null parent");
+    require(roots_out != nullptr || k == 0, GC_ERR_ARG, "null output");
+    require(xs != nullptr || k <= n, GC_ERR_ARG, "k > n without a query list");
+    if (k == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int g = grid_for(k, kEwBlock, 8);
+    switch (find_kind) {
+      case GC_FIND_NAIVE: (k_find_batch<GC_FIND_NAIVE><<<g, kEwBlock, 0, st>>>(parent, xs, k, roots_out), count_launch()); break;
+      case GC_FIND_SPLIT: (k_find_batch<GC_FIND_SPLIT><<<g, kEwBlock, 0, st>>>(parent, xs, k, roots_out), count_launch()); break;
+      case GC_FIND_HALVE: (k_find_batch<GC_FIND_HALVE><<<g, kEwBlock, 0, st>>>(parent, xs, k, roots_out), count_launch()); break;
+      case GC_FIND_COMPRESS: (k_find_batch<GC_FIND_COMPRESS><<<g, kEwBlock, 0, st>>>(parent, xs, k, roots_out), count_launch()); break;
+      case GC_FIND_TWO_TRY: (k_find_batch<GC_FIND_TWO_TRY><<<g, kEwBlock, 0, st>>>(parent, xs, k, roots_out), count_launch()); break;
+      default: throw Error(GC_ERR_CONFIG, "unknown find rule");
+    }
+    GC_CHECK_LAUNCH();
+  });
+}
+
+int gc_canonical_labels(int32_t* labels, int64_t n, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && n < (int64_t(1) << 31), GC_ERR_MALFORMED, "bad length");
+    if (n == 0) return;
+    require(labels != nullptr, GC_ERR_ARG, "null labels");
+    Arena a(ws, ws_bytes);
+    unsigned long long* ctr = a.take<unsigned long long>(C_COUNT_);
+    int32_t* mins = a.take<int32_t>(n);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int g = grid_for(n, kEwBlock, 8);
+    const int32_t nn = int32_t(n);
+    (k_set_noncanon<<<1, 1, 0, st>>>(ctr), count_launch());
+    (k_canon_init<<<g, kEwBlock, 0, st>>>(mins, nn, ctr), count_launch());
+    (k_canon_min<<<g, kEwBlock, 0, st>>>(labels, mins, nn, ctr), count_launch());
+    (k_canon_apply<<<g, kEwBlock, 0, st>>>(labels, mins, nn, ctr), count_launch());
+    GC_CHECK_LAUNCH();
+  });
+}
+
+int gc_edges_exist(const gc_csr* g, const int32_t* us, const int32_t* vs, int64_t k,
+                   unsigned long long* first_missing, void* stream) {
+  return guarded([&] {
+    require(g != nullptr && first_missing != nullptr, GC_ERR_ARG, "null argument");
+    require(k >= 0, GC_ERR_ARG, "negative count");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GC_CUDA(cudaMemsetAsync(first_missing, 0xff, sizeof(unsigned long long), st));
+    if (k == 0) return;
+    (k_edges_exist<<<grid_for(k, kEwBlock, 8), kEwBlock, 0, st>>>(g->offsets, g->targets, g->n, us, vs, k,
+                                                                 first_missing), count_launch());
+    GC_CHECK_LAUNCH();
+  });
+}
+
+}  // extern "C"

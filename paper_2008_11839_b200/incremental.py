@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .api import LoweredSpec, RunStats, _require_cuda, _stream
+from .api import LoweredSpec, RunStats, _require_cuda, _stream, host_int64
 from .errors import ConfigError
 from .graph import Graph
 from .spec import AlgorithmSpec, FinishKind, SpliceOp, format_spec
@@ -164,11 +164,11 @@ def incremental(init, spec: AlgorithmSpec, batches, workers=1, capacity=None, ra
         else:
             results.append(np.zeros(0, dtype=bool))
         if on_batch is not None:
-            on_batch(bi, inc.state().cpu().numpy().astype(np.int64))
+            on_batch(bi, host_int64(inc.state()))
     labels, comps = inc.labels()
     st = inc.stats
     stats.phase_times = {"insert": st.t_sample_ms / 1e3, "query": st.t_finish_ms / 1e3}
     stats.edge_inspections = {"insert": int(st.insp_finish)} if st.insp_finish else {}
     stats.rounds = int(st.rounds)
     stats.component_count = comps
-    return labels.cpu().numpy().astype(np.int64), results, stats
+    return host_int64(labels), results, stats

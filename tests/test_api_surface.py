@@ -1,0 +1,145 @@
+"""The rest of the reference's public API (connlab/__init__.py:12-82):
+DisjointSets + union_edge_list, validate.py helpers, graph files and the
+small generators — checked against fixtures produced by the reference
+(tests/golden/make_golden_api.py)."""
+import json
+
+import numpy as np
+import pytest
+
+from golden_data import G, h
+from paper_2008_11839_b200 import (DisjointSets, EdgeList, FindOp, ForestEdges, Graph, MalformedInputError,
+                                   SpliceOp, UnionConfig, UnionOp, all_valid_configs, canonical_labels,
+                                   check_forest, gen_ba, is_binary_graph, load_edge_list, partition_equal,
+                                   sampling_stats, save_edge_list, union_edge_list)
+
+API = json.loads((G / "api.json").read_text())
+
+
+# ----------------------------------------------------------------- CPU side
+
+def test_gen_ba_matches_reference():
+    for key, want in API["gen_ba"].items():
+        n, att, seed = (int(x) for x in key.split(","))
+        el = gen_ba(n, att, seed=seed)
+        assert el.n == want["n"] and len(el) == want["k"] and h(el.edges) == want["hash"], key
+        assert (el.edges[:, 1] < el.edges[:, 0]).all()
+
+
+def test_text_edge_list_roundtrip_and_errors(tmp_path):
+    p = tmp_path / "tiny.txt"
+    p.write_text("# n 4\n% another comment\n0 2\n3 1\n")
+    el = load_edge_list(p)
+    assert el.n == 4 and el.edges.tolist() == [[0, 2], [3, 1]]
+    q = tmp_path / "rt.txt"
+    save_edge_list(EdgeList(7, np.array([[1, 2], [6, 0]])), q)
+    back = load_edge_list(q)
+    assert back.n == 7 and back.edges.tolist() == [[1, 2], [6, 0]]
+    assert not is_binary_graph(q)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("# n 4\n0 2\nnot-an-edge\n")
+    with pytest.raises(MalformedInputError, match=":3:"):
+        load_edge_list(bad)
+    bad.write_text("0 1 2\n")
+    with pytest.raises(MalformedInputError, match="expected 'u v'"):
+        load_edge_list(bad)
+
+
+def test_census_helpers_match_reference():
+    from paper_2008_11839_b200 import build_csr  # noqa: F401  (GPU not needed below)
+    assert partition_equal([0, 0, 2, 3], [5, 5, 1, 0])
+    assert not partition_equal([0, 0, 2, 3], [5, 5, 5, 0])
+    assert canonical_labels([3, 3, 1, 1, 3]).tolist() == [0, 0, 2, 2, 0]
+    # census golden (test_validate.py:106-110): path-4, labels [0,0,2,3]
+    g = Graph(4, np.array([0, 1, 3, 5, 6]), np.array([1, 0, 2, 1, 3, 2]))
+    cov, ic = sampling_stats(g, [0, 0, 2, 3])
+    assert cov == 0.5 and ic == pytest.approx(4 / 6)
+
+
+def test_sampling_stats_cases():
+    # the fixture graph is gen_ba(300, 2, seed=3) symmetrised by the reference
+    el = gen_ba(300, 2, seed=3)
+    e = el.edges
+    u = np.concatenate([e[:, 0], e[:, 1]])
+    v = np.concatenate([e[:, 1], e[:, 0]])
+    order = np.lexsort((v, u))
+    u, v = u[order], v[order]
+    keep = np.ones(len(u), bool)
+    keep[1:] = (u[1:] != u[:-1]) | (v[1:] != v[:-1])
+    u, v = u[keep], v[keep]
+    off = np.zeros(301, np.int64)
+    np.add.at(off, u + 1, 1)
+    g = Graph(300, np.cumsum(off), v)
+    for case in API["sampling_stats"]["cases"]:
+        cov, ic = sampling_stats(g, case["labels"])
+        assert cov == case["cov"] and ic == case["ic"]
+
+
+# ----------------------------------------------------------------- GPU side
+
+@pytest.mark.gpu
+def test_find_traces_every_rule():
+    for f in FindOp:
+        union = UnionOp.JTB if f is FindOp.TWO_TRY else UnionOp.ASYNC
+        ds = DisjointSets(4, UnionConfig(union, f, SpliceOp.NONE))
+        import torch
+        ds.p.copy_(torch.tensor([0, 0, 1, 2], dtype=torch.int32))
+        want = API["find_traces"][f.value]
+        assert ds.find_root(3) == want["root"], f
+        assert ds.p.cpu().tolist() == want["p"], f
+
+
+@pytest.mark.gpu
+def test_disjoint_sets_every_config():
+    edges = np.array(API["ds_edges"], dtype=np.int64)
+    for cfg in all_valid_configs():
+        ds = DisjointSets(200, cfg)
+        union_edge_list(ds, edges[:, 0], edges[:, 1], workers=4)
+        lab = ds.labels_array()
+        assert h(canonical_labels(lab)) == API["ds_labels"], cfg
+        assert ds.same_set(int(edges[0, 0]), int(edges[0, 1]))
+
+
+@pytest.mark.gpu
+def test_disjoint_sets_single_unions_and_forest():
+    cfg = UnionConfig(UnionOp.REM_CAS, FindOp.HALVE, SpliceOp.SPLIT_ONE)
+    forest = [None] * 6
+    ds = DisjointSets(6, cfg, forest=forest)
+    assert ds.union(1, 2) is True
+    assert ds.union(2, 1) is False
+    assert ds.union(4, 5) is True
+    assert ds.union(5, 1) is True
+    assert not ds.same_set(0, 1) and ds.same_set(4, 2)
+    assert sum(e is not None for e in forest) == 3
+    assert ds.labels_array().tolist() == [0, 1, 1, 3, 1, 1]
+
+
+@pytest.mark.gpu
+def test_check_forest_reports_match_reference():
+    for gname, cases in API["check_forest"].items():
+        gd = cases["graph"]
+        g = Graph(gd["n"], np.array(gd["off"]), np.array(gd["tgt"]))
+        for cname, case in cases.items():
+            if cname == "graph":
+                continue
+            edges = [tuple(e) if e is not None else None for e in case["edges"]]
+            rep = json.loads(json.dumps(check_forest(g, ForestEdges(edges), np.array(gd["oracle"]))))
+            assert rep == case["report"], (gname, cname, rep)
+
+
+@pytest.mark.gpu
+def test_binary_graph_roundtrip(tmp_path):
+    from paper_2008_11839_b200 import gen_rmat, build_csr, load_graph, load_graph_binary, save_graph_binary
+    g = build_csr(gen_rmat(12, 8, seed=3))
+    p = tmp_path / "g.gcn1"
+    save_graph_binary(g, p)
+    assert is_binary_graph(p)
+    for dev in (False, True):
+        g2 = load_graph(p, device=dev)
+        assert g2.n == g.n and np.array_equal(g2.offsets, g.offsets) and np.array_equal(g2.targets, g.targets)
+    g3 = load_graph_binary(p, device=True)
+    off, tgt = g3.device_arrays()
+    assert np.array_equal(off.cpu().numpy(), g.offsets) and np.array_equal(tgt.cpu().numpy(), g.targets)
+    p.write_bytes(p.read_bytes()[:-3])
+    with pytest.raises(MalformedInputError, match="truncated"):
+        load_graph_binary(p)
