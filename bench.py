@@ -10,9 +10,10 @@ reference's throughput definition (bench.py:167).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank runs its own replica of the
-workload (weak scaling, no collective on the data path); value = all ranks'
-edges / max-over-ranks time.
+N > 1 (torchrun, one rank per GPU): the edge-sharded two-phase pipeline on
+an RMAT graph of scale 24 + log2(N) (weak scaling: each rank owns about one
+scale-24 graph's edges), merged with all-gathers over NCCL; value = the
+graph's undirected edges / max-over-ranks step time (see run_sharded).
 
 --impl reference times the reference algorithm's CPU restatement (oracle/,
 a C port of connlab's _pipeline with OpenMP on all host threads) on the same
@@ -163,6 +164,102 @@ def make_graph(scale: int, ef: int, seed: int):
     g = build_csr(el, keep_host=False)
     del el
     return g
+
+
+def run_sharded(args):
+    """N > 1: the edge-sharded two-phase pipeline on one graph.
+
+    Weak scaling: the RMAT scale grows by log2(N) so every rank owns about
+    one scale-24 graph's worth of edges.  Every rank generates the same graph
+    (deterministic stream), keeps only its edge-balanced row block, and each
+    step runs `sharded_two_phase`: local sampling over its rows, all-gather
+    of the sampled merging edges, the finish over its active rows, a second
+    all-gather, local finalisation.  The step time is CUDA events on the
+    rank's stream (host-side collective waits included), max over ranks."""
+    import math
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    backend = os.environ.get("GC_DIST_BACKEND", "nccl")
+    kw = {} if "RANK" in os.environ else {"rank": 0, "world_size": 1, "store": dist.HashStore()}
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local % ndev), **kw)
+    else:
+        dist.init_process_group(backend, **kw)
+    from paper_2008_11839_b200 import parse_spec
+    from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+
+    spec = parse_spec(SPEC)
+    scale = args.scale + int(math.ceil(math.log2(ws)))
+    g = make_graph(scale, args.edge_factor, args.seed)
+    n, m = g.n, g.m
+    lo, hi = shard_bounds(g._d_off, ws)[rank]
+    shard = shard_graph(g, lo, hi)
+    parity = None
+    res = sharded_two_phase(shard, spec)
+    if rank == 0 and not args.skip_check:
+        import oracle
+        ref, comps = oracle.components(n, g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy())
+        ok = bool(np.array_equal(res.labels.cpu().numpy().astype(np.int64), ref)) and res.components == comps
+        parity = {"labels_bit_exact": ok, "components": comps, "insp_sample": res.insp_sample,
+                  "insp_finish": res.insp_finish, "cov": res.lmax_count / n}
+        if not ok:
+            print(json.dumps({"error": "parity failure", "parity": parity}), file=sys.stderr)
+            sys.exit(3)
+    del g
+    torch.cuda.empty_cache()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        sharded_two_phase(shard, spec)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times, exchanged = [], 0
+    with ClockSampler(local % ndev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = sharded_two_phase(shard, spec)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            exchanged = r.exchanged_edges
+    torch.cuda.synchronize()
+    dist.barrier()
+    dev = "cuda" if backend == "nccl" else "cpu"
+    tmax = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms = float(tmax.item())
+    ms_per_step = total_ms / args.steps
+    value = (m / 2) * args.steps / (total_ms / 1e3)
+    peak, peak_kind = peaks()
+    step_bytes = 4 * (res.insp_sample + res.insp_finish) + 8 * (n + 1) + 4 * n * 7
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": {"workload": f"edge-sharded static CC {SPEC} on RMAT scale-{scale} ef{args.edge_factor} "
+                                       f"(avg degree 16) seed {args.seed}, {ws} row blocks",
+                           "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2,
+                           "parallelism": f"edge-sharded x{ws} ({backend}), two-phase all-gather merge",
+                           "exchanged_edges_per_step": exchanged,
+                           "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+                "e2e": None, "gpu_launches": None,
+                "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1e3) / 1e9 / ws,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / ws / peak, "traffic": None,
+                             "kernel": "whole sharded step (per-GPU share of the SURVEY 8(d) bytes)",
+                             "peak_source": peak_kind},
+                "cpu_baseline": None, "parity": parity, "clocks": clk.summary()}
+        print(json.dumps(line))
+    dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -361,6 +458,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--skip-check", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the edge-sharded path even at N=1 (used for tests)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     args = ap.parse_args()
@@ -368,6 +467,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[0] > 1 or args.sharded:
+        run_sharded(args)
     else:
         run_ours(args)
 

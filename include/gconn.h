@@ -187,6 +187,30 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
                         int32_t* aux, int32_t* out_u, int32_t* out_v,
                         unsigned long long* out_count, void* stream);
 
+/* ---- sharded two-phase pipeline (multi-GPU building blocks) ----
+ * The reference is single-process; these split `_pipeline`
+ * (driver.py:454-500) at its two exchange points so a driver can run it over
+ * edge-sharded CSR blocks (rows outside the block empty):
+ *   gc_shard_sample: parent := identity, then the sampler (none / k-out
+ *     FIRST_K / HB) over the block's rows.  Every union that merged two trees
+ *     appends its (u, v) to out_u/out_v (capacity n) and bumps *out_count
+ *     (device).  stats->insp_sample = this block's sample inspections.
+ *   -- exchange: all-gather the merging edges, union the foreign ones --
+ *   gc_shard_finish: compress, most-frequent label, active gather (identical
+ *     on every rank once the sampled partitions are merged), then the
+ *     union-find finish over the block's active rows, recording merging edges
+ *     the same way.  stats: insp_finish (block), l_max, lmax_count, n_active.
+ *   -- exchange again, union foreign edges, gc_label_finalization --
+ * Union-find finishes with root-based rules only. */
+int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent,
+                    int32_t* out_u, int32_t* out_v,
+                    unsigned long long* out_count, gc_stats* stats, void* ws,
+                    size_t ws_bytes, void* stream);
+int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent,
+                    int32_t* out_u, int32_t* out_v,
+                    unsigned long long* out_count, gc_stats* stats, void* ws,
+                    size_t ws_bytes, void* stream);
+
 /* ---- DisjointSets probes and validation (dset.py:381-399,
  *      validate.py:178-259) -------------------------------------------------
  * gc_find_batch: roots_out[i] = find(xs[i]) with the given gc_find_kind,

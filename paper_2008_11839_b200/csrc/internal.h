@@ -123,6 +123,9 @@ struct RowUnionArgs {
   int32_t take_max;
   int32_t lower_only;
   unsigned long long* insp;
+  int32_t* lu = nullptr;  // optional compact list of the edges that merged two trees
+  int32_t* lv = nullptr;
+  unsigned long long* lcount = nullptr;
 };
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st);
 

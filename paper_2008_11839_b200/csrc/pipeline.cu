@@ -332,6 +332,35 @@ __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long
   block_add<kEwBlock>(out, c);
 }
 
+// Root transitions of one phase: every v that was a root before it
+// (before == nullptr: identity) and is not one now emits (v, P[v]) — one
+// pair per merge, all inside one component, so unioning them elsewhere
+// reproduces the partition change whatever the linking rule.
+__global__ void k_root_transitions(const int32_t* P, const int32_t* before, int32_t n, int32_t* out_u,
+                                   int32_t* out_v, unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    int32_t p = 0;
+    bool moved = false;
+    if (v < n) {
+      p = P[v];
+      moved = p != int32_t(v) && (before == nullptr || before[v] == int32_t(v));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, moved);
+    if (!bal) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(count, static_cast<unsigned long long>(__popc(bal)));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (moved) {
+      const unsigned long long i = pos + __popc(bal & ((1u << lane) - 1u));
+      out_u[i] = int32_t(v);
+      out_v[i] = p;
+    }
+  }
+}
+
 namespace {
 std::atomic<long long> g_launches{0};
 }

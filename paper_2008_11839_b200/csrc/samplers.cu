@@ -56,7 +56,7 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
       g.offsets, g.targets, n, s.kout_k, s.kout_rand_offsets, w.coo_u, w.coo_v, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
   CooUnionArgs ca{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, w.coo_u, w.coo_v, int64_t(n) * s.kout_k,
-                  nullptr};
+                  nullptr, a.lu, a.lv, a.lcount};
   launch_union_coo(c, forest, ca, st);
 }
 
@@ -65,7 +65,8 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
 // first (smallest) neighbour when that is smaller — write-disjoint, no
 // atomics.  The surviving non-isolated roots form the phase-2 list.
 __global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int32_t n, int32_t* P,
-                            int32_t* fu, int32_t* fv, int32_t* roots, unsigned long long* ctr) {
+                            int32_t* fu, int32_t* fv, int32_t* roots, unsigned long long* ctr,
+                            int32_t* lu, int32_t* lv, unsigned long long* lcount) {
   unsigned long long nz = 0;
   const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -82,6 +83,11 @@ __global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int32_t n, i
           if (fu) {
             fu[v] = int32_t(v);
             fv[v] = first;
+          }
+          if (lu) {  // a phase-1 hook always merges two trees (v was a singleton root)
+            const unsigned long long i = atomicAdd(lcount, 1ull);
+            lu[i] = int32_t(v);
+            lv[i] = first;
           }
         } else {
           root = true;
@@ -105,7 +111,8 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
   if (n == 0 || g.m == 0) return;  // sampling.py:95-96
   GC_CUDA(cudaMemsetAsync(ctr + C_SCRATCH0, 0, 8, st));
   (k_hb_phase1<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, n, a.P, a.fu,
-                                                             a.fv, w.q0, ctr), ::gc::count_launch());
+                                                             a.fv, w.q0, ctr, a.lu, a.lv, a.lcount),
+   ::gc::count_launch());
   GC_CHECK_LAUNCH();
   // Phase 2 (sampling.py:110-116): union the first N edges of each root
   a.list = w.q0;

@@ -163,6 +163,9 @@ struct Pipeline {
   int32_t n;
   cudaEvent_t* kev = nullptr;  // [0,1] sampler kernel, [2,3] finish kernel
   bool timed_sample = false;
+  int32_t* lu = nullptr;  // sharded drivers: merging edges of the union kernels
+  int32_t* lv = nullptr;
+  unsigned long long* lcount = nullptr;
 
   Pipeline(const gc_csr& g_, const gc_spec& s_, int32_t* P_, int32_t* fu_, int32_t* fv_,
            void* wsp, size_t wsb, cudaStream_t st_)
@@ -183,6 +186,9 @@ struct Pipeline {
     a.n = n;
     a.off = g.offsets;
     a.tgt = g.targets;
+    a.lu = lu;
+    a.lv = lv;
+    a.lcount = lcount;
     return a;
   }
 
@@ -574,6 +580,105 @@ int gc_label_finalization(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
     GC_CUDA(cudaMemcpyAsync(&cyc, ctr + C_CYCLE, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
     require(cyc == 0, GC_ERR_MALFORMED, "label array contains a cycle");
+  });
+}
+
+// ---- sharded two-phase building blocks ------------------------
+namespace {
+
+void check_shard_spec(const gc_spec* spec) {
+  require(is_union_finish(spec->finish), GC_ERR_CONFIG, "sharded pipeline needs a union-find finish");
+  require(spec->sample == GC_SAMPLE_NONE || spec->sample == GC_SAMPLE_KOUT || spec->sample == GC_SAMPLE_HB,
+          GC_ERR_CONFIG, "sharded sampling supports none / k-out / hb");
+  require(spec->sample != GC_SAMPLE_KOUT || spec->kout_mode == GC_KOUT_FIRST_K, GC_ERR_CONFIG,
+          "sharded k-out needs FIRST_K (random offsets are drawn over the whole graph)");
+}
+
+void read_ctr(unsigned long long* dst, const unsigned long long* ctr, cudaStream_t st) {
+  GC_CUDA(cudaMemcpyAsync(dst, ctr, sizeof(unsigned long long) * C_COUNT_, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32_t* out_u, int32_t* out_v,
+                    unsigned long long* out_count, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    check_static_args(g, spec, parent);
+    check_shard_spec(spec);
+    require(out_u && out_v && out_count, GC_ERR_ARG, "null merging-edge output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    Pipeline pl(*g, *spec, parent, nullptr, nullptr, ws, ws_bytes, st);
+    const bool edges = spec->splice != GC_SPLICE_ATOMIC;  // root-based: record real merging edges
+    if (edges) {
+      pl.lu = out_u;
+      pl.lv = out_v;
+      pl.lcount = out_count;
+    }
+    const UFConfig sc = sampler_cfg(*spec);
+    pl.init_sets(sc);
+    if (spec->sample == GC_SAMPLE_KOUT) run_kout(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
+    if (spec->sample == GC_SAMPLE_HB) run_hb(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
+    if (!edges && pl.n) {
+      (k_root_transitions<<<grid_for(pl.n, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nullptr, pl.n, out_u, out_v,
+                                                                           out_count), count_launch());
+      GC_CHECK_LAUNCH();
+    }
+    unsigned long long c[C_COUNT_];
+    read_ctr(c, pl.ws.ctr, st);
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
+    }
+  });
+}
+
+int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32_t* out_u, int32_t* out_v,
+                    unsigned long long* out_count, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    check_static_args(g, spec, parent);
+    check_shard_spec(spec);
+    require(out_u && out_v && out_count, GC_ERR_ARG, "null merging-edge output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    Pipeline pl(*g, *spec, parent, nullptr, nullptr, ws, ws_bytes, st);
+    const bool edges = spec->splice != GC_SPLICE_ATOMIC;
+    if (edges) {
+      pl.lu = out_u;
+      pl.lv = out_v;
+      pl.lcount = out_count;
+    }
+    const UFConfig fc = finish_cfg(*spec);
+    if (pl.n && (fc.unite == GC_FINISH_HOOKS || fc.unite == GC_FINISH_REM_LOCK))
+      fill(fc.unite == GC_FINISH_HOOKS ? pl.ws.H : pl.ws.L, pl.n, fc.unite == GC_FINISH_HOOKS ? pl.n : 0, st);
+    if (spec->sample == GC_SAMPLE_NONE) {
+      pl.set_lmax_sentinel();
+    } else {
+      // the merged sampled partition is identical on every rank, so the
+      // compressed labels, L_max and the active set are too
+      run_post_sample(parent, pl.n, g->offsets, pl.ws.list, pl.ws.hist, pl.ws.ctr, true, st);
+    }
+    // non-root-based rules: snapshot the parents (the histogram buffer is
+    // free after the mode) and emit root transitions after the finish
+    if (!edges && pl.n)
+      GC_CUDA(cudaMemcpyAsync(pl.ws.hist, parent, size_t(pl.n) * 4, cudaMemcpyDeviceToDevice, st));
+    pl.finish();
+    if (!edges && pl.n) {
+      (k_root_transitions<<<grid_for(pl.n, kEwBlock, 8), kEwBlock, 0, st>>>(parent, pl.ws.hist, pl.n, out_u,
+                                                                           out_v, out_count), count_launch());
+      GC_CHECK_LAUNCH();
+    }
+    unsigned long long c[C_COUNT_];
+    read_ctr(c, pl.ws.ctr, st);
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->insp_finish = int64_t(c[C_INSP_FINISH]);
+      const bool none = spec->sample == GC_SAMPLE_NONE;
+      stats->l_max = none ? g->n : int64_t(c[C_LMAX]);
+      stats->lmax_count = none ? (g->n ? 1 : 0) : int64_t(c[C_LMAX_COUNT]);
+      stats->n_active = none ? g->n : int64_t(c[C_N_ACTIVE]);
+    }
   });
 }
 

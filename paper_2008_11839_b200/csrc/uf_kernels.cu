@@ -155,7 +155,7 @@ struct RowsLaunch {
   cudaStream_t st;
   template <class R>
   void go() const {
-    UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n};
+    UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     int64_t warps = (a.count_host + 31) / 32;
     int64_t blocks = (warps * 32 + kRowBlock - 1) / kRowBlock;
     // one resident wave, grid-stride over 32-row groups
@@ -262,7 +262,7 @@ void dispatch(const UFConfig& c, bool forest, const L& l) {
 
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st) {
   if (a.count_host <= 0) return;
-  dispatch(cfg, forest, RowsLaunch{a, st});
+  dispatch(cfg, forest || a.lu != nullptr, RowsLaunch{a, st});
 }
 
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st) {

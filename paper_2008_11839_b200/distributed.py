@@ -12,8 +12,12 @@ here follow the survey:
   forest edges are unioned into the receiver's state and the edges that merge
   two trees are added to its forest (``gc_union_edges_list``).  Rank 0 ends
   with a spanning forest of the union and broadcasts the canonical labels.
-  Sampled specs are not sound per shard (a per-shard L_max may skip an edge
-  between two different local giants, SURVEY §8e caveat) and are rejected.
+* **Sampled specs (k-out / HB): two-phase exchange.**  A per-shard L_max is
+  not sound (it may skip an edge between two different local giants, SURVEY
+  §8e caveat), so each rank samples its rows, the sampled merging edges are
+  all-gathered and unioned everywhere, and only then is the (now global and
+  identical) L_max taken and the finish run over each rank's active rows,
+  followed by a second all-gather (``sharded_two_phase``).
 * **Batch-sharded incremental.**  Every rank keeps a full replica.  Each
   batch's inserts are split 1/P; a rank unions its part recording the edges
   that merged trees (a spanning forest of the part w.r.t. its replica),
@@ -32,7 +36,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import ConfigError
-from .spec import AlgorithmSpec, SampleKind, format_spec
+from .spec import AlgorithmSpec, KOutMode, SampleKind, format_spec
 
 
 def _torch():
@@ -110,6 +114,57 @@ class GpuEngine:
                                                 out_u.data_ptr(), out_v.data_ptr(), cnt.data_ptr(), _stream()))
         c = int(cnt.item())
         return out_u[:c], out_v[:c]
+
+    def union_pairs(self, parent, us, vs, spec):
+        """Union without recording (gc_union_edges): any rule, root-based or not."""
+        import ctypes as C
+        from . import _native as N
+        from .api import LoweredSpec, _stream
+        torch = _torch()
+        k = int(us.numel())
+        if not k:
+            return
+        low = LoweredSpec(spec, None, parent.numel())
+        aux = None
+        if spec.cfg.union.value in ("hooks", "rem_lock"):
+            aux = torch.full((parent.numel(),), parent.numel() if spec.cfg.union.value == "hooks" else 0,
+                             dtype=torch.int32, device="cuda")
+        N.check(N.lib().gc_union_edges(parent.data_ptr(), parent.numel(), us.data_ptr(), vs.data_ptr(), k,
+                                       C.byref(low.s), aux.data_ptr() if aux is not None else None, None, None,
+                                       _stream()))
+
+    def _shard_call(self, fn, shard, spec, parent):
+        import ctypes as C
+        from . import _native as N
+        from .api import LoweredSpec, _csr, _stream, _workspace
+        torch = _torch()
+        n = shard.n
+        low = LoweredSpec(spec, shard, n)
+        csr, keep = _csr(shard)
+        lib = N.lib()
+        ws = _workspace(lib.gc_workspace_size(n, shard.m, C.byref(low.s)))
+        out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        st = N.Stats()
+        N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), parent.data_ptr(), out_u.data_ptr(),
+                                 out_v.data_ptr(), cnt.data_ptr(), C.byref(st), ws.data_ptr(), ws.numel(),
+                                 _stream()))
+        c = int(cnt.item())
+        return out_u[:c], out_v[:c], st
+
+    def shard_sample(self, shard, spec):
+        """gc_shard_sample: identity parent + the sampler over this block's rows."""
+        torch = _torch()
+        parent = torch.empty(max(shard.n, 1), dtype=torch.int32, device="cuda")
+        mu, mv, st = self._shard_call("gc_shard_sample", shard, spec, parent)
+        return parent, mu, mv, int(st.insp_sample)
+
+    def shard_finish(self, shard, spec, parent):
+        """gc_shard_finish: L_max + active gather + finish over this block's rows."""
+        mu, mv, st = self._shard_call("gc_shard_finish", shard, spec, parent)
+        return mu, mv, {"insp_finish": int(st.insp_finish), "l_max": int(st.l_max),
+                        "lmax_count": int(st.lmax_count), "n_active": int(st.n_active)}
 
     def finalize(self, parent):
         import ctypes as C
@@ -253,9 +308,100 @@ def sharded_spanning_forest(g_shard, spec: AlgorithmSpec, group=None, engine=Non
     return ShardedResult(labels, fbuf[0].to(dev_local), fbuf[1].to(dev_local), comps, rounds, int(tot.item()))
 
 
+def _check_two_phase_spec(spec: AlgorithmSpec):
+    if not spec.is_union_finish():
+        raise ConfigError(f"sharded connectivity needs a union-find finish; '{format_spec(spec)}' is not")
+    if spec.sample not in (SampleKind.NONE, SampleKind.KOUT, SampleKind.HB):
+        raise ConfigError(f"sharded sampling supports none / kout / hb, not '{spec.sample.value}' "
+                          "(BFS / LDD need a distributed traversal)")
+    if spec.sample is SampleKind.KOUT and spec.kout_mode is not KOutMode.FIRST_K:
+        raise ConfigError("sharded k-out needs FIRST_K: random offsets are drawn over the whole graph")
+
+
+@dataclass
+class TwoPhaseResult:
+    labels: object          # canonical labels (identical on every rank)
+    forest_u: object        # this rank's spanning forest of the whole graph
+    forest_v: object        # (None for non-root-based specs)
+    components: int
+    insp_sample: int        # whole-graph inspection counts (sum over ranks)
+    insp_finish: int
+    l_max: int
+    lmax_count: int
+    n_active: int
+    exchanged_edges: int    # merging edges all-gathered, both phases
+
+
+def _exchange_and_merge(parent, mu, mv, spec, engine, group, rank):
+    """All-gather every rank's merge list; union the foreign ones.  Returns
+    the edges that merged trees here (own + foreign) and the total exchanged.
+    Root-based rules exchange real merging edges (a forest); the others
+    (Rem with the atomic splice) exchange root transitions (v, P[v]), which
+    carry the partition but are not graph edges."""
+    fu, fv = [mu], [mv]
+    total = 0
+    record = spec.is_root_based()
+    for r, (ou, ov) in enumerate(all_gather_pairs(mu, mv, group)):
+        total += int(ou.numel())
+        if r != rank and ou.numel():
+            if record:
+                au, av = engine.union_list(parent, ou.to(parent.device), ov.to(parent.device), spec)
+                fu.append(au)
+                fv.append(av)
+            else:
+                engine.union_pairs(parent, ou.to(parent.device), ov.to(parent.device), spec)
+    torch = _torch()
+    return torch.cat(fu), torch.cat(fv), total
+
+
+def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> TwoPhaseResult:
+    """The two-phase pipeline over edge-sharded row blocks.
+
+    The skip of the finish is only sound for ONE global post-sample labelling
+    and ONE global L_max (a per-shard L_max could skip an edge
+    between two different local giants), so the sampled partitions are
+    merged before L_max is taken:
+
+      1. every rank samples its own rows, recording the merging edges;
+      2. all-gather them, union the foreign ones: every replica now induces
+         the global sampled partition, so compression gives identical labels,
+         L_max and active sets on every rank with no further collective;
+      3. every rank runs the finish over the active vertices of its rows,
+         recording merging edges; all-gather + union again;
+      4. finalise locally — identical canonical labels everywhere.
+
+    Each rank's kept merging edges form a spanning forest of the whole graph.
+    """
+    _check_two_phase_spec(spec)
+    dist = _dist()
+    engine = engine or GpuEngine()
+    rank = dist.get_rank(group)
+    parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec)
+    f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
+    mu, mv, info = engine.shard_finish(g_shard, spec, parent)
+    f2u, f2v, x2 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
+    torch = _torch()
+    labels = engine.finalize(parent)
+    n = g_shard.n
+    dev = _comm_device(group)
+    tot = torch.tensor([insp_s, info["insp_finish"]], dtype=torch.int64, device=dev)
+    dist.all_reduce(tot, group=group)
+    labels = labels[:n]
+    comps = int((labels == torch.arange(n, device=labels.device, dtype=labels.dtype)).sum().item())
+    fu = torch.cat([f1u, f2u]) if spec.is_root_based() else None
+    fv = torch.cat([f1v, f2v]) if spec.is_root_based() else None
+    return TwoPhaseResult(labels, fu, fv, comps, int(tot[0].item()), int(tot[1].item()), info["l_max"],
+                          info["lmax_count"], info["n_active"], x1 + x2)
+
+
 def sharded_static_connectivity(g_shard, spec: AlgorithmSpec, group=None, engine=None):
-    """Edge-sharded static connectivity: canonical labels on every rank."""
-    res = sharded_spanning_forest(g_shard, spec, group, engine)
+    """Edge-sharded static connectivity: canonical labels on every rank.
+    Unsampled specs merge forests tree-wise; sampled specs (k-out / HB) run
+    the two-phase exchange."""
+    if spec.sample is SampleKind.NONE:
+        res = sharded_spanning_forest(g_shard, spec, group, engine)
+    else:
+        res = sharded_two_phase(g_shard, spec, group, engine)
     return res.labels, res
 
 

@@ -56,6 +56,79 @@ class CpuEngine:
         parent.copy_(torch.from_numpy(p.astype(np.int32)))
         return torch.tensor(mu, dtype=torch.int32), torch.tensor(mv, dtype=torch.int32)
 
+    # two-phase sharded pipeline (gc_shard_sample / gc_shard_finish semantics)
+    def shard_sample(self, shard, spec):
+        n = shard.n
+        p = np.arange(n, dtype=np.int64)
+        off, tgt = shard.offsets, shard.targets
+        fu, fv = [], []
+        insp = 0
+
+        def rec(u, t):
+            if _union(p, u, t):
+                fu.append(u)
+                fv.append(t)
+        kind = spec.sample.value
+        if kind == "kout":
+            for u in range(n):
+                take = min(spec.kout_k, int(off[u + 1] - off[u]))
+                insp += take
+                for j in range(take):
+                    rec(u, int(tgt[off[u] + j]))
+        elif kind == "hb":
+            roots = []
+            for v in range(n):
+                if off[v + 1] > off[v]:
+                    insp += 1
+                    first = int(tgt[off[v]])
+                    if first < v:
+                        rec(v, first)
+                    else:
+                        roots.append(v)
+            for v in roots:
+                take = min(spec.hb_edges, int(off[v + 1] - off[v]))
+                insp += take
+                for j in range(take):
+                    rec(v, int(tgt[off[v] + j]))
+        return (torch.from_numpy(p.astype(np.int32)), torch.tensor(fu, dtype=torch.int32),
+                torch.tensor(fv, dtype=torch.int32), insp)
+
+    def shard_finish(self, shard, spec, parent):
+        n = shard.n
+        p = parent.numpy().astype(np.int64)
+        off, tgt = shard.offsets, shard.targets
+        lab = np.array([_find(p, v) for v in range(n)], dtype=np.int64)
+        fu, fv = [], []
+        insp = 0
+        if spec.sample.value == "none":
+            lmax, cnt, active = n, (1 if n else 0), n
+            for u in range(n):
+                for j in range(off[u], off[u + 1]):
+                    insp += 1
+                    t = int(tgt[j])
+                    if t < u and _union(p, u, t):
+                        fu.append(u)
+                        fv.append(t)
+        else:
+            counts = np.bincount(lab, minlength=n)
+            lmax = int(counts.argmax()) if n else 0
+            cnt = int(counts[lmax]) if n else 0
+            act = np.flatnonzero(lab != lmax)
+            active = len(act)
+            for u in act.tolist():
+                for j in range(off[u], off[u + 1]):
+                    insp += 1
+                    t = int(tgt[j])
+                    if _union(p, u, t):
+                        fu.append(u)
+                        fv.append(t)
+        parent.copy_(torch.from_numpy(p.astype(np.int32)))
+        return (torch.tensor(fu, dtype=torch.int32), torch.tensor(fv, dtype=torch.int32),
+                {"insp_finish": insp, "l_max": lmax, "lmax_count": cnt, "n_active": active})
+
+    def union_pairs(self, parent, us, vs, spec):
+        self.union_list(parent, us, vs, spec)
+
     def finalize(self, parent):
         p = parent.numpy().astype(np.int64)
         return torch.from_numpy(np.array([_find(p, v) for v in range(len(p))], dtype=np.int32))

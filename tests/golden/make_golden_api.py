@@ -97,6 +97,27 @@ def main():
         lab = rng.integers(0, 5, size=g.n) * (trial + 1) % g.n
         cov, ic = sampling_stats(g, lab)
         out["sampling_stats"]["cases"].append({"labels": lab.tolist(), "cov": cov, "ic": ic})
+    # make_stream op order (bench.py:179-193) on a small graph
+    from connlab.bench import CSV_COLUMNS, make_stream
+    from connlab.driver import Query
+    g = build_csr(gen_ba(300, 2, seed=3))
+    out["make_stream"] = {}
+    for ratio in (0, 1, 10):
+        ops = make_stream(g, ratio, seed=1)
+        arr = np.array([[op.u, op.v, int(isinstance(op, Query))] for op in ops], dtype=np.int64)
+        out["make_stream"][str(ratio)] = {"len": len(ops), "hash": h(arr)}
+    out["csv_columns"] = CSV_COLUMNS
+    # sweep rows (bench.py:131-240) without the timing columns
+    from connlab.bench import small_suite, sweep_incremental, sweep_static
+    keep = ["graph", "spec", "sample", "finish", "find", "splice", "workers", "batch_size", "ratio", "cov",
+            "ic", "inspections_sample", "inspections_finish", "rounds", "components"]
+    suite = [x for x in small_suite() if x[0] in ("comps_30", "rmat_s7_ef4", "grid_12x12", "ba_120_a3")]
+    specs = [parse_spec(t) for t in ("kout+rem_cas+halve+splice", "hb+sv", "none+lt_prs", "bfs+async+halve")]
+    rows = sweep_static(suite, specs, [1], repeats=1)
+    out["sweep_static"] = [{k: str(r[k]) for k in keep} for r in rows]
+    ispecs = [parse_spec(t) for t in ("none+async+halve", "none+sv")]
+    rows = sweep_incremental(suite[:2], ispecs, batch_sizes=[64, 256], ratios=[1, 10])
+    out["sweep_incremental"] = [{k: str(r[k]) for k in keep} for r in rows]
     (OUT / "api.json").write_text(json.dumps(out, sort_keys=True))
     print("wrote", OUT / "api.json")
 

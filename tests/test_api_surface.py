@@ -143,3 +143,52 @@ def test_binary_graph_roundtrip(tmp_path):
     p.write_bytes(p.read_bytes()[:-3])
     with pytest.raises(MalformedInputError, match="truncated"):
         load_graph_binary(p)
+
+
+def _ba_graph_host(n, att, seed):
+    el = gen_ba(n, att, seed=seed)
+    e = el.edges
+    u = np.concatenate([e[:, 0], e[:, 1]])
+    v = np.concatenate([e[:, 1], e[:, 0]])
+    order = np.lexsort((v, u))
+    u, v = u[order], v[order]
+    keep = np.ones(len(u), bool)
+    keep[1:] = (u[1:] != u[:-1]) | (v[1:] != v[:-1])
+    u, v = u[keep], v[keep]
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, u + 1, 1)
+    return Graph(n, np.cumsum(off), v)
+
+
+def test_make_stream_order_matches_reference():
+    from paper_2008_11839_b200.sweep import CSV_COLUMNS, make_stream, make_stream_columnar
+    assert CSV_COLUMNS == API["csv_columns"]
+    g = _ba_graph_host(300, 2, 3)
+    for ratio, want in API["make_stream"].items():
+        ratio = int(ratio)
+        us, vs, isq = make_stream_columnar(g, ratio, seed=1, device=False)
+        arr = np.stack([us, vs, isq], axis=1).astype(np.int64)
+        assert len(arr) == want["len"] and h(arr) == want["hash"], ratio
+        ops = make_stream(g, ratio, seed=1)
+        arr2 = np.array([[op.u, op.v, int(type(op).__name__ == "Query")] for op in ops], dtype=np.int64)
+        assert h(arr2) == want["hash"]
+
+
+_SWEEP_KEYS = ["graph", "spec", "sample", "finish", "find", "splice", "workers", "batch_size", "ratio", "cov",
+               "ic", "inspections_sample", "inspections_finish", "rounds", "components"]
+
+
+@pytest.mark.gpu
+def test_sweep_rows_match_reference():
+    from paper_2008_11839_b200 import parse_spec
+    from paper_2008_11839_b200.sweep import rows_to_csv_text, small_suite, sweep_incremental, sweep_static
+    suite = [x for x in small_suite() if x[0] in ("comps_30", "rmat_s7_ef4", "grid_12x12", "ba_120_a3")]
+    specs = [parse_spec(t) for t in ("kout+rem_cas+halve+splice", "hb+sv", "none+lt_prs", "bfs+async+halve")]
+    rows = sweep_static(suite, specs, [1], repeats=1)
+    got = [{k: str(r[k]) for k in _SWEEP_KEYS} for r in rows]
+    assert got == API["sweep_static"]
+    ispecs = [parse_spec(t) for t in ("none+async+halve", "none+sv")]
+    rows = sweep_incremental(suite[:2], ispecs, batch_sizes=[64, 256], ratios=[1, 10])
+    got = [{k: str(r[k]) for k in _SWEEP_KEYS} for r in rows]
+    assert got == API["sweep_incremental"]
+    assert rows_to_csv_text(rows).splitlines()[0] == ",".join(API["csv_columns"])

@@ -151,3 +151,58 @@ def test_sharded_incremental(world):
             assert got_bits[b].tolist() == exp_bits[b].tolist(), (rank, b)
         assert np.array_equal(got_lab, lab)
         assert comps == int(sum(1 for v in range(cap) if inited[v] and lab[v] == v))
+
+
+def _two_phase_worker(rank, world, port, names, specs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_engine import CpuEngine
+        from paper_2008_11839_b200 import Graph, parse_spec
+        from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+        gold = Golden()
+        out = {}
+        for name in names:
+            n, off, tgt, orc = gold.graphs[name]
+            g = Graph(n, off, tgt)
+            lo, hi = shard_bounds(off, world)[rank]
+            for text in specs:
+                r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec(text), engine=CpuEngine())
+                out[(name, text)] = (r.labels.numpy().astype(np.int64),
+                                     r.forest_u.numpy() if r.forest_u is not None else None,
+                                     r.forest_v.numpy() if r.forest_v is not None else None,
+                                     r.components, r.insp_sample, r.insp_finish, r.lmax_count, r.n_active)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_two_phase_matches_reference_stats(world):
+    """Sampled specs over row shards: labels bit-exact, every rank's forest
+    passes the four clauses, and the summed inspection counts / cov equal the
+    reference's single-process run (spec_stats.json)."""
+    gold = Golden()
+    names = ["rmat_s10_ef8", "comps_30", "star_150", "grid_12x12", "edgeless4", "ba_120_a3"]
+    specs = ["kout+async+halve", "hb+async+halve", "none+async+halve", "kout+rem_cas+halve+splice"]
+    res = _run(_two_phase_worker, world, names, specs)
+    for name in names:
+        n, off, tgt, orc = gold.graphs[name]
+        comps = len(np.unique(orc)) if n else 0
+        for text in specs:
+            want = gold.spec_stats[name][text]
+            for rank in range(world):
+                lab, fu, fv, c, i_s, i_f, lcnt, nact = res[rank][(name, text)]
+                assert np.array_equal(lab, orc), (name, text, rank)
+                assert c == comps
+                assert i_s == want["insp_sample"] and i_f == want["insp_finish"], (name, text, rank, i_s, i_f)
+                if n:
+                    assert lcnt / n == want["cov"], (name, text)
+                if fu is None:  # atomic splice: labels only
+                    continue
+                su = np.full(n, -1, np.int32)
+                sv = np.full(n, -1, np.int32)
+                su[:len(fu)] = fu
+                sv[:len(fv)] = fv
+                rep = oracle.check_forest(n, off, tgt, su, sv, orc)
+                assert rep["passed"], (name, text, rank, rep)

@@ -110,3 +110,56 @@ def test_two_ranks_share_one_gpu():
         assert oracle.check_forest(g.n, g.offsets, g.targets, su, sv, orc)["passed"]
         assert np.array_equal(ilab.astype(np.int64), orc)
         assert icomps == comps - iso
+
+
+def _two_phase_gpu_worker(rank, world, port, specs, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec
+        from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+        g = build_csr(gen_rmat(15, 8, seed=5, device=True))
+        lo, hi = shard_bounds(g.offsets, world)[rank]
+        out = {}
+        for text in specs:
+            r = sharded_two_phase(shard_graph(g.cuda(), lo, hi), parse_spec(text))
+            out[text] = (r.labels.cpu().numpy(), None if r.forest_u is None else r.forest_u.cpu().numpy(),
+                         None if r.forest_v is None else r.forest_v.cpu().numpy(), r.insp_sample, r.insp_finish,
+                         r.lmax_count, r.n_active)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_two_phase_sampled_ranks_share_one_gpu(world):
+    """Sampled specs over row shards on the GPU engine: labels bit-exact and
+    inspection counts / cov / active set equal to the single-GPU pipeline."""
+    import torch.multiprocessing as mp
+    from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec, static_connectivity_device
+    specs = ["kout+rem_cas+halve+splice", "kout+async+halve", "hb+rem_cas+split+halve", "none+hooks+compress"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_phase_gpu_worker, args=(r, world, port, specs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    g = build_csr(gen_rmat(15, 8, seed=5, device=True))
+    orc, comps = oracle.components(g.n, g.offsets, g.targets)
+    for text in specs:
+        _, st = static_connectivity_device(g, parse_spec(text))
+        for r in range(world):
+            labels, fu, fv, i_s, i_f, lcnt, nact = res[r][text]
+            assert np.array_equal(labels.astype(np.int64), orc), (text, r)
+            assert i_s == st.edge_inspections.get("sample", 0), (text, r)
+            assert i_f == st.edge_inspections.get("finish", 0), (text, r)
+            assert lcnt / g.n == st.cov and nact == st.active, (text, r)
+            if fu is not None:
+                su = np.full(g.n, -1, np.int32); sv = np.full(g.n, -1, np.int32)
+                su[:len(fu)] = fu; sv[:len(fv)] = fv
+                assert oracle.check_forest(g.n, g.offsets, g.targets, su, sv, orc)["passed"], (text, r)
