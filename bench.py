@@ -369,8 +369,13 @@ def run_ours(args):
     kms = statistics.mean(ksamp)
     achieved = kout_bytes / (kms / 1e3) / 1e9
     step_bytes = 4 * (e_s + e_f) + 8 * (n + 1) + 4 * n * 7  # SURVEY 8(d), P = 7 with sampling
+    traffic, traffic_src = args.traffic, "--traffic"
+    tj = ROOT / "profiles" / "traffic.json"
+    if traffic is None and tj.exists():
+        t = json.loads(tj.read_text())
+        traffic, traffic_src = t["traffic_bytes"], f"profiles/traffic.json ({t['source']})"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": args.traffic,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "k_union_rows<Rule<REM_CAS,HALVE,SPLICE>> (k-out sampling)",
                 "kernel_ms": kms, "kernel_bytes": kout_bytes, "peak_source": peak_kind,
                 "step_alg_bytes": step_bytes,

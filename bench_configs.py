@@ -100,16 +100,18 @@ def config3(args):
     side = args.grid_side
     el = grid3d_edges(side)
     g = build_csr(el, keep_host=False)
+    # LDD's shift rate has no reference default: sweep it, named in the spec string
     specs = ["ldd+sv", "ldd+lt_prs", "ldd+lt_crfa", "none+sv", "none+lt_prs", "none+lt_crfa", "kout+sv",
-             "bfs+sv"]
+             "bfs+sv"] + [f"ldd({b})+sv" for b in (0.1, 0.3, 0.5, 0.8)]
     static_config(f"3: 3-D grid {side}^3 natural ids", g, specs, args.reps, args.out)
     # randomly relabelled copy: exercises the high-diameter behaviour
     n = side ** 3
     perm = torch.randperm(n, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
     e = el.edges.to("cuda")
     g2 = build_csr(EdgeList(n, perm[e]), keep_host=False)
-    static_config(f"3: 3-D grid {side}^3 permuted ids", g2, ["ldd+sv", "ldd+lt_prs", "none+sv", "none+lt_prs"],
-                  args.reps, args.out)
+    static_config(f"3: 3-D grid {side}^3 permuted ids", g2,
+                  ["ldd+sv", "ldd+lt_prs", "none+sv", "none+lt_prs", "kout+sv"]
+                  + [f"ldd({b})+sv" for b in (0.1, 0.3, 0.5, 0.8)], args.reps, args.out)
 
 
 def config4(args):

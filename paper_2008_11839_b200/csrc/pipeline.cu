@@ -415,7 +415,9 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
   if (n > 0) {
     const int64_t nq = (int64_t(n) + 3) / 4;
     const int gq = grid_for(nq, kEwBlock, 4);
-    const int g = grid_for(n, kEwBlock, 4);
+    // the fallback kernels usually exit at once: one resident wave keeps
+    // their early exit cheap and still streams when they do run
+    const int g = grid_for(n, kEwBlock, 1);
     (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr), ::gc::count_launch());
     if (compress) (k_post_sample<true><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
     else (k_post_sample<false><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
@@ -426,7 +428,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
   }
   (k_mode_finish<<<1, 1, 0, st>>>(n, ctr), ::gc::count_launch());
   if (n > 0)
-    (k_gather_active<<<grid_for(n, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, off, list, ctr, 1),
+    (k_gather_active<<<grid_for(n, kEwBlock, 1), kEwBlock, 0, st>>>(P, n, off, list, ctr, 1),
      ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }

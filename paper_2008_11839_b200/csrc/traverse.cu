@@ -124,8 +124,8 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
         take(fresh, x);
       }
     }
-    bq.flush(qn, nstat);
   }
+  bq.flush(qn, nstat);  // once per launch; overflow went straight to the global queue
   if (insp) block_add<kTB>(insp, degs);
   my_min = warp_min(my_min);
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
@@ -389,7 +389,6 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
         }
         bq.push(fresh, x, qout, cout);
       }
-      bq.flush(qout, cout);
     }
   }
   if (r <= last_start) {
@@ -403,9 +402,11 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
         fresh = claim(key, v, r, uint32_t(v));
       }
       bq.push(fresh, v, qout, cout);
-      bq.flush(qout, cout);
     }
   }
+  // one block-wide flush per launch: items beyond the staging capacity
+  // already went straight to the global queue inside push()
+  bq.flush(qout, cout);
   block_add<kTB>(insp, my_insp);
 }
 
