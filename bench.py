@@ -173,8 +173,9 @@ def run_sharded(args):
     one scale-24 graph's worth of edges.  Every rank generates the same graph
     (deterministic stream), keeps only its edge-balanced row block, and each
     step runs `sharded_two_phase`: local sampling over its rows, all-gather
-    of the sampled merging edges, the finish over its active rows, a second
-    all-gather, local finalisation.  The step time is CUDA events on the
+    of a compact summary of the sampled partition (local giant as an n-bit
+    bitmap + the non-giant remainder as pairs), the finish over its active
+    rows, an all-gather of the finish's merging edges, local finalisation.  The step time is CUDA events on the
     rank's stream (host-side collective waits included), max over ranks."""
     import math
 
@@ -201,7 +202,7 @@ def run_sharded(args):
     lo, hi = shard_bounds(g._d_off, ws)[rank]
     shard = shard_graph(g, lo, hi)
     parity = None
-    res = sharded_two_phase(shard, spec)
+    res = sharded_two_phase(shard, spec, forest=False)
     if rank == 0 and not args.skip_check:
         import oracle
         ref, comps = oracle.components(n, g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy())
@@ -216,7 +217,7 @@ def run_sharded(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        sharded_two_phase(shard, spec)
+        sharded_two_phase(shard, spec, forest=False)
     torch.cuda.synchronize()
     dist.barrier()
     times, exchanged = [], 0
@@ -226,7 +227,7 @@ def run_sharded(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = sharded_two_phase(shard, spec)
+            r = sharded_two_phase(shard, spec, forest=False)
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -248,8 +249,10 @@ def run_sharded(args):
                 "config": {"workload": f"edge-sharded static CC {SPEC} on RMAT scale-{scale} ef{args.edge_factor} "
                                        f"(avg degree 16) seed {args.seed}, {ws} row blocks",
                            "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2,
-                           "parallelism": f"edge-sharded x{ws} ({backend}), two-phase all-gather merge",
-                           "exchanged_edges_per_step": exchanged,
+                           "parallelism": f"edge-sharded x{ws} ({backend}), two-phase: giant-bitmap + "
+                                          "remainder all-gather, then finish merging edges",
+                           "exchanged_pairs_per_step": exchanged,
+                           "exchanged_bitmap_bytes_per_step": ws * ((n + 31) // 32) * 4,
                            "l2": "256 MiB buffer written between timed steps (outside the step events)"},
                 "e2e": None, "gpu_launches": None,
                 "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1e3) / 1e9 / ws,

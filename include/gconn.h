@@ -211,6 +211,27 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent,
                     unsigned long long* out_count, gc_stats* stats, void* ws,
                     size_t ws_bytes, void* stream);
 
+/* Compact phase-1 exchange for labels-only runs (no forest): summarise this
+ * rank's sampled partition (after gc_shard_sample, compressed in place) as
+ * its most frequent class — an n-bit bitmap giant_bits[(n+31)/32] plus that
+ * class's label (*giant_label, device) — and a pair (v, label) for every
+ * other non-singleton vertex (out_u/out_v capacity n, *out_count device).
+ * ws: gc_shard_summary_workspace(n) bytes. */
+size_t gc_shard_summary_workspace(int64_t n);
+int gc_shard_summary(int32_t* parent, int64_t n, uint32_t* giant_bits,
+                     int64_t* giant_label, int32_t* out_u, int32_t* out_v,
+                     unsigned long long* out_count, void* ws, size_t ws_bytes,
+                     void* stream);
+/* Rebuild the join of all ranks' sampled partitions: bits = nranks
+ * consecutive bitmaps, giant_labels[nranks] (device); giants sharing a
+ * vertex form one class, every member points at the class's smallest giant
+ * label, then the k remainder pairs are unioned with the spec's rule.
+ * nranks <= 8.  ws: 4*n + 4096 bytes. */
+int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits,
+                  const int64_t* giant_labels, int32_t nranks,
+                  const int32_t* us, const int32_t* vs, int64_t k,
+                  const gc_spec* spec, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- DisjointSets probes and validation (dset.py:381-399,
  *      validate.py:178-259) -------------------------------------------------
  * gc_find_batch: roots_out[i] = find(xs[i]) with the given gc_find_kind,

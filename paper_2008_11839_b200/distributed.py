@@ -166,6 +166,39 @@ class GpuEngine:
         return mu, mv, {"insp_finish": int(st.insp_finish), "l_max": int(st.l_max),
                         "lmax_count": int(st.lmax_count), "n_active": int(st.n_active)}
 
+    def shard_summary(self, parent):
+        """gc_shard_summary: (giant bitmap int32 words, giant label, remainder pairs)."""
+        from . import _native as N
+        from .api import _stream, _workspace
+        torch = _torch()
+        n = parent.numel()
+        words = torch.zeros(max((n + 31) // 32, 1), dtype=torch.int32, device="cuda")
+        label = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws = _workspace(N.lib().gc_shard_summary_workspace(n))
+        N.check(N.lib().gc_shard_summary(parent.data_ptr(), n, words.data_ptr(), label.data_ptr(), out_u.data_ptr(),
+                                         out_v.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+        c = int(cnt.item())
+        return words, label, out_u[:c], out_v[:c]
+
+    def shard_join(self, parent, words_all, labels_all, us, vs, spec):
+        """gc_shard_join over all ranks' summaries (words_all: nranks x words)."""
+        import ctypes as C
+        from . import _native as N
+        from .api import LoweredSpec, _stream, _workspace
+        n = parent.numel()
+        low = LoweredSpec(spec, None, n)
+        ws = _workspace(4 * n + 8192)
+        words_all = words_all.contiguous()
+        labels_all = labels_all.contiguous()
+        k = int(us.numel())
+        N.check(N.lib().gc_shard_join(parent.data_ptr(), n, words_all.data_ptr(), labels_all.data_ptr(),
+                                      int(labels_all.numel()), us.data_ptr() if k else None,
+                                      vs.data_ptr() if k else None, k, C.byref(low.s), ws.data_ptr(), ws.numel(),
+                                      _stream()))
+
     def finalize(self, parent):
         import ctypes as C
         from . import _native as N
@@ -354,7 +387,29 @@ def _exchange_and_merge(parent, mu, mv, spec, engine, group, rank):
     return torch.cat(fu), torch.cat(fv), total
 
 
-def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> TwoPhaseResult:
+def _exchange_summary(parent, spec, engine, group):
+    """Phase-1 exchange for labels-only runs: each rank's local giant as an
+    n-bit bitmap + its label, and the non-giant remainder as pairs; every
+    rank rebuilds the exact join (gc_shard_join).  Returns the number of
+    remainder pairs exchanged."""
+    torch = _torch()
+    dist = _dist()
+    dev = _comm_device(group)
+    world = dist.get_world_size(group)
+    words, label, ru, rv = engine.shard_summary(parent)
+    wl = [torch.empty_like(words, device=dev) for _ in range(world)]
+    dist.all_gather(wl, words.to(dev), group=group)
+    ll = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(ll, label.to(dev), group=group)
+    pairs = all_gather_pairs(ru, rv, group)
+    us = torch.cat([p[0] for p in pairs]).to(parent.device)
+    vs = torch.cat([p[1] for p in pairs]).to(parent.device)
+    engine.shard_join(parent, torch.stack(wl).to(parent.device), torch.cat(ll).to(parent.device), us, vs, spec)
+    return int(us.numel())
+
+
+def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
+                      forest: bool = True) -> TwoPhaseResult:
     """The two-phase pipeline over edge-sharded row blocks.
 
     The skip of the finish is only sound for ONE global post-sample labelling
@@ -371,13 +426,24 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> 
       4. finalise locally — identical canonical labels everywhere.
 
     Each rank's kept merging edges form a spanning forest of the whole graph.
+
+    With ``forest=False`` (labels only) step 2 exchanges a compact summary
+    instead of the sampled merging edges: each rank's local giant as an
+    n-bit bitmap plus the pairs of its other non-singleton vertices, from
+    which every rank rebuilds the same join (``_exchange_summary``) — n/8
+    bytes and a small remainder instead of one pair per sampled row.
     """
     _check_two_phase_spec(spec)
     dist = _dist()
     engine = engine or GpuEngine()
     rank = dist.get_rank(group)
     parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec)
-    f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
+    torch = _torch()
+    if forest or spec.sample is SampleKind.NONE:
+        f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
+    else:
+        x1 = _exchange_summary(parent, spec, engine, group)
+        f1u = f1v = torch.empty(0, dtype=torch.int32, device=parent.device)
     mu, mv, info = engine.shard_finish(g_shard, spec, parent)
     f2u, f2v, x2 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
     torch = _torch()
@@ -388,8 +454,9 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> 
     dist.all_reduce(tot, group=group)
     labels = labels[:n]
     comps = int((labels == torch.arange(n, device=labels.device, dtype=labels.dtype)).sum().item())
-    fu = torch.cat([f1u, f2u]) if spec.is_root_based() else None
-    fv = torch.cat([f1v, f2v]) if spec.is_root_based() else None
+    keep = forest and spec.is_root_based()
+    fu = torch.cat([f1u, f2u]) if keep else None
+    fv = torch.cat([f1v, f2v]) if keep else None
     return TwoPhaseResult(labels, fu, fv, comps, int(tot[0].item()), int(tot[1].item()), info["l_max"],
                           info["lmax_count"], info["n_active"], x1 + x2)
 
@@ -401,7 +468,7 @@ def sharded_static_connectivity(g_shard, spec: AlgorithmSpec, group=None, engine
     if spec.sample is SampleKind.NONE:
         res = sharded_spanning_forest(g_shard, spec, group, engine)
     else:
-        res = sharded_two_phase(g_shard, spec, group, engine)
+        res = sharded_two_phase(g_shard, spec, group, engine, forest=False)
     return res.labels, res
 
 

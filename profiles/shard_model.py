@@ -1,0 +1,119 @@
+"""Multi-GPU model for the sharded two-phase pipeline, measured on ONE GPU.
+
+This environment exposes a single B200, so the P-rank run is replayed in one
+process: every rank's device work (sample its row block, summarise, join all
+summaries, finish its active rows, merge the finish edges, finalise) runs on
+the GPU one rank after another and is timed with CUDA events per stage; the
+collectives are replaced by in-memory concatenation and costed from the
+bytes they would move at the measured NVLink peer bandwidth (770 GB/s per
+direction, B200_PROFILING.md).  Predicted step = max over ranks of the
+device time + the collective time.  Labels are checked against the C oracle.
+
+  python profiles/shard_model.py [--ranks 1,2,4,8] [--scale0 24] [--reps 3]
+"""
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec  # noqa: E402
+from paper_2008_11839_b200.distributed import GpuEngine, shard_bounds, shard_graph  # noqa: E402
+
+NVLINK = 770e9  # bytes/s per direction, measured peer copy (B200_PROFILING.md)
+
+
+class Timer:
+    def __init__(self):
+        self.t = {}
+
+    def __call__(self, name, fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        e1.synchronize()
+        self.t[name] = self.t.get(name, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
+def run(P, scale0, check):
+    spec = parse_spec("kout+rem_cas+halve+splice")
+    scale = scale0 + int(math.ceil(math.log2(P)))
+    g = build_csr(gen_rmat(scale, 8, seed=1, device=True), keep_host=False)
+    n, m = g.n, g.m
+    eng = GpuEngine()
+    shards = [shard_graph(g, lo, hi) for lo, hi in shard_bounds(g._d_off, P)]
+    timers = [Timer() for _ in range(P)]
+    # phase 1: sample + summary on every rank
+    states = []
+    for r in range(P):
+        T = timers[r]
+        parent, _, _, _ = T("sample", lambda: eng.shard_sample(shards[r], spec))
+        words, label, ru, rv = T("summary", lambda: eng.shard_summary(parent))
+        states.append([parent, words, label, ru, rv])
+    words_all = torch.stack([s[1] for s in states])
+    labels_all = torch.cat([s[2] for s in states])
+    us = torch.cat([s[3] for s in states])
+    vs = torch.cat([s[4] for s in states])
+    bytes1 = words_all.numel() * 4 + us.numel() * 8 + 8 * P  # what each rank receives (upper bound)
+    fin = []
+    for r in range(P):
+        T = timers[r]
+        parent = states[r][0]
+        T("join", lambda: eng.shard_join(parent, words_all, labels_all, us, vs, spec))
+        mu, mv, _ = T("finish", lambda: eng.shard_finish(shards[r], spec, parent))
+        fin.append((mu, mv))
+    fu = torch.cat([f[0] for f in fin])
+    fv = torch.cat([f[1] for f in fin])
+    bytes2 = fu.numel() * 8
+    labels = None
+    for r in range(P):
+        T = timers[r]
+        parent = states[r][0]
+        for q in range(P):
+            if q != r and fin[q][0].numel():
+                T("merge2", lambda: eng.union_pairs(parent, fin[q][0], fin[q][1], spec))
+        lab = T("finalize", lambda: eng.finalize(parent))
+        if r == 0:
+            labels = lab
+    ok = None
+    if check:
+        import oracle
+        ref, _ = oracle.components(n, g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy())
+        ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref))
+    dev = [sum(T.t.values()) for T in timers]
+    comm_ms = (bytes1 + bytes2) / NVLINK * 1e3 if P > 1 else 0.0
+    step = max(dev) + comm_ms
+    return {"ranks": P, "scale": scale, "n": n, "m_directed": m, "labels_ok": ok,
+            "device_ms_max": max(dev), "comm_ms_model": comm_ms, "step_ms_model": step,
+            "edges_per_s_model": (m / 2) / (step / 1e3),
+            "stage_ms_rank0": {k: round(v, 4) for k, v in timers[0].t.items()},
+            "bytes_phase1_per_rank": bytes1, "bytes_phase2_per_rank": bytes2, "remainder_pairs": int(us.numel())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--scale0", type=int, default=24)
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    for P in (int(x) for x in a.ranks.split(",")):
+        best = None
+        for rep in range(a.reps):
+            r = run(P, a.scale0, a.check and rep == 0)
+            if best is None or r["step_ms_model"] < best["step_ms_model"]:
+                ok = best["labels_ok"] if best else r["labels_ok"]
+                best = r
+                best["labels_ok"] = ok if ok is not None else r["labels_ok"]
+            torch.cuda.empty_cache()
+        print(json.dumps(best), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -126,6 +126,51 @@ class CpuEngine:
         return (torch.tensor(fu, dtype=torch.int32), torch.tensor(fv, dtype=torch.int32),
                 {"insp_finish": insp, "l_max": lmax, "lmax_count": cnt, "n_active": active})
 
+    # compact summary exchange (gc_shard_summary / gc_shard_join semantics)
+    def shard_summary(self, parent):
+        p = parent.numpy().astype(np.int64)
+        n = len(p)
+        lab = np.array([_find(p, v) for v in range(n)], dtype=np.int64)
+        g = int(np.bincount(lab, minlength=n).argmax()) if n else 0
+        in_g = lab == g
+        nw = max((n + 31) // 32, 1)
+        bits = np.zeros(nw * 32, dtype=bool)
+        bits[:n] = in_g
+        words = np.packbits(bits, bitorder="little").view(np.uint32).view(np.int32)
+        pair = (~in_g) & (lab != np.arange(n))
+        parent.copy_(torch.from_numpy(lab.astype(np.int32)))
+        return (torch.from_numpy(words.copy()), torch.tensor([g], dtype=torch.int64),
+                torch.from_numpy(np.flatnonzero(pair).astype(np.int32)), torch.from_numpy(lab[pair].astype(np.int32)))
+
+    def shard_join(self, parent, words_all, labels_all, us, vs, spec):
+        n = parent.numel()
+        W = words_all.numpy().view(np.uint32)
+        R = W.shape[0]
+        bits = np.unpackbits(W.view(np.uint8).reshape(R, -1), axis=1, bitorder="little")[:, :n].astype(bool)
+        labels = labels_all.numpy()
+        par = list(range(R))
+
+        def root(x):
+            while par[x] != x:
+                x = par[x]
+            return x
+        for r in range(R):
+            for s in range(r + 1, R):
+                if (bits[r] & bits[s]).any():
+                    a, b = root(r), root(s)
+                    if a != b:
+                        par[max(a, b)] = min(a, b)
+        rep = [min(int(labels[s]) for s in range(R) if root(s) == root(r)) for r in range(R)]
+        p = np.arange(n, dtype=np.int64)
+        for v in range(n):
+            for r in range(R):
+                if bits[r, v]:
+                    p[v] = rep[r]
+                    break
+        for u, v in zip(us.tolist(), vs.tolist()):
+            _union(p, u, v)
+        parent.copy_(torch.from_numpy(p.astype(np.int32)))
+
     def union_pairs(self, parent, us, vs, spec):
         self.union_list(parent, us, vs, spec)
 

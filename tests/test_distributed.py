@@ -167,7 +167,9 @@ def _two_phase_worker(rank, world, port, names, specs, q):
             g = Graph(n, off, tgt)
             lo, hi = shard_bounds(off, world)[rank]
             for text in specs:
-                r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec(text), engine=CpuEngine())
+                forest = not text.startswith("~")
+                r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec(text.lstrip("~")), engine=CpuEngine(),
+                                      forest=forest)
                 out[(name, text)] = (r.labels.numpy().astype(np.int64),
                                      r.forest_u.numpy() if r.forest_u is not None else None,
                                      r.forest_v.numpy() if r.forest_v is not None else None,
@@ -184,13 +186,15 @@ def test_sharded_two_phase_matches_reference_stats(world):
     reference's single-process run (spec_stats.json)."""
     gold = Golden()
     names = ["rmat_s10_ef8", "comps_30", "star_150", "grid_12x12", "edgeless4", "ba_120_a3"]
-    specs = ["kout+async+halve", "hb+async+halve", "none+async+halve", "kout+rem_cas+halve+splice"]
+    # "~spec": labels only, compact giant-bitmap summary exchange
+    specs = ["kout+async+halve", "hb+async+halve", "none+async+halve", "kout+rem_cas+halve+splice",
+             "~kout+rem_cas+halve+splice", "~hb+async+halve"]
     res = _run(_two_phase_worker, world, names, specs)
     for name in names:
         n, off, tgt, orc = gold.graphs[name]
         comps = len(np.unique(orc)) if n else 0
         for text in specs:
-            want = gold.spec_stats[name][text]
+            want = gold.spec_stats[name][text.lstrip("~")]
             for rank in range(world):
                 lab, fu, fv, c, i_s, i_f, lcnt, nact = res[rank][(name, text)]
                 assert np.array_equal(lab, orc), (name, text, rank)

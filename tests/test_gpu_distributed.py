@@ -124,7 +124,8 @@ def _two_phase_gpu_worker(rank, world, port, specs, q):
         lo, hi = shard_bounds(g.offsets, world)[rank]
         out = {}
         for text in specs:
-            r = sharded_two_phase(shard_graph(g.cuda(), lo, hi), parse_spec(text))
+            r = sharded_two_phase(shard_graph(g.cuda(), lo, hi), parse_spec(text.lstrip("~")),
+                                  forest=not text.startswith("~"))
             out[text] = (r.labels.cpu().numpy(), None if r.forest_u is None else r.forest_u.cpu().numpy(),
                          None if r.forest_v is None else r.forest_v.cpu().numpy(), r.insp_sample, r.insp_finish,
                          r.lmax_count, r.n_active)
@@ -139,7 +140,9 @@ def test_two_phase_sampled_ranks_share_one_gpu(world):
     inspection counts / cov / active set equal to the single-GPU pipeline."""
     import torch.multiprocessing as mp
     from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec, static_connectivity_device
-    specs = ["kout+rem_cas+halve+splice", "kout+async+halve", "hb+rem_cas+split+halve", "none+hooks+compress"]
+    # "~spec": labels only through the compact giant-bitmap summary exchange
+    specs = ["kout+rem_cas+halve+splice", "kout+async+halve", "hb+rem_cas+split+halve", "none+hooks+compress",
+             "~kout+rem_cas+halve+splice", "~hb+jtb+twotry", "~kout+hooks+compress"]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -152,7 +155,7 @@ def test_two_phase_sampled_ranks_share_one_gpu(world):
     g = build_csr(gen_rmat(15, 8, seed=5, device=True))
     orc, comps = oracle.components(g.n, g.offsets, g.targets)
     for text in specs:
-        _, st = static_connectivity_device(g, parse_spec(text))
+        _, st = static_connectivity_device(g, parse_spec(text.lstrip("~")))
         for r in range(world):
             labels, fu, fv, i_s, i_f, lcnt, nact = res[r][text]
             assert np.array_equal(labels.astype(np.int64), orc), (text, r)
