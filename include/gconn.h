@@ -211,22 +211,31 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent,
                     unsigned long long* out_count, gc_stats* stats, void* ws,
                     size_t ws_bytes, void* stream);
 
-/* Compact phase-1 exchange for labels-only runs (no forest): summarise this
- * rank's sampled partition (after gc_shard_sample, compressed in place) as
- * its most frequent class — an n-bit bitmap giant_bits[(n+31)/32] plus that
- * class's label (*giant_label, device) — and a pair (v, label) for every
- * other non-singleton vertex (out_u/out_v capacity n, *out_count device).
- * ws: gc_shard_summary_workspace(n) bytes. */
+/* Compact phase-1 exchange for labels-only runs (no forest), in two rounds
+ * (csrc/shard.cu):
+ *   gc_shard_summary: compress parent in place and describe one class as an
+ *     n-bit bitmap giant_bits[(n+31)/32] with its label (*giant_label,
+ *     device): the class of *giant_hint (device vertex id) or, with a NULL
+ *     hint, the probe's most frequent label.  With out_u/out_v (capacity n)
+ *     every other non-singleton vertex v also emits (v, root(v)), counted in
+ *     *out_count (device); NULL pair outputs give the bitmap alone.
+ *   gc_shard_absorb (round A): union every vertex of every rank's bitmap
+ *     class with its class representative (bitmap classes sharing a vertex
+ *     are one class); *main_rep (device) receives rank 0's class
+ *     representative, the hint for round B's summary.
+ *   gc_shard_join (round B): parent := the join of all ranks' partitions
+ *     from their bitmaps + pairs (every bitmap member points at its class's
+ *     smallest label, then the pairs are unioned with the spec's rule).
+ * nranks <= 8.  ws: gc_shard_summary_workspace(n) bytes for the summary,
+ * 4*n + 4096 for absorb / join. */
 size_t gc_shard_summary_workspace(int64_t n);
-int gc_shard_summary(int32_t* parent, int64_t n, uint32_t* giant_bits,
-                     int64_t* giant_label, int32_t* out_u, int32_t* out_v,
-                     unsigned long long* out_count, void* ws, size_t ws_bytes,
-                     void* stream);
-/* Rebuild the join of all ranks' sampled partitions: bits = nranks
- * consecutive bitmaps, giant_labels[nranks] (device); giants sharing a
- * vertex form one class, every member points at the class's smallest giant
- * label, then the k remainder pairs are unioned with the spec's rule.
- * nranks <= 8.  ws: 4*n + 4096 bytes. */
+int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint,
+                     uint32_t* giant_bits, int64_t* giant_label, int32_t* out_u,
+                     int32_t* out_v, unsigned long long* out_count, void* ws,
+                     size_t ws_bytes, void* stream);
+int gc_shard_absorb(int32_t* parent, int64_t n, const uint32_t* bits,
+                    const int64_t* giant_labels, int32_t nranks,
+                    int32_t* main_rep, void* ws, size_t ws_bytes, void* stream);
 int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits,
                   const int64_t* giant_labels, int32_t nranks,
                   const int32_t* us, const int32_t* vs, int64_t k,

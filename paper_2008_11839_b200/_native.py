@@ -91,7 +91,8 @@ _SIGNATURES = {
     "gc_shard_finish": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _VP, _VP, C.POINTER(Stats),
                                   _VP, _SZ, _VP]),
     "gc_shard_summary_workspace": (_SZ, [_I64]),
-    "gc_shard_summary": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "gc_shard_summary": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "gc_shard_absorb": (C.c_int, [_VP, _I64, _VP, _VP, C.c_int32, _VP, _VP, _SZ, _VP]),
     "gc_shard_join": (C.c_int, [_VP, _I64, _VP, _VP, C.c_int32, _VP, _VP, _I64, C.POINTER(Spec), _VP, _SZ, _VP]),
     "gc_find_batch": (C.c_int, [_VP, _I64, _VP, _I64, C.c_int32, _VP, _VP]),
     "gc_canonical_labels": (C.c_int, [_VP, _I64, _VP, _SZ, _VP]),

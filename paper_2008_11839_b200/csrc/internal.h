@@ -145,6 +145,7 @@ struct CooUnionArgs {
   int32_t* lu = nullptr;  // optional: compact list of the edges that merged two trees
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
+  int32_t init_sentinel = -1;  // >= 0: lazily initialise both endpoints first (incremental)
 };
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st);
 

@@ -2,17 +2,19 @@
 //
 // After gc_shard_sample every rank holds the partition induced by the
 // sampled edges of its own rows.  Exchanging it edge by edge costs one pair
-// per sampled row; but almost every sampled vertex sits in the rank's most
-// frequent class (the local giant), so the summary is
-//   * the giant as an n-bit bitmap plus its label, and
-//   * a pair (v, label) for every other non-singleton vertex,
-// i.e. n/8 bytes plus the (small) non-giant remainder.  gc_shard_join
-// rebuilds the join of all ranks' partitions exactly: giants that share a
-// vertex are one class (an 8x8 overlap matrix reduced on the device), every
-// giant member points at its class representative, and the remainder pairs
-// are unioned with the spec's own rule.  The sampled partition — hence
-// L_max, cov, the active set and the finish inspections — equals the
-// single-GPU pipeline's.
+// per sampled row.  Instead each rank describes its partition by
+//   * one large class as an n-bit bitmap plus that class's label, and
+//   * a pair (v, root) for every other non-singleton vertex,
+// and the exchange runs in two rounds:
+//   A. bitmaps of the local giants only; every rank absorbs all of them into
+//      its local partition (giants sharing a vertex are one class; every
+//      member is unioned with its class representative), so local fragments
+//      that touch any giant join it;
+//   B. bitmaps of the now-dominant class plus the remainder pairs, which are
+//      few (fragments that touch no giant anywhere); gc_shard_join rebuilds
+//      the join of every rank's partition from them.
+// The result is exactly the partition of all sampled edges, so L_max, cov,
+// the active set and the finish inspections equal the single-GPU pipeline's.
 #include <climits>
 
 #include "internal.h"
@@ -24,7 +26,20 @@ namespace {
 
 constexpr int kMaxRanks = 8;  // one NVSwitch box; the overlap matrix is one u64
 
-// bitmap word per warp + block-aggregated remainder pairs
+// the bitmap class: the root of the hint vertex, else the probe's candidate
+// (any class gives an exact summary; a large one makes it compact)
+__global__ void k_pick_class(const int32_t* P, const int32_t* hint, unsigned long long* ctr, int64_t* label_out) {
+  int32_t g = int32_t(ctr[C_CAND]);
+  if (hint) {
+    g = *hint;
+    int32_t y;
+    while ((y = P[g]) != g) g = y;
+  }
+  ctr[C_LMAX] = static_cast<unsigned long long>(g);
+  *label_out = g;
+}
+
+// bitmap word per warp + block-aggregated remainder pairs (P compressed)
 __global__ void __launch_bounds__(kEwBlock)
 k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ctr, uint32_t* bits,
           int32_t* out_u, int32_t* out_v, unsigned long long* out_count) {
@@ -42,6 +57,7 @@ k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ct
     }
     const unsigned word = __ballot_sync(0xffffffffu, in_g);
     if (lane == 0 && base + (threadIdx.x & ~31) < n) bits[(base + (threadIdx.x & ~31)) >> 5] = word;
+    if (!out_u) continue;  // bitmap only (round A)
     const unsigned bal = __ballot_sync(0xffffffffu, pair);
     if (!bal) continue;
     unsigned long long pos = 0;
@@ -55,9 +71,6 @@ k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ct
   }
 }
 
-__global__ void k_store_label(const unsigned long long* ctr, int64_t* label_out) {
-  *label_out = int64_t(ctr[C_LMAX]);
-}
 
 // overlap matrix: bit (r * 8 + s) set when giants r < s share a vertex
 __global__ void __launch_bounds__(kEwBlock)
@@ -103,6 +116,95 @@ __global__ void k_giant_classes(const unsigned long long* mat, const int64_t* la
   }
 }
 
+// round A, streaming form (P compressed: P[v] is v's local root).
+// Pass 1: every member v of some giant marks its local root with the bit of
+// the giant's class (one byte per root); a root that collects bits of two
+// classes joins them (recorded in the class matrix).  Pass 2: every vertex
+// whose local root is marked points at its class representative.
+__device__ __forceinline__ int lowest_class(unsigned m) { return __ffs(int(m)) - 1; }
+
+__global__ void __launch_bounds__(kEwBlock)
+k_absorb_mark(const int32_t* __restrict__ P, int32_t n, const uint32_t* __restrict__ bits, int64_t words,
+              int32_t nranks, const int32_t* __restrict__ cls, uint32_t* mark, unsigned long long* mat) {
+  // the giant's root is shared by ~all members: a per-thread memo of the
+  // last (root, class) marked keeps the hot word from being hit 10^8 times
+  int32_t last_r = -1;
+  int last_c = -1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const int64_t w = v >> 5;
+    const uint32_t bit = 1u << (v & 31);
+    int c = -1;
+    for (int q = 0; q < nranks; ++q)
+      if (bits[int64_t(q) * words + w] & bit) {
+        c = cls[q];
+        break;
+      }
+    if (c < 0) continue;
+    const int32_t r = P[v];
+    if (r == last_r && c == last_c) continue;
+    last_r = r;
+    last_c = c;
+    uint32_t* word = mark + (r >> 2);
+    const uint32_t mine = (1u << c) << (8 * (r & 3));
+    if (ld_weak(reinterpret_cast<const int32_t*>(word)) & mine) continue;  // stale => one extra atomic
+    const uint32_t old = (atomicOr(word, mine) >> (8 * (r & 3))) & 0xffu;
+    if (old && !(old & (1u << c))) atomicOr(mat, 1ull << (lowest_class(old) * 8 + c));
+  }
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const int32_t* __restrict__ cls_rep) {
+  int32_t last_r = -1;
+  uint32_t m = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const int32_t r = P[v];
+    if (r != last_r) {
+      last_r = r;
+      m = (mark[r >> 2] >> (8 * (r & 3))) & 0xffu;
+    }
+    if (m) P[v] = cls_rep[lowest_class(m)];
+  }
+}
+
+// classes of the giants from a class matrix (bit i*8+j: i and j joined).
+// pass 0: over ranks, from the bitmap overlaps.  pass 1: merges the pass-0
+// classes that met at a shared local root.  Per rank: cls[r] = class index
+// (a rank id), rep[r] = the class's smallest giant label; cls_rep[c] = rep for
+// every class index c a mark byte can carry (pass-0 and merged ids alike).
+__global__ void k_absorb_classes(const unsigned long long* mat, const int64_t* labels, int32_t nranks,
+                                 int32_t* cls, int32_t* rep, int32_t* cls_rep, int pass) {
+  int par[kMaxRanks];
+  for (int r = 0; r < kMaxRanks; ++r) par[r] = r;
+  auto root = [&](int x) {
+    while (par[x] != x) x = par[x];
+    return x;
+  };
+  const unsigned long long m = *mat;
+  for (int r = 0; r < kMaxRanks; ++r)
+    for (int s = 0; s < kMaxRanks; ++s)
+      if (r != s && ((m >> (r * 8 + s)) & 1ull)) {
+        const int a = root(r), b = root(s);
+        if (a != b) par[a > b ? a : b] = a < b ? a : b;
+      }
+  int c0[kMaxRanks];
+  for (int r = 0; r < nranks; ++r) {
+    c0[r] = pass == 0 ? r : cls[r];
+    cls[r] = root(c0[r]);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    int64_t best = LLONG_MAX;
+    for (int s = 0; s < nranks; ++s)
+      if (cls[s] == cls[r] && labels[s] < best) best = labels[s];
+    rep[r] = int32_t(best);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    cls_rep[c0[r]] = rep[r];
+    cls_rep[cls[r]] = rep[r];
+  }
+}
+
 __global__ void __launch_bounds__(kEwBlock)
 k_join_init(int32_t* P, int32_t n, const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
             const int32_t* __restrict__ rep) {
@@ -128,28 +230,63 @@ using namespace gc;
 
 extern "C" {
 
-size_t gc_shard_summary_workspace(int64_t n) { return size_t(n > 0 ? n : 1) * 4 + 4096; }
+size_t gc_shard_summary_workspace(int64_t n) { (void)n; return 4096; }
 
-int gc_shard_summary(int32_t* parent, int64_t n, uint32_t* giant_bits, int64_t* giant_label, int32_t* out_u,
-                     int32_t* out_v, unsigned long long* out_count, void* ws, size_t ws_bytes, void* stream) {
+int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint, uint32_t* giant_bits,
+                     int64_t* giant_label, int32_t* out_u, int32_t* out_v, unsigned long long* out_count, void* ws,
+                     size_t ws_bytes, void* stream) {
   return guarded([&] {
     require(n >= 0 && n < (int64_t(1) << 31), GC_ERR_MALFORMED, "bad length");
-    require(giant_label && out_count && (n == 0 || (parent && giant_bits && out_u && out_v)), GC_ERR_ARG,
-            "null argument");
+    require(giant_label && (n == 0 || (parent && giant_bits)), GC_ERR_ARG, "null argument");
+    require((out_u == nullptr) == (out_v == nullptr) && (out_u == nullptr || out_count), GC_ERR_ARG,
+            "pairs need u, v and a count");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Arena a(ws, ws_bytes);
     unsigned long long* ctr = a.take<unsigned long long>(C_COUNT_);
-    int32_t* hist = a.take<int32_t>(n);
     GC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
-    GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    if (out_count) GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
     const int32_t nn = int32_t(n);
-    if (nn) {
-      (k_compress<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
-      run_mode(parent, nn, hist, ctr, st);  // the local giant: most frequent label, ties -> smaller
-      (k_summary<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,
-                                                                out_count), count_launch());
+    if (nn == 0) {
+      GC_CUDA(cudaMemsetAsync(giant_label, 0, sizeof(int64_t), st));
+      return;
     }
-    (k_store_label<<<1, 1, 0, st>>>(ctr, giant_label), count_launch());
+    (k_compress<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
+    if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr), count_launch());
+    (k_pick_class<<<1, 1, 0, st>>>(parent, giant_hint, ctr, giant_label), count_launch());
+    // a null pair output summarises the bitmap class only (round A)
+    (k_summary<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,
+                                                              out_count), count_launch());
+    GC_CHECK_LAUNCH();
+  });
+}
+
+int gc_shard_absorb(int32_t* parent, int64_t n, const uint32_t* bits, const int64_t* giant_labels,
+                    int32_t nranks, int32_t* main_rep, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && n < (int64_t(1) << 31), GC_ERR_MALFORMED, "bad length");
+    require(nranks >= 1 && nranks <= kMaxRanks, GC_ERR_ARG, "1..8 ranks supported");
+    require(main_rep != nullptr, GC_ERR_ARG, "null representative output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Arena a(ws, ws_bytes);
+    unsigned long long* mat = a.take<unsigned long long>(2);
+    int32_t* cls = a.take<int32_t>(kMaxRanks);
+    int32_t* rep = a.take<int32_t>(kMaxRanks);
+    int32_t* cls_rep = a.take<int32_t>(kMaxRanks);
+    const int32_t nn = int32_t(n);
+    if (nn == 0) return;
+    uint32_t* mark = a.take<uint32_t>((n + 3) / 4);  // one byte of class bits per local root
+    const int64_t words = (n + 31) / 32;
+    GC_CUDA(cudaMemsetAsync(mat, 0, 16, st));
+    GC_CUDA(cudaMemsetAsync(mark, 0, size_t((n + 3) / 4) * 4, st));
+    // parent is compressed by the preceding gc_shard_summary
+    (k_overlap<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, mat), count_launch());
+    (k_absorb_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, cls, rep, cls_rep, 0), count_launch());
+    (k_absorb_mark<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, cls,
+                                                                  mark, mat + 1), count_launch());
+    // classes joined through a shared local root
+    (k_absorb_classes<<<1, 1, 0, st>>>(mat + 1, giant_labels, nranks, cls, rep, cls_rep, 1), count_launch());
+    (k_absorb_apply<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, mark, cls_rep), count_launch());
+    GC_CUDA(cudaMemcpyAsync(main_rep, rep, 4, cudaMemcpyDeviceToDevice, st));  // rank 0's class
     GC_CHECK_LAUNCH();
   });
 }

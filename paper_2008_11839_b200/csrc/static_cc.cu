@@ -606,12 +606,14 @@ int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32
   return guarded([&] {
     check_static_args(g, spec, parent);
     check_shard_spec(spec);
-    require(out_u && out_v && out_count, GC_ERR_ARG, "null merging-edge output");
+    // NULL outputs: sample only (the compact summary exchange needs no list)
+    const bool record = out_u != nullptr;
+    require(!record || (out_v && out_count), GC_ERR_ARG, "null merging-edge output");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    if (record) GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
     Pipeline pl(*g, *spec, parent, nullptr, nullptr, ws, ws_bytes, st);
     const bool edges = spec->splice != GC_SPLICE_ATOMIC;  // root-based: record real merging edges
-    if (edges) {
+    if (record && edges) {
       pl.lu = out_u;
       pl.lv = out_v;
       pl.lcount = out_count;
@@ -620,7 +622,7 @@ int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32
     pl.init_sets(sc);
     if (spec->sample == GC_SAMPLE_KOUT) run_kout(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
     if (spec->sample == GC_SAMPLE_HB) run_hb(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
-    if (!edges && pl.n) {
+    if (record && !edges && pl.n) {
       (k_root_transitions<<<grid_for(pl.n, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nullptr, pl.n, out_u, out_v,
                                                                            out_count), count_launch());
       GC_CHECK_LAUNCH();

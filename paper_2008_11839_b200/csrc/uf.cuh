@@ -29,6 +29,11 @@ struct UFState {
   int32_t* lu = nullptr;  // optional compact list of merging edges (distributed exchange)
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
+  // L1-cacheable first reads (see Reader).  Kernels that initialise slots
+  // while other threads union (incremental lazy init) turn them off: a stale
+  // L1 line could still hold the uninitialised sentinel, which is not an
+  // ancestor of anything.
+  bool weak = true;
 };
 
 template <bool FOREST>
@@ -58,7 +63,8 @@ __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u
 constexpr int kWeakReads = 48;
 
 struct Reader {
-  int budget = kWeakReads;
+  int budget;
+  __device__ __forceinline__ explicit Reader(bool weak = true) : budget(weak ? kWeakReads : 0) {}
   __device__ __forceinline__ int32_t operator()(const int32_t* p) {
     if (budget > 0) {
       --budget;
@@ -70,8 +76,11 @@ struct Reader {
 
 // ---------------------------------------------------------------- finds ---
 
+// `known` (>= 0): a value of P[u] this thread already holds (one it just
+// wrote, or read this iteration) — used instead of the first read.  A held
+// value is at worst a stale read, which the rules already tolerate.
 template <int FIND>
-__device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd) {
+__device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd, int32_t known = -1) {
   if constexpr (FIND == GC_FIND_NAIVE) {
     // dset.py:109-112
     while (true) {
@@ -96,7 +105,7 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd) {
     return r;
   } else if constexpr (FIND == GC_FIND_SPLIT) {
     // dset.py:126-135
-    int32_t v = rd(P + u);
+    int32_t v = known >= 0 ? known : rd(P + u);
     int32_t w = rd(P + v);
     while (v != w) {
       atomicCAS(P + u, v, w);
@@ -106,12 +115,14 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd) {
     }
     return v;
   } else if constexpr (FIND == GC_FIND_HALVE) {
-    // dset.py:138-147
-    int32_t v = rd(P + u);
+    // dset.py:138-147.  `u = p[u]` after the CAS is the value the CAS left
+    // there: w when it succeeded, else the value it found — taken from the
+    // CAS result instead of a second dependent read of the same word.
+    int32_t v = known >= 0 ? known : rd(P + u);
     int32_t w = rd(P + v);
     while (v != w) {
-      atomicCAS(P + u, v, w);
-      u = rd(P + u);
+      const int32_t old = atomicCAS(P + u, v, w);
+      u = old == v ? w : old;
       v = rd(P + u);
       w = rd(P + v);
     }
@@ -166,7 +177,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t v) {
   // dset.py:222-234
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   int32_t pu = find<FIND>(u, P, rd);
   int32_t pv = find<FIND>(v, P, rd);
   while (pu != pv) {
@@ -185,7 +196,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_hooks(const UFState& s, int32_t u, int32_t v) {
   // dset.py:237-252: claim the hook slot, then an uncontended parent write.
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   const int32_t unhooked = s.n;
   int32_t pu = find<FIND>(u, P, rd);
   int32_t pv = find<FIND>(v, P, rd);
@@ -208,7 +219,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_early(const UFState& s, int32_t u, int32_t v) {
   // dset.py:255-274
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   int32_t pu = u, pv = v;
   bool merged = false;
   while (pu != pv) {
@@ -235,7 +246,7 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
   // dset.py:277-300.  A failed re-validation re-derives and loops, as the
   // reference does (the paper's pseudocode returns instead).
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   int32_t ru = u, rv = v;
   while (true) {
     int32_t pru = rd(P + ru);
@@ -275,7 +286,7 @@ template <int FIND, int SPLICE, bool FOREST>
 __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32_t v) {
   // dset.py:303-316
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   int32_t ru = u, rv = v;
   while (true) {
     int32_t pru = rd(P + ru);
@@ -288,8 +299,9 @@ __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32
     if (ru == pru && cas(P + ru, ru, prv)) {
       record<FOREST>(s, ru, u, v);
       if constexpr (FIND != GC_FIND_NAIVE) {
-        find<FIND>(u, P, rd);
-        find<FIND>(v, P, rd);
+        // P[ru] is now prv and P[rv] was just read as prv
+        find<FIND>(u, P, rd, (u == ru || u == rv) ? prv : -1);
+        find<FIND>(v, P, rd, (v == ru || v == rv) ? prv : -1);
       }
       return true;
     }
@@ -301,7 +313,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_jtb(const UFState& s, int32_t u, int32_t v) {
   // dset.py:319-331: link the lower (rank, id) root under the higher one
   int32_t* P = s.P;
-  Reader rd;
+  Reader rd(s.weak);
   while (true) {
     int32_t ru = find<FIND>(u, P, rd);
     int32_t rv = find<FIND>(v, P, rd);

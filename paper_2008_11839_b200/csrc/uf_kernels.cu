@@ -83,11 +83,20 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
 template <class R>
 __global__ void __launch_bounds__(256)
 k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
-            const uint8_t* __restrict__ skip) {
+            const uint8_t* __restrict__ skip, int32_t sentinel) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
     if (skip && skip[i]) continue;
-    R::unite(s, ldg32(us + i), ldg32(vs + i));
+    const int32_t u = ldg32(us + i), v = ldg32(vs + i);
+    if (sentinel >= 0) {
+      // ensure_init (driver.py:620-625) fused into the insert: every parent
+      // a union reads is either one of its own endpoints (initialised right
+      // here) or an ancestor, which was a root — hence initialised — when it
+      // was linked.  The launcher turns L1-cached reads off for this mode.
+      if (ld_acq(s.P + u) == sentinel) atomicCAS(s.P + u, sentinel, u);
+      if (ld_acq(s.P + v) == sentinel) atomicCAS(s.P + v, sentinel, v);
+    }
+    R::unite(s, u, v);
   }
 }
 
@@ -176,10 +185,12 @@ struct CooLaunch {
   void go() const {
     if (a.k <= 0) return;
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
+    s.weak = a.init_sentinel < 0;
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip), ::gc::count_launch());
+    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel),
+     ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
@@ -194,6 +205,7 @@ struct RacyLaunch {
   void go() const {
     if (a.k <= 0) return;
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n};
+    s.weak = false;  // slots are initialised inside this launch
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;

@@ -133,7 +133,7 @@ class GpuEngine:
                                        C.byref(low.s), aux.data_ptr() if aux is not None else None, None, None,
                                        _stream()))
 
-    def _shard_call(self, fn, shard, spec, parent):
+    def _shard_call(self, fn, shard, spec, parent, record=True):
         import ctypes as C
         from . import _native as N
         from .api import LoweredSpec, _csr, _stream, _workspace
@@ -143,21 +143,26 @@ class GpuEngine:
         csr, keep = _csr(shard)
         lib = N.lib()
         ws = _workspace(lib.gc_workspace_size(n, shard.m, C.byref(low.s)))
+        st = N.Stats()
+        if not record:
+            N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), parent.data_ptr(), None, None, None,
+                                     C.byref(st), ws.data_ptr(), ws.numel(), _stream()))
+            return None, None, st
         out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-        st = N.Stats()
         N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), parent.data_ptr(), out_u.data_ptr(),
                                  out_v.data_ptr(), cnt.data_ptr(), C.byref(st), ws.data_ptr(), ws.numel(),
                                  _stream()))
         c = int(cnt.item())
         return out_u[:c], out_v[:c], st
 
-    def shard_sample(self, shard, spec):
-        """gc_shard_sample: identity parent + the sampler over this block's rows."""
+    def shard_sample(self, shard, spec, record=True):
+        """gc_shard_sample: identity parent + the sampler over this block's rows
+        (record=False: no merge list, for the compact summary exchange)."""
         torch = _torch()
         parent = torch.empty(max(shard.n, 1), dtype=torch.int32, device="cuda")
-        mu, mv, st = self._shard_call("gc_shard_sample", shard, spec, parent)
+        mu, mv, st = self._shard_call("gc_shard_sample", shard, spec, parent, record)
         return parent, mu, mv, int(st.insp_sample)
 
     def shard_finish(self, shard, spec, parent):
@@ -166,22 +171,42 @@ class GpuEngine:
         return mu, mv, {"insp_finish": int(st.insp_finish), "l_max": int(st.l_max),
                         "lmax_count": int(st.lmax_count), "n_active": int(st.n_active)}
 
-    def shard_summary(self, parent):
-        """gc_shard_summary: (giant bitmap int32 words, giant label, remainder pairs)."""
+    def shard_summary(self, parent, hint=None, pairs=True):
+        """gc_shard_summary: (bitmap int32 words, class label, remainder pairs or None)."""
         from . import _native as N
         from .api import _stream, _workspace
         torch = _torch()
         n = parent.numel()
         words = torch.zeros(max((n + 31) // 32, 1), dtype=torch.int32, device="cuda")
         label = torch.zeros(1, dtype=torch.int64, device="cuda")
-        out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
-        out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
-        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out_u = out_v = cnt = None
+        if pairs:
+            out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         ws = _workspace(N.lib().gc_shard_summary_workspace(n))
-        N.check(N.lib().gc_shard_summary(parent.data_ptr(), n, words.data_ptr(), label.data_ptr(), out_u.data_ptr(),
-                                         out_v.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        N.check(N.lib().gc_shard_summary(parent.data_ptr(), n, ptr(hint), words.data_ptr(), label.data_ptr(),
+                                         ptr(out_u), ptr(out_v), ptr(cnt), ws.data_ptr(), ws.numel(), _stream()))
+        if not pairs:
+            return words, label, None, None
         c = int(cnt.item())
         return words, label, out_u[:c], out_v[:c]
+
+    def shard_absorb(self, parent, words_all, labels_all):
+        """gc_shard_absorb (round A); returns rank 0's class representative (device)."""
+        from . import _native as N
+        from .api import _stream, _workspace
+        torch = _torch()
+        n = parent.numel()
+        rep = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ws = _workspace(4 * n + 8192)
+        words_all = words_all.contiguous()
+        labels_all = labels_all.contiguous()
+        N.check(N.lib().gc_shard_absorb(parent.data_ptr(), n, words_all.data_ptr(), labels_all.data_ptr(),
+                                        int(labels_all.numel()), rep.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        _stream()))
+        return rep
 
     def shard_join(self, parent, words_all, labels_all, us, vs, spec):
         """gc_shard_join over all ranks' summaries (words_all: nranks x words)."""
@@ -387,24 +412,34 @@ def _exchange_and_merge(parent, mu, mv, spec, engine, group, rank):
     return torch.cat(fu), torch.cat(fv), total
 
 
-def _exchange_summary(parent, spec, engine, group):
-    """Phase-1 exchange for labels-only runs: each rank's local giant as an
-    n-bit bitmap + its label, and the non-giant remainder as pairs; every
-    rank rebuilds the exact join (gc_shard_join).  Returns the number of
-    remainder pairs exchanged."""
+def _gather_words(words, label, group):
     torch = _torch()
     dist = _dist()
     dev = _comm_device(group)
     world = dist.get_world_size(group)
-    words, label, ru, rv = engine.shard_summary(parent)
     wl = [torch.empty_like(words, device=dev) for _ in range(world)]
     dist.all_gather(wl, words.to(dev), group=group)
     ll = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(ll, label.to(dev), group=group)
+    return torch.stack(wl), torch.cat(ll)
+
+
+def _exchange_summary(parent, spec, engine, group):
+    """Phase-1 exchange for labels-only runs (csrc/shard.cu): round A
+    all-gathers each rank's local giant as an n-bit bitmap and absorbs all
+    of them locally; round B all-gathers the dominant class's bitmap plus the
+    few remaining non-singleton vertices as pairs, and every rank rebuilds
+    the same exact join.  Returns the number of remainder pairs exchanged."""
+    torch = _torch()
+    words, label, _, _ = engine.shard_summary(parent, pairs=False)
+    wa, la = _gather_words(words, label, group)
+    rep = engine.shard_absorb(parent, wa.to(parent.device), la.to(parent.device))
+    words, label, ru, rv = engine.shard_summary(parent, hint=rep, pairs=True)
+    wb, lb = _gather_words(words, label, group)
     pairs = all_gather_pairs(ru, rv, group)
     us = torch.cat([p[0] for p in pairs]).to(parent.device)
     vs = torch.cat([p[1] for p in pairs]).to(parent.device)
-    engine.shard_join(parent, torch.stack(wl).to(parent.device), torch.cat(ll).to(parent.device), us, vs, spec)
+    engine.shard_join(parent, wb.to(parent.device), lb.to(parent.device), us, vs, spec)
     return int(us.numel())
 
 
@@ -428,18 +463,18 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     Each rank's kept merging edges form a spanning forest of the whole graph.
 
     With ``forest=False`` (labels only) step 2 exchanges a compact summary
-    instead of the sampled merging edges: each rank's local giant as an
-    n-bit bitmap plus the pairs of its other non-singleton vertices, from
-    which every rank rebuilds the same join (``_exchange_summary``) — n/8
-    bytes and a small remainder instead of one pair per sampled row.
+    instead of the sampled merging edges (``_exchange_summary``): two rounds
+    of n-bit class bitmaps plus the few vertices outside the dominant class
+    as pairs, instead of one pair per sampled row.
     """
     _check_two_phase_spec(spec)
     dist = _dist()
     engine = engine or GpuEngine()
     rank = dist.get_rank(group)
-    parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec)
+    summary = not forest and spec.sample is not SampleKind.NONE
+    parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec, record=not summary)
     torch = _torch()
-    if forest or spec.sample is SampleKind.NONE:
+    if not summary:
         f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
     else:
         x1 = _exchange_summary(parent, spec, engine, group)

@@ -57,7 +57,7 @@ class CpuEngine:
         return torch.tensor(mu, dtype=torch.int32), torch.tensor(mv, dtype=torch.int32)
 
     # two-phase sharded pipeline (gc_shard_sample / gc_shard_finish semantics)
-    def shard_sample(self, shard, spec):
+    def shard_sample(self, shard, spec, record=True):
         n = shard.n
         p = np.arange(n, dtype=np.int64)
         off, tgt = shard.offsets, shard.targets
@@ -127,23 +127,28 @@ class CpuEngine:
                 {"insp_finish": insp, "l_max": lmax, "lmax_count": cnt, "n_active": active})
 
     # compact summary exchange (gc_shard_summary / gc_shard_join semantics)
-    def shard_summary(self, parent):
+    def shard_summary(self, parent, hint=None, pairs=True):
         p = parent.numpy().astype(np.int64)
         n = len(p)
         lab = np.array([_find(p, v) for v in range(n)], dtype=np.int64)
-        g = int(np.bincount(lab, minlength=n).argmax()) if n else 0
+        if hint is not None:
+            g = int(lab[int(hint.item())])
+        else:
+            g = int(np.bincount(lab, minlength=n).argmax()) if n else 0
         in_g = lab == g
         nw = max((n + 31) // 32, 1)
         bits = np.zeros(nw * 32, dtype=bool)
         bits[:n] = in_g
         words = np.packbits(bits, bitorder="little").view(np.uint32).view(np.int32)
-        pair = (~in_g) & (lab != np.arange(n))
         parent.copy_(torch.from_numpy(lab.astype(np.int32)))
+        if not pairs:
+            return torch.from_numpy(words.copy()), torch.tensor([g], dtype=torch.int64), None, None
+        pair = (~in_g) & (lab != np.arange(n))
         return (torch.from_numpy(words.copy()), torch.tensor([g], dtype=torch.int64),
                 torch.from_numpy(np.flatnonzero(pair).astype(np.int32)), torch.from_numpy(lab[pair].astype(np.int32)))
 
-    def shard_join(self, parent, words_all, labels_all, us, vs, spec):
-        n = parent.numel()
+    @staticmethod
+    def _classes(words_all, labels_all, n):
         W = words_all.numpy().view(np.uint32)
         R = W.shape[0]
         bits = np.unpackbits(W.view(np.uint8).reshape(R, -1), axis=1, bitorder="little")[:, :n].astype(bool)
@@ -161,9 +166,26 @@ class CpuEngine:
                     if a != b:
                         par[max(a, b)] = min(a, b)
         rep = [min(int(labels[s]) for s in range(R) if root(s) == root(r)) for r in range(R)]
+        return bits, rep
+
+    def shard_absorb(self, parent, words_all, labels_all):
+        p = parent.numpy().astype(np.int64)
+        n = len(p)
+        bits, rep = self._classes(words_all, labels_all, n)
+        for v in range(n):
+            for r in range(len(rep)):
+                if bits[r, v]:
+                    _union(p, v, rep[r])
+                    break
+        parent.copy_(torch.from_numpy(p.astype(np.int32)))
+        return torch.tensor([rep[0]], dtype=torch.int32)
+
+    def shard_join(self, parent, words_all, labels_all, us, vs, spec):
+        n = parent.numel()
+        bits, rep = self._classes(words_all, labels_all, n)
         p = np.arange(n, dtype=np.int64)
         for v in range(n):
-            for r in range(R):
+            for r in range(len(rep)):
                 if bits[r, v]:
                     p[v] = rep[r]
                     break
