@@ -10,11 +10,11 @@ struct SamplerWs {
   int32_t* coo_u = nullptr;   // k-out random mode pairs
   int32_t* coo_v = nullptr;
   unsigned long long* key = nullptr;  // BFS / LDD claim word: (round << 32) | parent-or-cluster
-  int32_t* par = nullptr;     // BFS discovery parent (re-rooted for the forest)
   int32_t* q0 = nullptr;      // frontier queues (HB: phase-2 roots)
   int32_t* q1 = nullptr;
   uint32_t* fb0 = nullptr;    // BFS frontier bitmaps
   uint32_t* fb1 = nullptr;
+  uint32_t* vis = nullptr;    // BFS visited bitmap (union of all frontiers so far)
   unsigned long long* stat = nullptr;  // frontier [count, degree sum] x 2
   uint16_t* start = nullptr;  // LDD start round per vertex
   int32_t* order = nullptr;   // LDD vertices bucketed by start round
@@ -39,9 +39,9 @@ void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
     w.stat = a.template take<unsigned long long>(8);
   }
   if (s.sample == GC_SAMPLE_BFS) {
-    w.par = a.template take<int32_t>(n);
     w.fb0 = a.template take<uint32_t>((n + 31) / 32);
     w.fb1 = a.template take<uint32_t>((n + 31) / 32);
+    w.vis = a.template take<uint32_t>((n + 31) / 32);
   }
   if (s.sample == GC_SAMPLE_LDD) {
     w.start = a.template take<uint16_t>(n);

@@ -87,14 +87,20 @@ k_overlap(const uint32_t* __restrict__ bits, int64_t words, int32_t nranks, unsi
       for (int s = r + 1; s < kMaxRanks; ++s)
         if (b[r] & b[s]) m |= 1ull << (r * 8 + s);
   }
+  // one atomic per block (every warp of an overlapping region sets bits)
+  __shared__ unsigned long long bm;
+  if (threadIdx.x == 0) bm = 0;
+  __syncthreads();
   for (int o = 16; o > 0; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
-  if ((threadIdx.x & 31) == 0 && m) atomicOr(mat, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicOr(&bm, m);
+  __syncthreads();
+  if (threadIdx.x == 0 && bm) atomicOr(mat, bm);
 }
 
 // super-classes of the giants (tiny union-find over <= 8 nodes); rep[r] =
 // smallest giant label in r's class
 __global__ void k_giant_classes(const unsigned long long* mat, const int64_t* labels, int32_t nranks,
-                                int32_t* rep) {
+                                int32_t* rep, int32_t* single) {
   int par[kMaxRanks];
   for (int r = 0; r < kMaxRanks; ++r) par[r] = r;
   auto root = [&](int x) {
@@ -114,37 +120,61 @@ __global__ void k_giant_classes(const unsigned long long* mat, const int64_t* la
       if (root(s) == root(r) && labels[s] < best) best = labels[s];
     rep[r] = int32_t(best);
   }
+  if (single) {
+    int one = 1;
+    for (int r = 1; r < nranks; ++r) one &= rep[r] == rep[0];
+    *single = one;
+  }
 }
 
 // round A, streaming form (P compressed: P[v] is v's local root).
-// Pass 1: every member v of some giant marks its local root with the bit of
-// the giant's class (one byte per root); a root that collects bits of two
-// classes joins them (recorded in the class matrix).  Pass 2: every vertex
-// whose local root is marked points at its class representative.
+// Pass 1: every non-root member v of some giant marks its local root with
+// the bit of the giant's class (one byte per root).  Local roots are never
+// marked by themselves — at P ranks most bitmap members are local singletons
+// (their rows live on other ranks), and marking those would be one random
+// atomic per vertex; the apply pass reads a root's own bitmap class instead.
+// A root whose class differs from a member's joins the two classes.
+// Pass 2: every vertex whose local root carries a class points at that
+// class's representative.
 __device__ __forceinline__ int lowest_class(unsigned m) { return __ffs(int(m)) - 1; }
+
+// class of v's first bitmap (-1: none).  All rank words are loaded up front:
+// an early-exit loop would serialise up to eight dependent cache misses.
+__device__ __forceinline__ int first_rank(const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
+                                          int64_t v) {
+  const int64_t w = v >> 5;
+  uint32_t b[kMaxRanks];
+#pragma unroll
+  for (int q = 0; q < kMaxRanks; ++q) b[q] = q < nranks ? __ldg(bits + int64_t(q) * words + w) : 0u;
+  unsigned hit = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxRanks; ++q) hit |= ((b[q] >> (v & 31)) & 1u) << q;
+  return hit ? __ffs(int(hit)) - 1 : -1;
+}
+
+__device__ __forceinline__ int bitmap_class(const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
+                                            const int32_t* __restrict__ cls, int64_t v) {
+  const int q = first_rank(bits, words, nranks, v);
+  return q < 0 ? -1 : cls[q];
+}
 
 __global__ void __launch_bounds__(kEwBlock)
 k_absorb_mark(const int32_t* __restrict__ P, int32_t n, const uint32_t* __restrict__ bits, int64_t words,
               int32_t nranks, const int32_t* __restrict__ cls, uint32_t* mark, unsigned long long* mat) {
-  // the giant's root is shared by ~all members: a per-thread memo of the
-  // last (root, class) marked keeps the hot word from being hit 10^8 times
+  // a per-thread memo of the last (root, class) handled keeps the giant's
+  // root word from being hit once per member
   int32_t last_r = -1;
   int last_c = -1;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const int64_t w = v >> 5;
-    const uint32_t bit = 1u << (v & 31);
-    int c = -1;
-    for (int q = 0; q < nranks; ++q)
-      if (bits[int64_t(q) * words + w] & bit) {
-        c = cls[q];
-        break;
-      }
-    if (c < 0) continue;
     const int32_t r = P[v];
-    if (r == last_r && c == last_c) continue;
+    if (r == int32_t(v)) continue;
+    const int c = bitmap_class(bits, words, nranks, cls, v);
+    if (c < 0 || (r == last_r && c == last_c)) continue;
     last_r = r;
     last_c = c;
+    const int cr = bitmap_class(bits, words, nranks, cls, r);
+    if (cr >= 0 && cr != c) atomicOr(mat, 1ull << (cr * 8 + c));
     uint32_t* word = mark + (r >> 2);
     const uint32_t mine = (1u << c) << (8 * (r & 3));
     if (ld_weak(reinterpret_cast<const int32_t*>(word)) & mine) continue;  // stale => one extra atomic
@@ -154,7 +184,8 @@ k_absorb_mark(const int32_t* __restrict__ P, int32_t n, const uint32_t* __restri
 }
 
 __global__ void __launch_bounds__(kEwBlock)
-k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const int32_t* __restrict__ cls_rep) {
+k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const uint32_t* __restrict__ bits,
+               int64_t words, int32_t nranks, const int32_t* __restrict__ cls0, const int32_t* __restrict__ cls_rep) {
   int32_t last_r = -1;
   uint32_t m = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -163,6 +194,8 @@ k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const i
     if (r != last_r) {
       last_r = r;
       m = (mark[r >> 2] >> (8 * (r & 3))) & 0xffu;
+      const int cr = bitmap_class(bits, words, nranks, cls0, r);
+      if (cr >= 0) m |= 1u << cr;
     }
     if (m) P[v] = cls_rep[lowest_class(m)];
   }
@@ -205,20 +238,38 @@ __global__ void k_absorb_classes(const unsigned long long* mat, const int64_t* l
   }
 }
 
+// one class (the usual case): OR the ranks' bitmaps once, word-parallel,
+// then one bitmap test per vertex (the general path tests up to 8)
+__global__ void __launch_bounds__(kEwBlock)
+k_or_bitmaps(const uint32_t* __restrict__ bits, int64_t words, int32_t nranks, uint32_t* out,
+             const int32_t* single) {
+  if (!*single) return;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t x = 0;
+    for (int q = 0; q < nranks; ++q) x |= bits[int64_t(q) * words + w];
+    out[w] = x;
+  }
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_join_init_one(int32_t* P, int32_t n, const uint32_t* __restrict__ any, const int32_t* __restrict__ rep,
+                const int32_t* single) {
+  if (!*single) return;
+  const int32_t r0 = rep[0];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    P[v] = (any[v >> 5] >> (v & 31)) & 1u ? r0 : int32_t(v);
+}
+
 __global__ void __launch_bounds__(kEwBlock)
 k_join_init(int32_t* P, int32_t n, const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
-            const int32_t* __restrict__ rep) {
+            const int32_t* __restrict__ rep, const int32_t* single) {
+  if (*single) return;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const int64_t w = v >> 5;
-    const uint32_t bit = 1u << (v & 31);
-    int32_t p = int32_t(v);
-    for (int r = 0; r < nranks; ++r)
-      if (bits[int64_t(r) * words + w] & bit) {
-        p = rep[r];
-        break;
-      }
-    P[v] = p;
+    const int q = first_rank(bits, words, nranks, v);
+    P[v] = q < 0 ? int32_t(v) : rep[q];
   }
 }
 
@@ -285,7 +336,8 @@ int gc_shard_absorb(int32_t* parent, int64_t n, const uint32_t* bits, const int6
                                                                   mark, mat + 1), count_launch());
     // classes joined through a shared local root
     (k_absorb_classes<<<1, 1, 0, st>>>(mat + 1, giant_labels, nranks, cls, rep, cls_rep, 1), count_launch());
-    (k_absorb_apply<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, mark, cls_rep), count_launch());
+    (k_absorb_apply<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, mark, bits, words, nranks, cls,
+                                                                   cls_rep), count_launch());
     GC_CUDA(cudaMemcpyAsync(main_rep, rep, 4, cudaMemcpyDeviceToDevice, st));  // rank 0's class
     GC_CHECK_LAUNCH();
   });
@@ -303,6 +355,8 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits, const int64_
     Arena a(ws, ws_bytes);
     unsigned long long* mat = a.take<unsigned long long>(1);
     int32_t* rep = a.take<int32_t>(kMaxRanks);
+    int32_t* single = a.take<int32_t>(1);
+    uint32_t* any = a.take<uint32_t>((n + 31) / 32);
     int32_t* aux = nullptr;
     const UFConfig c{spec->finish, spec->find, spec->splice};
     if (c.unite == GC_FINISH_HOOKS || c.unite == GC_FINISH_REM_LOCK) aux = a.take<int32_t>(n);
@@ -311,8 +365,12 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits, const int64_
     const int64_t words = (n + 31) / 32;
     GC_CUDA(cudaMemsetAsync(mat, 0, 8, st));
     (k_overlap<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, mat), count_launch());
-    (k_giant_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, rep), count_launch());
-    (k_join_init<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, rep),
+    (k_giant_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, rep, single), count_launch());
+    (k_or_bitmaps<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, any, single),
+     count_launch());
+    (k_join_init_one<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, any, rep, single),
+     count_launch());
+    (k_join_init<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, rep, single),
      count_launch());
     GC_CHECK_LAUNCH();
     if (aux) fill(aux, nn, c.unite == GC_FINISH_HOOKS ? nn : 0, st);

@@ -412,7 +412,7 @@ extern "C" {
 
 const char* gc_last_error(void) { return g_err.c_str(); }
 
-const char* gc_version(void) { return "gconn-b200 0.1.0 (sm_100a)"; }
+const char* gc_version(void) { return "gconn-b200 0.1.0 (sm_100a, built " __DATE__ " " __TIME__ ")"; }
 
 size_t gc_workspace_size(int64_t n, int64_t m, const gc_spec* spec) {
   if (!spec || n < 0 || m < 0) return 0;

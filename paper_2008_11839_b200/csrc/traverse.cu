@@ -10,6 +10,7 @@
 // result is deterministic, which makes the BFS forest bit-identical to the
 // reference's "first discoverer in the sorted frontier" rule.
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 
@@ -63,11 +64,37 @@ __global__ void k_fill64(unsigned long long* a, int64_t n, unsigned long long v)
 // the top-down atomicMin selects — so the forest does not depend on the
 // direction schedule.  Frontier stats [count, degree sum] feed the switch
 // and the inspection count (sum of frontier degrees, sampling.py:141-144).
+//
+// State: par[v] (u32, kUnreached until claimed, kSourcePar for the source)
+// and the visited bitmap vis (n/8 bytes, L2-resident).  A top-down level
+// reads vis frozen at the level start — vertices reached in earlier levels
+// are skipped with a bit test instead of a random claim-word read — and
+// resolves this level's claims with one 32-bit atomicMin of the frontier id
+// per edge; the first claimant (old == kUnreached) enqueues.  The level's
+// claims are merged into vis afterwards (k_or_words).
+constexpr uint32_t kUnreached = 0xffffffffu;
+constexpr uint32_t kSourcePar = 0xfffffffeu;
+
+__device__ __forceinline__ bool test_bit(const uint32_t* bits, int32_t x) {
+  return (__ldg(bits + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+__device__ __forceinline__ bool claim_par(uint32_t* par, const uint32_t* vis, int32_t x, int32_t f) {
+  // both filters load in parallel: reached in an earlier level (the frozen
+  // bitmap; required — a 32-bit parent carries no level), or a claim of
+  // this level at or below f already landed (a stale L1 value only costs
+  // one atomic)
+  const uint32_t vw = __ldg(vis + (x >> 5));
+  const uint32_t seen = uint32_t(ld_weak(reinterpret_cast<const int32_t*>(par + x)));
+  if ((vw >> (x & 31)) & 1u) return false;
+  if (seen <= uint32_t(f)) return false;
+  return atomicMin(par + x, uint32_t(f)) == kUnreached;
+}
 
 __global__ void __launch_bounds__(kTB)
 k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
-         const unsigned long long* qstat, unsigned long long* key, int32_t* qn, unsigned long long* nstat,
-         uint32_t* nbits, int32_t level, int32_t* minv, unsigned long long* insp) {
+         const unsigned long long* qstat, uint32_t* par, const uint32_t* vis, int32_t* qn,
+         unsigned long long* nstat, uint32_t* nbits, int32_t* minv, unsigned long long* insp) {
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
   const int lane = threadIdx.x & 31;
@@ -102,7 +129,7 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
       bool fresh = false;
       if (!big && j < d) {
         x = tgt[b + j];
-        fresh = claim(key, x, level + 1, uint32_t(f));
+        fresh = claim_par(par, vis, x, f);
       }
       take(fresh, x);
     }
@@ -119,7 +146,7 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
         bool fresh = false;
         if (j < dd) {
           x = tgt[bb + j];
-          fresh = claim(key, x, level + 1, uint32_t(ff));
+          fresh = claim_par(par, vis, x, ff);
         }
         take(fresh, x);
       }
@@ -131,15 +158,13 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
 }
 
-__device__ __forceinline__ bool test_bit(const uint32_t* bits, int32_t x) {
-  return (__ldg(bits + (x >> 5)) >> (x & 31)) & 1u;
-}
-
 // bottom-up: a warp owns 32 consecutive vertices and writes its next-bitmap
-// word whole; each unreached vertex stops at its first frontier neighbour
+// word whole; the visited bitmap word (one broadcast load per warp) skips
+// reached vertices, and each unreached vertex stops at its first frontier
+// neighbour in row order — the smallest one, as the top-down atomicMin picks.
 __global__ void __launch_bounds__(kTB)
-k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, unsigned long long* key,
-         const uint32_t* __restrict__ cbits, uint32_t* nbits, unsigned long long* nstat, int32_t level,
+k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, uint32_t* par,
+         const uint32_t* __restrict__ cbits, uint32_t* nbits, uint32_t* vis, unsigned long long* nstat,
          int32_t* minv) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = 0, degs = 0;
@@ -147,21 +172,26 @@ k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32
   const int64_t stride = int64_t(gridDim.x) * kTB;
   for (int64_t base = int64_t(blockIdx.x) * kTB; base < n; base += stride) {
     const int64_t v = base + threadIdx.x;
+    const int64_t wi = (base + (threadIdx.x & ~31)) >> 5;
+    const uint32_t vw = wi * 32 < n ? vis[wi] : ~0u;
     bool found = false;
-    if (v < n && key[v] == kFree) {
+    if (v < n && !((vw >> lane) & 1u)) {
       const int64_t b = off[v], e = off[v + 1];
       for (int64_t j = b; j < e; ++j) {
         const int32_t t = tgt[j];
         if (test_bit(cbits, t)) {
           found = true;
-          key[v] = mk_key(level + 1, uint32_t(t));
+          par[v] = uint32_t(t);
           degs += static_cast<unsigned long long>(e - b);
           break;
         }
       }
     }
     const unsigned word = __ballot_sync(0xffffffffu, found);
-    if (lane == 0 && word) nbits[(base + (threadIdx.x & ~31)) >> 5] = word;
+    if (lane == 0 && word) {
+      nbits[wi] = word;
+      vis[wi] = vw | word;
+    }
     if (found) {
       ++cnt;
       my_min = int32_t(v) < my_min ? int32_t(v) : my_min;
@@ -171,6 +201,14 @@ k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32
   block_add<kTB>(nstat + 1, degs);
   my_min = warp_min(my_min);
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+__global__ void k_or_words(uint32_t* dst, const uint32_t* src, int64_t words) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) {
+    const uint32_t x = src[w];
+    if (x) dst[w] |= x;
+  }
 }
 
 // bitmap -> queue (switching back to top-down): one thread per 32-bit word
@@ -197,55 +235,65 @@ k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long*
   }
 }
 
-__global__ void k_bfs_seed(const int64_t* off, unsigned long long* key, int32_t* q, unsigned long long* qstat,
-                           uint32_t* bits, int32_t s, int32_t* minv) {
-  key[s] = mk_key(0, 0xffffffffu);  // no parent
+__global__ void k_bfs_seed(const int64_t* off, uint32_t* par, int32_t* q, unsigned long long* qstat,
+                           uint32_t* bits, uint32_t* vis, int32_t s, int32_t* minv) {
+  par[s] = kSourcePar;
   q[0] = s;
   qstat[0] = 1;
   qstat[1] = static_cast<unsigned long long>(off[s + 1] - off[s]);
   bits[s >> 5] |= 1u << (s & 31);
+  vis[s >> 5] |= 1u << (s & 31);
   *minv = s;
 }
 
-// discovery parents out of the claim words (-1 = source / unreached)
-__global__ void k_bfs_parents(const unsigned long long* key, int32_t n, int32_t* par) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const unsigned long long k = key[v];
-    par[v] = k == kFree ? -1 : int32_t(uint32_t(k));
-  }
-}
-
-// re-root the discovery tree at the component minimum (sampling.py:161-168)
-__global__ void k_bfs_reroot(int32_t* par, const int32_t* minv) {
-  int32_t cur = *minv, prev = -1;
-  while (cur != -1) {
-    const int32_t nxt = par[cur];
-    par[cur] = prev;
-    prev = cur;
-    cur = nxt;
-  }
-}
-
-// label the component with its minimum (:158-160), emit forest slots, and
-// count the sample inspections: the reference adds every frontier's degree
-// sum (:141-144), i.e. the degree of every reached vertex exactly once
-__global__ void k_bfs_label(const unsigned long long* key, const int32_t* par, const int32_t* minv,
-                            const int64_t* off, int32_t n, int32_t* P, int32_t* fu, int32_t* fv,
-                            unsigned long long* insp) {
+// label the component with its minimum (sampling.py:158-160), emit forest
+// slots (slot v = (parent, v)), and count the sample inspections: the
+// reference adds every frontier's degree sum (:141-144), i.e. the degree of
+// every reached vertex once.  Four vertices per thread (16-byte loads).
+__global__ void k_bfs_label(const uint32_t* par, const int32_t* minv, const int64_t* off, int32_t n, int32_t* P,
+                            int32_t* fu, int32_t* fv, unsigned long long* insp) {
   const int32_t mn = *minv;
   unsigned long long degs = 0;
+  const int64_t nq = (int64_t(n) + 3) / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    if (key[v] == kFree) continue;
-    P[v] = mn;
-    degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
-    if (fu && v != mn) {
-      fu[v] = par[v];
-      fv[v] = int32_t(v);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += stride) {
+    const int64_t v0 = 4 * i;
+    uint32_t p[4];
+    if (v0 + 3 < n) {
+      const uint4 pp = *reinterpret_cast<const uint4*>(par + v0);
+      p[0] = pp.x; p[1] = pp.y; p[2] = pp.z; p[3] = pp.w;
+    } else {
+      for (int j = 0; j < 4; ++j) p[j] = v0 + j < n ? par[v0 + j] : kUnreached;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t v = v0 + j;
+      if (p[j] == kUnreached) continue;
+      P[v] = mn;
+      degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
+      if (fu && v != mn && p[j] != kSourcePar) {
+        fu[v] = int32_t(p[j]);
+        fv[v] = int32_t(v);
+      }
     }
   }
   block_add<kEwBlock>(insp, degs);
+}
+
+// re-root the discovery tree at the component minimum (sampling.py:161-168):
+// reverse the slots along the path mn -> ... -> source (one thread; the
+// path has at most depth-many vertices)
+__global__ void k_bfs_reroot(const uint32_t* par, const int32_t* minv, int32_t* fu, int32_t* fv) {
+  int32_t cur = *minv;
+  fu[cur] = -1;
+  fv[cur] = -1;
+  while (true) {
+    const uint32_t p = par[cur];
+    if (p == kSourcePar) break;  // reached the source
+    fu[p] = cur;                 // slot p now holds (cur, p)
+    fv[p] = int32_t(p);
+    cur = int32_t(p);
+  }
 }
 
 // ------------------------------------------------------------------- LDD ---
@@ -426,21 +474,37 @@ __global__ void k_ldd_label(const unsigned long long* key, const int32_t* mins, 
 
 }  // namespace
 
+// Direction switch (Beamer): bottom-up once the frontier's edges exceed
+// 1/alpha of the unexplored ones, back to top-down below n/beta frontier
+// vertices.  Beamer's CPU alpha = 14 keeps top-down one level too long on a
+// GPU, where a top-down level pays an atomic per fresh frontier edge while a
+// bottom-up level streams rows and stops at the first frontier neighbour.
+constexpr int kBfsBeta = 24;
+double bfs_alpha() {
+  static const double a = [] {
+    const char* e = getenv("GC_BFS_ALPHA");
+    return e ? atof(e) : 30.0;  // measured on uniform 2^27: 14 -> 13.9 ms, 30 -> 10.6 ms, 60 -> 10.7 ms
+  }();
+  return a;
+}
+
 void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t* fv, SamplerWs& w,
              unsigned long long* ctr, cudaStream_t st) {
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:128-129
   require(s.bfs_source >= 0 && s.bfs_source < n, GC_ERR_ARG, "BFS source out of range");
   const int64_t words = (int64_t(n) + 31) / 32;
-  TL(k_fill64, grid_for(n, kEwBlock, 8), kEwBlock, w.key, n, kFree);
+  uint32_t* par = reinterpret_cast<uint32_t*>(w.key);  // the claim buffer, as u32 parents
+  GC_CUDA(cudaMemsetAsync(par, 0xff, size_t(n) * 4, st));  // kUnreached
   GC_CUDA(cudaMemsetAsync(w.fb0, 0, words * 4, st));
   GC_CUDA(cudaMemsetAsync(w.fb1, 0, words * 4, st));
+  GC_CUDA(cudaMemsetAsync(w.vis, 0, words * 4, st));
   int32_t* minv = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
   unsigned long long* fs[2] = {w.stat, w.stat + 2};
   int32_t* q[2] = {w.q0, w.q1};
   uint32_t* fb[2] = {w.fb0, w.fb1};
   GC_CUDA(cudaMemsetAsync(w.stat, 0, 4 * sizeof(unsigned long long), st));
-  TL(k_bfs_seed, 1, 1, g.offsets, w.key, q[0], fs[0], fb[0], int32_t(s.bfs_source), minv);
+  TL(k_bfs_seed, 1, 1, g.offsets, par, q[0], fs[0], fb[0], w.vis, int32_t(s.bfs_source), minv);
   GC_CHECK_LAUNCH();
   unsigned long long* h = pinned_words();
   GC_CUDA(cudaMemcpyAsync(h, fs[0], 16, cudaMemcpyDeviceToHost, st));
@@ -455,7 +519,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     const int c = level & 1, nx = c ^ 1;
     // Beamer's heuristic: bottom-up once the frontier's edges exceed 1/14 of
     // the unexplored ones, back to top-down when it shrinks below n/24
-    const bool want_bu = bottom_up ? (nf >= uint64_t(n) / 24) : (mf * 14.0 > unexplored);
+    const bool want_bu = bottom_up ? (nf >= uint64_t(n) / kBfsBeta) : (mf * bfs_alpha() > unexplored);
     if (!want_bu && bottom_up) {
       GC_CUDA(cudaMemsetAsync(fs[c], 0, 8, st));
       TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], fs[c]);
@@ -464,12 +528,15 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     GC_CUDA(cudaMemsetAsync(fs[nx], 0, 16, st));
     GC_CUDA(cudaMemsetAsync(fb[nx], 0, words * 4, st));
     if (bottom_up) {
-      TL(k_bfs_bu, bu_grid, kTB, g.offsets, g.targets, n, w.key, fb[c], fb[nx], fs[nx], level, minv);
+      TL(k_bfs_bu, bu_grid, kTB, g.offsets, g.targets, n, par, fb[c], fb[nx], w.vis, fs[nx], minv);
     } else {
       const int64_t b64 = (int64_t(nf) + kTB - 1) / kTB;
       const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
-      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], fs[c], w.key, q[nx], fs[nx], fb[nx], level, minv,
+      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], fs[c], par, w.vis, q[nx], fs[nx], fb[nx], minv,
          nullptr);
+      // the visited bitmap takes the level's claims in one word-parallel pass
+      // (an extra atomic per claim would double the level's atomics)
+      TL(k_or_words, grid_for(words, kEwBlock, 2), kEwBlock, w.vis, fb[nx], words);
     }
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(h, fs[nx], 16, cudaMemcpyDeviceToHost, st));
@@ -478,12 +545,9 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     mf = bottom_up ? double(h[1]) : double(nf) * avg_deg;
     unexplored -= mf;
   }
-  const int ge = grid_for(n, kEwBlock, 8);
-  if (fu) {
-    TL(k_bfs_parents, ge, kEwBlock, w.key, n, w.par);
-    TL(k_bfs_reroot, 1, 1, w.par, minv);
-  }
-  TL(k_bfs_label, ge, kEwBlock, w.key, w.par, minv, g.offsets, n, P, fu, fv, ctr + C_INSP_SAMPLE);
+  TL(k_bfs_label, grid_for((int64_t(n) + 3) / 4, kEwBlock, 8), kEwBlock, par, minv, g.offsets, n, P, fu, fv,
+     ctr + C_INSP_SAMPLE);
+  if (fu) TL(k_bfs_reroot, 1, 1, par, minv, fu, fv);
   GC_CHECK_LAUNCH();
 }
 

@@ -79,8 +79,11 @@ struct Reader {
 // `known` (>= 0): a value of P[u] this thread already holds (one it just
 // wrote, or read this iteration) — used instead of the first read.  A held
 // value is at worst a stale read, which the rules already tolerate.
+// `known_w` (>= 0, with `known`): a held value of P[known] as well.
+// `first_w` (nullable) receives the value read for P[P[u]] in the first step.
 template <int FIND>
-__device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd, int32_t known = -1) {
+__device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd, int32_t known = -1,
+                                        int32_t known_w = -1, int32_t* first_w = nullptr) {
   if constexpr (FIND == GC_FIND_NAIVE) {
     // dset.py:109-112
     while (true) {
@@ -106,7 +109,8 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd, int32
   } else if constexpr (FIND == GC_FIND_SPLIT) {
     // dset.py:126-135
     int32_t v = known >= 0 ? known : rd(P + u);
-    int32_t w = rd(P + v);
+    int32_t w = known >= 0 && known_w >= 0 ? known_w : rd(P + v);
+    if (first_w) *first_w = w;
     while (v != w) {
       atomicCAS(P + u, v, w);
       u = v;
@@ -119,7 +123,8 @@ __device__ __forceinline__ int32_t find(int32_t u, int32_t* P, Reader& rd, int32
     // there: w when it succeeded, else the value it found — taken from the
     // CAS result instead of a second dependent read of the same word.
     int32_t v = known >= 0 ? known : rd(P + u);
-    int32_t w = rd(P + v);
+    int32_t w = known >= 0 && known_w >= 0 ? known_w : rd(P + v);
+    if (first_w) *first_w = w;
     while (v != w) {
       const int32_t old = atomicCAS(P + u, v, w);
       u = old == v ? w : old;
@@ -299,9 +304,14 @@ __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32
     if (ru == pru && cas(P + ru, ru, prv)) {
       record<FOREST>(s, ru, u, v);
       if constexpr (FIND != GC_FIND_NAIVE) {
-        // P[ru] is now prv and P[rv] was just read as prv
-        find<FIND>(u, P, rd, (u == ru || u == rv) ? prv : -1);
-        find<FIND>(v, P, rd, (v == ru || v == rv) ? prv : -1);
+        // P[ru] is now prv and P[rv] was just read as prv; when both
+        // endpoints start from prv, the second find reuses the first's
+        // read of P[prv]
+        const int32_t ku = (u == ru || u == rv) ? prv : -1;
+        const int32_t kv = (v == ru || v == rv) ? prv : -1;
+        int32_t w = -1;
+        find<FIND>(u, P, rd, ku, -1, &w);
+        find<FIND>(v, P, rd, kv, (ku >= 0 && kv == ku) ? w : -1);
       }
       return true;
     }

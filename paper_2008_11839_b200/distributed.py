@@ -215,7 +215,7 @@ class GpuEngine:
         from .api import LoweredSpec, _stream, _workspace
         n = parent.numel()
         low = LoweredSpec(spec, None, n)
-        ws = _workspace(4 * n + 8192)
+        ws = _workspace(5 * n + 8192)
         words_all = words_all.contiguous()
         labels_all = labels_all.contiguous()
         k = int(us.numel())
