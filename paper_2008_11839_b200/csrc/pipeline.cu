@@ -11,6 +11,17 @@ namespace gc {
 
 __global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (!H && !L && (reinterpret_cast<uintptr_t>(P) & 15) == 0) {
+    // 16-byte stores, four vertices per thread
+    const int64_t nq = int64_t(n) / 4;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+      const int32_t v = int32_t(4 * q);
+      reinterpret_cast<int4*>(P)[q] = make_int4(v, v + 1, v + 2, v + 3);
+    }
+    for (int64_t v = 4 * nq + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+      P[v] = int32_t(v);
+    return;
+  }
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
     P[v] = int32_t(v);
     if (H) H[v] = n;
@@ -109,24 +120,42 @@ constexpr int kProbe = 1024;
 
 __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t n,
                                                        unsigned long long* ctr) {
-  __shared__ int32_t lab[kProbe];
+  // sample labels counted in a shared-memory hash table (open addressing,
+  // warp-aggregated adds: the dominant label is one add per warp)
+  constexpr int kSlots = 2 * kProbe;
+  __shared__ int32_t key_[kSlots];
+  __shared__ unsigned cnt_[kSlots];
   __shared__ unsigned long long best;
   const int s = n < kProbe ? n : kProbe;
   const int i = threadIdx.x;
+  for (int k = i; k < kSlots; k += kProbe) {
+    key_[k] = -1;
+    cnt_[k] = 0;
+  }
   if (i == 0) best = 0ull;
+  int32_t x = -1;
   if (i < s) {
     // walk to the root so the probe can run before compression
-    int32_t x = ld_weak(P + (int64_t(i) * n) / s), y;
+    x = ld_weak(P + (int64_t(i) * n) / s);
+    int32_t y;
     while ((y = ld_weak(P + x)) != x) x = y;
-    lab[i] = x;
+  }
+  __syncthreads();
+  int slot = -1;
+  if (i < s) {
+    const unsigned same = __match_any_sync(__activemask(), x);
+    slot = int((uint32_t(x) * 2654435761u) % kSlots);
+    while (true) {
+      const int32_t k = atomicCAS(&key_[slot], -1, x);
+      if (k == -1 || k == x) break;
+      slot = (slot + 1) % kSlots;
+    }
+    if ((i & 31) == __ffs(int(same)) - 1) atomicAdd(&cnt_[slot], __popc(same));
   }
   __syncthreads();
   if (i < s) {
-    const int32_t me = lab[i];
-    unsigned c = 0;
-    for (int j = 0; j < s; ++j) c += lab[j] == me;
     const unsigned long long key =
-        (static_cast<unsigned long long>(c) << 32) | (0xffffffffull - uint32_t(me));
+        (static_cast<unsigned long long>(cnt_[slot]) << 32) | (0xffffffffull - uint32_t(x));
     atomicMax(&best, key);
   }
   __syncthreads();

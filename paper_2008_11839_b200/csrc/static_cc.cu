@@ -328,8 +328,11 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
   if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
   if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
+    // every label-crossing edge has an endpoint outside L_max, so the census
+    // only walks the active rows (Σ deg = the finish inspections), adding
+    // back the reverse entries from L_max rows
     (k_ic_census<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, g->offsets, g->targets,
-                                                               nullptr, pl.ws.ctr), ::gc::count_launch());
+                                                               pl.ws.list, pl.ws.ctr), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
   GC_CUDA(rec(ev[2], st));
