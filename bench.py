@@ -214,12 +214,17 @@ def run_sharded(args):
             sys.exit(3)
     del g
     torch.cuda.empty_cache()
+    from paper_2008_11839_b200 import Graph
+    from paper_2008_11839_b200 import _native as N
+    from paper_2008_11839_b200.api import host_int64
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         sharded_two_phase(shard, spec, forest=False)
     torch.cuda.synchronize()
     dist.barrier()
+    lib = N.lib()
+    l0 = lib.gc_launch_count()
     times, exchanged = [], 0
     with ClockSampler(local % ndev) as clk:
         for _ in range(args.steps):
@@ -233,6 +238,7 @@ def run_sharded(args):
             times.append(e0.elapsed_time(e1))
             exchanged = r.exchanged_edges
     torch.cuda.synchronize()
+    launches = lib.gc_launch_count() - l0
     dist.barrier()
     dev = "cuda" if backend == "nccl" else "cpu"
     tmax = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
@@ -240,6 +246,32 @@ def run_sharded(args):
     total_ms = float(tmax.item())
     ms_per_step = total_ms / args.steps
     value = (m / 2) * args.steps / (total_ms / 1e3)
+    # end to end: every rank copies its row block in from pinned host memory,
+    # runs the sharded pipeline and reads the labels back (int64, pinned);
+    # wall clock per step, max over ranks
+    e2e = None
+    if args.e2e_steps > 0:
+        off_h = shard._d_off.cpu().pin_memory()
+        tgt_h = shard._d_tgt.cpu().pin_memory()
+        sharded_two_phase(Graph(n, off_h, tgt_h).cuda(), spec, forest=False)
+        et = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            hg = Graph(n, off_h, tgt_h)
+            r = sharded_two_phase(hg.cuda(), spec, forest=False)
+            host_int64(r.labels)
+            torch.cuda.synchronize()
+            et.append(time.perf_counter() - t0)
+        tm = torch.tensor([statistics.median(et)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        e2e_t = float(tm.item())
+        e2e = {"value": (m / 2) / e2e_t, "unit": UNIT,
+               "h2d_bytes_per_step": int(off_h.numel() * 8 + tgt_h.numel() * 4), "d2h_bytes_per_step": 8 * n,
+               "seconds_per_step": e2e_t,
+               "timing": "wall clock per rank (pinned H2D of its row block, sharded pipeline, int64 labels "
+                         "D2H), max over ranks; bytes are rank 0's"}
     peak, peak_kind = peaks()
     step_bytes = 4 * (res.insp_sample + res.insp_finish) + 8 * (n + 1) + 4 * n * 7
     if rank == 0:
@@ -254,7 +286,7 @@ def run_sharded(args):
                            "exchanged_pairs_per_step": exchanged,
                            "exchanged_bitmap_bytes_per_step": ws * ((n + 31) // 32) * 4,
                            "l2": "256 MiB buffer written between timed steps (outside the step events)"},
-                "e2e": None, "gpu_launches": None,
+                "e2e": e2e, "gpu_launches": launches, "launches_per_step": launches / args.steps,
                 "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1e3) / 1e9 / ws,
                              "peak": peak, "unit": "GB/s",
                              "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / ws / peak, "traffic": None,
