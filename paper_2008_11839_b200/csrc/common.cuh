@@ -23,6 +23,14 @@ __device__ __forceinline__ int32_t ld_acq(const int32_t* p) {
   return v;
 }
 
+// plain global load the compiler may schedule freely (several in flight);
+// for reads where any stale value is acceptable
+__device__ __forceinline__ int32_t ld_free(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // plain global load (L1-cacheable), never hoisted across other memory ops
 __device__ __forceinline__ int32_t ld_weak(const int32_t* p) {
   int32_t v;

@@ -76,10 +76,16 @@ k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned
       }
       if (COMPRESS) {
         bool dirty = false;
+        // first hop of all four walks issued together (most labels are
+        // already roots after the union kernel's halving); only labels that
+        // moved continue walking
+        int32_t hop[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hop[j] = v0 + j < n ? ld_free(P + lab[j]) : lab[j];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (v0 + j >= n) continue;
-          const int32_t r = root_weak(P, lab[j]);
+          const int32_t r = hop[j] == lab[j] ? lab[j] : root_weak(P, hop[j]);
           dirty |= r != lab[j];
           lab[j] = r;
         }
@@ -277,6 +283,14 @@ __global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
       for (int j = 0; j < 4; ++j) lab[j] = v0 + j < n ? P[v0 + j] : int32_t(v0 + j);
     }
     bool dirty = false;
+    // first hop of the four walks issued together (labels are mostly
+    // compressed already); only labels whose parent moved keep walking
+    int32_t hop[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int32_t v = int32_t(v0 + j);
+      hop[j] = (v < n && lab[j] != v) ? ld_free(P + lab[j]) : lab[j];
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int32_t v = int32_t(v0 + j);
@@ -286,6 +300,12 @@ __global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
         ++roots;
         continue;
       }
+      if (hop[j] == r) {
+        noncanon |= r > v;
+        continue;  // already points at its root
+      }
+      r = hop[j];
+      dirty = true;
       int64_t steps = 0;
       int32_t y;
       while ((y = ld_weak(P + r)) != r) {

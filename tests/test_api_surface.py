@@ -192,3 +192,22 @@ def test_sweep_rows_match_reference():
     got = [{k: str(r[k]) for k in _SWEEP_KEYS} for r in rows]
     assert got == API["sweep_incremental"]
     assert rows_to_csv_text(rows).splitlines()[0] == ",".join(API["csv_columns"])
+
+
+def test_binary_graph_host_roundtrip_and_errors(tmp_path):
+    """GCN1 files (graphs.py:170-190) on the host path: no GPU needed."""
+    from paper_2008_11839_b200 import load_graph_binary, save_graph_binary
+    g = _ba_graph_host(300, 2, 3)
+    p = tmp_path / "g.gcn1"
+    save_graph_binary(g, p)
+    raw = p.read_bytes()
+    assert raw[:4] == b"GCN1" and len(raw) == 4 + 16 + 8 * (g.n + 1) + 4 * g.m
+    assert is_binary_graph(p)
+    g2 = load_graph_binary(p)
+    assert g2.n == g.n and np.array_equal(g2.offsets, g.offsets) and np.array_equal(g2.targets, g.targets)
+    (tmp_path / "bad.gcn1").write_bytes(b"GCN2" + raw[4:])
+    with pytest.raises(MalformedInputError, match="bad magic"):
+        load_graph_binary(tmp_path / "bad.gcn1")
+    (tmp_path / "short.gcn1").write_bytes(raw[:40])
+    with pytest.raises(MalformedInputError, match="truncated"):
+        load_graph_binary(tmp_path / "short.gcn1")
