@@ -10,6 +10,7 @@
 // result is deterministic, which makes the BFS forest bit-identical to the
 // reference's "first discoverer in the sorted frontier" rule.
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
@@ -94,16 +95,19 @@ __device__ __forceinline__ bool claim_par(uint32_t* par, const uint32_t* vis, in
 __global__ void __launch_bounds__(kTB)
 k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
          const unsigned long long* qstat, uint32_t* par, const uint32_t* vis, int32_t* qn,
-         unsigned long long* nstat, uint32_t* nbits, int32_t* minv, unsigned long long* insp) {
+         unsigned long long* nstat, uint32_t* nbits, int32_t* minv, unsigned long long* insp,
+         unsigned long long* zero_next) {
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
+  // batched levels: clear the stat slot the level after next will fill
+  if (zero_next && blockIdx.x == 0 && threadIdx.x == 0) zero_next[0] = zero_next[1] = 0;
   const int lane = threadIdx.x & 31;
   const int64_t count = int64_t(qstat[0]);
   unsigned long long degs = 0;
   int32_t my_min = INT_MAX;
   auto take = [&](bool fresh, int32_t x) {
     if (fresh) {
-      atomicOr(nbits + (x >> 5), 1u << (x & 31));
+      if (nbits) atomicOr(nbits + (x >> 5), 1u << (x & 31));
       my_min = x < my_min ? x : my_min;
     }
     bq.push(fresh, x, qn, nstat);
@@ -201,6 +205,29 @@ k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32
   block_add<kTB>(nstat + 1, degs);
   my_min = warp_min(my_min);
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+// narrow levels: the visited bitmap takes the claimed queue's vertices
+// (work ~ frontier, not n); `total` accumulates the reached count
+__global__ void k_mark_queue(const int32_t* q, const unsigned long long* qstat, uint32_t* vis,
+                             unsigned long long* total) {
+  const int64_t count = int64_t(qstat[0]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && count) atomicAdd(total, static_cast<unsigned long long>(count));
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const int32_t x = q[i];
+    atomicOr(vis + (x >> 5), 1u << (x & 31));
+  }
+}
+
+// frontier queue -> bitmap (leaving batched mode for a bottom-up level)
+__global__ void k_queue_to_bits(const int32_t* q, const unsigned long long* qstat, uint32_t* bits) {
+  const int64_t count = int64_t(qstat[0]);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const int32_t x = q[i];
+    atomicOr(bits + (x >> 5), 1u << (x & 31));
+  }
 }
 
 __global__ void k_or_words(uint32_t* dst, const uint32_t* src, int64_t words) {
@@ -500,46 +527,100 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   GC_CUDA(cudaMemsetAsync(w.fb1, 0, words * 4, st));
   GC_CUDA(cudaMemsetAsync(w.vis, 0, words * 4, st));
   int32_t* minv = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
-  unsigned long long* fs[2] = {w.stat, w.stat + 2};
+  // frontier stats [count, degree sum] per level in a ring of three slots
+  // (level L reads slot(L), writes slot(L+1)); slot 3 counts reached vertices
+  auto slot = [&](int64_t L) { return w.stat + 2 * (L % 3); };
+  unsigned long long* reached = w.stat + 6;
   int32_t* q[2] = {w.q0, w.q1};
   uint32_t* fb[2] = {w.fb0, w.fb1};
-  GC_CUDA(cudaMemsetAsync(w.stat, 0, 4 * sizeof(unsigned long long), st));
-  TL(k_bfs_seed, 1, 1, g.offsets, par, q[0], fs[0], fb[0], w.vis, int32_t(s.bfs_source), minv);
+  GC_CUDA(cudaMemsetAsync(w.stat, 0, 8 * sizeof(unsigned long long), st));
+  TL(k_bfs_seed, 1, 1, g.offsets, par, q[0], slot(0), fb[0], w.vis, int32_t(s.bfs_source), minv);
   GC_CHECK_LAUNCH();
   unsigned long long* h = pinned_words();
-  GC_CUDA(cudaMemcpyAsync(h, fs[0], 16, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaMemcpyAsync(h, slot(0), 16, cudaMemcpyDeviceToHost, st));
   GC_CUDA(cudaStreamSynchronize(st));
   unsigned long long nf = h[0];
   double mf = double(h[1]);  // frontier edges: exact for the seed / bottom-up levels, estimated top-down
   const double avg_deg = double(g.m) / double(n);
   double unexplored = double(g.m) - mf;
   bool bottom_up = false;
+  bool bits_stale = false;  // fb[current] not built (after batched levels)
   const int bu_grid = grid_for(n, kTB, 4);
-  for (int32_t level = 0; nf > 0; ++level) {
-    const int c = level & 1, nx = c ^ 1;
-    // Beamer's heuristic: bottom-up once the frontier's edges exceed 1/14 of
-    // the unexplored ones, back to top-down when it shrinks below n/24
+  const int narrow_grid = num_sms() * 8;
+  // Narrow frontiers (high-diameter graphs: a 256^3 grid has 765 levels)
+  // run kBfsBatch top-down levels per host round trip: the kernels read the
+  // frontier size on the device, claims go straight to the queue, and a
+  // queue-sized pass marks them visited.  The direction switch is checked
+  // between batches; parents are direction-independent, so the schedule
+  // never changes the result.
+  // The batch length is chosen so the frontier, growing at the observed
+  // per-level rate (avg degree before any observation), stays narrow.
+  constexpr int kBfsMaxBatch = 64;
+  double growth = avg_deg > 1.01 ? avg_deg : 1.01;
+  for (int64_t level = 0; nf > 0;) {
+    int batch = 0;
+    // batch while the predicted frontier stays well inside top-down
+    // territory (half the switch threshold)
+    const double limit = unexplored / (2.0 * bfs_alpha() * avg_deg);
+    if (!bottom_up && double(nf) < limit) {
+      const double k = std::log(limit / double(nf)) / std::log(growth);
+      batch = k > kBfsMaxBatch ? kBfsMaxBatch : int(k);
+    }
+    if (batch >= 2) {
+      const unsigned long long nf0 = nf;
+      GC_CUDA(cudaMemsetAsync(slot(level + 1), 0, 16, st));
+      for (int k = 0; k < batch; ++k) {
+        const int64_t L = level + k;
+        TL(k_bfs_td, narrow_grid, kTB, g.offsets, g.targets, q[L & 1], slot(L), par, w.vis, q[(L + 1) & 1],
+           slot(L + 1), static_cast<uint32_t*>(nullptr), minv, static_cast<unsigned long long*>(nullptr),
+           slot(L + 2));
+        TL(k_mark_queue, narrow_grid, kEwBlock, q[(L + 1) & 1], slot(L + 1), w.vis, reached);
+      }
+      GC_CHECK_LAUNCH();
+      level += batch;
+      GC_CUDA(cudaMemcpyAsync(h, slot(level), 16, cudaMemcpyDeviceToHost, st));
+      GC_CUDA(cudaMemcpyAsync(h + 2, reached, 8, cudaMemcpyDeviceToHost, st));
+      GC_CUDA(cudaStreamSynchronize(st));
+      nf = h[0];
+      mf = double(nf) * avg_deg;
+      unexplored = double(g.m) - double(h[2] + 1) * avg_deg;
+      if (nf > 0) {
+        const double observed = std::pow(double(nf) / double(nf0), 1.0 / batch);
+        growth = observed * 1.5 > 1.01 ? observed * 1.5 : 1.01;
+      }
+      bits_stale = true;
+      continue;
+    }
+    const int c = int(level & 1), nx = c ^ 1;
+    // Beamer's heuristic: bottom-up once the frontier's edges exceed
+    // 1/alpha of the unexplored ones, back to top-down below n/beta
     const bool want_bu = bottom_up ? (nf >= uint64_t(n) / kBfsBeta) : (mf * bfs_alpha() > unexplored);
+    if (want_bu && bits_stale) {
+      GC_CUDA(cudaMemsetAsync(fb[c], 0, words * 4, st));
+      TL(k_queue_to_bits, grid_for(int64_t(nf), kEwBlock, 4), kEwBlock, q[c], slot(level), fb[c]);
+    }
+    bits_stale = false;
     if (!want_bu && bottom_up) {
-      GC_CUDA(cudaMemsetAsync(fs[c], 0, 8, st));
-      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], fs[c]);
+      GC_CUDA(cudaMemsetAsync(slot(level), 0, 8, st));
+      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], slot(level));
     }
     bottom_up = want_bu;
-    GC_CUDA(cudaMemsetAsync(fs[nx], 0, 16, st));
+    GC_CUDA(cudaMemsetAsync(slot(level + 1), 0, 16, st));
     GC_CUDA(cudaMemsetAsync(fb[nx], 0, words * 4, st));
     if (bottom_up) {
-      TL(k_bfs_bu, bu_grid, kTB, g.offsets, g.targets, n, par, fb[c], fb[nx], w.vis, fs[nx], minv);
+      TL(k_bfs_bu, bu_grid, kTB, g.offsets, g.targets, n, par, fb[c], fb[nx], w.vis, slot(level + 1), minv);
     } else {
       const int64_t b64 = (int64_t(nf) + kTB - 1) / kTB;
       const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
-      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], fs[c], par, w.vis, q[nx], fs[nx], fb[nx], minv,
-         nullptr);
+      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], slot(level), par, w.vis, q[nx], slot(level + 1),
+         fb[nx], minv, static_cast<unsigned long long*>(nullptr), static_cast<unsigned long long*>(nullptr));
       // the visited bitmap takes the level's claims in one word-parallel pass
       // (an extra atomic per claim would double the level's atomics)
       TL(k_or_words, grid_for(words, kEwBlock, 2), kEwBlock, w.vis, fb[nx], words);
     }
     GC_CHECK_LAUNCH();
-    GC_CUDA(cudaMemcpyAsync(h, fs[nx], 16, cudaMemcpyDeviceToHost, st));
+    ++level;
+    GC_CUDA(cudaMemcpyAsync(h, slot(level), 16, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
     nf = h[0];
     mf = bottom_up ? double(h[1]) : double(nf) * avg_deg;
