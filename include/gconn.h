@@ -241,6 +241,13 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits,
                   const int32_t* us, const int32_t* vs, int64_t k,
                   const gc_spec* spec, void* ws, size_t ws_bytes, void* stream);
 
+/* Graph contract check (graphs.py:43-51) on device arrays: offsets start at
+ * 0, never decrease and end at m; every target in [0, n) -> else
+ * GC_ERR_MALFORMED.  One streaming pass; the Python layer runs it once per
+ * Graph before the first kernel touches it (an out-of-range target would
+ * otherwise be an out-of-bounds parent access). */
+int gc_check_csr(const gc_csr* g, void* stream);
+
 /* ---- DisjointSets probes and validation (dset.py:381-399,
  *      validate.py:178-259) -------------------------------------------------
  * gc_find_batch: roots_out[i] = find(xs[i]) with the given gc_find_kind,

@@ -48,6 +48,31 @@ __global__ void k_edges_exist(const int64_t* __restrict__ off, const int32_t* __
 
 __global__ void k_set_noncanon(unsigned long long* ctr) { ctr[C_NONCANON] = 1; }
 
+// CSR shape check (the Graph contract, graphs.py:43-51): offsets start at 0,
+// never decrease, end at m; every target lies in [0, n).  bad[0] collects
+// flags: 1 offsets, 2 targets.
+__global__ void k_check_csr(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int64_t n, int64_t m,
+                            int aligned, unsigned int* bad) {
+  unsigned flags = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t v = t0; v <= n; v += stride) {
+    const int64_t o = off[v];
+    if ((v == 0 && o != 0) || (v == n && o != m) || (v < n && off[v + 1] < o) || o < 0 || o > m) flags |= 1u;
+  }
+  const int64_t mq = aligned ? m / 4 : 0;
+  for (int64_t i = t0; i < mq; i += stride) {
+    const int4 t = reinterpret_cast<const int4*>(tgt)[i];
+    if (uint32_t(t.x) >= uint64_t(n) || uint32_t(t.y) >= uint64_t(n) || uint32_t(t.z) >= uint64_t(n) ||
+        uint32_t(t.w) >= uint64_t(n))
+      flags |= 2u;
+  }
+  for (int64_t i = 4 * mq + t0; i < m; i += stride)
+    if (uint32_t(tgt[i]) >= uint64_t(n)) flags |= 2u;
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(bad, flags);
+}
+
 }  // namespace
 
 }  // namespace gc
@@ -108,6 +133,32 @@ int gc_edges_exist(const gc_csr* g, const int32_t* us, const int32_t* vs, int64_
     (k_edges_exist<<<grid_for(k, kEwBlock, 8), kEwBlock, 0, st>>>(g->offsets, g->targets, g->n, us, vs, k,
                                                                  first_missing), count_launch());
     GC_CHECK_LAUNCH();
+  });
+}
+
+int gc_check_csr(const gc_csr* g, void* stream) {
+  return guarded([&] {
+    require(g != nullptr, GC_ERR_ARG, "null graph");
+    require(g->n >= 0 && g->n < (int64_t(1) << 31), GC_ERR_MALFORMED, "vertex count outside [0, 2^31)");
+    require(g->m >= 0, GC_ERR_MALFORMED, "negative edge count");
+    require(g->offsets != nullptr || g->n == 0, GC_ERR_ARG, "null offsets");
+    require(g->targets != nullptr || g->m == 0, GC_ERR_ARG, "null targets");
+    if (g->offsets == nullptr) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned int* h = reinterpret_cast<unsigned int*>(pinned_words());
+    unsigned int* d = nullptr;
+    GC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4, st));
+    GC_CUDA(cudaMemsetAsync(d, 0, 4, st));
+    const int64_t work = g->n + 1 > g->m / 4 ? g->n + 1 : g->m / 4;
+    const int aligned = reinterpret_cast<uintptr_t>(g->targets) % 16 == 0;
+    (k_check_csr<<<grid_for(work, kEwBlock, 4), kEwBlock, 0, st>>>(g->offsets, g->targets, g->n, g->m, aligned,
+                                                                  d), count_launch());
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaMemcpyAsync(h, d, 4, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaFreeAsync(d, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    require(!(h[0] & 1u), GC_ERR_MALFORMED, "CSR offsets must start at 0, never decrease and end at m");
+    require(!(h[0] & 2u), GC_ERR_MALFORMED, "CSR target outside [0, n)");
   });
 }
 

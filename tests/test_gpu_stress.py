@@ -102,3 +102,19 @@ def test_hub_rows_and_duplicate_input():
                  "bfs+early+compress", "ldd+lt_crfa", "none+jtb+twotry"):
         labels, st = static_connectivity(g, parse_spec(text))
         assert np.array_equal(labels, ref), text
+
+
+def test_malformed_csr_is_rejected_not_faulted():
+    """Out-of-range targets / broken offsets raise MalformedInputError before
+    any kernel reads them (the GPU context stays usable)."""
+    from paper_2008_11839_b200 import Graph, MalformedInputError, parse_spec, static_connectivity
+    spec = parse_spec("kout+rem_cas+halve+splice")
+    bad_tgt = Graph(4, np.array([0, 1, 2, 3, 4]), np.array([1, 0, 3, 9], dtype=np.int32))
+    with pytest.raises(MalformedInputError, match="target"):
+        static_connectivity(bad_tgt, spec)
+    bad_off = Graph(4, np.array([0, 2, 1, 3, 4]), np.array([1, 0, 3, 2], dtype=np.int32))
+    with pytest.raises(MalformedInputError, match="offsets"):
+        static_connectivity(bad_off, spec)
+    ok = Graph(4, np.array([0, 1, 2, 3, 4]), np.array([1, 0, 3, 2], dtype=np.int32))
+    labels, _ = static_connectivity(ok, spec)
+    assert labels.tolist() == [0, 0, 2, 2]
