@@ -246,21 +246,43 @@ __global__ void __launch_bounds__(kEwBlock)
 k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
                 unsigned long long* ctr, int only_fallback) {
   if (only_fallback && majority(ctr, n)) return;
+  // four vertices per thread (one 16-byte label load), one scan and one
+  // global atomic per 1024 vertices
   using Scan = cub::BlockScan<int, kEwBlock>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
   const int32_t lmax = int32_t(ctr[C_LMAX]);
+  const bool aligned = (reinterpret_cast<uintptr_t>(P) & 15) == 0;
   unsigned long long degsum = 0;
-  for (int64_t b0 = int64_t(blockIdx.x) * kEwBlock; b0 < n; b0 += int64_t(gridDim.x) * kEwBlock) {
-    const int64_t v = b0 + threadIdx.x;
-    const int act = v < n && P[v] != lmax;
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  for (int64_t q0 = int64_t(blockIdx.x) * kEwBlock; q0 < nq; q0 += int64_t(gridDim.x) * kEwBlock) {
+    const int64_t q = q0 + threadIdx.x;
+    const int64_t v0 = q * 4;
+    int32_t lab[4] = {lmax, lmax, lmax, lmax};
+    if (q < nq) {
+      if (aligned && v0 + 3 < n) {
+        const int4 p4 = *reinterpret_cast<const int4*>(P + v0);
+        lab[0] = p4.x; lab[1] = p4.y; lab[2] = p4.z; lab[3] = p4.w;
+      } else {
+        for (int j = 0; j < 4; ++j) if (v0 + j < n) lab[j] = P[v0 + j];
+      }
+    }
+    int act = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) act += lab[j] != lmax;
     int rank, total;
     Scan(tmp).ExclusiveSum(act, rank, total);
     if (threadIdx.x == 0) base = total ? atomicAdd(ctr + C_N_ACTIVE, static_cast<unsigned long long>(total)) : 0ull;
     __syncthreads();
     if (act) {
-      list[base + rank] = int32_t(v);
-      degsum += static_cast<unsigned long long>(off[v + 1] - off[v]);
+      unsigned long long pos = base + rank;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (lab[j] != lmax) {
+          list[pos++] = int32_t(v0 + j);
+          degsum += static_cast<unsigned long long>(off[v0 + j + 1] - off[v0 + j]);
+        }
+      }
     }
     __syncthreads();
   }
@@ -477,7 +499,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
   }
   (k_mode_finish<<<1, 1, 0, st>>>(n, ctr), ::gc::count_launch());
   if (n > 0)
-    (k_gather_active<<<grid_for(n, kEwBlock, 1), kEwBlock, 0, st>>>(P, n, off, list, ctr, 1),
+    (k_gather_active<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 1), kEwBlock, 0, st>>>(P, n, off, list, ctr, 1),
      ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
@@ -485,7 +507,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
 void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr,
                 cudaStream_t st) {
   if (n <= 0) return;
-  (k_gather_active<<<grid_for(n, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, off, list, ctr, 0),
+  (k_gather_active<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, off, list, ctr, 0),
    ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
