@@ -129,6 +129,10 @@ void ensure_coo(gc_incr* h, int64_t len) {
     GC_CUDA(cudaMalloc(&c->w, cap));
     c->idx = nullptr;
   }
+  cudaFree(h->rw.keep);
+  h->rw.keep = nullptr;
+  GC_CUDA(cudaMalloc(&h->rw.keep, cap));
+  if (!h->rw.chunks) GC_CUDA(cudaMalloc(&h->rw.chunks, (2 * kMaxChunks + 4) * sizeof(int64_t)));
   h->coo_cap = cap;
 }
 
@@ -262,6 +266,8 @@ void gc_incr_destroy(gc_incr* h) {
     cudaFree(c->v);
     cudaFree(c->w);
   }
+  cudaFree(h->rw.keep);
+  cudaFree(h->rw.chunks);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   delete h;

@@ -167,29 +167,110 @@ __global__ void k_fill_u64(unsigned long long* a, int64_t n, unsigned long long 
 // ------------------------------------------------------ Shiloach-Vishkin ---
 // minbased.py:124-155: hook the larger endpoint label onto the smaller when
 // the larger is a root of the snapshot, then fully shortcut.
-__global__ void k_sv_hook(Coo c, const unsigned long long* len, const int32_t* __restrict__ prev,
-                          int32_t* cur, Ctl ctl) {
+// SV over a chunked working list.  An edge whose endpoints share a snapshot
+// label never sends another message (SV moves only roots and every vertex
+// follows its label's chain, so equal labels stay equal), so after each
+// round's hook every block compacts its own chunk in place, keeping only the
+// differing edges: on a permuted grid 63% / 33% / 15% / 5% of the edges
+// remain after rounds 1-4.  Each block owns one chunk for the whole loop (no
+// global cursor); counted inspections keep the reference's full per-round
+// edge count.
+struct Chunks {
+  int64_t* start = nullptr;
+  int64_t* len = nullptr;
+  uint8_t* keep = nullptr;             // per working edge: snapshot labels differ
+  unsigned long long* count = nullptr; // [live, kept] per round parity: live[0..1], kept[2..3]
+};
+
+__global__ void k_chunk_init(Chunks ch, int nch, int64_t total) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) ch.count[0] = ch.count[1] = ch.count[2] = ch.count[3] = 0;
+  if (c >= nch) return;
+  const int64_t per = (total + nch - 1) / nch;
+  const int64_t s = int64_t(c) * per < total ? int64_t(c) * per : total;
+  const int64_t e = s + per < total ? s + per : total;
+  ch.start[c] = s;
+  ch.len[c] = e - s;
+}
+
+// hook: block b walks its chunk (no barriers, as a grid-stride loop would);
+// keep[k] marks the edges whose snapshot labels still differ
+__global__ void __launch_bounds__(kRB)
+k_sv_hook_chunk(Coo c, Chunks ch, const int32_t* __restrict__ prev, int32_t* cur, uint8_t* keep, int par,
+                Ctl ctl) {
   GC_SKIP_IF_DONE(ctl);
-  const int64_t m = int64_t(*len);
+  const int64_t s = ch.start[blockIdx.x], L = ch.len[blockIdx.x];
   bool any = false;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
+  int kept = 0;
+  for (int64_t t = threadIdx.x; t < L; t += kRB) {
+    const int64_t k = s + t;
     const int32_t pu = prev[c.u[k]], pv = prev[c.v[k]];
     const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
+    keep[k] = lo != hi;
+    kept += lo != hi;
     if (lo != hi && prev[hi] == hi) {
       if (lo < ld_acq(cur + hi)) red_min(cur + hi, lo);
       any = true;
     }
   }
+  kept = __reduce_add_sync(0xffffffffu, kept);
+  if ((threadIdx.x & 31) == 0 && kept) atomicAdd(ch.count + 2 + par, static_cast<unsigned long long>(kept));
+  if (threadIdx.x == 0 && L) atomicAdd(ch.count + par, static_cast<unsigned long long>(L));
   if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
-__global__ void k_sv_win(Coo c, const unsigned long long* len, const int32_t* __restrict__ prev,
-                         const int32_t* cur, unsigned long long* win, Ctl ctl) {
+// streaming in-place compaction of each chunk by its keep flags (tiles of
+// the block; every thread reads its entry before the scan's barrier, and a
+// write position never passes a read position)
+__global__ void __launch_bounds__(kRB)
+k_chunk_compact(Coo c, Chunks ch, const uint8_t* __restrict__ keep, int par, Ctl ctl) {
   GC_SKIP_IF_DONE(ctl);
-  const int64_t m = int64_t(*len);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
+  // the next round's hook counts into the other parity
+  if (blockIdx.x == 0 && threadIdx.x == 0) ch.count[par ^ 1] = ch.count[2 + (par ^ 1)] = 0;
+  // compaction pays when at least a third of the live edges closed (the
+  // first round never drops any: labels start as the identity)
+  const unsigned long long live = ch.count[par], kept = ch.count[2 + par];
+  if (3 * (live - kept) < live) return;
+  using Scan = cub::BlockScan<int, kRB>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t s = ch.start[blockIdx.x], L = ch.len[blockIdx.x];
+  int64_t wpos = 0;
+  for (int64_t t0 = 0; t0 < L; t0 += kRB) {
+    const int64_t k = s + t0 + threadIdx.x;
+    int kp = 0;
+    int32_t u = 0, v = 0;
+    uint8_t w = 0;
+    int64_t id = 0;
+    if (t0 + threadIdx.x < L && keep[k]) {
+      kp = 1;
+      u = c.u[k];
+      v = c.v[k];
+      w = c.w[k];
+      if (c.idx) id = c.idx[k];
+    }
+    int rank, total;
+    Scan(tmp).ExclusiveSum(kp, rank, total);
+    if (kp) {
+      const int64_t p = s + wpos + rank;
+      c.u[p] = u;
+      c.v[p] = v;
+      c.w[p] = w;
+      if (c.idx) c.idx[p] = id;
+    }
+    wpos += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ch.len[blockIdx.x] = wpos;
+}
+
+// forest winners over the compacted chunks (a winning edge has differing
+// snapshot labels, so compaction never drops one)
+__global__ void k_sv_win_chunk(Coo c, Chunks ch, const int32_t* __restrict__ prev, const int32_t* cur,
+                               unsigned long long* win, Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t s = ch.start[blockIdx.x], L = ch.len[blockIdx.x];
+  for (int64_t t = threadIdx.x; t < L; t += blockDim.x) {
+    const int64_t k = s + t;
     const int32_t pu = prev[c.u[k]], pv = prev[c.v[k]];
     const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
     if (lo != hi && prev[hi] == hi && cur[hi] == lo)
@@ -400,7 +481,8 @@ struct ForestOut {
 
 // Enqueue one round of the configured family (round `r`, parity r & 1).
 void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, RoundsWs& w, Ctl ctl,
-                   int64_t edge_cap, const ForestOut& fo, int32_t*& A, int32_t*& B, cudaStream_t st) {
+                   int64_t edge_cap, const ForestOut& fo, int32_t*& A, int32_t*& B, const Chunks& ch,
+                   cudaStream_t st) {
   const int par = r & 1;
   const int gv = grid_e(nl);
   const int ge = grid_e(edge_cap > 0 ? edge_cap : 1);
@@ -410,11 +492,12 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
   ((k_round_begin<<<1, 1, 0, st>>>(ctl, alter ? par : 0, int(alter))), ::gc::count_launch());
   if (s.finish == GC_FINISH_SV) {
     L1(k_copy, gv, B, A, nl, ctl);
-    L1(k_sv_hook, ge, cur, len, A, B, ctl);
+    L1(k_sv_hook_chunk, ge, cur, ch, A, B, ch.keep, par, ctl);
     if (fo.on()) {
-      L1(k_sv_win, ge, cur, len, A, B, w.win, ctl);
+      L1(k_sv_win_chunk, ge, cur, ch, A, B, w.win, ctl);
       L1(k_commit_win, gv, w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv, ctl);
     }
+    L1(k_chunk_compact, ge, cur, ch, ch.keep, par, ctl);
     L1(k_full_shortcut, gv, B, nl, ctl);
     std::swap(A, B);
   } else if (s.finish == GC_FINISH_LT) {
@@ -462,8 +545,20 @@ void loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsWs& 
   int32_t* A = P;
   int32_t* B = w.b;
   unsigned long long* h = host_words();
+  // SV: per-block chunks of the working list, compacted in place each round
+  Chunks ch;
+  const int nch = grid_e(len > 0 ? len : 1);
+  if (s.finish == GC_FINISH_SV) {
+    require(w.keep != nullptr && w.chunks != nullptr && nch <= kMaxChunks, GC_ERR_OOM, "SV chunk tables missing");
+    ch.start = w.chunks;
+    ch.len = w.chunks + kMaxChunks;
+    ch.keep = w.keep;
+    ch.count = reinterpret_cast<unsigned long long*>(w.chunks + 2 * kMaxChunks);
+    ((k_chunk_init<<<(nch + 255) / 256, 256, 0, st>>>(ch, nch, len)), ::gc::count_launch());
+    GC_CHECK_LAUNCH();
+  }
   for (int r = 0; nonempty;) {
-    for (int k = 0; k < kBatch; ++k, ++r) enqueue_round(s, r, P, nl, coo, w, ctl, len, fo, A, B, st);
+    for (int k = 0; k < kBatch; ++k, ++r) enqueue_round(s, r, P, nl, coo, w, ctl, len, fo, A, B, ch, st);
     GC_CUDA(cudaMemcpyAsync(h, ctl.done, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
     if (h[0]) break;

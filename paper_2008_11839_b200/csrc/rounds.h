@@ -35,7 +35,12 @@ struct RoundsWs {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   Coo work, spare;
+  uint8_t* keep = nullptr;   // SV: per working edge, snapshot labels differ
+  int64_t* chunks = nullptr; // SV: per-block chunk [start, len] tables
 };
+
+// upper bound of the edge-kernel grid (grid_for(.., 256, 8) on 148 SMs)
+constexpr int64_t kMaxChunks = 148 * 8 * 8;
 
 size_t rounds_cub_bytes(int64_t n);
 
@@ -54,6 +59,10 @@ void rounds_carve(A& a, RoundsWs& w, int64_t n, int64_t m, const gc_spec& s, boo
     c->v = a.template take<int32_t>(m);
     c->w = a.template take<uint8_t>(m);
     if (forest) c->idx = a.template take<int64_t>(m);
+  }
+  if (s.finish == GC_FINISH_SV) {
+    w.keep = a.template take<uint8_t>(m);
+    w.chunks = a.template take<int64_t>(2 * kMaxChunks + 4);
   }
 }
 

@@ -146,8 +146,10 @@ int gc_check_csr(const gc_csr* g, void* stream) {
     if (g->offsets == nullptr) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     unsigned int* h = reinterpret_cast<unsigned int*>(pinned_words());
-    unsigned int* d = nullptr;
-    GC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4, st));
+    // one device word per host thread, allocated once (a stream-ordered
+    // allocation would go back to the OS at every synchronisation)
+    static thread_local unsigned int* d = nullptr;
+    if (!d) GC_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), 16));
     GC_CUDA(cudaMemsetAsync(d, 0, 4, st));
     const int64_t work = g->n + 1 > g->m / 4 ? g->n + 1 : g->m / 4;
     const int aligned = reinterpret_cast<uintptr_t>(g->targets) % 16 == 0;
@@ -155,7 +157,6 @@ int gc_check_csr(const gc_csr* g, void* stream) {
                                                                   d), count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(h, d, 4, cudaMemcpyDeviceToHost, st));
-    GC_CUDA(cudaFreeAsync(d, st));
     GC_CUDA(cudaStreamSynchronize(st));
     require(!(h[0] & 1u), GC_ERR_MALFORMED, "CSR offsets must start at 0, never decrease and end at m");
     require(!(h[0] & 2u), GC_ERR_MALFORMED, "CSR target outside [0, n)");
