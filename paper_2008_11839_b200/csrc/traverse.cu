@@ -52,11 +52,6 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
   return v;
 }
 
-__global__ void k_fill64(unsigned long long* a, int64_t n, unsigned long long v) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
-}
-
 // ------------------------------------------------------------------- BFS ---
 // Direction-optimising level-synchronous BFS: top-down over a frontier
 // queue while the frontier is small, bottom-up over a frontier bitmap (n/8
