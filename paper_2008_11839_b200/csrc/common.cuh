@@ -93,12 +93,16 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// Block-wide sum of a 64-bit counter, one atomicAdd per block.
+// Block-wide sum of a 64-bit counter, one atomicAdd per block.  The staging
+// array is shared by every call in a kernel, so a call first waits until the
+// previous call's reader (warp 0) is done with it (compute-sanitizer
+// racecheck found the back-to-back calls racing).
 template <int BLOCK>
 __device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
   __shared__ unsigned long long part[BLOCK / kWarp];
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
   if (lane == 0) part[wid] = v;
   __syncthreads();
   if (wid == 0) {
