@@ -192,6 +192,10 @@ def test_sweep_rows_match_reference():
     got = [{k: str(r[k]) for k in _SWEEP_KEYS} for r in rows]
     assert got == API["sweep_incremental"]
     assert rows_to_csv_text(rows).splitlines()[0] == ",".join(API["csv_columns"])
+    static_rows = sweep_static(suite[:1], specs[:1], [1], repeats=1)
+    text = rows_to_csv_text(static_rows, roofline=True)
+    assert text.splitlines()[0].endswith("alg_bytes,hbm_gbs,hbm_frac")
+    assert float(static_rows[0]["hbm_frac"]) > 0
 
 
 def test_binary_graph_host_roundtrip_and_errors(tmp_path):
