@@ -20,6 +20,14 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0  # B200_PROFILING.md fallback
+
+
 def ev_time(fn, reps, warm=2):
     import torch
     for _ in range(warm):
@@ -137,7 +145,8 @@ def config4(args):
     # incremental counts only initialised vertices (driver.py:719-724): the
     # isolated vertices of the CSR are never touched by an insert
     comps_init = comps - int((np.diff(offh) == 0).sum())
-    del offh, tgth
+    g_deg_host = offh
+    del tgth
     for text in ["none+async+halve", "none+rem_cas+halve+split", "none+sv", "none+lt_prs"]:
         spec = parse_spec(text)
         best = None
@@ -158,9 +167,17 @@ def config4(args):
                 labels, c = inc.labels()
                 ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref)) and c == comps_init
             del inc
+        # B = 16 |ins| + 16 |qry| + 4 hooks + ceil(|ops| / 8); the
+        # hooks (successful unions) of an insert-only stream number
+        # (initialised vertices) - (their components)
+        inited = int((np.diff(g_deg_host) > 0).sum())
+        hooks = inited - comps_init
+        alg = 16 * total + 4 * hooks + (total + 7) // 8
         emit(args.out, {"config": f"4: incremental RMAT s{scale} ef8, {bs}-edge insert batches", "spec": text,
                         "n": n, "inserts": total, "batches": (total + bs - 1) // bs, "seconds": best,
-                        "ops_per_s": total / best, "labels_bit_exact": ok, "components": comps_init})
+                        "ops_per_s": total / best, "labels_bit_exact": ok, "components": comps_init,
+                        "alg_bytes": alg, "hbm_gbs": alg / best / 1e9,
+                        "hbm_frac": alg / best / 1e9 / hbm_peak()})
 
 
 def config5(args):

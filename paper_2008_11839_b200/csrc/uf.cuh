@@ -44,7 +44,15 @@ __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u
       s.fv[slot] = v;
     }
     if (s.lu) {
-      const unsigned long long i = atomicAdd(s.lcount, 1ull);
+      // warp-aggregated append: one counter atomic per group of lanes that
+      // reach the link together (early incremental batches merge ~every edge)
+      const unsigned m = __activemask();
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(int(m)) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(s.lcount, static_cast<unsigned long long>(__popc(m)));
+      base = __shfl_sync(m, base, leader);
+      const unsigned long long i = base + __popc(m & ((1u << lane) - 1u));
       s.lu[i] = u;
       s.lv[i] = v;
     }

@@ -130,5 +130,86 @@ def main():
         torch.cuda.empty_cache()
 
 
+
+
+def run_incremental(P, scale, batch, check):
+    """Batch-sharded incremental (ShardedIncremental) replayed on one GPU:
+    per batch every rank inserts its 1/P slice recording merging edges, the
+    merges are exchanged (costed at NVLink rate) and every rank inserts the
+    foreign ones; batch time = max over ranks + exchange."""
+    from paper_2008_11839_b200 import IncrementalConnectivity
+    g = build_csr(gen_rmat(scale, 8, seed=1, device=True), keep_host=False)
+    n = g.n
+    off, tgt = g._d_off, g._d_tgt
+    src = torch.repeat_interleave(torch.arange(n, device="cuda", dtype=torch.int32), off[1:] - off[:-1])
+    keep = src < tgt
+    us, vs = src[keep], tgt[keep]
+    del src, keep
+    perm = torch.randperm(us.numel(), device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    us, vs = us[perm].contiguous(), vs[perm].contiguous()
+    del perm
+    spec = parse_spec("none+async+halve")
+    reps = [IncrementalConnectivity(spec, n) for _ in range(P)]
+    total_ms, comm_bytes = 0.0, 0
+    for b0 in range(0, us.numel(), batch):
+        bu, bv = us[b0:b0 + batch], vs[b0:b0 + batch]
+        k = bu.numel()
+        t_rank = [0.0] * P
+        merges = []
+        for r in range(P):
+            lo, hi = (k * r) // P, (k * (r + 1)) // P
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            mu, mv = reps[r].insert_list(bu[lo:hi], bv[lo:hi])
+            e1.record()
+            e1.synchronize()
+            t_rank[r] += e0.elapsed_time(e1)
+            merges.append((mu, mv))
+        if P > 1:
+            for r in range(P):
+                fu = torch.cat([m[0] for q, m in enumerate(merges) if q != r])
+                fv = torch.cat([m[1] for q, m in enumerate(merges) if q != r])
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                if fu.numel():
+                    reps[r].insert(fu, fv)
+                e1.record()
+                e1.synchronize()
+                t_rank[r] += e0.elapsed_time(e1)
+            nbytes = sum(m[0].numel() for m in merges) * 8
+            comm_bytes += nbytes
+            total_ms += max(t_rank) + nbytes / NVLINK * 1e3
+        else:
+            total_ms += t_rank[0]
+    ok = None
+    if check:
+        import oracle
+        ref, _ = oracle.components(n, off.cpu().numpy(), tgt.cpu().numpy())
+        lab, _ = reps[0].labels()
+        lab = lab.cpu().numpy().astype(np.int64)
+        deg = np.diff(off.cpu().numpy())
+        ok = bool(np.array_equal(lab[deg > 0], ref[deg > 0]))
+    return {"mode": "incremental", "ranks": P, "scale": scale, "n": n, "inserts": int(us.numel()), "batch": batch,
+            "labels_ok": ok, "step_ms_model": total_ms, "inserts_per_s_model": us.numel() / (total_ms / 1e3),
+            "exchanged_bytes": comm_bytes}
+
+
+def main_incremental():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--incremental", action="store_true")
+    ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--scale", type=int, default=26)
+    ap.add_argument("--batch", type=int, default=10_000_000)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    for P in (int(x) for x in a.ranks.split(",")):
+        run_incremental(P, a.scale, a.batch, False)  # warm-up
+        print(json.dumps(run_incremental(P, a.scale, a.batch, a.check)), flush=True)
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    main()
+    if "--incremental" in sys.argv:
+        main_incremental()
+    else:
+        main()
