@@ -193,13 +193,13 @@ def run_sharded(args):
     else:
         dist.init_process_group(backend, **kw)
     from paper_2008_11839_b200 import parse_spec
-    from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+    from paper_2008_11839_b200.distributed import shard_balance, shard_bounds, shard_graph, sharded_two_phase
 
     spec = parse_spec(SPEC)
     scale = args.scale + int(math.ceil(math.log2(ws)))
     g = make_graph(scale, args.edge_factor, args.seed)
     n, m = g.n, g.m
-    lo, hi = shard_bounds(g._d_off, ws)[rank]
+    lo, hi = shard_bounds(g._d_off, ws, shard_balance(spec))[rank]
     shard = shard_graph(g, lo, hi)
     parity = None
     res = sharded_two_phase(shard, spec, forest=False)
@@ -253,14 +253,17 @@ def run_sharded(args):
     if args.e2e_steps > 0:
         off_h = shard._d_off.cpu().pin_memory()
         tgt_h = shard._d_tgt.cpu().pin_memory()
-        sharded_two_phase(Graph(n, off_h, tgt_h).cuda(), spec, forest=False)
+        def host_shard():
+            hg = Graph(n, off_h, tgt_h)
+            hg.row_block = shard.row_block
+            return hg
+        sharded_two_phase(host_shard().cuda(), spec, forest=False)
         et = []
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
-            hg = Graph(n, off_h, tgt_h)
-            r = sharded_two_phase(hg.cuda(), spec, forest=False)
+            r = sharded_two_phase(host_shard().cuda(), spec, forest=False)
             host_int64(r.labels)
             torch.cuda.synchronize()
             et.append(time.perf_counter() - t0)

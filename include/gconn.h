@@ -191,6 +191,8 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
  * The reference is single-process; these split `_pipeline`
  * (driver.py:454-500) at its two exchange points so a driver can run it over
  * edge-sharded CSR blocks (rows outside the block empty):
+ *   [row_lo, row_hi) is the block's row range (rows outside it are empty in
+ *   the block's CSR; the samplers and the unsampled finish walk only it).
  *   gc_shard_sample: parent := identity, then the sampler (none / k-out
  *     FIRST_K / HB) over the block's rows.  Every union that merged two trees
  *     appends its (u, v) to out_u/out_v (capacity n) and bumps *out_count
@@ -202,14 +204,14 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
  *     the same way.  stats: insp_finish (block), l_max, lmax_count, n_active.
  *   -- exchange again, union foreign edges, gc_label_finalization --
  * Union-find finishes with root-based rules only. */
-int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent,
-                    int32_t* out_u, int32_t* out_v,
-                    unsigned long long* out_count, gc_stats* stats, void* ws,
-                    size_t ws_bytes, void* stream);
-int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent,
-                    int32_t* out_u, int32_t* out_v,
-                    unsigned long long* out_count, gc_stats* stats, void* ws,
-                    size_t ws_bytes, void* stream);
+int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int64_t row_lo,
+                    int64_t row_hi, int32_t* parent, int32_t* out_u,
+                    int32_t* out_v, unsigned long long* out_count,
+                    gc_stats* stats, void* ws, size_t ws_bytes, void* stream);
+int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo,
+                    int64_t row_hi, int32_t* parent, int32_t* out_u,
+                    int32_t* out_v, unsigned long long* out_count,
+                    gc_stats* stats, void* ws, size_t ws_bytes, void* stream);
 
 /* Compact phase-1 exchange for labels-only runs (no forest), in two rounds
  * (csrc/shard.cu):

@@ -86,10 +86,10 @@ _SIGNATURES = {
     "gc_build_csr": (C.c_int, [_I64, _VP, _VP, _I64, _VP, _VP, C.POINTER(_I64), _VP, _SZ, _VP]),
     "gc_build_csr_workspace": (_SZ, [_I64, _I64]),
     "gc_mt19937_fill": (C.c_int, [_VP, C.c_int32, _VP, _I64]),
-    "gc_shard_sample": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _VP, _VP, C.POINTER(Stats),
-                                  _VP, _SZ, _VP]),
-    "gc_shard_finish": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _VP, _VP, _VP, _VP, C.POINTER(Stats),
-                                  _VP, _SZ, _VP]),
+    "gc_shard_sample": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _I64, _I64, _VP, _VP, _VP, _VP,
+                                  C.POINTER(Stats), _VP, _SZ, _VP]),
+    "gc_shard_finish": (C.c_int, [C.POINTER(Csr), C.POINTER(Spec), _I64, _I64, _VP, _VP, _VP, _VP,
+                                  C.POINTER(Stats), _VP, _SZ, _VP]),
     "gc_shard_summary_workspace": (_SZ, [_I64]),
     "gc_shard_summary": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "gc_shard_absorb": (C.c_int, [_VP, _I64, _VP, _VP, C.c_int32, _VP, _VP, _SZ, _VP]),

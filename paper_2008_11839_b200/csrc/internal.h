@@ -126,6 +126,7 @@ struct RowUnionArgs {
   int32_t* lu = nullptr;  // optional compact list of the edges that merged two trees
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
+  int64_t row_base = 0;   // list == nullptr: rows [row_base, row_base + count_host)
 };
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st);
 

@@ -36,13 +36,30 @@ __device__ __forceinline__ int32_t root_weak(const int32_t* P, int32_t x) {
 }
 
 __global__ void k_compress(int32_t* P, int32_t n) {
+  // four vertices per thread; the first hop of the four walks is issued
+  // together and only parents that moved keep walking
+  const bool aligned = (reinterpret_cast<uintptr_t>(P) & 15) == 0;
+  const int64_t nq = (int64_t(n) + 3) / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int32_t v = int32_t(i);
-    const int32_t p = ld_weak(P + v);
-    if (p == v) continue;
-    const int32_t r = root_weak(P, p);
-    if (r != p) P[v] = r;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int64_t v0 = 4 * q;
+    int32_t p[4];
+    if (aligned && v0 + 3 < n) {
+      const int4 p4 = *reinterpret_cast<const int4*>(P + v0);
+      p[0] = p4.x; p[1] = p4.y; p[2] = p4.z; p[3] = p4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) p[j] = v0 + j < n ? ld_weak(P + v0 + j) : int32_t(v0 + j);
+    }
+    int32_t hop[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) hop[j] = (v0 + j < n && p[j] != int32_t(v0 + j)) ? ld_free(P + p[j]) : p[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (v0 + j >= n || hop[j] == p[j]) continue;  // a root, or already points at its root
+      const int32_t r = root_weak(P, hop[j]);
+      P[v0 + j] = r;
+    }
   }
 }
 
@@ -150,7 +167,9 @@ __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t
   int slot = -1;
   if (i < s) {
     const unsigned same = __match_any_sync(__activemask(), x);
-    slot = int((uint32_t(x) * 2654435761u) % kSlots);
+    // multiplicative hash, high bits (the samples are evenly spaced ids, so
+    // the low bits of x * K can all coincide)
+    slot = int((uint32_t(x) * 2654435761u) >> (32 - 11));
     while (true) {
       const int32_t k = atomicCAS(&key_[slot], -1, x);
       if (k == -1 || k == x) break;

@@ -40,10 +40,14 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
   const int32_t n = int32_t(g.n);
   if (n == 0) return;
   if (s.kout_mode == GC_KOUT_FIRST_K) {
-    // sampling.py:68-71: the first min(k, deg) (smallest) neighbours
+    // sampling.py:68-71: the first min(k, deg) (smallest) neighbours; a
+    // sharded caller restricts the rows to its block (a.row_base/count_host)
     a.list = nullptr;
     a.count_dev = nullptr;
-    a.count_host = n;
+    if (a.count_host <= 0 || a.count_host > n) {
+      a.row_base = 0;
+      a.count_host = n;
+    }
     a.take_max = s.kout_k;
     a.lower_only = 0;
     a.insp = ctr + C_INSP_SAMPLE;
@@ -64,16 +68,16 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
 // Phase 1 (sampling.py:98-108): every non-isolated vertex points at its
 // first (smallest) neighbour when that is smaller — write-disjoint, no
 // atomics.  The surviving non-isolated roots form the phase-2 list.
-__global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int32_t n, int32_t* P,
+__global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int64_t lo, int64_t hi, int32_t* P,
                             int32_t* fu, int32_t* fv, int32_t* roots, unsigned long long* ctr,
                             int32_t* lu, int32_t* lv, unsigned long long* lcount) {
   unsigned long long nz = 0;
   const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+  for (int64_t base = lo + int64_t(blockIdx.x) * blockDim.x; base < hi; base += stride) {
     const int64_t v = base + threadIdx.x;
     bool root = false;
-    if (v < n) {
+    if (v < hi) {
       const int64_t b = off[v], e = off[v + 1];
       if (e > b) {
         ++nz;
@@ -110,14 +114,20 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:95-96
   GC_CUDA(cudaMemsetAsync(ctr + C_SCRATCH0, 0, 8, st));
-  (k_hb_phase1<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, n, a.P, a.fu,
-                                                             a.fv, w.q0, ctr, a.lu, a.lv, a.lcount),
+  int64_t lo = 0, hi = n;
+  if (a.count_host > 0 && a.count_host <= n) {  // sharded caller: its row block
+    lo = a.row_base;
+    hi = a.row_base + a.count_host;
+  }
+  (k_hb_phase1<<<grid_for(hi - lo, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, lo, hi, a.P, a.fu,
+                                                                   a.fv, w.q0, ctr, a.lu, a.lv, a.lcount),
    ::gc::count_launch());
   GC_CHECK_LAUNCH();
   // Phase 2 (sampling.py:110-116): union the first N edges of each root
   a.list = w.q0;
   a.count_dev = ctr + C_SCRATCH0;
   a.count_host = n;
+  a.row_base = 0;
   a.take_max = s.hb_edges;
   a.lower_only = 0;
   a.insp = ctr + C_INSP_SAMPLE;

@@ -160,6 +160,7 @@ struct Pipeline {
   int32_t* lu = nullptr;  // sharded drivers: merging edges of the union kernels
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
+  int64_t row_lo = 0, row_hi = -1;  // sharded drivers: the rows this block owns (-1: all)
 
   Pipeline(const gc_csr& g_, const gc_spec& s_, int32_t* P_, int32_t* fu_, int32_t* fv_,
            void* wsp, size_t wsb, cudaStream_t st_)
@@ -183,6 +184,10 @@ struct Pipeline {
     a.lu = lu;
     a.lv = lv;
     a.lcount = lcount;
+    if (row_hi >= 0) {  // samplers walk only this block's rows
+      a.row_base = row_lo;
+      a.count_host = row_hi - row_lo;
+    }
     return a;
   }
 
@@ -249,7 +254,8 @@ struct Pipeline {
         // count Σdeg is added analytically
         a.list = nullptr;
         a.count_dev = nullptr;
-        a.count_host = n;
+        a.row_base = row_hi >= 0 ? row_lo : 0;
+        a.count_host = row_hi >= 0 ? row_hi - row_lo : n;
         a.take_max = INT_MAX;
         a.lower_only = 1;
         a.insp = nullptr;
@@ -257,6 +263,7 @@ struct Pipeline {
       } else {
         a.list = ws.list;
         a.count_dev = ws.ctr + C_N_ACTIVE;
+        a.row_base = 0;
         a.count_host = n;
         a.take_max = INT_MAX;
         a.lower_only = 0;
@@ -598,8 +605,9 @@ void read_ctr(unsigned long long* dst, const unsigned long long* ctr, cudaStream
 
 }  // namespace
 
-int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32_t* out_u, int32_t* out_v,
-                    unsigned long long* out_count, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_t row_hi, int32_t* parent,
+                    int32_t* out_u, int32_t* out_v, unsigned long long* out_count, gc_stats* stats, void* ws,
+                    size_t ws_bytes, void* stream) {
   return guarded([&] {
     check_static_args(g, spec, parent);
     check_shard_spec(spec);
@@ -608,7 +616,10 @@ int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32
     require(!record || (out_v && out_count), GC_ERR_ARG, "null merging-edge output");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (record) GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    require(row_lo >= 0 && row_lo <= row_hi && row_hi <= g->n, GC_ERR_ARG, "row block outside [0, n]");
     Pipeline pl(*g, *spec, parent, nullptr, nullptr, ws, ws_bytes, st);
+    pl.row_lo = row_lo;
+    pl.row_hi = row_hi;
     const bool edges = spec->splice != GC_SPLICE_ATOMIC;  // root-based: record real merging edges
     if (record && edges) {
       pl.lu = out_u;
@@ -633,15 +644,19 @@ int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32
   });
 }
 
-int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int32_t* parent, int32_t* out_u, int32_t* out_v,
-                    unsigned long long* out_count, gc_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_t row_hi, int32_t* parent,
+                    int32_t* out_u, int32_t* out_v, unsigned long long* out_count, gc_stats* stats, void* ws,
+                    size_t ws_bytes, void* stream) {
   return guarded([&] {
     check_static_args(g, spec, parent);
     check_shard_spec(spec);
     require(out_u && out_v && out_count, GC_ERR_ARG, "null merging-edge output");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));
+    require(row_lo >= 0 && row_lo <= row_hi && row_hi <= g->n, GC_ERR_ARG, "row block outside [0, n]");
     Pipeline pl(*g, *spec, parent, nullptr, nullptr, ws, ws_bytes, st);
+    pl.row_lo = row_lo;
+    pl.row_hi = row_hi;
     const bool edges = spec->splice != GC_SPLICE_ATOMIC;
     if (edges) {
       pl.lu = out_u;

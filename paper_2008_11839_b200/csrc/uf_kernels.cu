@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(kRowBlock)
 k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
              const int32_t* __restrict__ list, const unsigned long long* count_dev,
              int64_t count_host, int32_t take_max, int32_t lower_only,
-             unsigned long long* insp) {
+             unsigned long long* insp, int64_t row_base) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (int64_t(blockIdx.x) * kRowBlock + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * kRowBlock) >> 5;
@@ -41,7 +41,7 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
     int64_t b = 0;
     int32_t take = 0;
     if (i < count) {
-      u = list ? ldg32(list + i) : int32_t(i);
+      u = list ? ldg32(list + i) : int32_t(row_base + i);
       // offsets stream through (no L1 allocation, L2 evict-first); targets
       // keep the default L1 path, which measured faster for the
       // neighbouring-row reuse within a warp
@@ -173,7 +173,7 @@ struct RowsLaunch {
     if (blocks < 1) blocks = 1;
     (k_union_rows<R><<<int(blocks), kRowBlock, 0, st>>>(s, a.off, a.tgt, a.list, a.count_dev,
                                                         a.count_host, a.take_max, a.lower_only,
-                                                        a.insp), ::gc::count_launch());
+                                                        a.insp, a.row_base), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };

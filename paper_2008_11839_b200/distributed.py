@@ -51,19 +51,31 @@ def _dist():
 
 # ------------------------------------------------------------------ sharding
 
-def shard_bounds(offsets, world: int) -> list[tuple[int, int]]:
-    """Contiguous row blocks [lo, hi) with (nearly) equal directed-edge counts."""
+def shard_bounds(offsets, world: int, by: str = "edges") -> list[tuple[int, int]]:
+    """Contiguous row blocks [lo, hi) with (nearly) equal directed-edge counts
+    (``by="edges"``: the unsampled finish walks every edge) or equal row
+    counts (``by="rows"``: k-out / HB sampling costs the same per row
+    whatever its degree, so edge-balanced blocks would leave the ranks that
+    hold the many low-degree rows with most of the work)."""
     off = np.asarray(offsets.cpu() if hasattr(offsets, "cpu") else offsets, dtype=np.int64)
     n = len(off) - 1
     m = int(off[-1])
     cuts = [0]
     for r in range(1, world):
-        cuts.append(int(np.searchsorted(off, (m * r) // world, side="left")))
+        if by == "rows":
+            cuts.append((n * r) // world)
+        else:
+            cuts.append(int(np.searchsorted(off, (m * r) // world, side="left")))
     cuts.append(n)
     cuts = [min(max(c, 0), n) for c in cuts]
     for i in range(1, len(cuts)):
         cuts[i] = max(cuts[i], cuts[i - 1])
     return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def shard_balance(spec: AlgorithmSpec) -> str:
+    """The shard_bounds balance for a spec (rows for the per-row samplers)."""
+    return "rows" if spec.sample in (SampleKind.KOUT, SampleKind.HB) else "edges"
 
 
 def shard_graph(g, lo: int, hi: int):
@@ -75,10 +87,13 @@ def shard_graph(g, lo: int, hi: int):
         idx = torch.arange(g.n + 1, device=off.device).clamp_(lo, hi)
         off_s = off[idx] - off[lo]
         tgt_s = tgt[off[lo]:off[hi]]
-        return Graph(g.n, off_s.contiguous(), tgt_s.contiguous())
-    off, tgt = g.offsets, g.targets
-    idx = np.clip(np.arange(g.n + 1), lo, hi)
-    return Graph(g.n, off[idx] - off[lo], tgt[off[lo]:off[hi]])
+        out = Graph(g.n, off_s.contiguous(), tgt_s.contiguous())
+    else:
+        off, tgt = g.offsets, g.targets
+        idx = np.clip(np.arange(g.n + 1), lo, hi)
+        out = Graph(g.n, off[idx] - off[lo], tgt[off[lo]:off[hi]])
+    out.row_block = (int(lo), int(hi))  # the kernels walk only these rows
+    return out
 
 
 # -------------------------------------------------------------------- engine
@@ -144,14 +159,15 @@ class GpuEngine:
         lib = N.lib()
         ws = _workspace(lib.gc_workspace_size(n, shard.m, C.byref(low.s)))
         st = N.Stats()
+        lo, hi = getattr(shard, "row_block", (0, n))
         if not record:
-            N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), parent.data_ptr(), None, None, None,
+            N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), lo, hi, parent.data_ptr(), None, None, None,
                                      C.byref(st), ws.data_ptr(), ws.numel(), _stream()))
             return None, None, st
         out_u = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         out_v = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-        N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), parent.data_ptr(), out_u.data_ptr(),
+        N.check(getattr(lib, fn)(C.byref(csr), C.byref(low.s), lo, hi, parent.data_ptr(), out_u.data_ptr(),
                                  out_v.data_ptr(), cnt.data_ptr(), C.byref(st), ws.data_ptr(), ws.numel(),
                                  _stream()))
         c = int(cnt.item())

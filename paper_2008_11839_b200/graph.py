@@ -132,6 +132,8 @@ class Graph:
         d_off, d_tgt = self.device_arrays()
         g = Graph(self.n, d_off, d_tgt)
         g._h_off, g._h_tgt = self._h_off, self._h_tgt
+        if hasattr(self, "row_block"):  # a sharded row block stays one
+            g.row_block = self.row_block
         return g
 
     def drop_host(self) -> None:

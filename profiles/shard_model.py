@@ -22,7 +22,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec  # noqa: E402
-from paper_2008_11839_b200.distributed import GpuEngine, shard_bounds, shard_graph  # noqa: E402
+from paper_2008_11839_b200.distributed import GpuEngine, shard_balance, shard_bounds, shard_graph  # noqa: E402
 
 NVLINK = 770e9  # bytes/s per direction, measured peer copy (B200_PROFILING.md)
 
@@ -44,7 +44,8 @@ class Timer:
 def build(P, scale0, strong=False):
     scale = scale0 if strong else scale0 + int(math.ceil(math.log2(P)))
     g = build_csr(gen_rmat(scale, 8, seed=1, device=True), keep_host=False)
-    return scale, g, [shard_graph(g, lo, hi) for lo, hi in shard_bounds(g._d_off, P)]
+    by = shard_balance(parse_spec("kout+rem_cas+halve+splice"))
+    return scale, g, [shard_graph(g, lo, hi) for lo, hi in shard_bounds(g._d_off, P, by)]
 
 
 def run(P, scale, g, shards, check):

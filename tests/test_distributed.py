@@ -92,6 +92,16 @@ def test_sharded_forest_and_labels(world):
             assert len(fu) == n - comps
 
 
+def test_shard_bounds_by_rows():
+    from paper_2008_11839_b200.distributed import shard_balance, shard_bounds
+    from paper_2008_11839_b200 import parse_spec
+    off = np.cumsum(np.concatenate([[0], np.arange(100)]))
+    b = shard_bounds(off, 4, "rows")
+    assert b == [(0, 25), (25, 50), (50, 75), (75, 100)]
+    assert shard_balance(parse_spec("kout+async+halve")) == "rows"
+    assert shard_balance(parse_spec("none+async+halve")) == "edges"
+
+
 def test_shard_bounds_balance():
     from paper_2008_11839_b200.distributed import shard_bounds
     gold = Golden()
