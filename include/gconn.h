@@ -229,7 +229,7 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo,
  *     from their bitmaps + pairs (every bitmap member points at its class's
  *     smallest label, then the pairs are unioned with the spec's rule).
  * nranks <= 8.  ws: gc_shard_summary_workspace(n) bytes for the summary,
- * n + 4096 for absorb, 5*n + 8192 for join. */
+ * n + n/8 + 8192 for absorb, 5*n + 8192 for join. */
 size_t gc_shard_summary_workspace(int64_t n);
 int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint,
                      uint32_t* giant_bits, int64_t* giant_label, int32_t* out_u,

@@ -422,32 +422,94 @@ __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long
   block_add<kEwBlock>(out, c);
 }
 
-// Root transitions of one phase: every v that was a root before it
-// (before == nullptr: identity) and is not one now emits (v, P[v]) — one
-// pair per merge, all inside one component, so unioning them elsewhere
-// reproduces the partition change whatever the linking rule.
-__global__ void k_root_transitions(const int32_t* P, const int32_t* before, int32_t n, int32_t* out_u,
-                                   int32_t* out_v, unsigned long long* count) {
+// Root bitmap: bit v set when P[v] == v (the snapshot a later
+// k_root_transitions compares against — n/8 bytes instead of a parent copy).
+// Four vertices per thread; the eight lanes holding one word OR it together.
+__global__ void __launch_bounds__(kEwBlock) k_root_bitmap(const int32_t* __restrict__ P, int32_t n, uint32_t* bits) {
   const int lane = threadIdx.x & 31;
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  const int64_t words = (int64_t(n) + 31) / 32;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t v = base + threadIdx.x;
-    int32_t p = 0;
-    bool moved = false;
-    if (v < n) {
-      p = P[v];
-      moved = p != int32_t(v) && (before == nullptr || before[v] == int32_t(v));
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nq; base += stride) {
+    const int64_t q = base + threadIdx.x;
+    const int64_t v0 = 4 * q;
+    unsigned nib = 0;
+    if (v0 + 3 < n) {
+      const int4 p = reinterpret_cast<const int4*>(P)[q];
+      nib = unsigned(p.x == int32_t(v0)) | unsigned(p.y == int32_t(v0 + 1)) << 1 |
+            unsigned(p.z == int32_t(v0 + 2)) << 2 | unsigned(p.w == int32_t(v0 + 3)) << 3;
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (v0 + k < n) nib |= unsigned(P[v0 + k] == int32_t(v0 + k)) << k;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, moved);
-    if (!bal) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(count, static_cast<unsigned long long>(__popc(bal)));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
+    unsigned word = nib << (4 * (lane & 7));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    if ((lane & 7) == 0 && (v0 >> 5) < words) bits[v0 >> 5] = word;
+  }
+}
+
+// Root transitions of one phase: every v that was a root before it
+// (before == nullptr: every vertex was) and is not one now emits (v, P[v]) —
+// one pair per merge, all inside one component, so unioning them elsewhere
+// reproduces the partition change whatever the linking rule.  Four vertices
+// per thread, one counter atomic per block (a per-warp atomic on the single
+// counter serialised the pass when merges are spread thinly).
+__global__ void __launch_bounds__(kEwBlock)
+k_root_transitions(const int32_t* __restrict__ P, const uint32_t* __restrict__ before, int32_t n, int32_t* out_u,
+                   int32_t* out_v, unsigned long long* count) {
+  constexpr int kWarps = kEwBlock / 32;
+  __shared__ unsigned warp_n[kWarps];
+  __shared__ unsigned long long block_pos;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nq; base += stride) {
+    const int64_t q = base + threadIdx.x;
+    const int64_t v0 = 4 * q;
+    int32_t p[4] = {0, 1, 2, 3};
+    unsigned moved = 0;
+    if (q < nq) {
+      if (v0 + 3 < n) {
+        const int4 x = reinterpret_cast<const int4*>(P)[q];
+        p[0] = x.x, p[1] = x.y, p[2] = x.z, p[3] = x.w;
+      } else {
+        for (int k = 0; k < 4; ++k) p[k] = v0 + k < n ? P[v0 + k] : int32_t(v0 + k);
+      }
+      const unsigned was = before ? (__ldg(before + (v0 >> 5)) >> (v0 & 31)) & 0xfu : 0xfu;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) moved |= unsigned(p[k] != int32_t(v0 + k) && ((was >> k) & 1u)) << k;
+    }
+    const unsigned mine = __popc(moved);
+    if (!__syncthreads_or(mine != 0)) continue;
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_n[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) tot += warp_n[w];
+      block_pos = atomicAdd(count, static_cast<unsigned long long>(tot));
+    }
+    __syncthreads();
     if (moved) {
-      const unsigned long long i = pos + __popc(bal & ((1u << lane) - 1u));
-      out_u[i] = int32_t(v);
-      out_v[i] = p;
+      unsigned long long i = block_pos + incl - mine;
+      for (int w = 0; w < warp; ++w) i += warp_n[w];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (moved & (1u << k)) {
+          out_u[i] = int32_t(v0 + k);
+          out_v[i] = p[k];
+          ++i;
+        }
     }
+    __syncthreads();
   }
 }
 

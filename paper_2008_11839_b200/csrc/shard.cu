@@ -39,35 +39,75 @@ __global__ void k_pick_class(const int32_t* P, const int32_t* hint, unsigned lon
   *label_out = g;
 }
 
-// bitmap word per warp + block-aggregated remainder pairs (P compressed)
+// bitmap words + block-aggregated remainder pairs (P compressed).  Four
+// vertices per thread (one 16-byte load): a warp covers 128 vertices = four
+// bitmap words, each OR-reduced over the eight lanes that hold it.
 __global__ void __launch_bounds__(kEwBlock)
 k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ctr, uint32_t* bits,
           int32_t* out_u, int32_t* out_v, unsigned long long* out_count) {
+  constexpr int kWarps = kEwBlock / 32;
+  __shared__ unsigned warp_n[kWarps];
+  __shared__ unsigned long long block_pos;
   const int32_t g = int32_t(ctr[C_LMAX]);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t v = base + threadIdx.x;
-    int32_t lab = 0;
-    bool in_g = false, pair = false;
-    if (v < n) {
-      lab = P[v];
-      in_g = lab == g;
-      pair = !in_g && lab != int32_t(v);
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  const int64_t words = (int64_t(n) + 31) / 32;
+  // the trip count is uniform per block (base is), so the barriers are safe
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nq; base += stride) {
+    const int64_t q = base + threadIdx.x;
+    const int64_t v0 = 4 * q;
+    int32_t lab[4] = {0, 0, 0, 0};
+    if (v0 + 3 < n) {
+      const int4 p = reinterpret_cast<const int4*>(P)[q];
+      lab[0] = p.x, lab[1] = p.y, lab[2] = p.z, lab[3] = p.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) lab[k] = v0 + k < n ? P[v0 + k] : g;
     }
-    const unsigned word = __ballot_sync(0xffffffffu, in_g);
-    if (lane == 0 && base + (threadIdx.x & ~31) < n) bits[(base + (threadIdx.x & ~31)) >> 5] = word;
+    unsigned nib = 0, pairs = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in_g = lab[k] == g && v0 + k < n;
+      nib |= unsigned(in_g) << k;
+      pairs |= unsigned(!in_g && v0 + k < n && lab[k] != int32_t(v0 + k)) << k;
+    }
+    unsigned word = nib << (4 * (lane & 7));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    if ((lane & 7) == 0 && (v0 >> 5) < words) bits[v0 >> 5] = word;
     if (!out_u) continue;  // bitmap only (round A)
-    const unsigned bal = __ballot_sync(0xffffffffu, pair);
-    if (!bal) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(out_count, static_cast<unsigned long long>(__popc(bal)));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (pair) {
-      const unsigned long long i = pos + __popc(bal & ((1u << lane) - 1u));
-      out_u[i] = int32_t(v);
-      out_v[i] = lab;
+    // one counter atomic per block: small fragments are spread over most
+    // blocks, and a per-warp atomic on the one counter serialised the pass
+    const unsigned mine = __popc(pairs);
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
+    if (lane == 31) warp_n[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) tot += warp_n[w];
+      block_pos = tot ? atomicAdd(out_count, static_cast<unsigned long long>(tot)) : 0ull;
+    }
+    __syncthreads();
+    if (pairs) {
+      unsigned long long i = block_pos + incl - mine;
+      for (int w = 0; w < warp; ++w) i += warp_n[w];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (pairs & (1u << k)) {
+          out_u[i] = int32_t(v0 + k);
+          out_v[i] = lab[k];
+          ++i;
+        }
+    }
+    __syncthreads();  // warp_n / block_pos are rewritten next iteration
   }
 }
 
@@ -158,45 +198,99 @@ __device__ __forceinline__ int bitmap_class(const uint32_t* __restrict__ bits, i
   return q < 0 ? -1 : cls[q];
 }
 
+// the class (through cls) of each of the four vertices 4q..4q+3, from one
+// load of every rank's bitmap word
+__device__ __forceinline__ void quad_classes(const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
+                                             const int32_t* __restrict__ cls, int64_t v0, int c[4]) {
+  uint32_t b[kMaxRanks];
+#pragma unroll
+  for (int q = 0; q < kMaxRanks; ++q) b[q] = q < nranks ? __ldg(bits + int64_t(q) * words + (v0 >> 5)) : 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    unsigned hit = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q) hit |= ((b[q] >> ((v0 + k) & 31)) & 1u) << q;
+    c[k] = hit ? cls[__ffs(int(hit)) - 1] : -1;
+  }
+}
+
+// Both passes take four vertices per thread per step (one 16-byte parent
+// load, one bitmap word per rank): the one-vertex form issued two dependent
+// DRAM round trips per vertex and ran latency-bound at ~1 TB/s.
+__device__ __forceinline__ void mark_one(int32_t v, int32_t r, int c, const uint32_t* __restrict__ bits,
+                                         int64_t words, int32_t nranks, const int32_t* __restrict__ cls,
+                                         uint32_t* mark, unsigned long long* mat, int32_t& last_r, int& last_c) {
+  if (r == v || c < 0 || (r == last_r && c == last_c)) return;
+  last_r = r;
+  last_c = c;
+  const int cr = bitmap_class(bits, words, nranks, cls, r);
+  if (cr >= 0 && cr != c) atomicOr(mat, 1ull << (cr * 8 + c));
+  uint32_t* word = mark + (r >> 2);
+  const uint32_t mine = (1u << c) << (8 * (r & 3));
+  if (ld_weak(reinterpret_cast<const int32_t*>(word)) & mine) return;  // stale => one extra atomic
+  const uint32_t old = (atomicOr(word, mine) >> (8 * (r & 3))) & 0xffu;
+  if (old && !(old & (1u << c))) atomicOr(mat, 1ull << (lowest_class(old) * 8 + c));
+}
+
 __global__ void __launch_bounds__(kEwBlock)
 k_absorb_mark(const int32_t* __restrict__ P, int32_t n, const uint32_t* __restrict__ bits, int64_t words,
-              int32_t nranks, const int32_t* __restrict__ cls, uint32_t* mark, unsigned long long* mat) {
+              int32_t nranks, const int32_t* __restrict__ cls, uint32_t* mark, unsigned long long* mat,
+              const int32_t* single) {
+  if (*single) return;
   // a per-thread memo of the last (root, class) handled keeps the giant's
   // root word from being hit once per member
   int32_t last_r = -1;
   int last_c = -1;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const int32_t r = P[v];
-    if (r == int32_t(v)) continue;
-    const int c = bitmap_class(bits, words, nranks, cls, v);
-    if (c < 0 || (r == last_r && c == last_c)) continue;
-    last_r = r;
-    last_c = c;
-    const int cr = bitmap_class(bits, words, nranks, cls, r);
-    if (cr >= 0 && cr != c) atomicOr(mat, 1ull << (cr * 8 + c));
-    uint32_t* word = mark + (r >> 2);
-    const uint32_t mine = (1u << c) << (8 * (r & 3));
-    if (ld_weak(reinterpret_cast<const int32_t*>(word)) & mine) continue;  // stale => one extra atomic
-    const uint32_t old = (atomicOr(word, mine) >> (8 * (r & 3))) & 0xffu;
-    if (old && !(old & (1u << c))) atomicOr(mat, 1ull << (lowest_class(old) * 8 + c));
+  const int64_t nq = n / 4;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int4 p = reinterpret_cast<const int4*>(P)[q];
+    int c[4];
+    quad_classes(bits, words, nranks, cls, 4 * q, c);
+    const int32_t v = int32_t(4 * q);
+    mark_one(v, p.x, c[0], bits, words, nranks, cls, mark, mat, last_r, last_c);
+    mark_one(v + 1, p.y, c[1], bits, words, nranks, cls, mark, mat, last_r, last_c);
+    mark_one(v + 2, p.z, c[2], bits, words, nranks, cls, mark, mat, last_r, last_c);
+    mark_one(v + 3, p.w, c[3], bits, words, nranks, cls, mark, mat, last_r, last_c);
   }
+  for (int64_t v = 4 * nq + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    mark_one(int32_t(v), P[v], bitmap_class(bits, words, nranks, cls, v), bits, words, nranks, cls, mark, mat,
+             last_r, last_c);
+}
+
+// class bits of local root r: its mark byte plus its own bitmap class
+__device__ __forceinline__ uint32_t root_classes(int32_t r, const uint32_t* __restrict__ mark,
+                                                 const uint32_t* __restrict__ bits, int64_t words, int32_t nranks,
+                                                 const int32_t* __restrict__ cls0) {
+  uint32_t m = (__ldg(mark + (r >> 2)) >> (8 * (r & 3))) & 0xffu;
+  const int cr = bitmap_class(bits, words, nranks, cls0, r);
+  return cr >= 0 ? m | (1u << cr) : m;
 }
 
 __global__ void __launch_bounds__(kEwBlock)
 k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const uint32_t* __restrict__ bits,
-               int64_t words, int32_t nranks, const int32_t* __restrict__ cls0, const int32_t* __restrict__ cls_rep) {
-  int32_t last_r = -1;
-  uint32_t m = 0;
+               int64_t words, int32_t nranks, const int32_t* __restrict__ cls0, const int32_t* __restrict__ cls_rep,
+               const int32_t* single) {
+  if (*single) return;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    const int32_t r = P[v];
-    if (r != last_r) {
-      last_r = r;
-      m = (mark[r >> 2] >> (8 * (r & 3))) & 0xffu;
-      const int cr = bitmap_class(bits, words, nranks, cls0, r);
-      if (cr >= 0) m |= 1u << cr;
-    }
+  const int64_t nq = n / 4;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    int4 p = reinterpret_cast<int4*>(P)[q];
+    // lookups for every distinct root of the quad, issued together (the
+    // repeated ones - a giant's members - hit L1)
+    const uint32_t m0 = root_classes(p.x, mark, bits, words, nranks, cls0);
+    const uint32_t m1 = p.y == p.x ? m0 : root_classes(p.y, mark, bits, words, nranks, cls0);
+    const uint32_t m2 = p.z == p.y ? m1 : root_classes(p.z, mark, bits, words, nranks, cls0);
+    const uint32_t m3 = p.w == p.z ? m2 : root_classes(p.w, mark, bits, words, nranks, cls0);
+    if (!(m0 | m1 | m2 | m3)) continue;
+    if (m0) p.x = cls_rep[lowest_class(m0)];
+    if (m1) p.y = cls_rep[lowest_class(m1)];
+    if (m2) p.z = cls_rep[lowest_class(m2)];
+    if (m3) p.w = cls_rep[lowest_class(m3)];
+    reinterpret_cast<int4*>(P)[q] = p;
+  }
+  for (int64_t v = 4 * nq + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const uint32_t m = root_classes(P[v], mark, bits, words, nranks, cls0);
     if (m) P[v] = cls_rep[lowest_class(m)];
   }
 }
@@ -207,7 +301,7 @@ k_absorb_apply(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const u
 // (a rank id), rep[r] = the class's smallest giant label; cls_rep[c] = rep for
 // every class index c a mark byte can carry (pass-0 and merged ids alike).
 __global__ void k_absorb_classes(const unsigned long long* mat, const int64_t* labels, int32_t nranks,
-                                 int32_t* cls, int32_t* rep, int32_t* cls_rep, int pass) {
+                                 int32_t* cls, int32_t* rep, int32_t* cls_rep, int pass, int32_t* single) {
   int par[kMaxRanks];
   for (int r = 0; r < kMaxRanks; ++r) par[r] = r;
   auto root = [&](int x) {
@@ -236,6 +330,77 @@ __global__ void k_absorb_classes(const unsigned long long* mat, const int64_t* l
     cls_rep[c0[r]] = rep[r];
     cls_rep[cls[r]] = rep[r];
   }
+  if (single) {
+    int one = 1;
+    for (int r = 1; r < nranks; ++r) one &= cls[r] == cls[0];
+    *single = one;
+  }
+}
+
+// One class (the usual case: every rank's giant is a piece of the one giant
+// component).  Then the class matrix has nothing to record, a vertex's class
+// is one bit of the OR of the bitmaps, and the per-root class byte shrinks to
+// one bit: mark1 sets bit r for every local root r with a member in the
+// class, apply1 points every vertex whose root is marked or in the class at
+// the representative.  Four vertices per thread, one bitmap word per quad.
+__device__ __forceinline__ bool bit_of(const uint32_t* __restrict__ b, int32_t x) {
+  return (__ldg(b + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_absorb_mark1(const int32_t* __restrict__ P, int32_t n, const uint32_t* __restrict__ any, uint32_t* mark,
+               const int32_t* single) {
+  if (!*single) return;
+  int32_t last_r = -1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t nq = (int64_t(n) + 3) / 4;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int64_t v0 = 4 * q;
+    int32_t r[4];
+    if (v0 + 3 < n) {
+      const int4 p = reinterpret_cast<const int4*>(P)[q];
+      r[0] = p.x, r[1] = p.y, r[2] = p.z, r[3] = p.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = v0 + k < n ? P[v0 + k] : int32_t(v0 + k);
+    }
+    const uint32_t w = __ldg(any + (v0 >> 5)) >> (v0 & 31);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t x = r[k];
+      if (x == int32_t(v0 + k) || !((w >> k) & 1u) || x == last_r) continue;
+      last_r = x;
+      const uint32_t bit = 1u << (x & 31);
+      if (ld_weak(reinterpret_cast<const int32_t*>(mark + (x >> 5))) & bit) continue;
+      atomicOr(mark + (x >> 5), bit);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_absorb_apply1(int32_t* P, int32_t n, const uint32_t* __restrict__ mark, const uint32_t* __restrict__ any,
+                const int32_t* __restrict__ rep, const int32_t* single) {
+  if (!*single) return;
+  const int32_t r0 = rep[0];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t nq = n / 4;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    int4 p = reinterpret_cast<int4*>(P)[q];
+    const bool m0 = bit_of(mark, p.x) || bit_of(any, p.x);
+    const bool m1 = p.y == p.x ? m0 : bit_of(mark, p.y) || bit_of(any, p.y);
+    const bool m2 = p.z == p.y ? m1 : bit_of(mark, p.z) || bit_of(any, p.z);
+    const bool m3 = p.w == p.z ? m2 : bit_of(mark, p.w) || bit_of(any, p.w);
+    if (!(m0 | m1 | m2 | m3)) continue;
+    if (m0) p.x = r0;
+    if (m1) p.y = r0;
+    if (m2) p.z = r0;
+    if (m3) p.w = r0;
+    reinterpret_cast<int4*>(P)[q] = p;
+  }
+  for (int64_t v = 4 * nq + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const int32_t x = P[v];
+    if (bit_of(mark, x) || bit_of(any, x)) P[v] = r0;
+  }
 }
 
 // one class (the usual case): OR the ranks' bitmaps once, word-parallel,
@@ -258,7 +423,14 @@ k_join_init_one(int32_t* P, int32_t n, const uint32_t* __restrict__ any, const i
   if (!*single) return;
   const int32_t r0 = rep[0];
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+  const int64_t nq = n / 4;  // four vertices per thread, one 16-byte store
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int32_t v = int32_t(4 * q);
+    const uint32_t w = __ldg(any + (v >> 5)) >> (v & 31);
+    reinterpret_cast<int4*>(P)[q] = make_int4(w & 1u ? r0 : v, w & 2u ? r0 : v + 1, w & 4u ? r0 : v + 2,
+                                              w & 8u ? r0 : v + 3);
+  }
+  for (int64_t v = 4 * nq + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
     P[v] = (any[v >> 5] >> (v & 31)) & 1u ? r0 : int32_t(v);
 }
 
@@ -305,7 +477,7 @@ int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint, uint
     if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr), count_launch());
     (k_pick_class<<<1, 1, 0, st>>>(parent, giant_hint, ctr, giant_label), count_launch());
     // a null pair output summarises the bitmap class only (round A)
-    (k_summary<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,
+    (k_summary<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,
                                                               out_count), count_launch());
     GC_CHECK_LAUNCH();
   });
@@ -323,21 +495,31 @@ int gc_shard_absorb(int32_t* parent, int64_t n, const uint32_t* bits, const int6
     int32_t* cls = a.take<int32_t>(kMaxRanks);
     int32_t* rep = a.take<int32_t>(kMaxRanks);
     int32_t* cls_rep = a.take<int32_t>(kMaxRanks);
+    int32_t* single = a.take<int32_t>(1);
     const int32_t nn = int32_t(n);
     if (nn == 0) return;
-    uint32_t* mark = a.take<uint32_t>((n + 3) / 4);  // one byte of class bits per local root
     const int64_t words = (n + 31) / 32;
+    // one byte of class bits per local root (general path); its first
+    // n/8 bytes double as the one-bit root marks of the single-class path
+    uint32_t* mark = a.take<uint32_t>((n + 3) / 4);
+    uint32_t* any = a.take<uint32_t>(words);
     GC_CUDA(cudaMemsetAsync(mat, 0, 16, st));
     GC_CUDA(cudaMemsetAsync(mark, 0, size_t((n + 3) / 4) * 4, st));
     // parent is compressed by the preceding gc_shard_summary
+    const int gq = grid_for((n + 3) / 4, kEwBlock, 8);
     (k_overlap<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, mat), count_launch());
-    (k_absorb_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, cls, rep, cls_rep, 0), count_launch());
-    (k_absorb_mark<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, cls,
-                                                                  mark, mat + 1), count_launch());
-    // classes joined through a shared local root
-    (k_absorb_classes<<<1, 1, 0, st>>>(mat + 1, giant_labels, nranks, cls, rep, cls_rep, 1), count_launch());
-    (k_absorb_apply<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, mark, bits, words, nranks, cls,
-                                                                   cls_rep), count_launch());
+    (k_absorb_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, cls, rep, cls_rep, 0, single), count_launch());
+    (k_or_bitmaps<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, any, single),
+     count_launch());
+    (k_absorb_mark1<<<gq, kEwBlock, 0, st>>>(parent, nn, any, mark, single), count_launch());
+    (k_absorb_mark<<<gq, kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, cls, mark, mat + 1, single),
+     count_launch());
+    // classes joined through a shared local root (general path only)
+    (k_absorb_classes<<<1, 1, 0, st>>>(mat + 1, giant_labels, nranks, cls, rep, cls_rep, 1, nullptr),
+     count_launch());
+    (k_absorb_apply1<<<gq, kEwBlock, 0, st>>>(parent, nn, mark, any, rep, single), count_launch());
+    (k_absorb_apply<<<gq, kEwBlock, 0, st>>>(parent, nn, mark, bits, words, nranks, cls, cls_rep, single),
+     count_launch());
     GC_CUDA(cudaMemcpyAsync(main_rep, rep, 4, cudaMemcpyDeviceToDevice, st));  // rank 0's class
     GC_CHECK_LAUNCH();
   });
@@ -368,7 +550,7 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits, const int64_
     (k_giant_classes<<<1, 1, 0, st>>>(mat, giant_labels, nranks, rep, single), count_launch());
     (k_or_bitmaps<<<grid_for(words, kEwBlock, 4), kEwBlock, 0, st>>>(bits, words, nranks, any, single),
      count_launch());
-    (k_join_init_one<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, any, rep, single),
+    (k_join_init_one<<<grid_for((n + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, any, rep, single),
      count_launch());
     (k_join_init<<<grid_for(nn, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, bits, words, nranks, rep, single),
      count_launch());

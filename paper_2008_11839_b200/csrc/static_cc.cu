@@ -631,8 +631,8 @@ int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_
     if (spec->sample == GC_SAMPLE_KOUT) run_kout(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
     if (spec->sample == GC_SAMPLE_HB) run_hb(*g, *spec, sc, pl.rows(sc), false, pl.ws.samp, pl.ws.ctr, st);
     if (record && !edges && pl.n) {
-      (k_root_transitions<<<grid_for(pl.n, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nullptr, pl.n, out_u, out_v,
-                                                                           out_count), count_launch());
+      (k_root_transitions<<<grid_for((int64_t(pl.n) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(
+           parent, nullptr, pl.n, out_u, out_v, out_count), count_launch());
       GC_CHECK_LAUNCH();
     }
     unsigned long long c[C_COUNT_];
@@ -673,14 +673,15 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_
       // compressed labels, L_max and the active set are too
       run_post_sample(parent, pl.n, g->offsets, pl.ws.list, pl.ws.hist, pl.ws.ctr, true, st);
     }
-    // non-root-based rules: snapshot the parents (the histogram buffer is
-    // free after the mode) and emit root transitions after the finish
-    if (!edges && pl.n)
-      GC_CUDA(cudaMemcpyAsync(pl.ws.hist, parent, size_t(pl.n) * 4, cudaMemcpyDeviceToDevice, st));
+    // non-root-based rules: snapshot which vertices are roots (a bitmap in
+    // the histogram buffer, free after the mode) and emit root transitions
+    // after the finish
+    uint32_t* roots = reinterpret_cast<uint32_t*>(pl.ws.hist);
+    const int gq = grid_for((int64_t(pl.n) + 3) / 4, kEwBlock, 8);
+    if (!edges && pl.n) (k_root_bitmap<<<gq, kEwBlock, 0, st>>>(parent, pl.n, roots), count_launch());
     pl.finish();
     if (!edges && pl.n) {
-      (k_root_transitions<<<grid_for(pl.n, kEwBlock, 8), kEwBlock, 0, st>>>(parent, pl.ws.hist, pl.n, out_u,
-                                                                           out_v, out_count), count_launch());
+      (k_root_transitions<<<gq, kEwBlock, 0, st>>>(parent, roots, pl.n, out_u, out_v, out_count), count_launch());
       GC_CHECK_LAUNCH();
     }
     unsigned long long c[C_COUNT_];
