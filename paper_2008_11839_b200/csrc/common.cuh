@@ -136,11 +136,24 @@ struct BlockQueue {
     int pos = 0;
     if (lane == 0) pos = atomicAdd(&count, __popc(bal));
     pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (p) {
-      const int mine = pos + __popc(bal & ((1u << lane) - 1u));
-      if (mine < CAP) items[mine] = x;
-      else q[atomicAdd(qc, 1ull)] = x;
-    }
+    const int mine = pos + __popc(bal & ((1u << lane) - 1u));
+    if (p && mine < CAP) items[mine] = x;
+    // staging full: the overflowing lanes append straight to the global
+    // queue with one counter atomic per warp (one per item serialised large
+    // frontiers on the single counter)
+    const unsigned over = __ballot_sync(0xffffffffu, p && mine >= CAP);
+    if (!over) return;
+    unsigned long long gpos = 0;
+    if (lane == __ffs(int(over)) - 1) gpos = atomicAdd(qc, static_cast<unsigned long long>(__popc(over)));
+    gpos = __shfl_sync(0xffffffffu, gpos, __ffs(int(over)) - 1);
+    if (p && mine >= CAP) q[gpos + __popc(over & ((1u << lane) - 1u))] = x;
+  }
+  // block-uniform call sites only (every thread of the block reaches it):
+  // flush once the staging is at least `threshold` full, so big frontiers
+  // rarely overflow
+  __device__ __forceinline__ void maybe_flush(int32_t* q, unsigned long long* qc, int threshold) {
+    __syncthreads();
+    if (count >= threshold) flush(q, qc);
   }
   __device__ __forceinline__ void flush(int32_t* q, unsigned long long* qc) {
     __syncthreads();

@@ -218,7 +218,9 @@ struct Pipeline {
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, true, st);
     } else if (s.sample == GC_SAMPLE_BFS) {
-      init_sets(sc);
+      // the BFS label pass writes every label (and forest slot) when it runs
+      // (m > 0); the init is still needed for the hook / lock arrays
+      if (g.m == 0 || sc.unite == GC_FINISH_HOOKS || sc.unite == GC_FINISH_REM_LOCK) init_sets(sc);
       if (kev) GC_CUDA(rec(kev[0], st));
       run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
       if (kev) GC_CUDA(rec(kev[1], st));
@@ -314,8 +316,11 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   const bool forest = fu != nullptr;
   if (forest) {
     require(fv != nullptr, GC_ERR_ARG, "null forest array");
-    fill(fu, g->n, -1, st);
-    fill(fv, g->n, -1, st);
+    // a BFS sample over edges writes every slot itself (k_bfs_label)
+    if (!(spec->sample == GC_SAMPLE_BFS && g->m > 0)) {
+      fill(fu, g->n, -1, st);
+      fill(fv, g->n, -1, st);
+    }
   }
   Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
   L2Residency keep_parents(st, labels, size_t(g->n) * 4);

@@ -11,6 +11,7 @@
 // reference's "first discoverer in the sorted frontier" rule.
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
@@ -150,11 +151,87 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
         take(fresh, x);
       }
     }
+    bq.maybe_flush(qn, nstat, kQCap / 2);
   }
-  bq.flush(qn, nstat);  // once per launch; overflow went straight to the global queue
+  bq.flush(qn, nstat);
   if (insp) block_add<kTB>(insp, degs);
   my_min = warp_min(my_min);
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+// Wide top-down levels (the frontier is no longer narrow) run in two
+// passes, neither of which touches the parent array at random:
+//   mark: every frontier row sets the next-frontier bit of each unvisited
+//     neighbour (red.or into the n/8-byte bitmap, which stays in L2; no lane
+//     waits on an atomic's result; rows are walked four entries at a time);
+//   pull: every newly reached vertex, in id order, takes the first frontier
+//     vertex of its ascending row as parent — the smallest frontier
+//     neighbour, which is what the returning atomicMin of the narrow form
+//     leaves — and writes it with a coalesced store.
+// A returning atomicMin per claim into the 4n-byte parent array (n = 2^27:
+// 537 MB, far beyond L2) made such a level a stream of random DRAM
+// read-modify-writes.
+__global__ void __launch_bounds__(kTB)
+k_bfs_td_mark(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
+              const unsigned long long* qstat, const uint32_t* __restrict__ vis, uint32_t* nbits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t count = int64_t(qstat[0]);
+  for (int64_t i = int64_t(blockIdx.x) * kTB + threadIdx.x; i - lane < count; i += int64_t(gridDim.x) * kTB) {
+    int64_t b = 0, d = 0;
+    if (i < count) {
+      const int32_t f = q[i];
+      b = off[f];
+      d = off[f + 1] - b;
+    }
+    const bool big = d > 32;
+    if (!big) {
+      for (int64_t j = 0; j < d; j += 4) {
+        int32_t x[4];
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = j + k < d ? tgt[b + j + k] : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = x[k] >= 0 ? __ldg(vis + (x[k] >> 5)) : ~0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (x[k] >= 0 && !((w[k] >> (x[k] & 31)) & 1u))
+            asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(nbits + (x[k] >> 5)),
+                         "r"(1u << (x[k] & 31))
+                         : "memory");
+      }
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, big);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int64_t bb = __shfl_sync(0xffffffffu, b, src);
+      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
+      for (int64_t j = lane; j < dd; j += 32) {
+        const int32_t x = tgt[bb + j];
+        if (!test_bit(vis, x))
+          asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(nbits + (x >> 5)), "r"(1u << (x & 31))
+                       : "memory");
+      }
+    }
+  }
+}
+
+// pull pass over the new frontier's queue (ascending ids: k_bits_to_queue)
+__global__ void __launch_bounds__(kTB)
+k_bfs_pull(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
+           const unsigned long long* qstat, const uint32_t* __restrict__ cbits, uint32_t* par) {
+  const int64_t count = int64_t(qstat[0]);
+  for (int64_t i = int64_t(blockIdx.x) * kTB + threadIdx.x; i < count; i += int64_t(gridDim.x) * kTB) {
+    const int32_t v = q[i];
+    const int64_t b = off[v], e = off[v + 1];
+    for (int64_t j = b; j < e; ++j) {
+      const int32_t t = tgt[j];
+      if (test_bit(cbits, t)) {
+        par[v] = uint32_t(t);
+        break;
+      }
+    }
+  }
 }
 
 // bottom-up: a warp owns 32 consecutive vertices and writes its next-bitmap
@@ -181,10 +258,10 @@ k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32
         if (test_bit(cbits, t)) {
           found = true;
           par[v] = uint32_t(t);
-          degs += static_cast<unsigned long long>(e - b);
           break;
         }
       }
+      if (found) degs += static_cast<unsigned long long>(e - b);
     }
     const unsigned word = __ballot_sync(0xffffffffu, found);
     if (lane == 0 && word) {
@@ -235,7 +312,7 @@ __global__ void k_or_words(uint32_t* dst, const uint32_t* src, int64_t words) {
 
 // bitmap -> queue (switching back to top-down): one thread per 32-bit word
 __global__ void __launch_bounds__(kEwBlock)
-k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc) {
+k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, int32_t* minv) {
   using Scan = cub::BlockScan<int, kEwBlock>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
@@ -248,6 +325,11 @@ k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long*
     if (threadIdx.x == 0) base = total ? atomicAdd(qc, static_cast<unsigned long long>(total)) : 0ull;
     __syncthreads();
     unsigned long long p = base + rank;
+    if (minv) {  // the smallest vertex reached (first set bit of the block's words)
+      int32_t lo = word ? int32_t(wi * 32 + __ffs(word) - 1) : INT_MAX;
+      lo = warp_min(lo);
+      if ((threadIdx.x & 31) == 0 && lo != INT_MAX) atomicMin(minv, lo);
+    }
     while (word) {
       const int bit = __ffs(word) - 1;
       word &= word - 1;
@@ -271,31 +353,58 @@ __global__ void k_bfs_seed(const int64_t* off, uint32_t* par, int32_t* q, unsign
 // label the component with its minimum (sampling.py:158-160), emit forest
 // slots (slot v = (parent, v)), and count the sample inspections: the
 // reference adds every frontier's degree sum (:141-144), i.e. the degree of
-// every reached vertex once.  Four vertices per thread (16-byte loads).
-__global__ void k_bfs_label(const uint32_t* par, const int32_t* minv, const int64_t* off, int32_t n, int32_t* P,
-                            int32_t* fu, int32_t* fv, unsigned long long* insp) {
+// every reached vertex once.  Every slot is written (unreached: P[v] = v,
+// empty forest slot), so the pipeline skips the label init and the forest
+// fill when this pass runs.  Four vertices per thread, 16-byte loads and
+// stores throughout.
+__global__ void k_bfs_label(const uint32_t* __restrict__ par, const int32_t* minv, const int64_t* __restrict__ off,
+                            int32_t n, int32_t* P, int32_t* fu, int32_t* fv, unsigned long long* insp, int vec) {
   const int32_t mn = *minv;
   unsigned long long degs = 0;
   const int64_t nq = (int64_t(n) + 3) / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += stride) {
     const int64_t v0 = 4 * i;
-    uint32_t p[4];
-    if (v0 + 3 < n) {
+    if (vec && v0 + 3 < n) {
       const uint4 pp = *reinterpret_cast<const uint4*>(par + v0);
-      p[0] = pp.x; p[1] = pp.y; p[2] = pp.z; p[3] = pp.w;
-    } else {
-      for (int j = 0; j < 4; ++j) p[j] = v0 + j < n ? par[v0 + j] : kUnreached;
-    }
+      const uint32_t p[4] = {pp.x, pp.y, pp.z, pp.w};
+      const int32_t v = int32_t(v0);
+      int32_t lab[4], u[4], w[4];
+      bool any = false;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t v = v0 + j;
-      if (p[j] == kUnreached) continue;
-      P[v] = mn;
-      degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
-      if (fu && v != mn && p[j] != kSourcePar) {
-        fu[v] = int32_t(p[j]);
-        fv[v] = int32_t(v);
+      for (int j = 0; j < 4; ++j) {
+        const bool r = p[j] != kUnreached;
+        any |= r;
+        lab[j] = r ? mn : v + j;
+        const bool slot = r && v + j != mn && p[j] != kSourcePar;
+        u[j] = slot ? int32_t(p[j]) : -1;
+        w[j] = slot ? v + j : -1;
+      }
+      reinterpret_cast<int4*>(P)[i] = make_int4(lab[0], lab[1], lab[2], lab[3]);
+      if (fu) {
+        reinterpret_cast<int4*>(fu)[i] = make_int4(u[0], u[1], u[2], u[3]);
+        reinterpret_cast<int4*>(fv)[i] = make_int4(w[0], w[1], w[2], w[3]);
+      }
+      if (any) {
+        const longlong2 o01 = *reinterpret_cast<const longlong2*>(off + v0);
+        const longlong2 o23 = *reinterpret_cast<const longlong2*>(off + v0 + 2);
+        const int64_t o4 = off[v0 + 4];
+        const int64_t o[5] = {o01.x, o01.y, o23.x, o23.y, o4};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (p[j] != kUnreached) degs += static_cast<unsigned long long>(o[j + 1] - o[j]);
+      }
+    } else {
+      for (int64_t v = v0; v < n; ++v) {
+        const uint32_t p = par[v];
+        const bool r = p != kUnreached;
+        P[v] = r ? mn : int32_t(v);
+        if (r) degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
+        if (fu) {
+          const bool slot = r && v != mn && p != kSourcePar;
+          fu[v] = slot ? int32_t(p) : -1;
+          fv[v] = slot ? int32_t(v) : -1;
+        }
       }
     }
   }
@@ -459,6 +568,7 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
         }
         bq.push(fresh, x, qout, cout);
       }
+      bq.maybe_flush(qout, cout, kQCap / 2);
     }
   }
   if (r <= last_start) {
@@ -472,10 +582,9 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
         fresh = claim(key, v, r, uint32_t(v));
       }
       bq.push(fresh, v, qout, cout);
+      bq.maybe_flush(qout, cout, kQCap / 2);
     }
   }
-  // one block-wide flush per launch: items beyond the staging capacity
-  // already went straight to the global queue inside push()
   bq.flush(qout, cout);
   block_add<kTB>(insp, my_insp);
 }
@@ -498,16 +607,34 @@ __global__ void k_ldd_label(const unsigned long long* key, const int32_t* mins, 
 
 // Direction switch (Beamer): bottom-up once the frontier's edges exceed
 // 1/alpha of the unexplored ones, back to top-down below n/beta frontier
-// vertices.  Beamer's CPU alpha = 14 keeps top-down one level too long on a
-// GPU, where a top-down level pays an atomic per fresh frontier edge while a
-// bottom-up level streams rows and stops at the first frontier neighbour.
+// vertices.  Beamer's alpha = 14 is also the GPU optimum once a top-down
+// level's queue appends are block-aggregated (with one counter atomic per
+// overflowing claim, the large top-down level serialised and alpha = 30 —
+// switching a level early — measured better).
 constexpr int kBfsBeta = 24;
 double bfs_alpha() {
   static const double a = [] {
     const char* e = getenv("GC_BFS_ALPHA");
-    return e ? atof(e) : 30.0;  // measured on uniform 2^27: 14 -> 13.9 ms, 30 -> 10.6 ms, 60 -> 10.7 ms
+    // measured on uniform 2^27 (forest): 8 -> 9.26 ms, 14 -> 9.27 ms, 30 -> 10.41 ms
+    return e ? atof(e) : 14.0;
   }();
   return a;
+}
+
+// frontier size from which a non-batched top-down level uses the
+// fire-and-forget claims (below it the returning atomics are cheap and the
+// queue is built in the same pass)
+unsigned long long bfs_wide_min() {
+  static const unsigned long long v = [] {
+    const char* e = getenv("GC_BFS_WIDE_MIN");
+    return e ? strtoull(e, nullptr, 10) : 65536ull;
+  }();
+  return v;
+}
+
+bool bfs_trace() {
+  static const bool t = getenv("GC_BFS_TRACE") != nullptr;
+  return t;
 }
 
 void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t* fv, SamplerWs& w,
@@ -590,14 +717,15 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     // Beamer's heuristic: bottom-up once the frontier's edges exceed
     // 1/alpha of the unexplored ones, back to top-down below n/beta
     const bool want_bu = bottom_up ? (nf >= uint64_t(n) / kBfsBeta) : (mf * bfs_alpha() > unexplored);
-    if (want_bu && bits_stale) {
+    if ((want_bu || nf >= bfs_wide_min()) && bits_stale) {
       GC_CUDA(cudaMemsetAsync(fb[c], 0, words * 4, st));
       TL(k_queue_to_bits, grid_for(int64_t(nf), kEwBlock, 4), kEwBlock, q[c], slot(level), fb[c]);
     }
     bits_stale = false;
     if (!want_bu && bottom_up) {
       GC_CUDA(cudaMemsetAsync(slot(level), 0, 8, st));
-      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], slot(level));
+      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], slot(level),
+         static_cast<int32_t*>(nullptr));
     }
     bottom_up = want_bu;
     GC_CUDA(cudaMemsetAsync(slot(level + 1), 0, 16, st));
@@ -607,8 +735,14 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     } else {
       const int64_t b64 = (int64_t(nf) + kTB - 1) / kTB;
       const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
-      TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], slot(level), par, w.vis, q[nx], slot(level + 1),
-         fb[nx], minv, static_cast<unsigned long long*>(nullptr), static_cast<unsigned long long*>(nullptr));
+      if (nf >= bfs_wide_min()) {
+        TL(k_bfs_td_mark, blocks, kTB, g.offsets, g.targets, q[c], slot(level), w.vis, fb[nx]);
+        TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[nx], n, q[nx], slot(level + 1), minv);
+        TL(k_bfs_pull, num_sms() * (2048 / kTB), kTB, g.offsets, g.targets, q[nx], slot(level + 1), fb[c], par);
+      } else {
+        TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], slot(level), par, w.vis, q[nx], slot(level + 1),
+           fb[nx], minv, static_cast<unsigned long long*>(nullptr), static_cast<unsigned long long*>(nullptr));
+      }
       // the visited bitmap takes the level's claims in one word-parallel pass
       // (an extra atomic per claim would double the level's atomics)
       TL(k_or_words, grid_for(words, kEwBlock, 2), kEwBlock, w.vis, fb[nx], words);
@@ -620,9 +754,13 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     nf = h[0];
     mf = bottom_up ? double(h[1]) : double(nf) * avg_deg;
     unexplored -= mf;
+    if (bfs_trace()) fprintf(stderr, "bfs level %lld %s next frontier %llu\n", (long long)level,
+                             bottom_up ? "bottom-up" : "top-down", nf);
   }
+  const auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  const int vec = al(g.offsets) && al(P) && (!fu || (al(fu) && al(fv)));
   TL(k_bfs_label, grid_for((int64_t(n) + 3) / 4, kEwBlock, 8), kEwBlock, par, minv, g.offsets, n, P, fu, fv,
-     ctr + C_INSP_SAMPLE);
+     ctr + C_INSP_SAMPLE, vec);
   if (fu) TL(k_bfs_reroot, 1, 1, par, minv, fu, fv);
   GC_CHECK_LAUNCH();
 }
