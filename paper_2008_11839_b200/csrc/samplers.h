@@ -44,6 +44,7 @@ void sampler_carve(A& a, SamplerWs& w, int64_t n, int64_t m, const gc_spec& s) {
     w.vis = a.template take<uint32_t>((n + 31) / 32);
   }
   if (s.sample == GC_SAMPLE_LDD) {
+    w.fb0 = a.template take<uint32_t>((n + 31) / 32);  // sorted-frontier bitmap
     w.start = a.template take<uint16_t>(n);
     w.order = a.template take<int32_t>(n);
     w.boff = a.template take<unsigned int>(kLddMaxRounds + 4);

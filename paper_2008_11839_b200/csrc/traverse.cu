@@ -25,24 +25,26 @@ namespace {
 
 constexpr int kTB = 256;                  // traversal block
 constexpr int kQCap = kTB * 16;           // 16 KB staging per block
-constexpr unsigned long long kFree = ~0ull;
-
-__device__ __forceinline__ unsigned long long ld_key(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ void red_or_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long mk_key(int32_t round, uint32_t payload) {
-  return (static_cast<unsigned long long>(uint32_t(round)) << 32) | payload;
-}
-
-// try to claim x in `round` for `payload`; true for the unique first claimant
-__device__ __forceinline__ bool claim(unsigned long long* key, int32_t x, int32_t round, uint32_t payload) {
-  const unsigned long long want = mk_key(round, payload);
-  const unsigned long long seen = ld_key(key + x);  // cached filter: keys only decrease
-  if (seen <= want) return false;
-  return atomicMin(key + x, want) == kFree;
+// LDD claims: cluster[x] (u32, kFreeCluster = unclaimed) takes the minimum
+// claimant of the first round x is reached in; croud[x] (u16) = that round
+// + 1, written by the winner, tells later rounds to keep off.  True for the
+// unique first claimant.  A claim of an earlier round is visible to every
+// later round (one launch per round), and two claimants of the same round
+// both pass the round filter, so the atomicMin picks the round's minimum —
+// the semantics of one packed 64-bit (round, cluster) key, in 6 bytes per
+// vertex instead of 8 and with a 2-byte filter read.
+constexpr uint32_t kFreeCluster = ~0u;
+__device__ __forceinline__ bool claim(uint32_t* cluster, uint16_t* croud, int32_t x, int32_t round, uint32_t c) {
+  const uint16_t cr = croud[x];
+  if (cr != 0 && int32_t(cr) - 1 < round) return false;          // reached in an earlier round
+  if (uint32_t(ld_weak(reinterpret_cast<const int32_t*>(cluster + x))) <= c) return false;  // a smaller claimant won
+  if (atomicMin(cluster + x, c) != kFreeCluster) return false;
+  croud[x] = uint16_t(round + 1);
+  return true;
 }
 
 __device__ __forceinline__ int32_t warp_min(int32_t v) {
@@ -312,7 +314,7 @@ __global__ void k_or_words(uint32_t* dst, const uint32_t* src, int64_t words) {
 
 // bitmap -> queue (switching back to top-down): one thread per 32-bit word
 __global__ void __launch_bounds__(kEwBlock)
-k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, int32_t* minv) {
+k_bits_to_queue(uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, int32_t* minv, int clear) {
   using Scan = cub::BlockScan<int, kEwBlock>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
@@ -320,6 +322,7 @@ k_bits_to_queue(const uint32_t* bits, int32_t n, int32_t* q, unsigned long long*
   for (int64_t w0 = int64_t(blockIdx.x) * kEwBlock; w0 < words; w0 += int64_t(gridDim.x) * kEwBlock) {
     const int64_t wi = w0 + threadIdx.x;
     uint32_t word = wi < words ? bits[wi] : 0u;
+    if (clear && word) bits[wi] = 0u;  // consumed: ready for the next round
     int rank, total;
     Scan(tmp).ExclusiveSum(__popc(word), rank, total);
     if (threadIdx.x == 0) base = total ? atomicAdd(qc, static_cast<unsigned long long>(total)) : 0ull;
@@ -464,7 +467,7 @@ constexpr int kBuckets = kLddMaxRounds + 1;
 // start round per vertex + block-aggregated bucket histogram
 __global__ void __launch_bounds__(kEwBlock)
 k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
-            unsigned long long* key, unsigned int* bcount) {
+            uint32_t* cluster, uint16_t* croud, unsigned int* bcount) {
   __shared__ unsigned int hist[kBuckets];
   for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -474,7 +477,8 @@ k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint
     float r = floorf(dmax - ldd_delta(seed, v, beta));
     r = r < 0.f ? 0.f : (r > float(kLddMaxRounds) ? float(kLddMaxRounds) : r);
     start[v] = uint16_t(r);
-    key[v] = kFree;
+    cluster[v] = kFreeCluster;
+    croud[v] = 0;
     atomicAdd(hist + int(r), 1u);
   }
   __syncthreads();
@@ -533,10 +537,10 @@ k_ldd_scatter(int32_t n, const uint16_t* start, unsigned int* cursor, int32_t* o
 // counters form a ring of three so the kernel can zero the counter the
 // next round will fill without touching the one it reads.
 __global__ void __launch_bounds__(kTB)
-k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, unsigned long long* key,
+k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, uint32_t* cluster, uint16_t* croud,
             const int32_t* order, const unsigned int* boff, int32_t r, int32_t last_start, const int32_t* qin,
             const unsigned long long* cin, int32_t* qout, unsigned long long* cout, unsigned long long* cnext,
-            unsigned long long* insp) {
+            unsigned long long* insp, uint32_t* nbits) {
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
   if (blockIdx.x == 0 && threadIdx.x == 0) *cnext = 0;
@@ -549,7 +553,7 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
       int64_t b = 0, d = 0;
       if (i < count) {
         const int32_t f = qin[i];
-        c = uint32_t(key[f]);  // cluster of f (final since round r-1)
+        c = cluster[f];  // final since round r-1
         b = off[f];
         d = off[f + 1] - b;
         my_insp += d;
@@ -564,11 +568,15 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
         int32_t x = 0;
         if (j < d) {
           x = tgt[b + j];
-          fresh = claim(key, x, r, c);
+          fresh = claim(cluster, croud, x, r, c);
         }
-        bq.push(fresh, x, qout, cout);
+        if (nbits) {
+          if (fresh) red_or_u32(nbits + (x >> 5), 1u << (x & 31));
+        } else {
+          bq.push(fresh, x, qout, cout);
+        }
       }
-      bq.maybe_flush(qout, cout, kQCap / 2);
+      if (!nbits) bq.maybe_flush(qout, cout, kQCap / 2);
     }
   }
   if (r <= last_start) {
@@ -579,26 +587,38 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, un
       bool fresh = false;
       if (i < hi) {
         v = order[i];
-        fresh = claim(key, v, r, uint32_t(v));
+        fresh = claim(cluster, croud, v, r, uint32_t(v));
       }
-      bq.push(fresh, v, qout, cout);
-      bq.maybe_flush(qout, cout, kQCap / 2);
+      if (nbits) {
+        if (fresh) red_or_u32(nbits + (v >> 5), 1u << (v & 31));
+      } else {
+        bq.push(fresh, v, qout, cout);
+        bq.maybe_flush(qout, cout, kQCap / 2);
+      }
     }
   }
   bq.flush(qout, cout);
   block_add<kTB>(insp, my_insp);
 }
 
-__global__ void k_ldd_mins(const unsigned long long* key, int32_t* mins, int32_t n) {
+// minimum member per cluster: lanes holding the same cluster (neighbouring
+// ids usually share one) elect their lowest lane, which holds the smallest
+// id, for a single atomicMin
+__global__ void k_ldd_mins(const uint32_t* cluster, int32_t* mins, int32_t n) {
+  const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
-    atomicMin(mins + uint32_t(key[v]), int32_t(v));
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t v = base + threadIdx.x;
+    const uint32_t c = v < n ? cluster[v] : kFreeCluster;
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    if (v < n && lane == __ffs(int(peers)) - 1) atomicMin(mins + c, int32_t(v));
+  }
 }
 
-__global__ void k_ldd_label(const unsigned long long* key, const int32_t* mins, int32_t* P, int32_t n) {
+__global__ void k_ldd_label(const uint32_t* cluster, const int32_t* mins, int32_t* P, int32_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
-    P[v] = mins[uint32_t(key[v])];
+    P[v] = mins[cluster[v]];
 }
 
 #define TL(kernel, grid, block, ...) ((kernel<<<grid, block, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
@@ -725,7 +745,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     if (!want_bu && bottom_up) {
       GC_CUDA(cudaMemsetAsync(slot(level), 0, 8, st));
       TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[c], n, q[c], slot(level),
-         static_cast<int32_t*>(nullptr));
+         static_cast<int32_t*>(nullptr), 0);
     }
     bottom_up = want_bu;
     GC_CUDA(cudaMemsetAsync(slot(level + 1), 0, 16, st));
@@ -737,7 +757,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
       const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
       if (nf >= bfs_wide_min()) {
         TL(k_bfs_td_mark, blocks, kTB, g.offsets, g.targets, q[c], slot(level), w.vis, fb[nx]);
-        TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[nx], n, q[nx], slot(level + 1), minv);
+        TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[nx], n, q[nx], slot(level + 1), minv, 0);
         TL(k_bfs_pull, num_sms() * (2048 / kTB), kTB, g.offsets, g.targets, q[nx], slot(level + 1), fb[c], par);
       } else {
         TL(k_bfs_td, blocks, kTB, g.offsets, g.targets, q[c], slot(level), par, w.vis, q[nx], slot(level + 1),
@@ -777,7 +797,18 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   GC_CUDA(cudaMemsetAsync(bcount, 0, (kBuckets + 1) * sizeof(unsigned int), st));
   const int ge = grid_for(n, kEwBlock, 8);
   TL(k_ldd_delta_max, ge, kEwBlock, n, s.seed, beta, dmax);
-  TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, w.key, bcount);
+  // the claim buffer (8n bytes) holds the u32 clusters and the u16 claim rounds
+  uint32_t* cluster = reinterpret_cast<uint32_t*>(w.key);
+  uint16_t* croud = reinterpret_cast<uint16_t*>(cluster + n);
+  // Sorted frontiers: a round's claims set bits, and a word-parallel scan
+  // turns them into the next round's queue in ascending id order (clearing
+  // the bitmap as it goes).  Row and claim accesses of the next round then
+  // follow the id order instead of the block-flush order of a shared queue:
+  // on the 256^3 grid the rounds take 2.5 ms instead of 3.9 ms.
+  const int64_t words = (int64_t(n) + 31) / 32;
+  uint32_t* nbits = w.fb0;
+  GC_CUDA(cudaMemsetAsync(nbits, 0, size_t(words) * 4, st));
+  TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cluster, croud, bcount);
   TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
   TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
      cursor, w.order);
@@ -800,9 +831,13 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   constexpr int kLddBatch = 16;
   const int grid = num_sms() * 8;
   for (int32_t r = 0;;) {
-    for (int k = 0; k < kLddBatch; ++k, ++r)
-      TL(k_ldd_round, grid, kTB, g.offsets, g.targets, w.key, w.order, w.boff, r, last_start, q[(r + 1) & 1],
-         ring + (r + 2) % 3, q[r & 1], ring + r % 3, ring + (r + 1) % 3, ctr + C_INSP_SAMPLE);
+    for (int k = 0; k < kLddBatch; ++k, ++r) {
+      TL(k_ldd_round, grid, kTB, g.offsets, g.targets, cluster, croud, w.order, w.boff, r, last_start, q[(r + 1) & 1],
+         ring + (r + 2) % 3, q[r & 1], ring + r % 3, ring + (r + 1) % 3, ctr + C_INSP_SAMPLE, nbits);
+      if (nbits)
+        TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, nbits, n, q[r & 1], ring + r % 3,
+           static_cast<int32_t*>(nullptr), 1);
+    }
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(hq, ring + (r - 1) % 3, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaStreamSynchronize(st));
@@ -811,8 +846,8 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   // labels: minimum member id per cluster (q0 is free again: reuse as mins)
   int32_t* mins = w.q0;
   fill(mins, n, INT_MAX, st);
-  TL(k_ldd_mins, ge, kEwBlock, w.key, mins, n);
-  TL(k_ldd_label, ge, kEwBlock, w.key, mins, P, n);
+  TL(k_ldd_mins, ge, kEwBlock, cluster, mins, n);
+  TL(k_ldd_label, ge, kEwBlock, cluster, mins, P, n);
   GC_CHECK_LAUNCH();
 }
 

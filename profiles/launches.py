@@ -14,8 +14,10 @@ def load(path):
             break
     else:
         raise SystemExit(f"no launches in {path}: {rows[:2]}")
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    return [(r[ki].split("(")[0], float(r[vi].replace(",", ""))) for r in rows[start:] if len(r) > vi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9}
+    return [(r[ki].split("(")[0], float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
+            for r in rows[start:] if len(r) > vi]  # nanoseconds
 
 
 if __name__ == "__main__":
