@@ -10,6 +10,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <cub/cub.cuh>
 
 #include "pipeline.cuh"
 #include "rounds.h"
@@ -57,23 +58,36 @@ __global__ void k_incr_query(const int32_t* P, const int32_t* us, const int32_t*
 __global__ void __launch_bounds__(kIB)
 k_incr_coo(const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len,
            const int32_t* labels, int map, Coo out, unsigned long long* cnt) {
-  const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (!isq) {  // insert-only batch: entry i is insert i, no compaction
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
+      const int32_t u = us[i], v = vs[i];
+      out.u[i] = map ? labels[u] : u;
+      out.v[i] = map ? labels[v] : v;
+      out.w[i] = 1;
+    }
+    return;
+  }
+  // mixed batch: inserts compacted in order within a block, one counter
+  // atomic per block step (a per-warp atomic on the one counter serialised)
+  using Scan = cub::BlockScan<int, kIB>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long bpos;
   for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < len; base += stride) {
     const int64_t i = base + threadIdx.x;
-    const bool ins = i < len && !(isq && isq[i]);
-    const unsigned bal = __ballot_sync(0xffffffffu, ins);
-    if (!bal) continue;
-    unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(cnt, static_cast<unsigned long long>(__popc(bal)));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const int ins = i < len && !isq[i];
+    int rank, total;
+    Scan(tmp).ExclusiveSum(ins, rank, total);
+    if (threadIdx.x == 0) bpos = total ? atomicAdd(cnt, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
     if (ins) {
-      const unsigned long long p = pos + __popc(bal & ((1u << lane) - 1u));
+      const unsigned long long p = bpos + rank;
       const int32_t u = us[i], v = vs[i];
       out.u[p] = map ? labels[u] : u;
       out.v[p] = map ? labels[v] : v;
       out.w[p] = 1;
     }
+    __syncthreads();
   }
 }
 

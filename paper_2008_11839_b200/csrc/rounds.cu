@@ -219,6 +219,116 @@ k_sv_hook_chunk(Coo c, Chunks ch, const int32_t* __restrict__ prev, int32_t* cur
   if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
 }
 
+// In-place SV (no forest): one label array instead of a snapshot copy per
+// round.  During the hook only roots' entries change, so the snapshot value
+// of x is x itself when x was a root at the round's start and L[x] (not
+// written this round) otherwise; the roots bitmap records the start-of-round
+// roots and is rebuilt by the full shortcut that ends every round.  Same
+// messages, same rounds and inspections as the snapshot form, without its
+// two full-array passes per round.
+__device__ __forceinline__ bool root_bit(const uint32_t* __restrict__ roots, int32_t x) {
+  return (__ldg(roots + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(kRB)
+k_sv_hook_inplace(Coo c, Chunks ch, int32_t* L, const uint32_t* __restrict__ roots, uint8_t* keep, int par,
+                  Ctl ctl) {
+  GC_SKIP_IF_DONE(ctl);
+  const int64_t s = ch.start[blockIdx.x], len = ch.len[blockIdx.x];
+  bool any = false;
+  int kept = 0;
+  for (int64_t t = threadIdx.x; t < len; t += kRB) {
+    const int64_t k = s + t;
+    const int32_t u = c.u[k], v = c.v[k];
+    const int32_t pu = root_bit(roots, u) ? u : ld_free(L + u);
+    const int32_t pv = root_bit(roots, v) ? v : ld_free(L + v);
+    const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
+    keep[k] = lo != hi;
+    kept += lo != hi;
+    if (lo != hi && root_bit(roots, hi)) {
+      if (lo < ld_free(L + hi)) red_min(L + hi, lo);  // stale: one extra red
+      any = true;
+    }
+  }
+  kept = __reduce_add_sync(0xffffffffu, kept);
+  if ((threadIdx.x & 31) == 0 && kept) atomicAdd(ch.count + 2 + par, static_cast<unsigned long long>(kept));
+  if (threadIdx.x == 0 && len) atomicAdd(ch.count + par, static_cast<unsigned long long>(len));
+  if (__syncthreads_or(any) && threadIdx.x == 0) *ctl.changed = 1;
+}
+
+// full shortcut in place, writing the roots bitmap of the result.  Four
+// vertices per thread (one 16-byte load; a stale value is an ancestor, so a
+// plain load is safe while other threads shorten their own entries), the
+// four first hops issued together, one 16-byte store when any moved; a warp
+// covers 128 vertices = four bitmap words, each OR-reduced over its eight
+// lanes.  A round without a hook changed nothing, so its shortcut (and
+// bitmap) is skipped.  init: only the bitmap of the array as given.
+__global__ void __launch_bounds__(kRB)
+k_shortcut_roots(int32_t* a, int64_t n, uint32_t* roots, Ctl ctl, int init) {
+  if (!init) {
+    GC_SKIP_IF_DONE(ctl);
+    if (*ctl.changed == 0) return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t nq = (n + 3) / 4;
+  const int64_t words = (n + 31) / 32;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nq; base += stride) {
+    const int64_t q = base + threadIdx.x;
+    const int64_t v0 = 4 * q;
+    unsigned nib = 0;
+    if (q < nq) {
+      int32_t r[4];
+      const bool full = v0 + 3 < n;
+      if (full) {
+        const int4 x = reinterpret_cast<const int4*>(a)[q];
+        r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = v0 + k < n ? ld_acq(a + v0 + k) : int32_t(v0 + k);
+      }
+      bool moved = false;
+      if (!init) {
+        // the four chains advance in lock step (four loads in flight per
+        // hop): the step count is the longest chain, not the sum — a
+        // natural-order grid builds chains hundreds of hops long.  Loads are
+        // L1-cacheable: roots do not move during the pass and other threads
+        // only shorten entries, so a stale value is an ancestor, and most
+        // chains end at one hot root (an L2-only load per vertex piled onto
+        // one L2 slice)
+        int32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = ld_free(a + r[k]);
+        unsigned live = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) live |= unsigned(h[k] != r[k]) << k;
+        moved = live != 0;
+        while (live) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) r[k] = (live >> k) & 1u ? h[k] : r[k];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) h[k] = (live >> k) & 1u ? ld_free(a + r[k]) : h[k];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) live &= ~(unsigned(h[k] == r[k]) << k);
+        }
+      }
+      if (moved) {
+        if (full) reinterpret_cast<int4*>(a)[q] = make_int4(r[0], r[1], r[2], r[3]);
+        else
+          for (int k = 0; k < 4; ++k)
+            if (v0 + k < n) st_rlx(a + v0 + k, r[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nib |= unsigned(v0 + k < n && r[k] == int32_t(v0 + k)) << k;
+    }
+    unsigned word = nib << (4 * (lane & 7));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    if ((lane & 7) == 0 && (v0 >> 5) < words) roots[v0 >> 5] = word;
+  }
+}
+
 // streaming in-place compaction of each chunk by its keep flags (tiles of
 // the block; every thread reads its entry before the scan's barrier, and a
 // write position never passes a read position)
@@ -490,7 +600,12 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
   Coo& cur = alter ? coo[par] : coo[0];
   const unsigned long long* len = alter ? ctl.len + par : ctl.len;
   ((k_round_begin<<<1, 1, 0, st>>>(ctl, alter ? par : 0, int(alter))), ::gc::count_launch());
-  if (s.finish == GC_FINISH_SV) {
+  if (s.finish == GC_FINISH_SV && !fo.on()) {
+    uint32_t* roots = reinterpret_cast<uint32_t*>(w.b);  // the snapshot buffer is free in this form
+    L1(k_sv_hook_inplace, ge, cur, ch, A, roots, ch.keep, par, ctl);
+    L1(k_chunk_compact, ge, cur, ch, ch.keep, par, ctl);
+    L1(k_shortcut_roots, grid_e((nl + 3) / 4), A, nl, roots, ctl, 0);
+  } else if (s.finish == GC_FINISH_SV) {
     L1(k_copy, gv, B, A, nl, ctl);
     L1(k_sv_hook_chunk, ge, cur, ch, A, B, ch.keep, par, ctl);
     if (fo.on()) {
@@ -555,6 +670,10 @@ void loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsWs& 
     ch.keep = w.keep;
     ch.count = reinterpret_cast<unsigned long long*>(w.chunks + 2 * kMaxChunks);
     ((k_chunk_init<<<(nch + 255) / 256, 256, 0, st>>>(ch, nch, len)), ::gc::count_launch());
+    // in-place form: the start-of-round roots of the first round
+    if (!fo.on())
+      ((k_shortcut_roots<<<grid_e((nl + 3) / 4), kRB, 0, st>>>(P, nl, reinterpret_cast<uint32_t*>(w.b), ctl, 1)),
+       ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
   for (int r = 0; nonempty;) {
