@@ -72,10 +72,19 @@ __global__ void k_round_end(Ctl c) {
 #define GC_SKIP_IF_DONE(ctl) \
   if (*(ctl).done) return
 
+// full-array passes take four entries per thread (16-byte accesses) when
+// both arrays are 16-byte aligned, which every caller's buffers are
+__device__ __forceinline__ bool aligned16(const void* a, const void* b) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
 __global__ void k_copy(int32_t* dst, const int32_t* src, int64_t n, Ctl ctl) {
   GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nq = aligned16(dst, src) ? n / 4 : 0;
+  for (int64_t q = t0; q < nq; q += stride) reinterpret_cast<int4*>(dst)[q] = reinterpret_cast<const int4*>(src)[q];
+  for (int64_t i = 4 * nq + t0; i < n; i += stride) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- gather ---
@@ -209,7 +218,7 @@ k_sv_hook_chunk(Coo c, Chunks ch, const int32_t* __restrict__ prev, int32_t* cur
     keep[k] = lo != hi;
     kept += lo != hi;
     if (lo != hi && prev[hi] == hi) {
-      if (lo < ld_acq(cur + hi)) red_min(cur + hi, lo);
+      if (lo < ld_free(cur + hi)) red_min(cur + hi, lo);
       any = true;
     }
   }
@@ -392,12 +401,12 @@ __global__ void k_full_shortcut(int32_t* a, int64_t n, Ctl ctl) {
   GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    int32_t r = ld_acq(a + v);
-    int32_t q = ld_acq(a + r);
+    int32_t r = ld_free(a + v);
+    int32_t q = ld_free(a + r);
     if (q == r) continue;
     while (q != r) {
       r = q;
-      q = ld_acq(a + r);
+      q = ld_free(a + r);
     }
     st_rlx(a + v, r);
   }
@@ -432,7 +441,7 @@ __global__ void k_lt_connect(Coo c, const unsigned long long* len, const int32_t
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m; k += stride) {
     lt_messages(connect, c.u[k], c.v[k], L, [&](int32_t r, int32_t x) {
-      if (x < ld_acq(msg + r)) red_min(msg + r, x);  // msg only decreases
+      if (x < ld_free(msg + r)) red_min(msg + r, x);  // msg only decreases: a stale (L1) value costs one extra red
     });
   }
 }
@@ -455,7 +464,20 @@ __global__ void k_lt_win(Coo c, const unsigned long long* len, const int32_t* __
 __global__ void k_lt_update(const int32_t* L, int32_t* msg, int64_t n, Ctl ctl) {
   GC_SKIP_IF_DONE(ctl);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nq = aligned16(L, msg) ? n / 4 : 0;
+  for (int64_t q = t0; q < nq; q += stride) {
+    const int4 l = reinterpret_cast<const int4*>(L)[q];
+    const int32_t v = int32_t(4 * q);
+    if (l.x == v && l.y == v + 1 && l.z == v + 2 && l.w == v + 3) continue;  // four roots: nothing to take
+    int4 m = reinterpret_cast<const int4*>(msg)[q];
+    if (l.x != v) m.x = l.x;
+    if (l.y != v + 1) m.y = l.y;
+    if (l.z != v + 2) m.z = l.z;
+    if (l.w != v + 3) m.w = l.w;
+    reinterpret_cast<int4*>(msg)[q] = m;
+  }
+  for (int64_t v = 4 * nq + t0; v < n; v += stride) {
     const int32_t l = L[v];
     if (l != v) msg[v] = l;
   }
@@ -467,7 +489,32 @@ __global__ void k_lt_shortcut(int32_t* L, const int32_t* msg, int64_t n, int ful
   GC_SKIP_IF_DONE(ctl);
   bool any = false;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nq = aligned16(L, msg) ? n / 4 : 0;
+  for (int64_t q = t0; q < nq; q += stride) {
+    const int4 m4 = reinterpret_cast<const int4*>(msg)[q];
+    int32_t x[4] = {m4.x, m4.y, m4.z, m4.w};
+    int32_t y[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = msg[x[k]];  // four first hops in flight
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        while (y[k] != x[k]) {
+          x[k] = y[k];
+          y[k] = msg[x[k]];
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = y[k];
+    }
+    const int4 l = reinterpret_cast<const int4*>(L)[q];
+    if (l.x != x[0] || l.y != x[1] || l.z != x[2] || l.w != x[3]) {
+      any = true;
+      reinterpret_cast<int4*>(L)[q] = make_int4(x[0], x[1], x[2], x[3]);
+    }
+  }
+  for (int64_t v = 4 * nq + t0; v < n; v += stride) {
     int32_t x = msg[v];
     if (full) {
       int32_t y = msg[x];
@@ -595,6 +642,7 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
                    cudaStream_t st) {
   const int par = r & 1;
   const int gv = grid_e(nl);
+  const int gq = grid_e((nl + 3) / 4);  // quad-vectorised full-array passes
   const int ge = grid_e(edge_cap > 0 ? edge_cap : 1);
   const bool alter = s.finish == GC_FINISH_LT && s.lt_alter;
   Coo& cur = alter ? coo[par] : coo[0];
@@ -606,7 +654,7 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
     L1(k_chunk_compact, ge, cur, ch, ch.keep, par, ctl);
     L1(k_shortcut_roots, grid_e((nl + 3) / 4), A, nl, roots, ctl, 0);
   } else if (s.finish == GC_FINISH_SV) {
-    L1(k_copy, gv, B, A, nl, ctl);
+    L1(k_copy, gq, B, A, nl, ctl);
     L1(k_sv_hook_chunk, ge, cur, ch, A, B, ch.keep, par, ctl);
     if (fo.on()) {
       L1(k_sv_win_chunk, ge, cur, ch, A, B, w.win, ctl);
@@ -617,14 +665,14 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
     std::swap(A, B);
   } else if (s.finish == GC_FINISH_LT) {
     int32_t* msg = w.b;
-    L1(k_copy, gv, msg, P, nl, ctl);
+    L1(k_copy, gq, msg, P, nl, ctl);
     L1(k_lt_connect, ge, cur, len, P, msg, s.lt_connect, ctl);
     if (fo.on()) {
       L1(k_lt_win, ge, cur, len, P, msg, s.lt_connect, w.win, ctl);
       L1(k_commit_win, gv, w.win, nl, fo.off, fo.tgt, fo.fu, fo.fv, ctl);
     }
-    if (s.lt_update == GC_LT_UPDATE_ROOTS) L1(k_lt_update, gv, P, msg, nl, ctl);
-    L1(k_lt_shortcut, gv, P, msg, nl, int(s.lt_shortcut == GC_LT_SHORTCUT_FULL), ctl);
+    if (s.lt_update == GC_LT_UPDATE_ROOTS) L1(k_lt_update, gq, P, msg, nl, ctl);
+    L1(k_lt_shortcut, gq, P, msg, nl, int(s.lt_shortcut == GC_LT_SHORTCUT_FULL), ctl);
     if (alter)
       ((k_lt_alter<<<ge, kRB, 0, st>>>(cur, len, coo[par ^ 1], ctl.len + (par ^ 1), ctl.wt + (par ^ 1), P,
                                        ctl)), ::gc::count_launch());
@@ -635,7 +683,7 @@ void enqueue_round(const gc_spec& s, int r, int32_t* P, int64_t nl, Coo* coo, Ro
     std::swap(A, B);
   } else {
     int32_t* snap = w.a;
-    L1(k_copy, gv, snap, P, nl, ctl);
+    L1(k_copy, gq, snap, P, nl, ctl);
     L1(k_lp, ge, cur, len, snap, P, ctl);
   }
   ((k_round_end<<<1, 1, 0, st>>>(ctl)), ::gc::count_launch());
