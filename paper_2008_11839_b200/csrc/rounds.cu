@@ -307,7 +307,7 @@ k_shortcut_roots(int32_t* a, int64_t n, uint32_t* roots, Ctl ctl, int init) {
         // one L2 slice)
         int32_t h[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) h[k] = ld_free(a + r[k]);
+        for (int k = 0; k < 4; ++k) h[k] = v0 + k < n ? ld_free(a + r[k]) : r[k];  // tail lanes: no read
         unsigned live = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) live |= unsigned(h[k] != r[k]) << k;
