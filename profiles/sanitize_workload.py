@@ -9,7 +9,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2008_11839_b200 import (DisjointSets, FindOp, IncrementalConnectivity, SpliceOp, UnionConfig,  # noqa: E402
-                                   UnionOp, build_csr, check_forest, gen_rmat, parse_spec, spanning_forest_device,
+                                   UnionOp, build_csr, check_forest, gen_rmat, gen_uniform_pairs, parse_spec, spanning_forest_device,
                                    static_connectivity)
 from paper_2008_11839_b200.distributed import GpuEngine, shard_bounds, shard_graph  # noqa: E402
 
@@ -24,6 +24,11 @@ for text in ["none+rem_cas+naive+splice", "kout+rem_cas+halve+splice", "hb+hooks
 for text in ["bfs+async+halve", "none+sv", "kout+rem_cas+split+split", "none+lt_prf"]:
     df, st = spanning_forest_device(g, parse_spec(text))
     assert check_forest(g, df, ref)["passed"], text
+# a frontier above the wide top-down threshold (2^16): bitmap mark + parent pull
+gu = build_csr(gen_uniform_pairs(18, 4 << 18, seed=1, device=True))
+refu = static_connectivity(gu, parse_spec("none+async+halve"))[0]
+df, st = spanning_forest_device(gu, parse_spec("bfs+async+halve"))
+assert check_forest(gu, df, refu)["passed"]
 ue = g.undirected_edges()
 us = torch.from_numpy(ue[:, 0].astype(np.int32)).cuda()
 vs = torch.from_numpy(ue[:, 1].astype(np.int32)).cuda()
