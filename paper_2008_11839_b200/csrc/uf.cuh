@@ -187,12 +187,28 @@ __device__ __forceinline__ int32_t splice(int32_t u, int32_t pu_seen, int32_t pv
 // All return true iff this call merged two trees.
 
 template <int FIND, bool FOREST>
-__device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t v) {
-  // dset.py:222-234
+__device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t v, int32_t ku = -1,
+                                            int32_t kv = -1) {
+  // dset.py:222-234.  ku / kv (>= 0): values of P[u] / P[v] the caller just
+  // read; for the one-step finds the grandparent reads of both endpoints are
+  // then issued together before either walk starts.
   int32_t* P = s.P;
   Reader rd(s.weak);
-  int32_t pu = find<FIND>(u, P, rd);
-  int32_t pv = find<FIND>(v, P, rd);
+  int32_t pu, pv;
+  if (FIND == GC_FIND_HALVE || FIND == GC_FIND_SPLIT) {
+    if (ku >= 0 && kv >= 0) {
+      const int32_t wu = ku == u ? u : rd(P + ku);
+      const int32_t wv = kv == v ? v : rd(P + kv);
+      pu = find<FIND>(u, P, rd, ku, wu);
+      pv = find<FIND>(v, P, rd, kv, wv);
+    } else {
+      pu = find<FIND>(u, P, rd);
+      pv = find<FIND>(v, P, rd);
+    }
+  } else {
+    pu = find<FIND>(u, P, rd);
+    pv = find<FIND>(v, P, rd);
+  }
   while (pu != pv) {
     if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
     if (rd(P + pu) == pu && cas(P + pu, pu, pv)) {
@@ -296,14 +312,17 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
 }
 
 template <int FIND, int SPLICE, bool FOREST>
-__device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32_t v) {
-  // dset.py:303-316
+__device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32_t v, int32_t ku = -1,
+                                              int32_t kv = -1) {
+  // dset.py:303-316 (ku / kv: held values of P[u] / P[v] for the first step)
   int32_t* P = s.P;
   Reader rd(s.weak);
   int32_t ru = u, rv = v;
+  bool first = ku >= 0 && kv >= 0;
   while (true) {
-    int32_t pru = rd(P + ru);
-    int32_t prv = rd(P + rv);
+    int32_t pru = first ? ku : rd(P + ru);
+    int32_t prv = first ? kv : rd(P + rv);
+    first = false;
     if (pru == prv) return false;
     if (pru < prv) {
       int32_t t = ru; ru = rv; rv = t;
@@ -360,6 +379,13 @@ struct Rule {
     else if constexpr (UNION == GC_FINISH_REM_LOCK) return union_rem_lock<FIND, SPLICE, FOREST>(s, u, v);
     else if constexpr (UNION == GC_FINISH_REM_CAS) return union_rem_cas<FIND, SPLICE, FOREST>(s, u, v);
     else return union_jtb<FIND, FOREST>(s, u, v);
+  }
+  // as unite, with pu0 / pv0 = values of P[u] / P[v] just read (or written)
+  __device__ __forceinline__ static bool unite_known(const UFState& s, int32_t u, int32_t v, int32_t pu0,
+                                                     int32_t pv0) {
+    if constexpr (UNION == GC_FINISH_ASYNC) return union_async<FIND, FOREST>(s, u, v, pu0, pv0);
+    else if constexpr (UNION == GC_FINISH_REM_CAS) return union_rem_cas<FIND, SPLICE, FOREST>(s, u, v, pu0, pv0);
+    else return unite(s, u, v);
   }
 };
 

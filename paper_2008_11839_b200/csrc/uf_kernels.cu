@@ -93,8 +93,20 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
       // a union reads is either one of its own endpoints (initialised right
       // here) or an ancestor, which was a root — hence initialised — when it
       // was linked.  The launcher turns L1-cached reads off for this mode.
-      if (ld_acq(s.P + u) == sentinel) atomicCAS(s.P + u, sentinel, u);
-      if (ld_acq(s.P + v) == sentinel) atomicCAS(s.P + v, sentinel, v);
+      // Both endpoint reads are issued together and handed to the union as
+      // its first parent reads (a CAS result is a held value too).
+      int32_t pu = ld_acq(s.P + u);
+      int32_t pv = ld_acq(s.P + v);
+      if (pu == sentinel) {
+        const int32_t o = atomicCAS(s.P + u, sentinel, u);
+        pu = o == sentinel ? u : o;
+      }
+      if (pv == sentinel) {
+        const int32_t o = atomicCAS(s.P + v, sentinel, v);
+        pv = o == sentinel ? v : o;
+      }
+      R::unite_known(s, u, v, pu, pv);
+      continue;
     }
     R::unite(s, u, v);
   }
