@@ -644,12 +644,16 @@ double bfs_alpha() {
 // frontier size from which a non-batched top-down level uses the
 // fire-and-forget claims (below it the returning atomics are cheap and the
 // queue is built in the same pass)
-unsigned long long bfs_wide_min() {
-  static const unsigned long long v = [] {
+// (n/2048: 65536 at n = 2^27; small graphs take the wide form from 256
+// frontier vertices on, which keeps it covered by the test graphs)
+unsigned long long bfs_wide_min(int64_t n) {
+  static const long long v = [] {
     const char* e = getenv("GC_BFS_WIDE_MIN");
-    return e ? strtoull(e, nullptr, 10) : 65536ull;
+    return e ? atoll(e) : -1ll;
   }();
-  return v;
+  if (v >= 0) return static_cast<unsigned long long>(v);
+  const int64_t t = n >> 11;
+  return static_cast<unsigned long long>(t > 256 ? t : 256);
 }
 
 bool bfs_trace() {
@@ -737,7 +741,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     // Beamer's heuristic: bottom-up once the frontier's edges exceed
     // 1/alpha of the unexplored ones, back to top-down below n/beta
     const bool want_bu = bottom_up ? (nf >= uint64_t(n) / kBfsBeta) : (mf * bfs_alpha() > unexplored);
-    if ((want_bu || nf >= bfs_wide_min()) && bits_stale) {
+    if ((want_bu || nf >= bfs_wide_min(n)) && bits_stale) {
       GC_CUDA(cudaMemsetAsync(fb[c], 0, words * 4, st));
       TL(k_queue_to_bits, grid_for(int64_t(nf), kEwBlock, 4), kEwBlock, q[c], slot(level), fb[c]);
     }
@@ -755,7 +759,7 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     } else {
       const int64_t b64 = (int64_t(nf) + kTB - 1) / kTB;
       const int blocks = int(b64 < int64_t(num_sms()) * 8 ? (b64 > 0 ? b64 : 1) : int64_t(num_sms()) * 8);
-      if (nf >= bfs_wide_min()) {
+      if (nf >= bfs_wide_min(n)) {
         TL(k_bfs_td_mark, blocks, kTB, g.offsets, g.targets, q[c], slot(level), w.vis, fb[nx]);
         TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, fb[nx], n, q[nx], slot(level + 1), minv, 0);
         TL(k_bfs_pull, num_sms() * (2048 / kTB), kTB, g.offsets, g.targets, q[nx], slot(level + 1), fb[c], par);
