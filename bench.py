@@ -418,7 +418,11 @@ def run_ours(args):
                 "kernel_ms": kms, "kernel_bytes": kout_bytes, "peak_source": peak_kind,
                 "step_alg_bytes": step_bytes,
                 "step_frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak,
-                "kernel_share_of_step": kms / ms_per_step}
+                "kernel_share_of_step": kms / ms_per_step,
+                # the measured DRAM bytes (ncu) over the live kernel time: how
+                # close the kernel runs to the HBM floor of the traffic the CSR
+                # layout forces (each 8-byte row head costs a 64-byte burst)
+                "traffic_frac": (traffic / (kms / 1e3) / 1e9 / peak) if traffic else None}
 
     cpu = None
     if rank == 0 and args.cpu_baseline:
