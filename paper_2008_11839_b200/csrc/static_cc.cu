@@ -261,6 +261,7 @@ struct Pipeline {
         a.take_max = INT_MAX;
         a.lower_only = 1;
         a.insp = nullptr;
+        if (row_hi < 0) a.all_edges = g.m;
         set_ctr(ws.ctr, C_INSP_FINISH, static_cast<unsigned long long>(g.m), st);
       } else {
         a.list = ws.list;

@@ -80,6 +80,28 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
   if (insp) block_add<kRowBlock>(insp, my_insp);
 }
 
+// Edge-parallel form of the all-active lower-only finish for graphs with
+// fewer rows than resident threads (RMAT s16: 65k rows on 303k thread slots,
+// each lane walking a whole row): one thread per CSR entry, its row by a
+// binary search over the (cached) offsets; entry (u, t) is unioned when t < u
+// — the same edge set as the row form.
+template <class R>
+__global__ void __launch_bounds__(256)
+k_union_csr_edges(UFState s, const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n,
+                  int64_t m) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const int32_t t = ldg32(tgt + j);
+    int32_t lo = 0, hi = n - 1;  // last row with off[row] <= j
+    while (lo < hi) {
+      const int32_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(off + mid) <= j) lo = mid;
+      else hi = mid - 1;
+    }
+    if (t < lo) R::unite(s, lo, t);
+  }
+}
+
 template <class R>
 __global__ void __launch_bounds__(256)
 k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
@@ -177,6 +199,17 @@ struct RowsLaunch {
   template <class R>
   void go() const {
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
+    if (a.all_edges >= 0 && !a.list && a.lower_only && a.count_host == a.n &&
+        a.count_host < int64_t(num_sms()) * 2048) {
+      if (a.all_edges == 0) return;
+      int64_t blocks = (a.all_edges + 255) / 256;
+      const int64_t cap = int64_t(num_sms()) * 8 * 16;
+      if (blocks > cap) blocks = cap;
+      (k_union_csr_edges<R><<<int(blocks), 256, 0, st>>>(s, a.off, a.tgt, a.n, a.all_edges),
+       ::gc::count_launch());
+      GC_CHECK_LAUNCH();
+      return;
+    }
     int64_t warps = (a.count_host + 31) / 32;
     int64_t blocks = (warps * 32 + kRowBlock - 1) / kRowBlock;
     // one resident wave, grid-stride over 32-row groups
