@@ -314,10 +314,16 @@ __global__ void k_or_words(uint32_t* dst, const uint32_t* src, int64_t words) {
 
 // bitmap -> queue (switching back to top-down): one thread per 32-bit word
 __global__ void __launch_bounds__(kEwBlock)
-k_bits_to_queue(uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, int32_t* minv, int clear) {
+k_bits_to_queue(uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, int32_t* minv, int clear,
+                const unsigned int* gate = nullptr, unsigned int* gate_next = nullptr) {
   using Scan = cub::BlockScan<int, kEwBlock>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
+  // LDD rounds: gate = "the round claimed something" (an empty bitmap has
+  // nothing to scan); gate_next is the other parity's flag, which no kernel
+  // reads now, cleared for the next round to set
+  if (gate_next && blockIdx.x == 0 && threadIdx.x == 0) *gate_next = 0u;
+  if (gate && *gate == 0u) return;
   const int64_t words = (int64_t(n) + 31) / 32;
   for (int64_t w0 = int64_t(blockIdx.x) * kEwBlock; w0 < words; w0 += int64_t(gridDim.x) * kEwBlock) {
     const int64_t wi = w0 + threadIdx.x;
@@ -540,11 +546,12 @@ __global__ void __launch_bounds__(kTB)
 k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, uint32_t* cluster, uint16_t* croud,
             const int32_t* order, const unsigned int* boff, int32_t r, int32_t last_start, const int32_t* qin,
             const unsigned long long* cin, int32_t* qout, unsigned long long* cout, unsigned long long* cnext,
-            unsigned long long* insp, uint32_t* nbits) {
+            unsigned long long* insp, uint32_t* nbits, unsigned int* any_claim) {
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
   if (blockIdx.x == 0 && threadIdx.x == 0) *cnext = 0;
   unsigned long long my_insp = 0;
+  bool claimed = false;
   if (r > 0) {
     const int64_t count = int64_t(*cin);
     for (int64_t base = int64_t(blockIdx.x) * kTB; base < count; base += int64_t(gridDim.x) * kTB) {
@@ -572,6 +579,7 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, ui
         }
         if (nbits) {
           if (fresh) red_or_u32(nbits + (x >> 5), 1u << (x & 31));
+          claimed |= fresh;
         } else {
           bq.push(fresh, x, qout, cout);
         }
@@ -591,6 +599,7 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, ui
       }
       if (nbits) {
         if (fresh) red_or_u32(nbits + (v >> 5), 1u << (v & 31));
+        claimed |= fresh;
       } else {
         bq.push(fresh, v, qout, cout);
         bq.maybe_flush(qout, cout, kQCap / 2);
@@ -599,6 +608,7 @@ k_ldd_round(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, ui
   }
   bq.flush(qout, cout);
   block_add<kTB>(insp, my_insp);
+  if (any_claim && __syncthreads_or(int(claimed)) && threadIdx.x == 0) *any_claim = 1u;
 }
 
 // minimum member per cluster: lanes holding the same cluster (neighbouring
@@ -812,6 +822,9 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   const int64_t words = (int64_t(n) + 31) / 32;
   uint32_t* nbits = w.fb0;
   GC_CUDA(cudaMemsetAsync(nbits, 0, size_t(words) * 4, st));
+  // per-parity "round claimed something" flags (in the free tail of stat)
+  unsigned int* flag = reinterpret_cast<unsigned int*>(w.stat + 4);
+  GC_CUDA(cudaMemsetAsync(flag, 0, 2 * sizeof(unsigned int), st));
   TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cluster, croud, bcount);
   TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
   TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
@@ -837,10 +850,9 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   for (int32_t r = 0;;) {
     for (int k = 0; k < kLddBatch; ++k, ++r) {
       TL(k_ldd_round, grid, kTB, g.offsets, g.targets, cluster, croud, w.order, w.boff, r, last_start, q[(r + 1) & 1],
-         ring + (r + 2) % 3, q[r & 1], ring + r % 3, ring + (r + 1) % 3, ctr + C_INSP_SAMPLE, nbits);
-      if (nbits)
-        TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, nbits, n, q[r & 1], ring + r % 3,
-           static_cast<int32_t*>(nullptr), 1);
+         ring + (r + 2) % 3, q[r & 1], ring + r % 3, ring + (r + 1) % 3, ctr + C_INSP_SAMPLE, nbits, flag + (r & 1));
+      TL(k_bits_to_queue, grid_for(words, kEwBlock, 4), kEwBlock, nbits, n, q[r & 1], ring + r % 3,
+         static_cast<int32_t*>(nullptr), 1, flag + (r & 1), flag + ((r + 1) & 1));
     }
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaMemcpyAsync(hq, ring + (r - 1) % 3, 8, cudaMemcpyDeviceToHost, st));
