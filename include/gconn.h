@@ -203,7 +203,12 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
  *     union-find finish over the block's active rows, recording merging edges
  *     the same way.  stats: insp_finish (block), l_max, lmax_count, n_active.
  *   -- exchange again, union foreign edges, gc_label_finalization --
- * Union-find finishes with root-based rules only. */
+ * Union-find finishes only.  Root-based rules record the merging edges
+ * themselves; the atomic splice (not root-based: it re-points non-roots)
+ * records root transitions instead — every vertex that was a root before the
+ * phase and is not one after emits (v, P[v]), one pair per merge, which
+ * reproduces the partition change when unioned anywhere.  NULL outputs in
+ * gc_shard_sample: sample only (the compact summary exchange). */
 int gc_shard_sample(const gc_csr* g, const gc_spec* spec, int64_t row_lo,
                     int64_t row_hi, int32_t* parent, int32_t* out_u,
                     int32_t* out_v, unsigned long long* out_count,
