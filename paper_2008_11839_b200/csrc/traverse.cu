@@ -742,7 +742,11 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
       unexplored = double(g.m) - double(h[2] + 1) * avg_deg;
       if (nf > 0) {
         const double observed = std::pow(double(nf) / double(nf0), 1.0 / batch);
-        growth = observed * 1.5 > 1.01 ? observed * 1.5 : 1.01;
+        // safety margin on the exponent, not the factor: a slowly growing
+        // frontier (a 3-D grid grows ~1% per level) keeps long batches
+        // instead of one host round trip every few levels
+        const double g15 = std::pow(observed > 1.0 ? observed : 1.0, 1.5);
+        growth = g15 > 1.01 ? g15 : 1.01;
       }
       bits_stale = true;
       continue;
