@@ -96,53 +96,61 @@ __device__ __forceinline__ bool keep_entry(int32_t u, int32_t t, bool all_active
   return t > u && (all_active || P[u] != P[t]);
 }
 
-__global__ void k_coo_count(const int64_t* off, const int32_t* tgt, const int32_t* P,
-                            const int32_t* list, int64_t count, int32_t lmax, int all_active,
-                            int64_t* cnt) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= count; i += stride) {
-    if (i == count) {
-      cnt[i] = 0;
-      continue;
-    }
-    const int32_t u = list ? list[i] : int32_t(i);
-    const int64_t b = off[u], e = off[u + 1];
-    int64_t c = 0;
-    if (all_active) {
-      // rows are sorted: the kept entries t > u are a suffix
-      int64_t lo = b, hi = e;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (tgt[mid] > u) hi = mid; else lo = mid + 1;
+// Single-pass gather: a block takes 256 rows, counts their kept entries (all
+// active: the sorted suffix t > u, found by binary search), scans the counts
+// in the block, reserves its output range with one atomic on a cursor and
+// writes.  Replaces count pass + device scan + host read + write pass; the
+// entry order is then block-arrival order, which no round rule depends on
+// (rounds are Jacobi, forest winners compare CSR indices).
+__global__ void __launch_bounds__(kRB)
+k_coo_gather(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ P,
+             const int32_t* __restrict__ list, int64_t count, int32_t lmax, int all_active, int map_labels,
+             Coo out, unsigned long long* cursor) {
+  using Scan = cub::BlockScan<int, kRB>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long base;
+  const int64_t stride = int64_t(gridDim.x) * kRB;
+  for (int64_t i0 = int64_t(blockIdx.x) * kRB; i0 < count; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    int32_t u = 0;
+    int64_t b = 0, e = 0;
+    int c = 0;
+    if (i < count) {
+      u = list ? list[i] : int32_t(i);
+      b = off[u];
+      e = off[u + 1];
+      if (all_active) {
+        int64_t lo = b, hi = e;  // rows are sorted: the kept entries t > u are a suffix
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (tgt[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        b = lo;
+        c = int(e - lo);
+      } else {
+        bool twin;
+        for (int64_t j = b; j < e; ++j) c += keep_entry(u, tgt[j], false, P, lmax, twin);
       }
-      c = e - lo;
-    } else {
-      bool twin;
-      for (int64_t j = b; j < e; ++j) c += keep_entry(u, tgt[j], false, P, lmax, twin);
     }
-    cnt[i] = c;
-  }
-}
-
-__global__ void k_coo_write(const int64_t* off, const int32_t* tgt, const int32_t* P,
-                            const int32_t* list, int64_t count, int32_t lmax, int all_active,
-                            int map_labels, const int64_t* pos, Coo out) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const int32_t u = list ? list[i] : int32_t(i);
-    const int32_t lu = map_labels ? P[u] : u;
-    int64_t p = pos[i];
-    const int64_t b = off[u], e = off[u + 1];
-    for (int64_t j = b; j < e; ++j) {
-      const int32_t t = tgt[j];
-      bool twin;
-      if (!keep_entry(u, t, all_active, P, lmax, twin)) continue;
-      out.u[p] = lu;
-      out.v[p] = map_labels ? P[t] : t;
-      out.w[p] = twin ? 2 : 1;
-      if (out.idx) out.idx[p] = j;
-      ++p;
+    int rank, total;
+    Scan(tmp).ExclusiveSum(c, rank, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(cursor, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    if (c) {
+      const int32_t lu = map_labels ? P[u] : u;
+      unsigned long long p = base + rank;
+      for (int64_t j = b; j < e; ++j) {
+        const int32_t t = tgt[j];
+        bool twin = true;
+        if (!all_active && !keep_entry(u, t, false, P, lmax, twin)) continue;
+        out.u[p] = lu;
+        out.v[p] = map_labels ? P[t] : t;
+        out.w[p] = twin ? 2 : 1;
+        if (out.idx) out.idx[p] = j;
+        ++p;
+      }
     }
+    __syncthreads();  // base is rewritten next step
   }
 }
 
@@ -758,24 +766,21 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
     GC_CHECK_LAUNCH();
     return 0;
   }
-  // gather the working COO (driver.py:325-330), twin-deduplicated:
-  // per-row kept counts, exclusive scan, then a write pass
+  // gather the working COO (driver.py:325-330), twin-deduplicated, in one
+  // pass (the cursor is the first word of the per-row count buffer)
   const bool map_labels = s.finish == GC_FINISH_LT || s.finish == GC_FINISH_LP;
-  (k_coo_count<<<grid_e(count + 1), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax,
-                                                 all_active, w.cnt), ::gc::count_launch());
-  GC_CHECK_LAUNCH();
-  size_t tb = w.cub_bytes;
-  GC_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt, w.pos, int(count + 1), st));
-  GC_CUDA(cudaMemcpyAsync(h, w.pos + count, 8, cudaMemcpyDeviceToHost, st));
-  GC_CUDA(cudaStreamSynchronize(st));
   Coo& work = w.work;
-  work.len = int64_t(h[0]);
-  work.weight = degsum;
   Coo out = work;
   if (!fu) out.idx = nullptr;
-  (k_coo_write<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
-                                             map_labels, w.pos, out), ::gc::count_launch());
+  unsigned long long* cursor = reinterpret_cast<unsigned long long*>(w.cnt);
+  GC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+  (k_coo_gather<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
+                                              map_labels, out, cursor), ::gc::count_launch());
   GC_CHECK_LAUNCH();
+  GC_CUDA(cudaMemcpyAsync(h, cursor, 8, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  work.len = int64_t(h[0]);
+  work.weight = degsum;
   work.idx = out.idx;
   ForestOut fo;
   if (fu) fo = ForestOut{g.offsets, g.targets, fu, fv};
