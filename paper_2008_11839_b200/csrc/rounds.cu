@@ -794,12 +794,6 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
   return rounds;
 }
 
-size_t rounds_cub_bytes(int64_t n) {
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<int64_t*>(nullptr),
-                                static_cast<int64_t*>(nullptr), int(n + 1));
-  return b;
-}
 
 int64_t run_rounds_coo(const gc_spec& s, int32_t* labels, int64_t nl, Coo& work, RoundsWs& w,
                        unsigned long long* ctr, int counter_slot, cudaStream_t st) {

@@ -30,10 +30,7 @@ struct RoundsWs {
   int32_t* a = nullptr;      // prev / snapshot
   int32_t* b = nullptr;      // cur / msg
   unsigned long long* win = nullptr;  // forest winner edge index per root
-  int64_t* cnt = nullptr;    // per-row kept counts (gather)
-  int64_t* pos = nullptr;    // their exclusive scan
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
+  int64_t* cnt = nullptr;    // gather cursor (one word)
   Coo work, spare;
   uint8_t* keep = nullptr;   // SV: per working edge, snapshot labels differ
   int64_t* chunks = nullptr; // SV: per-block chunk [start, len] tables
@@ -42,7 +39,6 @@ struct RoundsWs {
 // upper bound of the edge-kernel grid (grid_for(.., 256, 8) on 148 SMs)
 constexpr int64_t kMaxChunks = 148 * 8 * 8;
 
-size_t rounds_cub_bytes(int64_t n);
 
 template <class A>
 void rounds_carve(A& a, RoundsWs& w, int64_t n, int64_t m, const gc_spec& s, bool forest) {
@@ -50,10 +46,7 @@ void rounds_carve(A& a, RoundsWs& w, int64_t n, int64_t m, const gc_spec& s, boo
   w.a = a.template take<int32_t>(n + 1);
   w.b = a.template take<int32_t>(n + 1);
   if (forest) w.win = a.template take<unsigned long long>(n + 1);
-  w.cnt = a.template take<int64_t>(n + 2);
-  w.pos = a.template take<int64_t>(n + 2);
-  w.cub_bytes = rounds_cub_bytes(n);
-  w.cub_tmp = a.template take<char>(int64_t(w.cub_bytes));
+  w.cnt = a.template take<int64_t>(2);
   for (Coo* c : {&w.work, &w.spare}) {
     c->u = a.template take<int32_t>(m);
     c->v = a.template take<int32_t>(m);
