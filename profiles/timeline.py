@@ -18,6 +18,14 @@ from paper_2008_11839_b200 import (build_csr, gen_rmat, gen_uniform_pairs, grid3
 
 
 def workload(name):
+    if name.startswith("forest_uniform27"):  # forest_uniform27[:spec]
+        g = build_csr(gen_uniform_pairs(27, 4 << 27, seed=1), keep_host=False)
+        sp = parse_spec(name.split(":")[1] if ":" in name else "bfs+async+halve")
+        return lambda: spanning_forest_device(g, sp)
+    if name.startswith("static_uniform27"):  # static_uniform27:spec
+        g = build_csr(gen_uniform_pairs(27, 4 << 27, seed=1), keep_host=False)
+        sp = parse_spec(name.split(":")[1])
+        return lambda: static_connectivity_device(g, sp, metrics=False)
     if name == "bfs_uniform27":
         g = build_csr(gen_uniform_pairs(27, 4 << 27, seed=1), keep_host=False)
         return lambda: spanning_forest_device(g, parse_spec("bfs+async+halve"))
