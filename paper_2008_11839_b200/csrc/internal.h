@@ -127,6 +127,7 @@ struct RowUnionArgs {
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
   int64_t row_base = 0;   // list == nullptr: rows [row_base, row_base + count_host)
+  int2* fpair = nullptr;   // forest slots as pairs (see UFState::fpair)
   int64_t all_edges = -1;  // >= 0: the rows are the whole graph with this many entries
                            // (all-active lower-only finish; small graphs go edge-parallel)
 };

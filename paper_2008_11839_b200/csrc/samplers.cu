@@ -70,7 +70,7 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
 // atomics.  The surviving non-isolated roots form the phase-2 list.
 __global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int64_t lo, int64_t hi, int32_t* P,
                             int32_t* fu, int32_t* fv, int32_t* roots, unsigned long long* ctr,
-                            int32_t* lu, int32_t* lv, unsigned long long* lcount) {
+                            int32_t* lu, int32_t* lv, unsigned long long* lcount, int2* fpair) {
   unsigned long long nz = 0;
   const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -84,7 +84,9 @@ __global__ void k_hb_phase1(const int64_t* off, const int32_t* tgt, int64_t lo, 
         const int32_t first = tgt[b];
         if (first < v) {
           P[v] = first;
-          if (fu) {
+          if (fpair) {
+            fpair[v] = make_int2(int32_t(v), first);
+          } else if (fu) {
             fu[v] = int32_t(v);
             fv[v] = first;
           }
@@ -120,7 +122,8 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
     hi = a.row_base + a.count_host;
   }
   (k_hb_phase1<<<grid_for(hi - lo, kEwBlock, 8), kEwBlock, 0, st>>>(g.offsets, g.targets, lo, hi, a.P, a.fu,
-                                                                   a.fv, w.q0, ctr, a.lu, a.lv, a.lcount),
+                                                                   a.fv, w.q0, ctr, a.lu, a.lv, a.lcount,
+                                                                   a.fpair),
    ::gc::count_launch());
   GC_CHECK_LAUNCH();
   // Phase 2 (sampling.py:110-116): union the first N edges of each root

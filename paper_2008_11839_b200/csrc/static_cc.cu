@@ -122,6 +122,19 @@ void validate_csr(const gc_csr* g) {
   require(g->m == 0 || g->targets != nullptr, GC_ERR_ARG, "null targets");
 }
 
+__global__ void k_split_pairs(const int2* __restrict__ pr, int32_t n, int32_t* fu, int32_t* fv,
+                              unsigned long long* count) {
+  unsigned long long c = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const int2 p = pr[v];
+    fu[v] = p.x;
+    fv[v] = p.y;
+    c += p.x != -1;
+  }
+  block_add<kEwBlock>(count, c);
+}
+
 // Workspace layout shared by every static entry point.
 template <class A>
 struct Layout {
@@ -130,11 +143,18 @@ struct Layout {
   int32_t* L = nullptr;
   int32_t* list = nullptr;
   int32_t* hist = nullptr;
+  int2* fpair = nullptr;  // union-find forests of none / k-out / HB samplers
   RoundsWs rounds;
   SamplerWs samp;
 
+  static bool pair_forest(const gc_spec& s) {
+    return is_union_finish(s.finish) &&
+           (s.sample == GC_SAMPLE_NONE || s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB);
+  }
+
   void carve(A& a, int64_t n, int64_t m, const gc_spec& s, bool forest) {
     ctr = a.template take<unsigned long long>(C_COUNT_);
+    if (forest && pair_forest(s)) fpair = a.template take<int2>(n);
     const UFConfig sc = sampler_cfg(s);
     const bool any_uf = is_union_finish(s.finish) || s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB;
     if (any_uf && sc.unite == GC_FINISH_HOOKS) H = a.template take<int32_t>(n);
@@ -178,6 +198,7 @@ struct Pipeline {
     a.R = s.jtb_ranks;
     a.fu = fu;
     a.fv = fv;
+    a.fpair = fu ? ws.fpair : nullptr;
     a.n = n;
     a.off = g.offsets;
     a.tgt = g.targets;
@@ -315,15 +336,17 @@ void check_static_args(const gc_csr* g, const gc_spec* spec, int32_t* labels) {
 void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32_t* post, int want_ic,
                     int32_t* fu, int32_t* fv, void* ws, size_t wsb, cudaStream_t st, RunState& rs) {
   const bool forest = fu != nullptr;
+  if (forest) require(fv != nullptr, GC_ERR_ARG, "null forest array");
+  Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
   if (forest) {
-    require(fv != nullptr, GC_ERR_ARG, "null forest array");
-    // a BFS sample over edges writes every slot itself (k_bfs_label)
-    if (!(spec->sample == GC_SAMPLE_BFS && g->m > 0)) {
+    if (pl.ws.fpair) {
+      fill(reinterpret_cast<int32_t*>(pl.ws.fpair), 2 * g->n, -1, st);  // pairs, split at the end
+    } else if (!(spec->sample == GC_SAMPLE_BFS && g->m > 0)) {
+      // a BFS sample over edges writes every slot itself (k_bfs_label)
       fill(fu, g->n, -1, st);
       fill(fv, g->n, -1, st);
     }
   }
-  Pipeline pl(*g, *spec, labels, fu, fv, ws, wsb, st);
   L2Residency keep_parents(st, labels, size_t(g->n) * 4);
   cudaEvent_t* ev = rs.ev.e;
   pl.kev = ev + 5;
@@ -347,10 +370,15 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   GC_CUDA(rec(ev[3], st));
   if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
   if (forest && n) {
-    // spanning_forest: component_count = n - |forest| (driver.py:535)
+    // spanning_forest: component_count = n - |forest| (driver.py:535); the
+    // pair form is split into fu / fv and counted in the same pass
     set_ctr(pl.ws.ctr, C_SCRATCH1, 0, st);
-    (k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, pl.ws.ctr + C_SCRATCH1),
-     ::gc::count_launch());
+    if (pl.ws.fpair)
+      (k_split_pairs<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(pl.ws.fpair, n, fu, fv,
+                                                                   pl.ws.ctr + C_SCRATCH1), ::gc::count_launch());
+    else
+      (k_count_ne<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(fu, n, -1, pl.ws.ctr + C_SCRATCH1),
+       ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
   GC_CUDA(rec(ev[4], st));

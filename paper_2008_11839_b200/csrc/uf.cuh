@@ -29,6 +29,10 @@ struct UFState {
   int32_t* lu = nullptr;  // optional compact list of merging edges (distributed exchange)
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
+  // forest slots as (u, v) pairs: one 8-byte store per recorded link instead
+  // of two 4-byte stores to two arrays (each a random DRAM read-modify-write
+  // once the slot arrays outgrow L2); split into fu / fv by one pass at the end
+  int2* fpair = nullptr;
   // L1-cacheable first reads (see Reader).  Kernels that initialise slots
   // while other threads union (incremental lazy init) turn them off: a stale
   // L1 line could still hold the uninitialised sentinel, which is not an
@@ -39,7 +43,9 @@ struct UFState {
 template <bool FOREST>
 __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u, int32_t v) {
   if constexpr (FOREST) {
-    if (s.fu) {
+    if (s.fpair) {
+      s.fpair[slot] = make_int2(u, v);
+    } else if (s.fu) {
       s.fu[slot] = u;
       s.fv[slot] = v;
     }

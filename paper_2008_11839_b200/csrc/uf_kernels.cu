@@ -199,6 +199,7 @@ struct RowsLaunch {
   template <class R>
   void go() const {
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
+    s.fpair = a.fpair;
     if (a.all_edges >= 0 && !a.list && a.lower_only && a.count_host == a.n &&
         a.count_host < int64_t(num_sms()) * 2048) {
       if (a.all_edges == 0) return;
