@@ -642,6 +642,17 @@ void set_ctr_add(unsigned long long* ctr, int idx, unsigned long long v, cudaStr
   GC_CHECK_LAUNCH();
 }
 
+__global__ void k_zero_words(unsigned long long* a, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = 0;
+}
+
+// zero a few counter words with a kernel node: a captured memset node ahead
+// of the first kernel of a graph replay measured ~20-50 us of idle time
+void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st) {
+  (k_zero_words<<<1, 32, 0, st>>>(ctr, words), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
   (k_set_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
   GC_CHECK_LAUNCH();

@@ -187,7 +187,7 @@ struct Pipeline {
       : g(g_), s(s_), P(P_), fu(fu_), fv(fv_), st(st_), n(int32_t(g_.n)) {
     Arena a(wsp, wsb);
     ws.carve(a, g.n, g.m, s, fu != nullptr);
-    GC_CUDA(cudaMemsetAsync(ws.ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
+    zero_ctr(ws.ctr, C_COUNT_, st);
   }
 
   RowUnionArgs rows(const UFConfig& c) const {

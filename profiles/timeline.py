@@ -48,6 +48,12 @@ def workload(name):
             for b0 in range(0, us.numel(), 10_000_000):
                 inc.insert(us[b0:b0 + 10_000_000], vs[b0:b0 + 10_000_000])
         return run
+    if name.startswith("plan"):  # plan24:spec — the captured StaticConnectivity plan (bench.py's step)
+        scale, spec = name[4:].split(":")
+        from paper_2008_11839_b200 import StaticConnectivity
+        g = build_csr(gen_rmat(int(scale), 8, seed=1, device=True), keep_host=False)
+        plan = StaticConnectivity(g, parse_spec(spec))
+        return lambda: plan.run()
     if name.startswith("rmat"):
         scale, spec = name[4:].split(":")
         g = build_csr(gen_rmat(int(scale), 8, seed=1, device=True), keep_host=False)
