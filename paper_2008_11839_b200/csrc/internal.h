@@ -90,7 +90,8 @@ enum Counter : int {
   C_WLEN1,
   C_WWT0,          // round loops: working weight, parity 0 / 1
   C_WWT1,
-  C_COUNT_ = 32
+  C_STAMP0,        // 10 %globaltimer stamps of the static pipeline's phases
+  C_COUNT_ = C_STAMP0 + 10
 };
 
 struct UFConfig {

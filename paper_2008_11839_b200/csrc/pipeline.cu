@@ -653,6 +653,20 @@ void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st) {
   GC_CHECK_LAUNCH();
 }
 
+// Phase timestamps as kernel nodes writing %globaltimer: captured event
+// record nodes left 5-10 us of idle between the kernels around them in a
+// plan replay; a one-thread kernel node costs ~1.5 us
+__global__ void k_stamp(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
+void stamp(unsigned long long* ctr, int i, cudaStream_t st) {
+  (k_stamp<<<1, 1, 0, st>>>(ctr + C_STAMP0 + i), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
   (k_set_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
   GC_CHECK_LAUNCH();

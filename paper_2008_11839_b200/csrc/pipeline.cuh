@@ -68,6 +68,7 @@ void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr,
 void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st);
+void stamp(unsigned long long* ctr, int i, cudaStream_t st);
 void set_ctr_add(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 
 }  // namespace gc

@@ -229,29 +229,29 @@ struct Pipeline {
     }
     if (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB) {
       init_sets(sc);
-      if (kev) GC_CUDA(rec(kev[0], st));
+      if (kev) stamp(ws.ctr, 5, st);
       if (s.sample == GC_SAMPLE_KOUT) {
         run_kout(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       } else {
         run_hb(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
       }
-      if (kev) GC_CUDA(rec(kev[1], st));
+      if (kev) stamp(ws.ctr, 6, st);
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, true, st);
     } else if (s.sample == GC_SAMPLE_BFS) {
       // the BFS label pass writes every label (and forest slot) when it runs
       // (m > 0); the init is still needed for the hook / lock arrays
       if (g.m == 0 || sc.unite == GC_FINISH_HOOKS || sc.unite == GC_FINISH_REM_LOCK) init_sets(sc);
-      if (kev) GC_CUDA(rec(kev[0], st));
+      if (kev) stamp(ws.ctr, 5, st);
       run_bfs(g, s, P, fu, fv, ws.samp, ws.ctr, st);
-      if (kev) GC_CUDA(rec(kev[1], st));
+      if (kev) stamp(ws.ctr, 6, st);
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     } else {
       init_sets(sc);
-      if (kev) GC_CUDA(rec(kev[0], st));
+      if (kev) stamp(ws.ctr, 5, st);
       run_ldd(g, s, P, ws.samp, ws.ctr, st);
-      if (kev) GC_CUDA(rec(kev[1], st));
+      if (kev) stamp(ws.ctr, 6, st);
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
     }
@@ -293,15 +293,15 @@ struct Pipeline {
         a.lower_only = 0;
         a.insp = nullptr;  // counted by the gather
       }
-      if (kev) GC_CUDA(rec(kev[2], st));
+      if (kev) stamp(ws.ctr, 7, st);
       launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
-      if (kev) GC_CUDA(rec(kev[3], st));
+      if (kev) stamp(ws.ctr, 8, st);
       return 0;
     }
-    if (kev) GC_CUDA(rec(kev[2], st));
+    if (kev) stamp(ws.ctr, 7, st);
     const int64_t r =
         run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
-    if (kev) GC_CUDA(rec(kev[3], st));
+    if (kev) stamp(ws.ctr, 8, st);
     return r;
   }
 };
@@ -352,9 +352,9 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   pl.kev = ev + 5;
   const int32_t n = pl.n;
 
-  GC_CUDA(rec(ev[0], st));
+  stamp(pl.ws.ctr, 0, st);
   pl.sample();
-  GC_CUDA(rec(ev[1], st));
+  stamp(pl.ws.ctr, 1, st);
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
   if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
   if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
@@ -365,9 +365,9 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
                                                                pl.ws.list, pl.ws.ctr), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  GC_CUDA(rec(ev[2], st));
+  stamp(pl.ws.ctr, 2, st);
   rs.rounds = pl.finish();
-  GC_CUDA(rec(ev[3], st));
+  stamp(pl.ws.ctr, 3, st);
   if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
   if (forest && n) {
     // spanning_forest: component_count = n - |forest| (driver.py:535); the
@@ -381,7 +381,7 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
        ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  GC_CUDA(rec(ev[4], st));
+  stamp(pl.ws.ctr, 4, st);
   GC_CUDA(cudaMemcpyAsync(rs.host_ctr, pl.ws.ctr, sizeof(unsigned long long) * C_COUNT_,
                           cudaMemcpyDeviceToHost, st));
   rs.timed_sample = pl.timed_sample;
@@ -394,12 +394,12 @@ void collect_static(const gc_csr* g, const gc_spec* spec, bool forest, int want_
   const int64_t n = g->n;
   require(c[C_CYCLE] == 0, GC_ERR_MALFORMED, "label array contains a cycle");
   if (!stats) return;
-  cudaEvent_t* ev = rs.ev.e;
-  stats->t_sample_ms = ms(ev[0], ev[1]);
-  stats->t_finish_ms = ms(ev[2], ev[3]);
-  stats->t_finalize_ms = forest ? 0.0 : ms(ev[3], ev[4]);
-  stats->t_sample_kernel_ms = rs.timed_sample ? ms(ev[5], ev[6]) : 0.0;
-  stats->t_finish_kernel_ms = ms(ev[7], ev[8]);
+  const auto span = [&](int a, int b) { return double(c[C_STAMP0 + b] - c[C_STAMP0 + a]) * 1e-6; };  // ns -> ms
+  stats->t_sample_ms = span(0, 1);
+  stats->t_finish_ms = span(2, 3);
+  stats->t_finalize_ms = forest ? 0.0 : span(3, 4);
+  stats->t_sample_kernel_ms = rs.timed_sample ? span(5, 6) : 0.0;
+  stats->t_finish_kernel_ms = span(7, 8);
   stats->insp_sample = int64_t(c[C_INSP_SAMPLE]);
   stats->insp_finish = int64_t(c[C_INSP_FINISH]);
   stats->rounds = rs.rounds;
