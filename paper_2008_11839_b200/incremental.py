@@ -72,6 +72,10 @@ class IncrementalConnectivity:
                 pass
             self._h = None
 
+    def reserve(self, batch_len: int) -> None:
+        """Pre-size the round finishes' per-batch buffers (gc_incr_reserve)."""
+        N.check(N.lib().gc_incr_reserve(self._h, int(batch_len)))
+
     def insert(self, us, vs) -> None:
         """Insert-only batch (columnar device tensors, int32)."""
         n = int(us.numel())
