@@ -290,6 +290,11 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs,
 /* Columnar insert-only / query-only fast paths (no per-op flag array). */
 int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs,
                    int64_t len, gc_stats* stats);
+/* As gc_incr_insert, but for union-find specs the batch is only enqueued on
+ * the handle's stream (no synchronisation, no per-batch phase time): a stream
+ * of inserts then runs back to back; gc_incr_query / gc_incr_labels /
+ * gc_incr_state order after it.  Round finishes behave as gc_incr_insert. */
+int gc_incr_insert_async(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, gc_stats* stats);
 /* Insert-only batch that also records the edges that merged two trees
  * (capacity len) — the per-batch exchange of the sharded incremental driver. */
 int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs,

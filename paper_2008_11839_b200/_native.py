@@ -79,6 +79,7 @@ _SIGNATURES = {
     "gc_incr_labels": (C.c_int, [_VP, _VP, C.POINTER(_I64)]),
     "gc_incr_capacity": (_I64, [_VP]),
     "gc_incr_reserve": (C.c_int, [_VP, _I64]),
+    "gc_incr_insert_async": (C.c_int, [_VP, _VP, _VP, _I64, _VP]),
     "gc_incr_destroy": (None, [_VP]),
     "gc_gen_rmat": (C.c_int, [_I32, _I64, _VP, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                               _VP, _VP, _VP]),

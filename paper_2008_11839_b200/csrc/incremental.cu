@@ -347,6 +347,24 @@ int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len
   });
 }
 
+int gc_incr_insert_async(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, gc_stats* stats) {
+  return guarded([&] {
+    require(h && len >= 0, GC_ERR_ARG, "bad arguments");
+    if (len == 0) return;
+    if (!h->uf) {  // the round finishes synchronise inside every batch anyway
+      GC_CUDA(cudaEventRecord(h->ev[0], h->st));
+      insert_phase(h, us, vs, nullptr, len, len, stats);
+      GC_CUDA(cudaEventRecord(h->ev[1], h->st));
+      GC_CUDA(cudaEventSynchronize(h->ev[1]));
+      if (stats) stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
+      return;
+    }
+    // union-find inserts: enqueue and return (the stream orders batches;
+    // queries, labels and the state copy synchronise); no per-batch timing
+    insert_phase(h, us, vs, nullptr, len, len, stats);
+  });
+}
+
 int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, int32_t* out_u,
                         int32_t* out_v, unsigned long long* out_count, gc_stats* stats) {
   return guarded([&] {

@@ -76,11 +76,13 @@ class IncrementalConnectivity:
         """Pre-size the round finishes' per-batch buffers (gc_incr_reserve)."""
         N.check(N.lib().gc_incr_reserve(self._h, int(batch_len)))
 
-    def insert(self, us, vs) -> None:
-        """Insert-only batch (columnar device tensors, int32)."""
+    def insert(self, us, vs, sync: bool = True) -> None:
+        """Insert-only batch (columnar device tensors, int32).  sync=False
+        (union-find specs): enqueue only; later queries / labels order after
+        it, and the caller keeps us / vs alive until then."""
         n = int(us.numel())
-        N.check(N.lib().gc_incr_insert(self._h, us.data_ptr() if n else None,
-                                       vs.data_ptr() if n else None, n, C.byref(self.stats)))
+        fn = N.lib().gc_incr_insert if sync else N.lib().gc_incr_insert_async
+        N.check(fn(self._h, us.data_ptr() if n else None, vs.data_ptr() if n else None, n, C.byref(self.stats)))
 
     def insert_list(self, us, vs):
         """Insert-only batch that also returns the edges that merged two trees

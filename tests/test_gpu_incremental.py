@@ -85,3 +85,24 @@ def test_lazy_capacity():
     labels, _, st = incremental(None, parse_spec("none+async+naive"), [[Insert(97, 99)]])
     assert len(labels) == 100 and labels[97] == labels[99] == 97 and labels[98] == 98
     assert st.component_count == 1
+
+
+@pytest.mark.parametrize("text", ["none+async+halve", "none+rem_cas+halve+split", "none+sv"])
+def test_async_insert_stream(text):
+    """insert(sync=False) enqueues union-find batches back to back; labels and
+    queries order after them (round finishes fall back to the synchronous form)."""
+    import torch
+    from paper_2008_11839_b200 import IncrementalConnectivity, build_csr, gen_rmat
+    g = build_csr(gen_rmat(14, 8, seed=3, device=True))
+    ref, comps = oracle.components(g.n, g.offsets, g.targets)
+    ue = g.undirected_edges()
+    us = torch.from_numpy(ue[:, 0].astype(np.int32)).cuda()
+    vs = torch.from_numpy(ue[:, 1].astype(np.int32)).cuda()
+    inc = IncrementalConnectivity(parse_spec(text), g.n)
+    inc.reserve(50_000)
+    for b0 in range(0, us.numel(), 50_000):
+        inc.insert(us[b0:b0 + 50_000], vs[b0:b0 + 50_000], sync=False)
+    labels, _ = inc.labels()
+    lab = labels.cpu().numpy().astype(np.int64)
+    touched = np.diff(g.offsets) > 0
+    assert np.array_equal(lab[touched], ref[touched])
