@@ -166,3 +166,53 @@ def test_two_phase_sampled_ranks_share_one_gpu(world):
                 su = np.full(g.n, -1, np.int32); sv = np.full(g.n, -1, np.int32)
                 su[:len(fu)] = fu; sv[:len(fv)] = fv
                 assert oracle.check_forest(g.n, g.offsets, g.targets, su, sv, orc)["passed"], (text, r)
+
+
+def _two_giants_graph():
+    """Two disjoint RMAT s13 halves: with two row blocks each rank's local
+    giant lies in a different component, so the absorb takes its general
+    multi-class path (the single-class fast path does not apply)."""
+    import torch
+    from paper_2008_11839_b200 import EdgeList, build_csr, gen_rmat
+    a = gen_rmat(13, 8, seed=7, device=True).edges.to("cuda")
+    b = gen_rmat(13, 8, seed=8, device=True).edges.to("cuda") + (1 << 13)
+    return build_csr(EdgeList(1 << 14, torch.cat([a, b])))
+
+
+def _two_giants_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2008_11839_b200 import parse_spec
+        from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+        g = _two_giants_graph()
+        lo, hi = shard_bounds(g.offsets, world, "rows")[rank]
+        r = sharded_two_phase(shard_graph(g.cuda(), lo, hi), parse_spec("kout+rem_cas+halve+splice"), forest=False)
+        q.put((rank, (r.labels.cpu().numpy(), r.insp_sample, r.insp_finish, r.lmax_count, r.n_active)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_summary_exchange_disjoint_giants(world):
+    import torch.multiprocessing as mp
+    from paper_2008_11839_b200 import parse_spec, static_connectivity_device
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_giants_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    g = _two_giants_graph()
+    orc, _ = oracle.components(g.n, g.offsets, g.targets)
+    _, st = static_connectivity_device(g, parse_spec("kout+rem_cas+halve+splice"))
+    for r in range(world):
+        labels, i_s, i_f, lcnt, nact = res[r]
+        assert np.array_equal(labels.astype(np.int64), orc), r
+        assert i_s == st.edge_inspections.get("sample", 0) and i_f == st.edge_inspections.get("finish", 0), r
+        assert lcnt / g.n == st.cov and nact == st.active, r
