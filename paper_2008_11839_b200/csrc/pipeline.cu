@@ -695,7 +695,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
                      unsigned long long* ctr, bool compress, cudaStream_t st) {
   if (n > 0) {
     const int64_t nq = (int64_t(n) + 3) / 4;
-    const int gq = grid_for(nq, kEwBlock, 4);
+    const int gq = grid_for(nq, kEwBlock, 1);
     // the fallback kernels usually exit at once: one resident wave keeps
     // their early exit cheap and still streams when they do run
     const int g = grid_for(n, kEwBlock, 1);
