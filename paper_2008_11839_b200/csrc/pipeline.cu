@@ -667,6 +667,27 @@ void stamp(unsigned long long* ctr, int i, cudaStream_t st) {
   GC_CHECK_LAUNCH();
 }
 
+// phase boundaries with no work between them share one stamp node
+__global__ void k_stamp_mask(unsigned long long* ctr, unsigned mask) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  for (int i = 0; i < 10; ++i)
+    if (mask & (1u << i)) ctr[C_STAMP0 + i] = t;
+}
+
+namespace {
+thread_local unsigned t_pending_stamps = 0;
+}
+
+void stamp_defer(int i) { t_pending_stamps |= 1u << i; }
+
+void stamp_flush(unsigned long long* ctr, cudaStream_t st) {
+  if (!t_pending_stamps) return;
+  (k_stamp_mask<<<1, 1, 0, st>>>(ctr, t_pending_stamps), ::gc::count_launch());
+  t_pending_stamps = 0;
+  GC_CHECK_LAUNCH();
+}
+
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st) {
   (k_set_ctr<<<1, 1, 0, st>>>(ctr, idx, v), ::gc::count_launch());
   GC_CHECK_LAUNCH();

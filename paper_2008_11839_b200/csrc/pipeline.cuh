@@ -69,6 +69,8 @@ void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st);
 void stamp(unsigned long long* ctr, int i, cudaStream_t st);
+void stamp_defer(int i);
+void stamp_flush(unsigned long long* ctr, cudaStream_t st);
 void set_ctr_add(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 
 }  // namespace gc

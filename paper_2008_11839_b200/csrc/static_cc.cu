@@ -293,15 +293,17 @@ struct Pipeline {
         a.lower_only = 0;
         a.insp = nullptr;  // counted by the gather
       }
-      if (kev) stamp(ws.ctr, 7, st);
+      if (kev) stamp_defer(7);
+      stamp_flush(ws.ctr, st);
       launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
-      if (kev) stamp(ws.ctr, 8, st);
+      if (kev) stamp_defer(8);
       return 0;
     }
-    if (kev) stamp(ws.ctr, 7, st);
+    if (kev) stamp_defer(7);
+    stamp_flush(ws.ctr, st);
     const int64_t r =
         run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
-    if (kev) stamp(ws.ctr, 8, st);
+    if (kev) stamp_defer(8);
     return r;
   }
 };
@@ -354,10 +356,14 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
 
   stamp(pl.ws.ctr, 0, st);
   pl.sample();
-  stamp(pl.ws.ctr, 1, st);
+  stamp_defer(1);  // shares a node with the finish-phase stamps when nothing runs between
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
-  if (post && n) GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+  if (post && n) {
+    stamp_flush(pl.ws.ctr, st);
+    GC_CUDA(cudaMemcpyAsync(post, labels, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+  }
   if (want_ic && n && spec->sample != GC_SAMPLE_NONE) {
+    stamp_flush(pl.ws.ctr, st);
     // every label-crossing edge has an endpoint outside L_max, so the census
     // only walks the active rows (Σ deg = the finish inspections), adding
     // back the reverse entries from L_max rows
@@ -365,9 +371,10 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
                                                                pl.ws.list, pl.ws.ctr), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  stamp(pl.ws.ctr, 2, st);
+  stamp_defer(2);
   rs.rounds = pl.finish();
-  stamp(pl.ws.ctr, 3, st);
+  stamp_defer(3);
+  stamp_flush(pl.ws.ctr, st);
   if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
   if (forest && n) {
     // spanning_forest: component_count = n - |forest| (driver.py:535); the
@@ -381,7 +388,8 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
        ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
-  stamp(pl.ws.ctr, 4, st);
+  stamp_defer(4);
+  stamp_flush(pl.ws.ctr, st);
   GC_CUDA(cudaMemcpyAsync(rs.host_ctr, pl.ws.ctr, sizeof(unsigned long long) * C_COUNT_,
                           cudaMemcpyDeviceToHost, st));
   rs.timed_sample = pl.timed_sample;
