@@ -151,6 +151,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
+L2_NOTE = ("inputs (offsets + targets, 1.2 GB at scale 24) exceed the 126 MB L2; the GPU arm also "
+           "writes a 256 MiB buffer between timed steps (outside the step events)")
+
+
+def bench_config(scale: int, ef: int, seed: int, n: int, m: int, ws: int) -> dict:
+    """The workload description both arms print (identical dicts, so the
+    driver can match the reference arm's line to ours)."""
+    shards = f", {ws} row blocks" if ws > 1 else ""
+    return {"workload": f"static CC {SPEC} on RMAT scale-{scale} ef{ef} (avg degree 16) seed {seed}{shards}",
+            "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2, "l2": L2_NOTE}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -281,14 +293,11 @@ def run_sharded(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-                "config": {"workload": f"edge-sharded static CC {SPEC} on RMAT scale-{scale} ef{args.edge_factor} "
-                                       f"(avg degree 16) seed {args.seed}, {ws} row blocks",
-                           "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2,
-                           "parallelism": f"edge-sharded x{ws} ({backend}), two-phase: giant-bitmap + "
-                                          "remainder all-gather, then finish merging edges",
-                           "exchanged_pairs_per_step": exchanged,
-                           "exchanged_bitmap_bytes_per_step": ws * ((n + 31) // 32) * 4,
-                           "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+                "config": bench_config(scale, args.edge_factor, args.seed, n, m, ws),
+                "parallelism": f"edge-sharded x{ws} ({backend}), two-phase: giant-bitmap + remainder "
+                               "all-gather, then finish merging edges",
+                "exchanged_pairs_per_step": exchanged,
+                "exchanged_bitmap_bytes_per_step": ws * ((n + 31) // 32) * 4,
                 "e2e": e2e, "gpu_launches": launches, "launches_per_step": launches / args.steps,
                 "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1e3) / 1e9 / ws,
                              "peak": peak, "unit": "GB/s",
@@ -339,6 +348,15 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     plan = StaticConnectivity(g, spec)  # graph-captured pipeline, replayed per step
+    if rank == 0 and not args.skip_check:
+        # the timed path is the captured plan: check one replay as well
+        plan.run()  # first run captures
+        plab, pst = plan.run()
+        pok = bool(np.array_equal(plab.cpu().numpy().astype(np.int64), ref)) and pst.component_count == comps
+        parity["plan_labels_bit_exact"] = pok
+        if not pok:
+            print(json.dumps({"error": "parity failure on the plan replay", "parity": parity}), file=sys.stderr)
+            sys.exit(3)
 
     def step():
         _, st = plan.run()
@@ -432,11 +450,8 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-                "config": {"workload": f"static CC {SPEC} on RMAT scale-{args.scale} ef{args.edge_factor} "
-                                       f"(avg degree 16) seed {args.seed}",
-                           "spec": SPEC, "n": n, "m_directed": m, "undirected_edges": m // 2,
-                           "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
-                           "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+                "config": bench_config(args.scale, args.edge_factor, args.seed, n, m, ws),
+                "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
                 "e2e": e2e, "gpu_launches": launches, "launches_per_step": launches / args.steps,
                 "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
                 "clocks": clk.summary()}
@@ -463,15 +478,27 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    import numpy as np
+    import math
+
     import oracle
-    n, e = oracle.gen_rmat(args.scale, args.edge_factor, seed=args.seed)
+    # the same workload as our arm at this N (weak scaling: scale 24 + log2 N)
+    scale = args.scale + (int(math.ceil(math.log2(ws))) if ws > 1 else 0)
+    n, e = oracle.gen_rmat(scale, args.edge_factor, seed=args.seed)
     off, tgt = oracle.build_csr(n, e)
     del e
     m = len(tgt)
     threads = oracle.max_threads()
     for _ in range(args.warmup):
-        oracle.static_uf(n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
+        lab, st, _ = oracle.static_uf(n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
+    parity = None
+    if not args.skip_check:
+        # the arm itself is checked: its labels against the sequential
+        # union-find oracle (validate.py:101-122), as our arm's are
+        import numpy as np
+        ref, comps = oracle.components(n, off, tgt)
+        parity = {"labels_bit_exact": bool(np.array_equal(lab, ref)) and st["components"] == comps,
+                  "components": comps, "insp_sample": st["insp_sample"], "insp_finish": st["insp_finish"],
+                  "cov": st["lmax_count"] / n if n else 1.0}
     times = []
     for _ in range(args.steps):
         _, st, tm = oracle.static_uf(n, off, tgt, "kout", 2, "rem_cas", "halve", "splice", threads)
@@ -482,14 +509,15 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
-            "config": {"workload": f"static CC {SPEC} on RMAT scale-{args.scale} ef{args.edge_factor} "
-                                   f"(avg degree 16) seed {args.seed}", "spec": SPEC, "n": n,
-                       "m_directed": m},
+            "config": bench_config(scale, args.edge_factor, args.seed, n, m, ws),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": "the full workload per step: C/OpenMP restatement of connlab "
-                                       "_pipeline (oracle/gconn_oracle.c or_static_uf); the reference "
-                                       "itself is pure Python and takes ~45 s per run at this size"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                                       "_pipeline (oracle/gconn_oracle.c or_pipeline, pinned to the "
+                                       "reference's own labels and statistics by tests/test_oracle.py); "
+                                       "the reference itself is pure Python and takes ~45 s per run "
+                                       "at this size"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "parity": parity}
     print(json.dumps(line))
 
 

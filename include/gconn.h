@@ -173,7 +173,9 @@ int gc_label_finalization(int32_t* labels, int64_t n, void* ws,
 
 /* ---- batch union seam (dset.py:402-416 `union_edge_list`) ----------------
  * Applies the spec's union rule to k edge pairs over parent[n] (in place).
- * aux: 4*n bytes of zeroed scratch for HOOKS / REM_LOCK (else may be NULL). */
+ * aux: 4*n bytes of zeroed scratch for HOOKS / REM_LOCK (else may be NULL).
+ * Endpoints outside [0, n) -> GC_ERR_MALFORMED before any union runs (a
+ * synchronous range check on the stream). */
 int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us,
                    const int32_t* vs, int64_t k, const gc_spec* spec,
                    int32_t* aux, int32_t* fu, int32_t* fv, void* stream);
@@ -281,12 +283,23 @@ int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream,
                    gc_incr** out);
 /* One batch: ops[i] = (us[i], vs[i]) is an insert if is_query[i]==0, else a
  * query.  Insert sub-phase, barrier, query sub-phase (driver.py:695-708);
- * racy != 0 interleaves them (driver.py:674-694).  bits_out receives one
- * byte per op (1 = query answered connected).  Times are accumulated into
- * stats->t_sample_ms (insert) and stats->t_finish_ms (query). */
+ * racy != 0 interleaves them (driver.py:674-694).  bits_out receives one bit
+ * per op packed LSB-first into ceil(len/32) words (bit i%32 of word i/32;
+ * 1 = query answered connected, inserts read 0) — the reference's per-op
+ * result bits (driver.py:658-668), written as one __ballot_sync word per 32
+ * ops.  Times are accumulated into stats->t_sample_ms (insert) and
+ * stats->t_finish_ms (query).
+ * Endpoints must lie in [0, capacity): an op with an endpoint outside it is
+ * skipped on the device (never touching the state) and the call returns
+ * GC_ERR_MALFORMED (for gc_incr_insert_async: the next synchronising call
+ * on the handle does). */
 int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs,
-                  const uint8_t* is_query, int64_t len, uint8_t* bits_out,
+                  const uint8_t* is_query, int64_t len, uint32_t* bits_out,
                   int racy, gc_stats* stats);
+/* Enqueue all later work of the handle on `stream` (ordered after the work
+ * already enqueued on the previous stream).  The Python layer calls it so a
+ * handle always runs on the caller's current stream. */
+int gc_incr_set_stream(gc_incr* h, void* stream);
 /* Columnar insert-only / query-only fast paths (no per-op flag array). */
 int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs,
                    int64_t len, gc_stats* stats);
@@ -300,10 +313,17 @@ int gc_incr_insert_async(gc_incr* h, const int32_t* us, const int32_t* vs, int64
 int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs,
                         int64_t len, int32_t* out_u, int32_t* out_v,
                         unsigned long long* out_count, gc_stats* stats);
+/* Query-only batch; bits_out packed as in gc_incr_batch. */
 int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs,
-                  int64_t len, uint8_t* bits_out, gc_stats* stats);
+                  int64_t len, uint32_t* bits_out, gc_stats* stats);
 /* Copy of the live state with the sentinel convention (driver.py:656,710). */
 int gc_incr_state(gc_incr* h, int32_t* state_out);
+/* The live state itself (driver.py:710-711 hands `on_batch` the live parent
+ * list / label array): after synchronising the handle's stream, *state
+ * receives the device pointer of the state array and *slots its length
+ * (capacity, or capacity + 1 for SV / LT).  Valid until the next call that
+ * mutates the handle; the caller must not write it. */
+int gc_incr_state_view(gc_incr* h, int32_t** state, int64_t* slots);
 /* Final labels (driver.py:715-725); returns the component count of the
  * initialized vertices in *components. */
 int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components);

@@ -115,9 +115,22 @@ def incremental_replay(cap, us, vs, isq, batch):
     return bits[:len(us)].astype(bool), lab[:cap].astype(np.int64)
 
 
-_UNION = {"async": 0, "rem_cas": 4}
+_UNION = {"async": 0, "rem_cas": 4, "sv": 6, "lt": 7}
 _FIND = {"naive": 0, "split": 1, "halve": 2, "compress": 3}
 _SPLICE = {"none": 0, "split": 1, "halve": 2, "splice": 3}
+_SAMPLE = {"none": 0, "kout": 1, "bfs": 3}
+# minbased.py:58-79 LT_VARIANTS: name -> (connect, update, shortcut, alter)
+_LT = {"cusa": (0, 0, 0, 1), "crsa": (0, 1, 0, 1), "pusa": (1, 0, 0, 1), "prsa": (1, 1, 0, 1),
+       "pus": (1, 0, 0, 0), "prs": (1, 1, 0, 0), "eusa": (2, 0, 0, 1), "eus": (2, 0, 0, 0),
+       "cufa": (0, 0, 1, 1), "crfa": (0, 1, 1, 1), "pufa": (1, 0, 1, 1), "prfa": (1, 1, 1, 1),
+       "puf": (1, 0, 1, 0), "prf": (1, 1, 1, 0), "eufa": (2, 0, 1, 1), "euf": (2, 0, 1, 0)}
+
+
+class _OrSpec(C.Structure):
+    _fields_ = [("sample", C.c_int32), ("kout_k", C.c_int32), ("finish", C.c_int32), ("find", C.c_int32),
+                ("splice", C.c_int32), ("lt_connect", C.c_int32), ("lt_update", C.c_int32),
+                ("lt_shortcut", C.c_int32), ("lt_alter", C.c_int32), ("pad", C.c_int32),
+                ("bfs_source", C.c_int64)]
 
 
 def max_threads() -> int:
@@ -126,19 +139,83 @@ def max_threads() -> int:
     return int(h.or_max_threads())
 
 
-def static_uf(n, off, tgt, sample="kout", k=2, union="rem_cas", find="halve", splice="splice",
-              threads=0):
-    """CPU port of the union-find static pipeline (driver.py:454-500) — the
-    bench.py CPU baseline.  Returns (labels int32, stats dict, (t_sample, t_finish, t_finalize))."""
+def parse(text: str) -> dict:
+    """A connlab spec string (driver.py:197-276) for the spec subset the port
+    covers: samplers none / kout / bfs; union-find async / rem_cas with
+    their find and splice rules, sv, and every lt_<variant>."""
+    parts = text.split("+")
+    sample, finish = parts[0], parts[1]
+    d = {"sample": sample, "finish": finish, "find": "naive", "splice": "splice"}
+    if finish == "async":
+        d["find"] = parts[2] if len(parts) > 2 else "naive"
+        d["splice"] = "none"
+    elif finish == "rem_cas":
+        d["find"] = parts[2] if len(parts) > 2 else "naive"
+        d["splice"] = parts[3] if len(parts) > 3 else "splice"
+    elif finish.startswith("lt_"):
+        d["lt"] = finish[3:]
+        d["finish"] = "lt"
+    elif finish != "sv":
+        raise ValueError(f"the C port does not cover finish '{finish}'")
+    if sample not in _SAMPLE:
+        raise ValueError(f"the C port does not cover sampler '{sample}'")
+    return d
+
+
+def pipeline(n, off, tgt, spec: str, threads=0, forest=False, k=2, bfs_source=-1):
+    """CPU port of _pipeline / spanning_forest (driver.py:454-536): returns
+    (labels int32, stats dict, (t_sample, t_finish, t_finalize)[, (fu, fv)])."""
     h = lib()
-    h.or_static_uf.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
-                               C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    h.or_pipeline.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(_OrSpec), C.c_int, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    d = parse(spec)
+    sp = _OrSpec()
+    sp.sample = _SAMPLE[d["sample"]]
+    sp.kout_k = k
+    sp.finish = _UNION[d["finish"]]
+    sp.find = _FIND[d["find"]]
+    sp.splice = _SPLICE[d["splice"]]
+    if d["finish"] == "lt":
+        sp.lt_connect, sp.lt_update, sp.lt_shortcut, sp.lt_alter = _LT[d["lt"]]
+    sp.bfs_source = bfs_source
+    if d["sample"] == "bfs" and bfs_source < 0 and n and len(tgt):
+        raise ValueError("BFS sampling needs the source vertex (driver.bfs_source semantics)")
     off = np.ascontiguousarray(off, dtype=np.int64)
     tgt = np.ascontiguousarray(tgt, dtype=np.int32)
     P = np.empty(max(n, 1), dtype=np.int32)
+    fu = np.empty(max(n, 1), dtype=np.int32) if forest else None
+    fv = np.empty(max(n, 1), dtype=np.int32) if forest else None
     st = np.zeros(8, dtype=np.int64)
     tm = np.zeros(3, dtype=np.float64)
-    h.or_static_uf(n, _p(off), _p(tgt), {"none": 0, "kout": 1}[sample], k, _UNION[union], _FIND[find],
-                   _SPLICE[splice], threads, P.ctypes.data, st.ctypes.data, tm.ctypes.data)
-    return P[:n], {"insp_sample": int(st[0]), "insp_finish": int(st[1]), "l_max": int(st[2]),
-                   "components": int(st[3]), "active": int(st[4])}, tuple(tm.tolist())
+    h.or_pipeline(n, _p(off), _p(tgt), C.byref(sp), threads, P.ctypes.data,
+                  fu.ctypes.data if forest else None, fv.ctypes.data if forest else None,
+                  st.ctypes.data, tm.ctypes.data)
+    stats = {"insp_sample": int(st[0]), "insp_finish": int(st[1]), "l_max": int(st[2]),
+             "components": int(st[3]), "active": int(st[4]), "lmax_count": int(st[5]),
+             "rounds": int(st[6]), "bfs_levels": int(st[7])}
+    out = (P[:n], stats, tuple(tm.tolist()))
+    if forest:
+        out = out + ((fu[:n], fv[:n]),)
+    return out
+
+
+def static_uf(n, off, tgt, sample="kout", k=2, union="rem_cas", find="halve", splice="splice",
+              threads=0):
+    """The union-find static pipeline (the bench.py reference arm): returns
+    (labels int32, stats dict, (t_sample, t_finish, t_finalize))."""
+    text = f"{sample}+{union}+{find}" + (f"+{splice}" if union == "rem_cas" else "")
+    return pipeline(n, off, tgt, text, threads, k=k)
+
+
+def incr_insert(cap, P, us, vs, union="async", find="halve", splice="none", threads=0) -> float:
+    """One insert-only batch (driver.py:620-649) into the parent array P
+    (cap slots, sentinel cap); returns the seconds it took."""
+    h = lib()
+    h.or_incr_insert.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                 C.c_int, C.c_int, C.c_void_p]
+    us = np.ascontiguousarray(us, dtype=np.int32)
+    vs = np.ascontiguousarray(vs, dtype=np.int32)
+    sec = C.c_double(0)
+    h.or_incr_insert(cap, P.ctypes.data, _p(us), _p(vs), len(us), _UNION[union], _FIND[find], _SPLICE[splice],
+                     threads, C.byref(sec))
+    return sec.value

@@ -242,19 +242,32 @@ void or_incremental_replay(int64_t cap, const int32_t* us, const int32_t* vs, co
 }
 
 /* ===================================================================== *
- * Static pipeline port (the CPU baseline arm of bench.py).               *
- * driver.py:454-500 `_pipeline` for union-find finishes with the none /  *
- * k-out (FIRST_K) samplers, over the dset.py union / find / splice menu, *
+ * Pipeline port (the CPU baseline arm of bench.py / bench_configs.py).   *
+ * driver.py:454-536 `_pipeline` / `spanning_forest` and driver.py:567-   *
+ * 725 `incremental` restated over the dset.py union / find / splice      *
+ * menu, the samplers of sampling.py (none / k-out FIRST_K / BFS) and the *
+ * Jacobi round finishes of minbased.py (SV, the Liu-Tarjan family),      *
  * multi-threaded with OpenMP; CAS = __atomic compare-exchange (the       *
- * reference's striped-lock CAS, parallel.py:17-36).                      *
+ * reference's striped-lock CAS, parallel.py:17-36), np.minimum.at = an   *
+ * atomic-min loop.  Every phase reads the snapshot the reference reads   *
+ * (e.g. the active set is taken before the finish starts linking,        *
+ * driver.py:473), so counters and labels are deterministic.              *
  * ===================================================================== */
-enum { OR_ASYNC = 0, OR_REM_CAS = 4 };
+enum { OR_ASYNC = 0, OR_REM_CAS = 4, OR_SV = 6, OR_LT = 7 };
 enum { OR_NAIVE = 0, OR_SPLIT = 1, OR_HALVE = 2, OR_COMPRESS = 3 };
 enum { OR_SPLIT_ONE = 1, OR_HALVE_ONE = 2, OR_SPLICE = 3 };
+enum { OR_S_NONE = 0, OR_S_KOUT = 1, OR_S_BFS = 3 };
 
 static inline int32_t ld(int32_t* p) { return __atomic_load_n(p, __ATOMIC_RELAXED); }
+static inline void st(int32_t* p, int32_t v) { __atomic_store_n(p, v, __ATOMIC_RELAXED); }
 static inline int casw(int32_t* p, int32_t e, int32_t d) {
   return __atomic_compare_exchange_n(p, &e, d, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED);
+}
+/* np.minimum.at (minbased.py) as an atomic min */
+static inline void amin(int32_t* p, int32_t v) {
+  int32_t cur = ld(p);
+  while (v < cur && !__atomic_compare_exchange_n(p, &cur, v, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+  }
 }
 
 /* dset.py:109-147 */
@@ -280,25 +293,32 @@ static int32_t or_find(int find, int32_t u, int32_t* P) {
   return v;
 }
 
+/* forest slot r <- (u, v) when root r is hooked (dset.py:391-393) */
+static inline void rec(int32_t* fu, int32_t* fv, int32_t r, int32_t u, int32_t v) {
+  if (fu) { fu[r] = u; fv[r] = v; }
+}
+
 /* dset.py:222-234 */
-static void or_union_async(int find, int32_t u, int32_t v, int32_t* P) {
+static void or_union_async(int find, int32_t u, int32_t v, int32_t* P, int32_t* fu, int32_t* fv) {
   int32_t pu = or_find(find, u, P), pv = or_find(find, v, P);
   while (pu != pv) {
     if (pu < pv) { int32_t t = pu; pu = pv; pv = t; }
-    if (ld(P + pu) == pu && casw(P + pu, pu, pv)) return;
+    if (ld(P + pu) == pu && casw(P + pu, pu, pv)) { rec(fu, fv, pu, u, v); return; }
     pu = or_find(find, u, P);
     pv = or_find(find, v, P);
   }
 }
 
 /* dset.py:303-316 with the splices of dset.py:180-207 */
-static void or_union_rem(int find, int splice, int32_t u, int32_t v, int32_t* P) {
+static void or_union_rem(int find, int splice, int32_t u, int32_t v, int32_t* P, int32_t* fu,
+                         int32_t* fv) {
   int32_t ru = u, rv = v;
   for (;;) {
     int32_t pru = ld(P + ru), prv = ld(P + rv);
     if (pru == prv) return;
     if (pru < prv) { int32_t t = ru; ru = rv; rv = t; t = pru; pru = prv; prv = t; }
     if (ru == pru && casw(P + ru, ru, prv)) {
+      rec(fu, fv, ru, u, v);
       if (find != OR_NAIVE) { or_find(find, u, P); or_find(find, v, P); }
       return;
     }
@@ -313,9 +333,10 @@ static void or_union_rem(int find, int splice, int32_t u, int32_t v, int32_t* P)
   }
 }
 
-static inline void or_unite(int uni, int find, int splice, int32_t u, int32_t v, int32_t* P) {
-  if (uni == OR_REM_CAS) or_union_rem(find, splice, u, v, P);
-  else or_union_async(find, u, v, P);
+static inline void or_unite(int uni, int find, int splice, int32_t u, int32_t v, int32_t* P,
+                            int32_t* fu, int32_t* fv) {
+  if (uni == OR_REM_CAS) or_union_rem(find, splice, u, v, P, fu, fv);
+  else or_union_async(find, u, v, P, fu, fv);
 }
 
 static double wall(void) {
@@ -326,56 +347,316 @@ static double wall(void) {
 #endif
 }
 
-/* stats[0] insp_sample, [1] insp_finish, [2] l_max, [3] components,
- * [4] active vertices; times[0..2] sample / finish / finalize seconds. */
-int or_static_uf(int64_t n, const int64_t* off, const int32_t* tgt, int sample, int k, int uni,
-                 int find, int splice, int threads, int32_t* P, int64_t* stats, double* times) {
-  if (threads > 0) {
-#ifdef _OPENMP
-    omp_set_num_threads(threads);
-#endif
+/* full pointer jump to the fixpoint (sampling.py:38-47 compress_all,
+ * minbased.py:87-92 _full_shortcut): order-free, every value is an ancestor */
+static void full_shortcut(int32_t* L, int64_t n) {
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) {
+    int32_t r = ld(L + v);
+    while (ld(L + r) != r) r = ld(L + r);
+    st(L + v, r);
   }
-  int64_t insp_s = 0, insp_f = 0;
+}
+
+/* most_frequent_label (sampling.py:29-35): exact histogram, ties low */
+static int32_t mode_label(const int32_t* L, int64_t n, int64_t* count) {
+  int32_t* cnt = calloc((size_t)(n ? n : 1), sizeof(int32_t));
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) __atomic_fetch_add(cnt + L[v], 1, __ATOMIC_RELAXED);
+  int64_t best = -1;
+  int32_t lmax = 0;
+  for (int64_t v = 0; v < n; ++v)
+    if (cnt[v] > best) { best = cnt[v]; lmax = (int32_t)v; }
+  free(cnt);
+  *count = n ? best : 0;
+  return lmax;
+}
+
+/* ------------------------------------------------------------ BFS sample
+ * sampling.py:120-172: level-synchronous BFS from `s`; a vertex reached at a
+ * level takes as parent its smallest frontier neighbour (the reference's
+ * frontier is ascending and the first discoverer wins); the reached set takes
+ * the minimum id.  Forest: the discovery tree re-rooted at that minimum.
+ * Returns the inspections (sum of frontier degrees per level). */
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+static int64_t or_bfs(int64_t n, const int64_t* off, const int32_t* tgt, int64_t s, int32_t* labels,
+                      int32_t* fu, int32_t* fv, int64_t* levels_out) {
+  int32_t* parent = malloc(sizeof(int32_t) * (size_t)n);
+  uint8_t* seen = calloc((size_t)n, 1);
+  int32_t* front = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* next = malloc(sizeof(int32_t) * (size_t)n);
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v) parent[v] = INT32_MAX;
+  int64_t nf = 1, insp = 0, levels = 0, mn = s;
+  front[0] = (int32_t)s;
+  seen[s] = 1;
+  parent[s] = -1;
+  while (nf) {
+    int64_t tot = 0, nn = 0;
+    /* claim: parent[t] = min frontier neighbour among this level's finders */
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : tot)
+    for (int64_t i = 0; i < nf; ++i) {
+      const int32_t u = front[i];
+      tot += off[u + 1] - off[u];
+      for (int64_t j = off[u]; j < off[u + 1]; ++j) {
+        const int32_t t = tgt[j];
+        if (__atomic_load_n(seen + t, __ATOMIC_RELAXED)) continue;
+        int32_t cur = ld(parent + t);
+        if (cur == INT32_MAX && casw(parent + t, INT32_MAX, u)) {
+          int64_t slot = __atomic_fetch_add(&nn, 1, __ATOMIC_RELAXED);
+          next[slot] = t;
+        } else {
+          amin(parent + t, u);
+        }
+      }
+    }
+    insp += tot;
+    if (tot == 0) break;
+    /* the next frontier in ascending id order, marked seen */
+    qsort(next, (size_t)nn, sizeof(int32_t), cmp_i32);
+#pragma omp parallel for schedule(static) reduction(min : mn)
+    for (int64_t i = 0; i < nn; ++i) {
+      seen[next[i]] = 1;
+      if (next[i] < mn) mn = next[i];
+    }
+    int32_t* t = front; front = next; next = t;
+    nf = nn;
+    ++levels;
+  }
+  /* labels: the reached set takes its minimum (sampling.py:158-160) */
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; ++v)
+    if (seen[v]) labels[v] = (int32_t)mn;
+  if (fu) {
+    /* re-root at the minimum (sampling.py:161-171) */
+    int32_t cur = (int32_t)mn, prev = -1;
+    while (cur != -1) {
+      int32_t nx = parent[cur];
+      parent[cur] = prev;
+      prev = cur;
+      cur = nx;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n; ++r)
+      if (seen[r] && r != mn) { fu[r] = parent[r]; fv[r] = (int32_t)r; }
+  }
+  free(parent); free(seen); free(front); free(next);
+  if (levels_out) *levels_out = levels;
+  return insp;
+}
+
+/* ------------------------------------------------------ round finishes
+ * minbased.py:124-155 shiloach_vishkin and :163-243 liu_tarjan (Jacobi
+ * rounds over the gathered COO of the active vertices).  Returns rounds;
+ * *insp += the working-edge count charged per round. */
+typedef struct { int32_t* u; int32_t* v; int64_t len; } coo_t;
+
+static coo_t gather_coo(const int64_t* off, const int32_t* tgt, const int32_t* act, int64_t na) {
+  /* driver.py:325-330 _gather_edges: all directed edges of the active rows */
+  int64_t* pos = malloc(sizeof(int64_t) * (size_t)(na + 1));
+  pos[0] = 0;
+  for (int64_t i = 0; i < na; ++i) pos[i + 1] = pos[i] + (off[act[i] + 1] - off[act[i]]);
+  coo_t c;
+  c.len = pos[na];
+  c.u = malloc(sizeof(int32_t) * (size_t)(c.len ? c.len : 1));
+  c.v = malloc(sizeof(int32_t) * (size_t)(c.len ? c.len : 1));
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < na; ++i) {
+    const int32_t u = act[i];
+    int64_t p = pos[i];
+    for (int64_t j = off[u]; j < off[u + 1]; ++j, ++p) { c.u[p] = u; c.v[p] = tgt[j]; }
+  }
+  free(pos);
+  return c;
+}
+
+static int64_t or_sv(int64_t n, coo_t c, int32_t* L, int64_t* insp) {
+  int32_t* prev = malloc(sizeof(int32_t) * (size_t)n);
+  memcpy(prev, L, sizeof(int32_t) * (size_t)n);
+  int64_t rounds = 0;
+  for (;;) {
+    ++rounds;
+    *insp += c.len;
+    int changed = 0;
+#pragma omp parallel for schedule(static) reduction(| : changed)
+    for (int64_t e = 0; e < c.len; ++e) {
+      const int32_t pu = prev[c.u[e]], pv = prev[c.v[e]];
+      /* labels[eu] / labels[ev] are read before any write of the round: the
+       * snapshot prev equals labels at the round start */
+      const int32_t lo = pu < pv ? pu : pv, hi = pu < pv ? pv : pu;
+      if (lo != hi && prev[hi] == hi) { amin(L + hi, lo); changed = 1; }
+    }
+    full_shortcut(L, n);
+    memcpy(prev, L, sizeof(int32_t) * (size_t)n);
+    if (!changed) break;
+  }
+  free(prev);
+  return rounds;
+}
+
+static int64_t or_lt(int64_t n, coo_t c, int32_t* L, int connect, int update, int shortcut, int alter,
+                     int64_t* insp) {
+  /* working edges start mapped through the labels (minbased.py:176-177) */
+  int64_t w = c.len;
+  int32_t* wu = malloc(sizeof(int32_t) * (size_t)(w ? w : 1));
+  int32_t* wv = malloc(sizeof(int32_t) * (size_t)(w ? w : 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < w; ++e) { wu[e] = L[c.u[e]]; wv[e] = L[c.v[e]]; }
+  int32_t* xu = alter ? malloc(sizeof(int32_t) * (size_t)(w ? w : 1)) : NULL;
+  int32_t* xv = alter ? malloc(sizeof(int32_t) * (size_t)(w ? w : 1)) : NULL;
+  int32_t* start = malloc(sizeof(int32_t) * (size_t)n);
+  int32_t* msg = malloc(sizeof(int32_t) * (size_t)n);
+  int nt = 1;
+#ifdef _OPENMP
+  nt = omp_get_max_threads();
+#endif
+  int64_t* cnt = malloc(sizeof(int64_t) * (size_t)(nt + 1));
+  int64_t rounds = 0;
+  for (;;) {
+    ++rounds;
+    *insp += w;
+    memcpy(start, L, sizeof(int32_t) * (size_t)n);
+    memcpy(msg, L, sizeof(int32_t) * (size_t)n);
+    /* connect (minbased.py:188-208) */
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < w; ++e) {
+      const int32_t a = wu[e], b = wv[e];
+      if (connect == 0) { amin(msg + a, b); amin(msg + b, a); }
+      else {
+        const int32_t pa = start[a], pb = start[b];
+        amin(msg + pa, pb); amin(msg + pb, pa);
+        if (connect == 2) { amin(msg + a, pb); amin(msg + b, pa); }
+      }
+    }
+    /* update (minbased.py:213-219) */
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v)
+      if (update == 0 || start[v] == v) L[v] = msg[v];
+    /* shortcut (minbased.py:227-230) */
+    if (shortcut) full_shortcut(L, n);
+    else {
+      memcpy(msg, L, sizeof(int32_t) * (size_t)n);
+#pragma omp parallel for schedule(static)
+      for (int64_t v = 0; v < n; ++v) L[v] = msg[msg[v]];
+    }
+    /* alter (minbased.py:233-239): rewrite, drop closed edges, keeping
+     * the order (a per-thread count, a prefix, then each thread copies its
+     * kept entries into the spare buffers) */
+    if (alter) {
+#pragma omp parallel
+      {
+        int t = 0, T = 1;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+        T = omp_get_num_threads();
+#endif
+        const int64_t lo = w * t / T, hi = w * (t + 1) / T;
+        int64_t k = 0;
+        for (int64_t e = lo; e < hi; ++e) {
+          wu[e] = L[wu[e]];
+          wv[e] = L[wv[e]];
+          k += wu[e] != wv[e];
+        }
+        cnt[t + 1] = k;
+#pragma omp barrier
+#pragma omp single
+        {
+          cnt[0] = 0;
+          for (int i = 1; i <= T; ++i) cnt[i] += cnt[i - 1];
+        }
+        int64_t p = cnt[t];
+        for (int64_t e = lo; e < hi; ++e)
+          if (wu[e] != wv[e]) { xu[p] = wu[e]; xv[p] = wv[e]; ++p; }
+#pragma omp single
+        w = cnt[T];
+      }
+      int32_t* tu = wu; wu = xu; xu = tu;
+      int32_t* tv = wv; wv = xv; xv = tv;
+    }
+    int same = 1;
+#pragma omp parallel for schedule(static) reduction(& : same)
+    for (int64_t v = 0; v < n; ++v) same &= L[v] == start[v];
+    if (same) break;
+  }
+  free(wu); free(wv); free(xu); free(xv); free(start); free(msg); free(cnt);
+  return rounds;
+}
+
+/* ----------------------------------------------------------- pipeline
+ * stats: [0] insp_sample [1] insp_finish [2] l_max [3] components
+ *        [4] active vertices [5] l_max count [6] rounds [7] BFS levels
+ * times: sample / finish / finalize seconds.  fu/fv (nullable): forest
+ * slots (-1 = empty), union-find and BFS recording (driver.py:523-536). */
+typedef struct {
+  int32_t sample, kout_k, finish, find, splice, lt_connect, lt_update, lt_shortcut, lt_alter;
+  int32_t pad;
+  int64_t bfs_source;
+} or_spec;
+
+int or_pipeline(int64_t n, const int64_t* off, const int32_t* tgt, const or_spec* sp, int threads,
+                int32_t* P, int32_t* fu, int32_t* fv, int64_t* stats, double* times) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#endif
+  const int uf = sp->finish == OR_ASYNC || sp->finish == OR_REM_CAS;
+  int64_t insp_s = 0, insp_f = 0, rounds = 0, levels = 0, lmax_count = n ? 1 : 0; /* identity labels */
+  if (fu) {
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v) { fu[v] = -1; fv[v] = -1; }
+  }
   double t0 = wall();
-  /* DisjointSets.__init__ (dset.py:359) */
+  /* DisjointSets.__init__ (dset.py:359) / identity labels */
 #pragma omp parallel for schedule(static)
   for (int64_t v = 0; v < n; ++v) P[v] = (int32_t)v;
   int32_t lmax = (int32_t)n;
-  if (sample == 1) {
-    /* kout_sample FIRST_K (sampling.py:61-86) */
+  if (sp->sample == OR_S_KOUT) {
+    /* kout_sample FIRST_K (sampling.py:61-86) on the finish's own rule, or
+     * the async + halve fallback for round finishes (driver.py:96) */
+    const int su = uf ? sp->finish : OR_ASYNC, sf = uf ? sp->find : OR_HALVE, ss = uf ? sp->splice : 0;
+    const int64_t k = sp->kout_k;
 #pragma omp parallel for schedule(dynamic, 4096) reduction(+ : insp_s)
     for (int64_t v = 0; v < n; ++v) {
       int64_t b = off[v], d = off[v + 1] - b, take = d < k ? d : k;
       insp_s += take;
-      for (int64_t j = 0; j < take; ++j) or_unite(uni, find, splice, (int32_t)v, tgt[b + j], P);
+      for (int64_t j = 0; j < take; ++j) or_unite(su, sf, ss, (int32_t)v, tgt[b + j], P, fu, fv);
     }
-    /* compress_all (sampling.py:38-47) */
-#pragma omp parallel for schedule(static)
-    for (int64_t v = 0; v < n; ++v) {
-      int32_t r = P[v];
-      while (P[r] != r) r = P[r];
-      P[v] = r;
-    }
-    /* most_frequent_label (sampling.py:29-35): exact histogram, ties low */
-    int32_t* cnt = calloc((size_t)(n ? n : 1), sizeof(int32_t));
-#pragma omp parallel for schedule(static)
-    for (int64_t v = 0; v < n; ++v) __atomic_fetch_add(cnt + P[v], 1, __ATOMIC_RELAXED);
-    int64_t best = -1;
-    lmax = 0;
-    for (int64_t v = 0; v < n; ++v)
-      if (cnt[v] > best) { best = cnt[v]; lmax = (int32_t)v; }
-    free(cnt);
+    full_shortcut(P, n);
+    lmax = mode_label(P, n, &lmax_count);
+  } else if (sp->sample == OR_S_BFS) {
+    if (n && off[n]) insp_s = or_bfs(n, off, tgt, sp->bfs_source, P, fu, fv, &levels);
+    lmax = mode_label(P, n, &lmax_count);
   }
   double t1 = wall();
-  /* _union_finish over the active vertices (driver.py:333-348, :473) */
-  int64_t active = 0;
-#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : insp_f, active)
-  for (int64_t u = 0; u < n; ++u) {
-    if (P[u] == lmax) continue;
-    ++active;
-    insp_f += off[u + 1] - off[u];
-    for (int64_t j = off[u]; j < off[u + 1]; ++j) or_unite(uni, find, splice, (int32_t)u, tgt[j], P);
+  /* the active set, snapshotted before the finish links anything
+   * (driver.py:473 np.flatnonzero(post_sample != l_max)) */
+  int32_t* act = malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int64_t na = 0;
+  for (int64_t u = 0; u < n; ++u)
+    if (P[u] != lmax) act[na++] = (int32_t)u;
+  if (uf) {
+    /* _union_finish (driver.py:333-348) */
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : insp_f)
+    for (int64_t i = 0; i < na; ++i) {
+      const int32_t u = act[i];
+      insp_f += off[u + 1] - off[u];
+      for (int64_t j = off[u]; j < off[u + 1]; ++j)
+        or_unite(sp->finish, sp->find, sp->splice, u, tgt[j], P, fu, fv);
+    }
+  } else if (na) {
+    /* _rounds_finish (driver.py:351-375, skipped when nothing is active,
+     * driver.py:475): gather once (charged once), then the rounds charge
+     * their working set per round */
+    coo_t c = gather_coo(off, tgt, act, na);
+    insp_f += c.len;
+    if (sp->finish == OR_SV) rounds = or_sv(n, c, P, &insp_f);
+    else rounds = or_lt(n, c, P, sp->lt_connect, sp->lt_update, sp->lt_shortcut, sp->lt_alter, &insp_f);
+    free(c.u); free(c.v);
   }
+  free(act);
   double t2 = wall();
   /* label_finalization (driver.py:420-429): roots are component minima */
   int64_t comps = 0;
@@ -387,8 +668,44 @@ int or_static_uf(int64_t n, const int64_t* off, const int32_t* tgt, int sample, 
     comps += r == v;
   }
   double t3 = wall();
-  stats[0] = insp_s; stats[1] = insp_f; stats[2] = lmax; stats[3] = comps; stats[4] = active;
+  stats[0] = insp_s; stats[1] = insp_f; stats[2] = lmax; stats[3] = comps; stats[4] = na;
+  stats[5] = lmax_count; stats[6] = rounds; stats[7] = levels;
   times[0] = t1 - t0; times[1] = t2 - t1; times[2] = t3 - t2;
+  return 0;
+}
+
+/* the union-find static pipeline (bench.py reference arm) */
+int or_static_uf(int64_t n, const int64_t* off, const int32_t* tgt, int sample, int k, int uni,
+                 int find, int splice, int threads, int32_t* P, int64_t* stats, double* times) {
+  or_spec sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.sample = sample;
+  sp.kout_k = k;
+  sp.finish = uni;
+  sp.find = find;
+  sp.splice = splice;
+  return or_pipeline(n, off, tgt, &sp, threads, P, NULL, NULL, stats, times);
+}
+
+/* ------------------------------------------------------ incremental
+ * One insert-only batch (driver.py:620-649): ensure_init by CAS(sentinel ->
+ * v) for both endpoints, then the union rule, all pairs in parallel.  P has
+ * cap slots with the sentinel `cap` for uninitialised ones. */
+int or_incr_insert(int64_t cap, int32_t* P, const int32_t* us, const int32_t* vs, int64_t len, int uni,
+                   int find, int splice, int threads, double* seconds) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#endif
+  const int32_t sentinel = (int32_t)cap;
+  double t0 = wall();
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < len; ++i) {
+    const int32_t u = us[i], v = vs[i];
+    casw(P + u, sentinel, u);
+    casw(P + v, sentinel, v);
+    or_unite(uni, find, splice, u, v, P, NULL, NULL);
+  }
+  *seconds = wall() - t0;
   return 0;
 }
 

@@ -76,6 +76,8 @@ _SIGNATURES = {
     "gc_incr_insert": (C.c_int, [_VP, _VP, _VP, _I64, C.POINTER(Stats)]),
     "gc_incr_query": (C.c_int, [_VP, _VP, _VP, _I64, _VP, C.POINTER(Stats)]),
     "gc_incr_state": (C.c_int, [_VP, _VP]),
+    "gc_incr_state_view": (C.c_int, [_VP, C.POINTER(_VP), C.POINTER(_I64)]),
+    "gc_incr_set_stream": (C.c_int, [_VP, _VP]),
     "gc_incr_labels": (C.c_int, [_VP, _VP, C.POINTER(_I64)]),
     "gc_incr_capacity": (_I64, [_VP]),
     "gc_incr_reserve": (C.c_int, [_VP, _I64]),

@@ -22,6 +22,7 @@ struct gc_incr {
   int32_t* state = nullptr;   // cap (UF) or cap+1 (rounds) entries
   int32_t* aux = nullptr;     // hooks / locks
   unsigned long long* ctr = nullptr;
+  unsigned int* bad = nullptr;  // sticky device flag: an op had an endpoint outside [0, cap)
   // rounds scratch
   gc::RoundsWs rw;
   int64_t coo_cap = 0;
@@ -34,22 +35,35 @@ namespace {
 
 constexpr int kIB = 256;
 
+// Read-only root chase of every query (driver.py:556-564, 658-668); a warp
+// owns 32 consecutive ops and writes their bits as one packed word
+// (__ballot_sync, LSB = lowest op index).  Inserts of a mixed batch (isq[i]
+// == 0) read as 0.
 __global__ void k_incr_query(const int32_t* P, const int32_t* us, const int32_t* vs,
-                             const uint8_t* isq, int64_t len, int32_t sentinel, uint8_t* bits) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
-    if (isq && !isq[i]) {
-      bits[i] = 0;
-      continue;
+                             const uint8_t* isq, int64_t len, int32_t sentinel, uint32_t* bits,
+                             unsigned int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (len + 31) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < words; w += nwarps) {
+    const int64_t i = (w << 5) + lane;
+    bool hit = false;
+    if (i < len && (!isq || isq[i])) {
+      int32_t x = us[i], y = vs[i];
+      if (uint32_t(x) >= uint32_t(sentinel) || uint32_t(y) >= uint32_t(sentinel)) {
+        atomicOr(bad, 1u);
+      } else {
+        int32_t px = P[x];
+        if (px != sentinel)
+          while (px != x) { x = px; px = P[x]; }
+        int32_t py = P[y];
+        if (py != sentinel)
+          while (py != y) { y = py; py = P[y]; }
+        hit = x == y;
+      }
     }
-    int32_t x = us[i], y = vs[i];
-    int32_t px = P[x];
-    if (px != sentinel)
-      while (px != x) { x = px; px = P[x]; }
-    int32_t py = P[y];
-    if (py != sentinel)
-      while (py != y) { y = py; py = P[y]; }
-    bits[i] = x == y;
+    const uint32_t word = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) bits[w] = word;
   }
 }
 
@@ -97,7 +111,7 @@ __global__ void k_label_init(int32_t* L, const int32_t* us, const int32_t* vs, c
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
     if (isq && isq[i]) continue;
-    const int32_t u = us[i], v = vs[i];
+    const int32_t u = us[i], v = vs[i];  // range-checked before the launch
     if (L[u] == sentinel) L[u] = u;
     if (L[v] == sentinel) L[v] = v;
   }
@@ -168,7 +182,25 @@ CooUnionArgs uf_args(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t l
   a.vs = vs;
   a.k = len;
   a.skip = skip;
+  a.bad = h->bad;
   return a;
+}
+
+// The sticky input flag: kernels skip ops with an endpoint outside
+// [0, cap) and set h->bad; every synchronising entry point reads it with its
+// own completion sync (fetch before, raise after) and reports
+// GC_ERR_MALFORMED once, then clears it.
+unsigned int* bad_word() { return reinterpret_cast<unsigned int*>(pinned_words() + 32); }
+void fetch_bad(gc_incr* h) {
+  GC_CUDA(cudaMemcpyAsync(bad_word(), h->bad, 4, cudaMemcpyDeviceToHost, h->st));
+}
+void raise_bad(gc_incr* h) {
+  unsigned int* w = bad_word();
+  if (*w) {
+    *w = 0;
+    GC_CUDA(cudaMemsetAsync(h->bad, 0, 4, h->st));
+    throw Error(GC_ERR_MALFORMED, "an op endpoint lies outside [0, capacity) (op skipped)");
+  }
 }
 
 // insert sub-phase; returns added inspections (driver.py:627-649)
@@ -185,6 +217,9 @@ void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     if (stats) stats->insp_finish += n_ins;
     return;
   }
+  // the label-array kernels index with the endpoints directly
+  check_ids(us, len, h->cap, st, "op endpoint");
+  check_ids(vs, len, h->cap, st, "op endpoint");
   ensure_coo(h, len);
   (k_label_init<<<g1(len), kIB, 0, st>>>(h->state, us, vs, isq, len, sentinel), ::gc::count_launch());
   unsigned long long* cnt = h->ctr + C_SCRATCH0;
@@ -248,7 +283,9 @@ int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream, gc_incr*
       const int64_t slots = uf ? capacity : capacity + 1;
       GC_CUDA(cudaMalloc(&h->state, (slots > 0 ? slots : 1) * 4));
       GC_CUDA(cudaMalloc(&h->ctr, sizeof(unsigned long long) * C_COUNT_));
+      GC_CUDA(cudaMalloc(&h->bad, 16));
       GC_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long) * C_COUNT_, h->st));
+      GC_CUDA(cudaMemsetAsync(h->bad, 0, 16, h->st));
       fill(h->state, slots, int32_t(capacity), h->st);  // every slot = sentinel
       if (spec->finish == GC_FINISH_HOOKS || spec->finish == GC_FINISH_REM_LOCK) {
         GC_CUDA(cudaMalloc(&h->aux, (capacity > 0 ? capacity : 1) * 4));
@@ -273,6 +310,7 @@ void gc_incr_destroy(gc_incr* h) {
   cudaFree(h->state);
   cudaFree(h->aux);
   cudaFree(h->ctr);
+  cudaFree(h->bad);
   cudaFree(h->rw.a);
   cudaFree(h->rw.b);
   for (Coo* c : {&h->rw.work, &h->rw.spare}) {
@@ -289,6 +327,19 @@ void gc_incr_destroy(gc_incr* h) {
 
 int64_t gc_incr_capacity(gc_incr* h) { return h ? h->cap : -1; }
 
+int gc_incr_set_stream(gc_incr* h, void* stream) {
+  return guarded([&] {
+    require(h != nullptr, GC_ERR_ARG, "null handle");
+    cudaStream_t ns = static_cast<cudaStream_t>(stream);
+    if (ns == h->st) return;
+    // everything enqueued on the old stream happens before later work on
+    // the new one
+    GC_CUDA(cudaEventRecord(h->ev[3], h->st));
+    GC_CUDA(cudaStreamWaitEvent(ns, h->ev[3], 0));
+    h->st = ns;
+  });
+}
+
 int gc_incr_reserve(gc_incr* h, int64_t batch_len) {
   return guarded([&] {
     require(h != nullptr && batch_len >= 0, GC_ERR_ARG, "bad reserve");
@@ -297,7 +348,7 @@ int gc_incr_reserve(gc_incr* h, int64_t batch_len) {
 }
 
 int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* is_query,
-                  int64_t len, uint8_t* bits_out, int racy, gc_stats* stats) {
+                  int64_t len, uint32_t* bits_out, int racy, gc_stats* stats) {
   return guarded([&] {
     require(h && len >= 0, GC_ERR_ARG, "bad arguments");
     if (len == 0) return;
@@ -313,7 +364,9 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
       launch_incr_racy(UFConfig{h->spec.finish, h->spec.find, h->spec.splice},
                        uf_args(h, us, vs, len, nullptr), is_query, sentinel, bits_out, st);
       GC_CUDA(cudaEventRecord(h->ev[1], st));
-      GC_CUDA(cudaEventSynchronize(h->ev[1]));
+      fetch_bad(h);
+      GC_CUDA(cudaStreamSynchronize(st));
+      raise_bad(h);
       if (stats) {
         stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
         stats->insp_finish += n_ins;
@@ -324,10 +377,13 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     GC_CUDA(cudaEventRecord(h->ev[0], st));
     if (n_ins) insert_phase(h, us, vs, is_query, len, n_ins, stats);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
-    (k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out), ::gc::count_launch());
+    (k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out, h->bad),
+     ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[2], st));
-    GC_CUDA(cudaEventSynchronize(h->ev[2]));
+    fetch_bad(h);
+    GC_CUDA(cudaStreamSynchronize(st));
+    raise_bad(h);
     if (stats) {
       stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
       stats->t_finish_ms += elapsed(h->ev[1], h->ev[2]);
@@ -339,10 +395,13 @@ int gc_incr_insert(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len
   return guarded([&] {
     require(h && len >= 0, GC_ERR_ARG, "bad arguments");
     if (len == 0) return;
+    require(us && vs, GC_ERR_ARG, "null batch arrays");
     GC_CUDA(cudaEventRecord(h->ev[0], h->st));
     insert_phase(h, us, vs, nullptr, len, len, stats);
     GC_CUDA(cudaEventRecord(h->ev[1], h->st));
-    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    fetch_bad(h);
+    GC_CUDA(cudaStreamSynchronize(h->st));
+    raise_bad(h);
     if (stats) stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
   });
 }
@@ -351,16 +410,20 @@ int gc_incr_insert_async(gc_incr* h, const int32_t* us, const int32_t* vs, int64
   return guarded([&] {
     require(h && len >= 0, GC_ERR_ARG, "bad arguments");
     if (len == 0) return;
+    require(us && vs, GC_ERR_ARG, "null batch arrays");
     if (!h->uf) {  // the round finishes synchronise inside every batch anyway
       GC_CUDA(cudaEventRecord(h->ev[0], h->st));
       insert_phase(h, us, vs, nullptr, len, len, stats);
       GC_CUDA(cudaEventRecord(h->ev[1], h->st));
-      GC_CUDA(cudaEventSynchronize(h->ev[1]));
+      fetch_bad(h);
+      GC_CUDA(cudaStreamSynchronize(h->st));
+      raise_bad(h);
       if (stats) stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
       return;
     }
     // union-find inserts: enqueue and return (the stream orders batches;
-    // queries, labels and the state copy synchronise); no per-batch timing
+    // queries, labels and the state copy synchronise and report a malformed
+    // endpoint seen by any earlier batch); no per-batch timing
     insert_phase(h, us, vs, nullptr, len, len, stats);
   });
 }
@@ -372,6 +435,7 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
     require(h->uf && h->spec.splice != GC_SPLICE_ATOMIC, GC_ERR_CONFIG,
             "recording merging edges needs a root-based union-find rule");
     if (len == 0) return;
+    require(us && vs, GC_ERR_ARG, "null batch arrays");
     cudaStream_t st = h->st;
     GC_CUDA(cudaEventRecord(h->ev[0], st));
     CooUnionArgs a = uf_args(h, us, vs, len, nullptr);
@@ -381,7 +445,9 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
     a.lcount = out_count;
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
-    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    fetch_bad(h);
+    GC_CUDA(cudaStreamSynchronize(st));
+    raise_bad(h);
     if (stats) {
       stats->t_sample_ms += elapsed(h->ev[0], h->ev[1]);
       stats->insp_finish += len;
@@ -389,17 +455,20 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
   });
 }
 
-int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, uint8_t* bits_out,
+int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len, uint32_t* bits_out,
                   gc_stats* stats) {
   return guarded([&] {
     require(h && len >= 0, GC_ERR_ARG, "bad arguments");
     if (len == 0) return;
+    require(us && vs && bits_out, GC_ERR_ARG, "null batch arrays");
     GC_CUDA(cudaEventRecord(h->ev[0], h->st));
-    (k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap),
-                                             bits_out), ::gc::count_launch());
+    (k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap), bits_out,
+                                             h->bad), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[1], h->st));
-    GC_CUDA(cudaEventSynchronize(h->ev[1]));
+    fetch_bad(h);
+    GC_CUDA(cudaStreamSynchronize(h->st));
+    raise_bad(h);
     if (stats) stats->t_finish_ms += elapsed(h->ev[0], h->ev[1]);
   });
 }
@@ -410,7 +479,20 @@ int gc_incr_state(gc_incr* h, int32_t* state_out) {
     const int64_t slots = h->uf ? h->cap : h->cap + 1;
     if (slots > 0)
       GC_CUDA(cudaMemcpyAsync(state_out, h->state, slots * 4, cudaMemcpyDeviceToDevice, h->st));
+    fetch_bad(h);
     GC_CUDA(cudaStreamSynchronize(h->st));
+    raise_bad(h);
+  });
+}
+
+int gc_incr_state_view(gc_incr* h, int32_t** state, int64_t* slots) {
+  return guarded([&] {
+    require(h && state && slots, GC_ERR_ARG, "bad arguments");
+    fetch_bad(h);
+    GC_CUDA(cudaStreamSynchronize(h->st));
+    raise_bad(h);
+    *state = h->state;
+    *slots = h->uf ? h->cap : h->cap + 1;
   });
 }
 
@@ -433,7 +515,9 @@ int gc_incr_labels(gc_incr* h, int32_t* labels_out, int64_t* components) {
     unsigned long long* hw = pinned_words();
     GC_CUDA(cudaMemcpyAsync(hw, h->ctr + C_SCRATCH0, 8, cudaMemcpyDeviceToHost, st));
     GC_CUDA(cudaFreeAsync(mins, st));
+    fetch_bad(h);
     GC_CUDA(cudaStreamSynchronize(st));
+    raise_bad(h);
     *components = int64_t(hw[0]);
   });
 }

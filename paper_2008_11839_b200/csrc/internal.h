@@ -151,14 +151,17 @@ struct CooUnionArgs {
   int32_t* lv = nullptr;
   unsigned long long* lcount = nullptr;
   int32_t init_sentinel = -1;  // >= 0: lazily initialise both endpoints first (incremental)
+  unsigned int* bad = nullptr;  // non-null: pairs with an endpoint outside [0, n) are skipped
+                                // and set *bad (the incremental handle's sticky input flag)
 };
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st);
 
 // Racy incremental batch (driver.py:674-694): each op is either a lazy-init
 // + union (is_query[i] == 0) or a read-only root-chase query, interleaved in
-// one launch.  sentinel marks uninitialised slots.
+// one launch.  sentinel marks uninitialised slots.  bits: one bit per op,
+// packed LSB-first into 32-bit words (a warp's ballot per word).
 void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t* is_query,
-                      int32_t sentinel, uint8_t* bits, cudaStream_t st);
+                      int32_t sentinel, uint32_t* bits, cudaStream_t st);
 
 int num_sms();
 
@@ -191,6 +194,11 @@ int guarded(F&& f) {
     return GC_ERR_CUDA;
   }
 }
+
+// Synchronous range check: every a[i] in [0, bound), else GC_ERR_MALFORMED
+// naming `what` (one streaming pass; entry points whose kernels would index
+// with the values call it before launching them).
+void check_ids(const int32_t* a, int64_t len, int64_t bound, cudaStream_t st, const char* what);
 
 // 64 pinned host words per thread for flag / count read-backs.
 unsigned long long* pinned_words();

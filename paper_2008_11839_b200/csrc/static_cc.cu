@@ -580,6 +580,9 @@ int gc_finish_phase(const gc_csr* g, const gc_spec* spec, int32_t* labels_io, in
     require(spec != nullptr, GC_ERR_ARG, "null spec");
     validate_spec(*spec);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the finish kernels use labels as parent indices (driver.py:440 copies
+    // them into ds.p): an id outside [0, n) is malformed input, not a fault
+    check_ids(labels_io, g->n, g->n, st, "finish_phase label");
     gc_spec s2 = *spec;
     s2.sample = GC_SAMPLE_KOUT;  // force the gather path (labels are given)
     Pipeline pl(*g, s2, labels_io, nullptr, nullptr, ws, ws_bytes, st);
@@ -749,6 +752,10 @@ int gc_union_edges(int32_t* parent, int64_t n, const int32_t* us, const int32_t*
     require(c.unite != GC_FINISH_JTB || spec->jtb_ranks, GC_ERR_ARG, "JTB needs ranks");
     require((c.unite != GC_FINISH_HOOKS && c.unite != GC_FINISH_REM_LOCK) || aux, GC_ERR_ARG,
             "hooks / rem_lock need aux scratch");
+    require(n >= 0 && n < (int64_t(1) << 31) && k >= 0, GC_ERR_ARG, "bad size");
+    // endpoints index the parent array: reject out-of-range pairs up front
+    check_ids(us, k, n, static_cast<cudaStream_t>(stream), "union endpoint");
+    check_ids(vs, k, n, static_cast<cudaStream_t>(stream), "union endpoint");
     CooUnionArgs a{};
     a.P = parent;
     a.H = c.unite == GC_FINISH_HOOKS ? aux : nullptr;
@@ -778,6 +785,9 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us, const int
     require(c.unite != GC_FINISH_JTB || spec->jtb_ranks, GC_ERR_ARG, "JTB needs ranks");
     require((c.unite != GC_FINISH_HOOKS && c.unite != GC_FINISH_REM_LOCK) || aux, GC_ERR_ARG,
             "hooks / rem_lock need aux scratch");
+    require(n >= 0 && n < (int64_t(1) << 31) && k >= 0, GC_ERR_ARG, "bad size");
+    check_ids(us, k, n, static_cast<cudaStream_t>(stream), "union endpoint");
+    check_ids(vs, k, n, static_cast<cudaStream_t>(stream), "union endpoint");
     CooUnionArgs a{};
     a.P = parent;
     a.H = c.unite == GC_FINISH_HOOKS ? aux : nullptr;

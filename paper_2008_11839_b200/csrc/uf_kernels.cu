@@ -105,11 +105,15 @@ k_union_csr_edges(UFState s, const int64_t* __restrict__ off, const int32_t* __r
 template <class R>
 __global__ void __launch_bounds__(256)
 k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
-            const uint8_t* __restrict__ skip, int32_t sentinel) {
+            const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
     if (skip && skip[i]) continue;
     const int32_t u = ldg32(us + i), v = ldg32(vs + i);
+    if (bad && (uint32_t(u) >= uint32_t(s.n) || uint32_t(v) >= uint32_t(s.n))) {
+      atomicOr(bad, 1u);  // malformed pair: never touches the parent array
+      continue;
+    }
     if (sentinel >= 0) {
       // ensure_init (driver.py:620-625) fused into the insert: every parent
       // a union reads is either one of its own endpoints (initialised right
@@ -148,18 +152,28 @@ __device__ __forceinline__ int32_t chase(const int32_t* P, int32_t x, int32_t se
 template <class R>
 __global__ void __launch_bounds__(256)
 k_incr_racy(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
-            const uint8_t* __restrict__ is_query, int32_t sentinel, uint8_t* bits) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
-    const int32_t u = us[i], v = vs[i];
-    if (is_query[i]) {
-      bits[i] = chase(s.P, u, sentinel) == chase(s.P, v, sentinel);
-    } else {
-      atomicCAS(s.P + u, sentinel, u);  // ensure_init (driver.py:620-625)
-      atomicCAS(s.P + v, sentinel, v);
-      R::unite(s, u, v);
-      bits[i] = 0;
+            const uint8_t* __restrict__ is_query, int32_t sentinel, uint32_t* bits, unsigned int* bad) {
+  // a warp owns 32 consecutive ops = one packed result word
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (k + 31) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < words; w += nwarps) {
+    const int64_t i = (w << 5) + lane;
+    bool hit = false;
+    if (i < k) {
+      const int32_t u = us[i], v = vs[i];
+      if (bad && (uint32_t(u) >= uint32_t(s.n) || uint32_t(v) >= uint32_t(s.n))) {
+        atomicOr(bad, 1u);
+      } else if (is_query[i]) {
+        hit = chase(s.P, u, sentinel) == chase(s.P, v, sentinel);
+      } else {
+        atomicCAS(s.P + u, sentinel, u);  // ensure_init (driver.py:620-625)
+        atomicCAS(s.P + v, sentinel, v);
+        R::unite(s, u, v);
+      }
     }
+    const uint32_t word = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) bits[w] = word;
   }
 }
 
@@ -235,7 +249,7 @@ struct CooLaunch {
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel),
+    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel, a.bad),
      ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
@@ -245,7 +259,7 @@ struct RacyLaunch {
   const CooUnionArgs& a;
   const uint8_t* is_query;
   int32_t sentinel;
-  uint8_t* bits;
+  uint32_t* bits;
   cudaStream_t st;
   template <class R>
   void go() const {
@@ -255,7 +269,8 @@ struct RacyLaunch {
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    (k_incr_racy<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, is_query, sentinel, bits), ::gc::count_launch());
+    (k_incr_racy<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, is_query, sentinel, bits, a.bad),
+     ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
@@ -328,7 +343,7 @@ void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, c
 }
 
 void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t* is_query,
-                      int32_t sentinel, uint8_t* bits, cudaStream_t st) {
+                      int32_t sentinel, uint32_t* bits, cudaStream_t st) {
   dispatch(cfg, false, RacyLaunch{a, is_query, sentinel, bits, st});
 }
 

@@ -48,6 +48,17 @@ __global__ void k_edges_exist(const int64_t* __restrict__ off, const int32_t* __
 
 __global__ void k_set_noncanon(unsigned long long* ctr) { ctr[C_NONCANON] = 1; }
 
+// any id of a[0..len) outside [0, bound) sets *bad (one warp vote, one atomic
+// per warp that saw a bad id)
+__global__ void k_check_ids(const int32_t* __restrict__ a, int64_t len, uint32_t bound, unsigned int* bad) {
+  unsigned f = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride)
+    f |= uint32_t(a[i]) >= bound;
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(bad, 1u);
+}
+
 // CSR shape check (the Graph contract, graphs.py:43-51): offsets start at 0,
 // never decrease, end at m; every target lies in [0, n).  bad[0] collects
 // flags: 1 offsets, 2 targets.
@@ -74,6 +85,20 @@ __global__ void k_check_csr(const int64_t* __restrict__ off, const int32_t* __re
 }
 
 }  // namespace
+
+void check_ids(const int32_t* a, int64_t len, int64_t bound, cudaStream_t st, const char* what) {
+  if (len <= 0) return;
+  require(a != nullptr, GC_ERR_ARG, std::string("null ") + what);
+  unsigned int* h = reinterpret_cast<unsigned int*>(pinned_words());
+  static thread_local unsigned int* d = nullptr;
+  if (!d) GC_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), 16));
+  GC_CUDA(cudaMemsetAsync(d, 0, 4, st));
+  (k_check_ids<<<grid_for(len, kEwBlock, 8), kEwBlock, 0, st>>>(a, len, uint32_t(bound), d), count_launch());
+  GC_CHECK_LAUNCH();
+  GC_CUDA(cudaMemcpyAsync(h, d, 4, cudaMemcpyDeviceToHost, st));
+  GC_CUDA(cudaStreamSynchronize(st));
+  require(h[0] == 0, GC_ERR_MALFORMED, std::string(what) + " outside [0, " + std::to_string(bound) + ")");
+}
 
 }  // namespace gc
 

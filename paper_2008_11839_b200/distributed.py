@@ -512,14 +512,22 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
                           info["lmax_count"], info["n_active"], x1 + x2)
 
 
+# gc_shard_absorb / gc_shard_join combine at most this many ranks' bitmap
+# summaries (kMaxRanks in csrc/shard.cu); wider groups exchange edges instead
+MAX_SUMMARY_RANKS = 8
+
+
 def sharded_static_connectivity(g_shard, spec: AlgorithmSpec, group=None, engine=None):
     """Edge-sharded static connectivity: canonical labels on every rank.
-    Unsampled specs merge forests tree-wise; sampled specs (k-out / HB) run
-    the two-phase exchange."""
-    if spec.sample is SampleKind.NONE:
+    Unsampled root-based specs merge forests tree-wise; every other
+    union-find spec (sampled, or Rem with the atomic splice) runs the
+    two-phase exchange, with the compact bitmap summary up to
+    MAX_SUMMARY_RANKS ranks and the merging-edge exchange beyond."""
+    if spec.sample is SampleKind.NONE and spec.is_union_finish() and spec.is_root_based():
         res = sharded_spanning_forest(g_shard, spec, group, engine)
     else:
-        res = sharded_two_phase(g_shard, spec, group, engine, forest=False)
+        wide = _dist().get_world_size(group) > MAX_SUMMARY_RANKS
+        res = sharded_two_phase(g_shard, spec, group, engine, forest=wide)
     return res.labels, res
 
 

@@ -28,9 +28,18 @@ def _torch():
 
 
 def _as_device_i32(x, n: int):
+    """Endpoints as a contiguous int32 CUDA tensor.  Host inputs are range
+    checked here; device tensors by gc_union_edges itself (MalformedInputError
+    either way, before any union runs)."""
     torch = _torch()
     if isinstance(x, torch.Tensor):
-        t = x.to("cuda", torch.int32)
+        if x.dtype.is_floating_point or x.dtype is torch.bool:
+            raise MalformedInputError(f"endpoints must be integer ids, not {x.dtype}")
+        if x.dtype is torch.int64 and x.numel():
+            lo, hi = torch.aminmax(x)
+            if int(lo) < 0 or int(hi) >= n:  # narrowing to int32 would wrap
+                raise MalformedInputError(f"endpoint outside [0, {n})")
+        t = x.reshape(-1).to("cuda", torch.int32)
     else:
         a = np.asarray(x, dtype=np.int64).reshape(-1)
         if a.size and (a.min() < 0 or a.max() >= n):

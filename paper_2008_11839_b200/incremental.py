@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as N
 from .api import LoweredSpec, RunStats, _require_cuda, _stream, host_int64
-from .errors import ConfigError
+from .errors import ConfigError, MalformedInputError
 from .graph import Graph
 from .spec import AlgorithmSpec, FinishKind, SpliceOp, format_spec
 
@@ -48,8 +48,91 @@ def _check_incremental(spec: AlgorithmSpec, racy: bool) -> None:
                               "queries would observe torn components - use the batched (non-racy) mode")
 
 
+class PackedBits:
+    """Query results as one bit per op, packed LSB-first into 32-bit words
+    on the device (gc_incr_query / gc_incr_batch write one __ballot_sync word
+    per 32 ops): ``words`` is the int32 CUDA tensor, ``numpy()`` unpacks to
+    the reference's per-op bool array (driver.py:658-668) on the host."""
+
+    def __init__(self, words, n: int):
+        self.words = words
+        self.n = int(n)
+
+    def __len__(self) -> int:
+        return self.n
+
+    def numpy(self) -> np.ndarray:
+        if self.n == 0:
+            return np.zeros(0, dtype=bool)
+        raw = self.words.cpu().numpy().view(np.uint8)
+        return np.unpackbits(raw, bitorder="little")[: self.n].astype(bool)
+
+    def tolist(self) -> list:
+        return self.numpy().tolist()
+
+
+class LiveState:
+    """The live incremental state handed to ``on_batch`` (driver.py:710-711
+    passes the live parent list / label array, not a copy): a zero-copy view
+    of the handle's device array with the sentinel convention.  It exposes
+    ``__cuda_array_interface__`` (``torch.as_tensor(state, device="cuda")``
+    aliases it) and converts to a host int64 array only when read as numpy
+    (``np.asarray(state)``, indexing).  Valid during the callback; later
+    batches mutate it."""
+
+    def __init__(self, ptr: int, slots: int, owner):
+        self._ptr = int(ptr or 0)
+        self._slots = int(slots)
+        self._owner = owner  # keeps the handle alive while the view exists
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self._slots,), "typestr": "<i4", "data": (self._ptr, True), "version": 3,
+                "strides": None}
+
+    def tensor(self):
+        torch = _torch()
+        if self._slots == 0:
+            return torch.empty(0, dtype=torch.int32, device="cuda")
+        return torch.as_tensor(self, device="cuda")
+
+    def __len__(self) -> int:
+        return self._slots
+
+    def __array__(self, dtype=None, copy=None):
+        out = self.tensor().cpu().numpy().astype(np.int64)
+        return out if dtype is None else out.astype(dtype)
+
+    def __getitem__(self, idx):
+        return np.asarray(self)[idx]
+
+    def tolist(self) -> list:
+        return np.asarray(self).tolist()
+
+
+def _ids(x, what: str):
+    """Endpoint arrays as contiguous int32 CUDA tensors on the current device
+    (a strided or int64 tensor would otherwise be reinterpreted by the ABI)."""
+    torch = _torch()
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+    if t.dim() != 1:
+        raise ValueError(f"{what} must be one-dimensional")
+    if t.dtype not in (torch.int8, torch.int16, torch.int32, torch.int64, torch.uint8):
+        raise TypeError(f"{what} must hold integer vertex ids, not {t.dtype}")
+    if t.dtype is torch.int64 and t.numel():
+        lo, hi = torch.aminmax(t)
+        if int(lo) < 0 or int(hi) >= 2 ** 31:  # narrowing would wrap into valid ids
+            raise MalformedInputError(f"{what}: vertex id outside [0, 2^31)")
+    return t.to("cuda", torch.int32).contiguous()
+
+
 class IncrementalConnectivity:
-    """Device-resident incremental state over `capacity` vertex slots."""
+    """Device-resident incremental state over `capacity` vertex slots.
+
+    Every entry point runs on the caller's current CUDA stream.  Endpoints
+    are coerced to contiguous int32 device tensors; an endpoint outside
+    [0, capacity) raises MalformedInputError (the op itself is skipped on
+    the device, so the state is never written out of bounds)."""
 
     def __init__(self, spec: AlgorithmSpec, capacity: int, racy: bool = False):
         _check_incremental(spec, racy)
@@ -61,7 +144,21 @@ class IncrementalConnectivity:
         self._lowered = lowered
         self._h = C.c_void_p()
         N.check(N.lib().gc_incr_create(self.capacity, C.byref(lowered.s), _stream(), C.byref(self._h)))
+        self._stream = _stream().value
         self.stats = N.Stats()
+
+    def _on_current_stream(self):
+        cur = _stream()
+        if cur.value != self._stream:
+            N.check(N.lib().gc_incr_set_stream(self._h, cur))
+            self._stream = cur.value
+
+    def _pair(self, us, vs):
+        us, vs = _ids(us, "us"), _ids(vs, "vs")
+        if us.numel() != vs.numel():
+            raise ValueError("us and vs must have the same length")
+        self._on_current_stream()
+        return us, vs
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -77,9 +174,13 @@ class IncrementalConnectivity:
         N.check(N.lib().gc_incr_reserve(self._h, int(batch_len)))
 
     def insert(self, us, vs, sync: bool = True) -> None:
-        """Insert-only batch (columnar device tensors, int32).  sync=False
-        (union-find specs): enqueue only; later queries / labels order after
-        it, and the caller keeps us / vs alive until then."""
+        """Insert-only batch (columnar, int32 ids).  sync=False (union-find
+        specs): enqueue only on the current stream; later calls order after
+        it, and a malformed endpoint is reported by the next synchronising
+        call.  The kernel runs on the current stream, so the caching allocator
+        cannot hand the (possibly coerced) id buffers to later work before it
+        has read them."""
+        us, vs = self._pair(us, vs)
         n = int(us.numel())
         fn = N.lib().gc_incr_insert if sync else N.lib().gc_incr_insert_async
         N.check(fn(self._h, us.data_ptr() if n else None, vs.data_ptr() if n else None, n, C.byref(self.stats)))
@@ -88,6 +189,7 @@ class IncrementalConnectivity:
         """Insert-only batch that also returns the edges that merged two trees
         (the exchange unit of the sharded driver; root-based rules only)."""
         torch = _torch()
+        us, vs = self._pair(us, vs)
         n = int(us.numel())
         ou = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         ov = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
@@ -98,37 +200,52 @@ class IncrementalConnectivity:
         c = int(cnt.item())
         return ou[:c], ov[:c]
 
-    def query(self, us, vs):
-        """Query-only batch; returns a uint8 CUDA tensor of connected bits."""
+    def query(self, us, vs) -> PackedBits:
+        """Query-only batch; returns the connected bits packed 32 per word."""
         torch = _torch()
+        us, vs = self._pair(us, vs)
         n = int(us.numel())
-        bits = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
-        N.check(N.lib().gc_incr_query(self._h, us.data_ptr() if n else None,
-                                      vs.data_ptr() if n else None, n, bits.data_ptr(),
-                                      C.byref(self.stats)))
-        return bits[:n]
-
-    def batch(self, us, vs, is_query):
-        """Mixed batch in reference order; returns uint8 bits (1 = connected query)."""
-        torch = _torch()
-        n = int(us.numel())
-        bits = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+        words = torch.zeros(max((n + 31) // 32, 1), dtype=torch.int32, device="cuda")
         if n:
-            N.check(N.lib().gc_incr_batch(self._h, us.data_ptr(), vs.data_ptr(), is_query.data_ptr(), n,
-                                          bits.data_ptr(), int(self.racy), C.byref(self.stats)))
-        return bits[:n]
+            N.check(N.lib().gc_incr_query(self._h, us.data_ptr(), vs.data_ptr(), n, words.data_ptr(),
+                                          C.byref(self.stats)))
+        return PackedBits(words, n)
+
+    def batch(self, us, vs, is_query) -> PackedBits:
+        """Mixed batch in reference order; returns packed bits (1 = connected query)."""
+        torch = _torch()
+        us, vs = self._pair(us, vs)
+        n = int(us.numel())
+        isq = torch.as_tensor(is_query).to("cuda", torch.uint8).contiguous()
+        if isq.numel() != n:
+            raise ValueError("is_query must have one flag per op")
+        words = torch.zeros(max((n + 31) // 32, 1), dtype=torch.int32, device="cuda")
+        if n:
+            N.check(N.lib().gc_incr_batch(self._h, us.data_ptr(), vs.data_ptr(), isq.data_ptr(), n,
+                                          words.data_ptr(), int(self.racy), C.byref(self.stats)))
+        return PackedBits(words, n)
 
     def state(self):
         """Copy of the live state with the sentinel convention (driver.py:656, 710)."""
         torch = _torch()
+        self._on_current_stream()
         slots = self.capacity if self.spec.is_union_finish() else self.capacity + 1
         out = torch.empty(max(slots, 1), dtype=torch.int32, device="cuda")
         N.check(N.lib().gc_incr_state(self._h, out.data_ptr()))
         return out[:slots]
 
+    def live_state(self) -> LiveState:
+        """The live device state itself (no copy), as on_batch receives it."""
+        self._on_current_stream()
+        ptr = C.c_void_p()
+        slots = C.c_int64(0)
+        N.check(N.lib().gc_incr_state_view(self._h, C.byref(ptr), C.byref(slots)))
+        return LiveState(ptr.value, slots.value, self)
+
     def labels(self):
         """(finalized int32 labels tensor, component count of initialised vertices)."""
         torch = _torch()
+        self._on_current_stream()
         out = torch.empty(max(self.capacity, 1), dtype=torch.int32, device="cuda")
         comps = C.c_int64(0)
         N.check(N.lib().gc_incr_labels(self._h, out.data_ptr(), C.byref(comps)))
@@ -166,11 +283,11 @@ def incremental(init, spec: AlgorithmSpec, batches, workers=1, capacity=None, ra
         if k:
             bits = inc.batch(torch.from_numpy(us).to("cuda"), torch.from_numpy(vs).to("cuda"),
                              torch.from_numpy(isq).to("cuda"))
-            results.append(bits.cpu().numpy().astype(bool))
+            results.append(bits.numpy())
         else:
             results.append(np.zeros(0, dtype=bool))
         if on_batch is not None:
-            on_batch(bi, host_int64(inc.state()))
+            on_batch(bi, inc.live_state())
     labels, comps = inc.labels()
     st = inc.stats
     stats.phase_times = {"insert": st.t_sample_ms / 1e3, "query": st.t_finish_ms / 1e3}
