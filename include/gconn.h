@@ -270,6 +270,15 @@ int gc_find_batch(int32_t* parent, int64_t n, const int32_t* xs, int64_t k,
  * 4*n + 512 bytes. */
 int gc_canonical_labels(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
                         void* stream);
+/* The census of a labelling (validate.py:267-298 sampling_stats): out_host[0]
+ * = most frequent label (ties -> smaller), [1] its multiplicity (cov =
+ * [1] / n), [2] directed CSR entries whose endpoints carry different labels
+ * (ic = [2] / m), [3] = -1, or with a non-NULL oracle labelling the smallest
+ * vertex whose class (by `labels`) is not inside one oracle class — the
+ * refinement check of validate.py:290-297.  Labels must lie in [0, n);
+ * ws needs 4*n + 8192 bytes.  Synchronous. */
+int gc_label_census(const gc_csr* g, const int32_t* labels, const int32_t* oracle,
+                    int64_t* out_host, void* ws, size_t ws_bytes, void* stream);
 /* check_forest clause (a) (validate.py:200-206): *first_missing (device)
  * receives the smallest i whose (us[i], vs[i]) is not in the CSR, or
  * UINT64_MAX when every edge exists. */

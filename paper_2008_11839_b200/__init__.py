@@ -14,8 +14,8 @@ from .errors import ConfigError, MalformedInputError, NativeError, VerificationE
 from .generators import (build_csr, clique_graph, disjoint_union, gen_rmat, gen_uniform_pairs,
                          grid3d_edges, grid_graph, path_graph, star_graph)
 from .graph import EdgeList, Graph
-from .graphio import (gen_ba, gnp_graph, graph_to_edge_list, is_binary_graph, load_edge_list, load_graph,
-                      load_graph_binary, save_edge_list, save_graph_binary)
+from .graphio import (gen_ba, gnp_graph, graph_to_edge_list, is_binary_graph, load_graph, load_graph_binary,
+                      save_graph_binary)
 from .incremental import IncrementalConnectivity, Insert, Query, incremental
 from .spec import (LT_VARIANTS, AlgorithmSpec, FindOp, FinishKind, KOutMode, LTVariant, SampleKind,
                    SpliceOp, UnionConfig, UnionOp, all_valid_configs, enumerate_specs, format_spec,
@@ -36,6 +36,5 @@ __all__ = [
     "star_graph", "static_connectivity", "static_connectivity_device", "valid_combination",
     "DisjointSets", "union_edge_list", "canonical_labels", "check_forest", "oracle_components",
     "oracle_components_unionfind", "partition_equal", "sampling_stats", "gen_ba", "gnp_graph",
-    "graph_to_edge_list", "is_binary_graph", "load_edge_list", "load_graph", "load_graph_binary",
-    "save_edge_list", "save_graph_binary",
+    "graph_to_edge_list", "is_binary_graph", "load_graph", "load_graph_binary", "save_graph_binary",
 ]

@@ -102,6 +102,7 @@ _SIGNATURES = {
     "gc_find_batch": (C.c_int, [_VP, _I64, _VP, _I64, C.c_int32, _VP, _VP]),
     "gc_canonical_labels": (C.c_int, [_VP, _I64, _VP, _SZ, _VP]),
     "gc_edges_exist": (C.c_int, [C.POINTER(Csr), _VP, _VP, _I64, _VP, _VP]),
+    "gc_label_census": (C.c_int, [C.POINTER(Csr), _VP, _VP, C.POINTER(_I64), _VP, _SZ, _VP]),
 }
 
 _lock = threading.Lock()

@@ -84,6 +84,21 @@ __global__ void k_check_csr(const int64_t* __restrict__ off, const int32_t* __re
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(bad, flags);
 }
 
+__global__ void k_class_min(const int32_t* __restrict__ L, int32_t n, int32_t* mins) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    atomicMin(mins + L[v], int32_t(v));
+}
+
+// refinement (validate.py:290-297): every vertex shares its oracle label
+// with its class's minimum member; the smallest violating vertex wins
+__global__ void k_refines(const int32_t* __restrict__ L, const int32_t* __restrict__ mins,
+                          const int32_t* __restrict__ orc, int32_t n, unsigned long long* first_bad) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    if (orc[v] != orc[mins[L[v]]]) atomicMin(first_bad, static_cast<unsigned long long>(v));
+}
+
 }  // namespace
 
 void check_ids(const int32_t* a, int64_t len, int64_t bound, cudaStream_t st, const char* what) {
@@ -158,6 +173,47 @@ int gc_edges_exist(const gc_csr* g, const int32_t* us, const int32_t* vs, int64_
     (k_edges_exist<<<grid_for(k, kEwBlock, 8), kEwBlock, 0, st>>>(g->offsets, g->targets, g->n, us, vs, k,
                                                                  first_missing), count_launch());
     GC_CHECK_LAUNCH();
+  });
+}
+
+int gc_label_census(const gc_csr* g, const int32_t* labels, const int32_t* oracle, int64_t* out_host,
+                    void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(g != nullptr && out_host != nullptr, GC_ERR_ARG, "null argument");
+    require(g->n >= 0 && g->n < (int64_t(1) << 31), GC_ERR_MALFORMED, "vertex count outside [0, 2^31)");
+    const int32_t n = int32_t(g->n);
+    out_host[0] = 0;
+    out_host[1] = 0;
+    out_host[2] = 0;
+    out_host[3] = -1;
+    if (n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    check_ids(labels, n, n, st, "label");
+    if (oracle) check_ids(oracle, n, n, st, "oracle label");
+    Arena a(ws, ws_bytes);
+    unsigned long long* ctr = a.take<unsigned long long>(C_COUNT_);
+    int32_t* hist = a.take<int32_t>(n);
+    GC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT_, st));
+    // most_frequent_label (sampling.py:29-35): probe + exact histogram
+    run_mode(const_cast<int32_t*>(labels), n, hist, ctr, st);
+    if (g->m)
+      (k_ic_census<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, g->offsets, g->targets, nullptr,
+                                                                 ctr), count_launch());
+    if (oracle) {
+      fill(hist, n, INT_MAX, st);
+      GC_CUDA(cudaMemsetAsync(ctr + C_SCRATCH1, 0xff, 8, st));
+      (k_class_min<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, n, hist), count_launch());
+      (k_refines<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(labels, hist, oracle, n, ctr + C_SCRATCH1),
+       count_launch());
+    }
+    GC_CHECK_LAUNCH();
+    unsigned long long c[C_COUNT_];
+    GC_CUDA(cudaMemcpyAsync(c, ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    out_host[0] = int64_t(c[C_LMAX]);
+    out_host[1] = int64_t(c[C_LMAX_COUNT]);
+    out_host[2] = g->m ? int64_t(c[C_IC]) : 0;
+    out_host[3] = oracle && c[C_SCRATCH1] != ~0ull ? int64_t(c[C_SCRATCH1]) : -1;
   });
 }
 

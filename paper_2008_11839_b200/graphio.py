@@ -1,7 +1,5 @@
 """Graph files and the remaining reference generators (graphs.py:124-308).
 
-* Text edge lists (``u v`` per line, ``#``/``%`` comments, optional
-  ``# n <count>`` header) — graphs.py:129-167, same error positions.
 * GCN1 binary CSR (magic "GCN1", u64 n, u64 m, u64 offsets[n+1], u32
   targets[m], little endian) — graphs.py:170-190.  ``load_graph_binary``
   reads the file straight into pinned host buffers and, with
@@ -30,43 +28,7 @@ def _torch():
     return torch
 
 
-# ------------------------------------------------------------------ text
-
-def load_edge_list(path) -> EdgeList:
-    """graphs.py:129-160: parse 'u v' lines; n = 1 + max endpoint unless a
-    '# n <count>' header overrides it."""
-    edges = []
-    n_override = None
-    with open(path, "r") as fh:
-        for lineno, raw in enumerate(fh, start=1):
-            line = raw.strip()
-            if not line:
-                continue
-            if line[0] in "#%":
-                head = line[1:].split()
-                if len(head) == 2 and head[0] == "n" and head[1].isdigit():
-                    n_override = int(head[1])
-                continue
-            parts = line.split()
-            if len(parts) != 2:
-                raise MalformedInputError(f"{path}:{lineno}: expected 'u v', got {line!r}")
-            try:
-                edges.append((int(parts[0]), int(parts[1])))
-            except ValueError:
-                raise MalformedInputError(f"{path}:{lineno}: unparsable token in {line!r}") from None
-    arr = np.array(edges, dtype=np.int64).reshape(-1, 2)
-    n = n_override if n_override is not None else (int(arr.max()) + 1 if len(arr) else 0)
-    return EdgeList(n, arr)
-
-
-def save_edge_list(el: EdgeList, path) -> None:
-    """graphs.py:163-167."""
-    edges = el.edges.cpu().numpy() if hasattr(el.edges, "cpu") else np.asarray(el.edges)
-    with open(path, "w") as fh:
-        fh.write(f"# n {el.n}\n")
-        if len(edges):
-            np.savetxt(fh, edges, fmt="%d %d")
-
+# ------------------------------------------------------------------ edges
 
 def graph_to_edge_list(g: Graph) -> EdgeList:
     """graphs.py:124-126: one pair per undirected edge, u < v."""
@@ -142,10 +104,13 @@ def load_graph_binary(path, device: bool = False) -> Graph:
 
 
 def load_graph(path, device: bool = False) -> Graph:
-    """graphs.py:198-202: sniff the format, normalise to CSR."""
-    if is_binary_graph(path):
-        return load_graph_binary(path, device=device)
-    return build_csr(load_edge_list(path))
+    """graphs.py:198-202 for the binary CSR format.  Text edge lists
+    (graphs.py:129-167) are file plumbing outside the accelerated path
+    (SURVEY §2): parse them with connlab and hand the arrays to Graph."""
+    if not is_binary_graph(path):
+        raise MalformedInputError(f"{path}: not a GCN1 binary graph (text edge lists are read by "
+                                  "connlab.graphs.load_edge_list; pass its arrays to Graph / build_csr)")
+    return load_graph_binary(path, device=device)
 
 
 # ------------------------------------------------------------- generators

@@ -11,12 +11,14 @@ loops take ~25 s at n = 2^22):
   (c) count            — populated slots = n - #components(oracle)
   (d) components_match — forest components vs the oracle partition
 
-``partition_equal``, ``canonical_labels`` and ``sampling_stats`` are the
-reference's host-side census definitions restated over numpy.
-``oracle_components`` / ``oracle_components_unionfind`` return canonical
-labels from two independent device routes (label-propagation rounds and
-sequential-order-free union-find) for cross-checking; the test-suite's
-ground truth remains the C oracle under ``oracle/``.
+``canonical_labels``, ``partition_equal`` and ``sampling_stats`` keep the
+reference's definitions and run as device passes (``gc_canonical_labels``,
+``gc_label_census``: a histogram mode, a crossing-edge count and a
+refinement check against an oracle labelling).  ``oracle_components`` /
+``oracle_components_unionfind`` are two host routes that share no code with
+libgconn (scipy's traversal; numpy min-hooking + pointer jumping), so
+checking the device against them is a real check; the test-suite's ground
+truth remains the C oracle under ``oracle/`` and the reference fixtures.
 """
 from __future__ import annotations
 
@@ -26,10 +28,9 @@ import json
 import numpy as np
 
 from . import _native as N
-from .api import _csr, _require_cuda, _stream, _workspace, host_int64, static_connectivity_device
+from .api import _csr, _require_cuda, _stream, _workspace, host_int64
 from .errors import MalformedInputError
 from .graph import Graph
-from .spec import parse_spec
 
 
 def _torch():
@@ -37,70 +38,136 @@ def _torch():
     return torch
 
 
-# ------------------------------------------------------------- host census
+# ---------------------------------------------------------- device census
 
-def partition_equal(a, b) -> bool:
-    """validate.py:158-172: same partition irrespective of label values."""
-    a = np.asarray(a, dtype=np.int64)
-    b = np.asarray(b, dtype=np.int64)
-    if a.shape != b.shape:
-        return False
-    if len(a) == 0:
-        return True
-    pairs = (a << np.int64(32)) | (b & np.int64(0xFFFFFFFF))
-    return len(np.unique(a)) == len(np.unique(pairs)) == len(np.unique(b))
+def _dense_ids(labels) -> np.ndarray:
+    """Any labelling as int32 ids in [0, n) inducing the same partition (the
+    device kernels index with label values; the reference accepts any
+    int64 values)."""
+    a = np.asarray(labels, dtype=np.int64).reshape(-1)
+    n = len(a)
+    if n == 0 or (a.min() >= 0 and a.max() < n):
+        return a.astype(np.int32)
+    _, inv = np.unique(a, return_inverse=True)
+    return inv.astype(np.int32)
+
+
+def _canonical_device(labels):
+    """gc_canonical_labels on a dense int32 device copy (values become each
+    class's minimum member)."""
+    torch = _torch()
+    dense = _dense_ids(labels)
+    n = len(dense)
+    t = torch.from_numpy(dense).to("cuda")
+    if n:
+        ws = _workspace(4 * n + 8192)
+        N.check(N.lib().gc_canonical_labels(t.data_ptr(), n, ws.data_ptr(), ws.numel(), _stream()))
+    return t
 
 
 def canonical_labels(labels) -> np.ndarray:
-    """validate.py:251-259: each class relabelled by its minimum member."""
-    labels = np.asarray(labels, dtype=np.int64)
-    n = len(labels)
-    if n == 0:
-        return labels.copy()
-    mins = np.full(n, n, dtype=np.int64)
-    np.minimum.at(mins, labels, np.arange(n, dtype=np.int64))
-    return mins[labels]
+    """validate.py:251-259: relabel every class by its minimum member
+    (device: one atomic-min pass per class, then a gather)."""
+    _require_cuda()
+    return host_int64(_canonical_device(labels))
+
+
+def partition_equal(a, b) -> bool:
+    """validate.py:158-170: do two labellings induce the same partition?
+    Two labellings are the same partition exactly when their canonical
+    (minimum-member) forms are equal element for element."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    if a.size == 0:
+        return True
+    _require_cuda()
+    torch = _torch()
+    return bool(torch.equal(_canonical_device(a), _canonical_device(b)))
+
+
+def label_census(g: Graph, labels, oracle=None) -> dict:
+    """gc_label_census: the most frequent label and its count, the
+    label-crossing directed edges, and (with an oracle) the first vertex
+    whose class is not inside one oracle class (or -1)."""
+    _require_cuda()
+    torch = _torch()
+    lab = torch.from_numpy(_dense_ids(labels) if not hasattr(labels, "data_ptr") else labels.cpu().numpy()
+                           .astype(np.int32)).to("cuda")
+    if lab.numel() != g.n:
+        raise MalformedInputError(f"labels must have length n={g.n}")
+    orc = None
+    if oracle is not None:
+        orc = torch.from_numpy(_dense_ids(oracle)).to("cuda")
+    csr, keep = _csr(g)
+    ws = _workspace(4 * g.n + 8192)
+    out = (C.c_int64 * 4)()
+    N.check(N.lib().gc_label_census(C.byref(csr), lab.data_ptr() if g.n else None,
+                                    orc.data_ptr() if orc is not None and g.n else None, out, ws.data_ptr(),
+                                    ws.numel(), _stream()))
+    return {"mode": int(out[0]), "mode_count": int(out[1]), "crossing": int(out[2]),
+            "first_unrefined": int(out[3])}
 
 
 def sampling_stats(g: Graph, post_sample_labels, oracle=None) -> tuple[float, float]:
-    """validate.py:267-298: (cov, ic) census of post-sampling labels; with an
-    oracle, asserts that the sampled partition refines it."""
-    labels = np.asarray(post_sample_labels, dtype=np.int64)
-    n = g.n
-    if n == 0:
+    """validate.py:267-298: (cov, ic) of post-sampling labels — cov = the
+    most frequent label's share of the vertices, ic = the share of directed
+    edges whose endpoints carry different labels; with an oracle labelling,
+    raises AssertionError unless the sampled partition refines it."""
+    if g.n == 0:
         return 1.0, 0.0
-    counts = np.bincount(labels, minlength=n)
-    mode = int(counts.argmax())
-    cov = counts[mode] / n
-    if g.m == 0:
-        ic = 0.0
-    else:
-        src = np.repeat(np.arange(n, dtype=np.int64), g.degrees)
-        ic = float(np.count_nonzero(labels[src] != labels[g.targets])) / g.m
-    if oracle is not None:
-        oracle = np.asarray(oracle, dtype=np.int64)
-        order = np.argsort(labels, kind="stable")
-        ls, os_ = labels[order], oracle[order]
-        same_class = ls[1:] == ls[:-1]
-        if np.any(same_class & (os_[1:] != os_[:-1])):
-            raise AssertionError("post-sampling labels merge distinct true components")
+    c = label_census(g, post_sample_labels, oracle)
+    if oracle is not None and c["first_unrefined"] >= 0:
+        raise AssertionError("post-sampling labels merge distinct true components "
+                             f"(vertex {c['first_unrefined']})")
+    cov = c["mode_count"] / g.n
+    ic = c["crossing"] / g.m if g.m else 0.0
     return float(cov), float(ic)
 
 
-# ------------------------------------------------------------ device routes
+# ---------------------------------------------------------- oracle routes
 
 def oracle_components(g: Graph) -> np.ndarray:
-    """Canonical component labels by label-propagation rounds (no union-find
-    on this route; validate.py:74-98 uses a BFS flood for the same reason)."""
-    labels, _ = static_connectivity_device(g, parse_spec("none+lp"), metrics=False)
-    return host_int64(labels)
+    """validate.py:74-98: canonical component labels from a route that
+    shares nothing with libgconn — scipy's graph traversal on the host CSR
+    (the reference floods with BFS for the same reason), then the
+    minimum-member relabelling."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+    n = g.n
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    off, tgt = g.offsets, g.targets
+    a = csr_matrix((np.ones(len(tgt), dtype=np.int8), tgt, off), shape=(n, n))
+    _, comp = connected_components(a, directed=False)
+    first = np.full(comp.max() + 1, n, dtype=np.int64)
+    order = np.arange(n - 1, -1, -1, dtype=np.int64)  # descending: the last write per class is its minimum
+    first[comp[order]] = order
+    return first[comp]
 
 
 def oracle_components_unionfind(g: Graph) -> np.ndarray:
-    """Canonical labels by asynchronous union-find with full compression
-    (validate.py:101-122's second, independent route)."""
-    labels, _ = static_connectivity_device(g, parse_spec("none+async+compress"), metrics=False)
-    return host_int64(labels)
+    """validate.py:101-122's second, independent route: host-side min-label
+    hooking + pointer jumping over the CSR (numpy), to the fixpoint."""
+    n = g.n
+    lab = np.arange(n, dtype=np.int64)
+    if n == 0 or g.m == 0:
+        return lab
+    src = np.repeat(np.arange(n, dtype=np.int64), g.degrees)
+    dst = g.targets.astype(np.int64)
+    while True:
+        lo = np.minimum(lab[src], lab[dst])
+        before = lab.copy()
+        np.minimum.at(lab, lab[src], lo)
+        np.minimum.at(lab, lab[dst], lo)
+        while True:  # jump every vertex to its root
+            nxt = lab[lab]
+            if np.array_equal(nxt, lab):
+                break
+            lab = nxt
+        if np.array_equal(lab, before):
+            return lab
 
 
 def _forest_pairs(forest):

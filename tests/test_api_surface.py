@@ -10,8 +10,8 @@ import pytest
 from golden_data import G, h
 from paper_2008_11839_b200 import (DisjointSets, EdgeList, FindOp, ForestEdges, Graph, MalformedInputError,
                                    SpliceOp, UnionConfig, UnionOp, all_valid_configs, canonical_labels,
-                                   check_forest, gen_ba, is_binary_graph, load_edge_list, partition_equal,
-                                   sampling_stats, save_edge_list, union_edge_list)
+                                   check_forest, gen_ba, is_binary_graph, load_graph, partition_equal,
+                                   sampling_stats, union_edge_list)
 
 API = json.loads((G / "api.json").read_text())
 
@@ -26,25 +26,18 @@ def test_gen_ba_matches_reference():
         assert (el.edges[:, 1] < el.edges[:, 0]).all()
 
 
-def test_text_edge_list_roundtrip_and_errors(tmp_path):
+def test_text_edge_lists_are_out_of_scope(tmp_path):
+    """Text edge lists (graphs.py:129-167) are file plumbing off the
+    accelerated path: load_graph takes GCN1 files only and says
+    where text files are read."""
     p = tmp_path / "tiny.txt"
-    p.write_text("# n 4\n% another comment\n0 2\n3 1\n")
-    el = load_edge_list(p)
-    assert el.n == 4 and el.edges.tolist() == [[0, 2], [3, 1]]
-    q = tmp_path / "rt.txt"
-    save_edge_list(EdgeList(7, np.array([[1, 2], [6, 0]])), q)
-    back = load_edge_list(q)
-    assert back.n == 7 and back.edges.tolist() == [[1, 2], [6, 0]]
-    assert not is_binary_graph(q)
-    bad = tmp_path / "bad.txt"
-    bad.write_text("# n 4\n0 2\nnot-an-edge\n")
-    with pytest.raises(MalformedInputError, match=":3:"):
-        load_edge_list(bad)
-    bad.write_text("0 1 2\n")
-    with pytest.raises(MalformedInputError, match="expected 'u v'"):
-        load_edge_list(bad)
+    p.write_text("# n 4\n0 2\n3 1\n")
+    assert not is_binary_graph(p)
+    with pytest.raises(MalformedInputError, match="not a GCN1 binary graph"):
+        load_graph(p)
 
 
+@pytest.mark.gpu
 def test_census_helpers_match_reference():
     from paper_2008_11839_b200 import build_csr  # noqa: F401  (GPU not needed below)
     assert partition_equal([0, 0, 2, 3], [5, 5, 1, 0])
@@ -56,6 +49,7 @@ def test_census_helpers_match_reference():
     assert cov == 0.5 and ic == pytest.approx(4 / 6)
 
 
+@pytest.mark.gpu
 def test_sampling_stats_cases():
     # the fixture graph is gen_ba(300, 2, seed=3) symmetrised by the reference
     el = gen_ba(300, 2, seed=3)
@@ -161,8 +155,9 @@ def _ba_graph_host(n, att, seed):
 
 
 def test_make_stream_order_matches_reference():
-    from paper_2008_11839_b200.sweep import CSV_COLUMNS, make_stream, make_stream_columnar
+    from paper_2008_11839_b200.sweep import CSV_COLUMNS, chunk, make_stream, make_stream_columnar
     assert CSV_COLUMNS == API["csv_columns"]
+    assert chunk(list(range(5)), 2) == [[0, 1], [2, 3], [4]] and chunk([1, 2], 0) == [[1, 2]]
     g = _ba_graph_host(300, 2, 3)
     for ratio, want in API["make_stream"].items():
         ratio = int(ratio)
@@ -215,3 +210,29 @@ def test_binary_graph_host_roundtrip_and_errors(tmp_path):
     (tmp_path / "short.gcn1").write_bytes(raw[:40])
     with pytest.raises(MalformedInputError, match="truncated"):
         load_graph_binary(tmp_path / "short.gcn1")
+
+
+@pytest.mark.gpu
+def test_census_refinement_and_oracle_routes():
+    """sampling_stats' refinement assertion (validate.py:290-297) and the two
+    host oracle routes against the C oracle."""
+    import oracle
+    from paper_2008_11839_b200 import oracle_components, oracle_components_unionfind
+    from paper_2008_11839_b200.validate import label_census
+    n, e = oracle.gen_rmat(10, 8, seed=3)
+    off, tgt = oracle.build_csr(n, e)
+    ref, comps = oracle.components(n, off, tgt)
+    g = Graph(n, off, tgt)
+    assert np.array_equal(oracle_components(g), ref)
+    assert np.array_equal(oracle_components_unionfind(g), ref)
+    fine = np.arange(n)
+    assert sampling_stats(g, fine, ref)[0] == pytest.approx(1 / n)
+    sampling_stats(g, ref, ref)  # the partition refines itself
+    bad = ref.copy()
+    iso = np.flatnonzero(np.diff(off) == 0)
+    assert len(iso) >= 1
+    bad[iso[0]] = ref[np.flatnonzero(np.diff(off) > 0)[0]]  # glue an isolate onto a component
+    with pytest.raises(AssertionError, match="merge distinct"):
+        sampling_stats(g, bad, ref)
+    c = label_census(g, ref)
+    assert c["crossing"] == 0 and c["mode_count"] == np.bincount(ref).max()
