@@ -49,12 +49,54 @@ def host_csr(g):
     return g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy()
 
 
+SPECS = None  # --specs filter
+
+
+def want(specs):
+    return [t for t in specs if SPECS is None or t in SPECS]
+
+
 def emit(out, rec):
     line = json.dumps(rec)
     print(line, flush=True)
     if out:
         with open(out, "a") as f:
             f.write(line + "\n")
+
+
+def alg_bytes_static(n, insp_sample, insp_finish, sampled, rounds, forest_edges=0):
+    """B = 4 E_insp + 8 (n+1) + 4 n P (+ 8 (n - c) forest
+    slots); P = 4 label passes unsampled, 7 sampled, + 3 per finish round."""
+    passes = (7 if sampled else 4) + 3 * int(rounds or 0)
+    return 4 * (insp_sample + insp_finish) + 8 * (n + 1) + 4 * n * passes + 8 * forest_edges
+
+
+def roofline_fields(alg, seconds):
+    gbs = alg / seconds / 1e9
+    return {"alg_bytes": int(alg), "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak()}
+
+
+def cpu_line(out, tag, spec, seconds, units, unit, threads, sample, extra=None):
+    rec = {"config": tag, "cpu_baseline": True, "kind": "port", "cores": threads, "spec": spec,
+           "seconds": seconds, unit: units / seconds, "sample": sample}
+    if extra:
+        rec.update(extra)
+    emit(out, rec)
+
+
+def cpu_static(out, tag, g, off, tgt, ref, specs, forest=False, bfs_source=-1):
+    """The C/OpenMP port of the reference pipeline (oracle/gconn_oracle.c,
+    test infrastructure) on all host threads, same graph, labels checked."""
+    import numpy as np
+    import oracle
+    threads = oracle.max_threads()
+    for text in specs:
+        res = oracle.pipeline(g.n, off, tgt, text, threads, forest=forest, bfs_source=bfs_source)
+        lab, st, tm = res[0], res[1], res[2]
+        ok = bool(np.array_equal(lab.astype(np.int64), ref))
+        cpu_line(out, tag, text, sum(tm), g.m / 2, "edges_per_s", threads, "the whole workload",
+                 {"labels_bit_exact": ok, "rounds": st["rounds"], "insp_sample": st["insp_sample"],
+                  "insp_finish": st["insp_finish"]})
 
 
 def static_config(tag, g, specs, reps, out, cpu_spec=None, extra=None):
@@ -65,7 +107,7 @@ def static_config(tag, g, specs, reps, out, cpu_spec=None, extra=None):
     t0 = time.perf_counter()
     ref, comps = oracle.components(g.n, off, tgt)
     t_oracle = time.perf_counter() - t0
-    for text in specs:
+    for text in want(specs):
         spec = parse_spec(text)
         labels, st = static_connectivity_device(g, spec, metrics=True)
         ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref))
@@ -79,16 +121,13 @@ def static_config(tag, g, specs, reps, out, cpu_spec=None, extra=None):
                "phase_ms": {k: v * 1e3 for k, v in st2.phase_times.items()},
                "kernel_ms": {"sample": st2.kernel_ms_sample, "finish": st2.kernel_ms_finish},
                "oracle_seconds": t_oracle}
+        rec.update(roofline_fields(alg_bytes_static(g.n, rec["insp_sample"], rec["insp_finish"],
+                                                    spec.sample.value != "none", st.rounds), med))
         if extra:
             rec.update(extra)
         emit(out, rec)
     if cpu_spec:
-        samp, uni, find, spl = cpu_spec
-        threads = oracle.max_threads()
-        _, st, tm = oracle.static_uf(g.n, off, tgt, samp, 2, uni, find, spl, threads)
-        emit(out, {"config": tag, "cpu_baseline": True, "kind": "port", "cores": threads,
-                   "spec": f"{samp}+{uni}+{find}+{spl}", "seconds": sum(tm),
-                   "edges_per_s": (g.m / 2) / sum(tm)})
+        cpu_static(out, tag, g, off, tgt, ref, cpu_spec)
 
 
 def config1(args):
@@ -99,7 +138,7 @@ def config1(args):
     # link companion async+compress
     static_config("1: static RMAT s16 ef8", g, ["none+rem_cas+naive+splice", "none+async+compress",
                                                  "kout+rem_cas+halve+splice"], args.reps, args.out,
-                  cpu_spec=("none", "rem_cas", "naive", "splice"))
+                  cpu_spec=["none+rem_cas+naive+splice", "kout+rem_cas+halve+splice"])
 
 
 def config3(args):
@@ -111,7 +150,12 @@ def config3(args):
     # LDD's shift rate has no reference default: sweep it, named in the spec string
     specs = ["ldd+sv", "ldd+lt_prs", "ldd+lt_crfa", "none+sv", "none+lt_prs", "none+lt_crfa", "kout+sv",
              "bfs+sv"] + [f"ldd({b})+sv" for b in (0.1, 0.3, 0.5, 0.8)]
-    static_config(f"3: 3-D grid {side}^3 natural ids", g, specs, args.reps, args.out)
+    # the port has no LDD (absent from the reference): its CPU baseline is
+    # the oracle-checkable companions
+    cpu = ["none+sv", "none+lt_prs", "kout+sv"] if args.cpu else None
+    static_config(f"3: 3-D grid {side}^3 natural ids", g, specs, args.reps, args.out, cpu_spec=cpu)
+    if args.no_permuted:
+        return
     # randomly relabelled copy: exercises the high-diameter behaviour
     n = side ** 3
     perm = torch.randperm(n, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
@@ -119,7 +163,7 @@ def config3(args):
     g2 = build_csr(EdgeList(n, perm[e]), keep_host=False)
     static_config(f"3: 3-D grid {side}^3 permuted ids", g2,
                   ["ldd+sv", "ldd+lt_prs", "none+sv", "none+lt_prs", "kout+sv"]
-                  + [f"ldd({b})+sv" for b in (0.1, 0.3, 0.5, 0.8)], args.reps, args.out)
+                  + [f"ldd({b})+sv" for b in (0.1, 0.3, 0.5, 0.8)], args.reps, args.out, cpu_spec=cpu)
 
 
 def config4(args):
@@ -147,7 +191,7 @@ def config4(args):
     comps_init = comps - int((np.diff(offh) == 0).sum())
     g_deg_host = offh
     del tgth
-    for text in ["none+async+halve", "none+rem_cas+halve+split", "none+sv", "none+lt_prs"]:
+    for text in want(["none+async+halve", "none+rem_cas+halve+split", "none+sv", "none+lt_prs"]):
         spec = parse_spec(text)
         best = None
         for rep in range(args.reps_incr):
@@ -186,11 +230,28 @@ def config4(args):
         inited = int((np.diff(g_deg_host) > 0).sum())
         hooks = inited - comps_init
         alg = 16 * total + 4 * hooks + (total + 7) // 8
-        emit(args.out, {"config": f"4: incremental RMAT s{scale} ef8, {bs}-edge insert batches", "spec": text,
+        tag4 = f"4: incremental RMAT s{scale} ef8, {bs}-edge insert batches"
+        emit(args.out, {"config": tag4, "spec": text,
                         "n": n, "inserts": total, "batches": (total + bs - 1) // bs, "seconds": best,
                         "ops_per_s": total / best, "labels_bit_exact": ok, "components": comps_init,
                         "alg_bytes": alg, "hbm_gbs": alg / best / 1e9,
                         "hbm_frac": alg / best / 1e9 / hbm_peak()})
+        if args.cpu and text in ("none+async+halve", "none+rem_cas+halve+split"):
+            # bounded sample: the first two batches of the same
+            # stream into an empty s26-capacity parent array, C/OpenMP port
+            threads = oracle.max_threads()
+            P = np.full(n, n, dtype=np.int32)
+            nb = min(2, (total + bs - 1) // bs)
+            secs, done = 0.0, 0
+            for b0 in range(0, nb * bs, bs):
+                hu = us[b0:b0 + bs].cpu().numpy()
+                hv = vs[b0:b0 + bs].cpu().numpy()
+                parts = text.split("+")
+                secs += oracle.incr_insert(n, P, hu, hv, parts[1], parts[2],
+                                           parts[3] if len(parts) > 3 else "none", threads)
+                done += len(hu)
+            cpu_line(args.out, tag4, text, secs, done, "ops_per_s", threads,
+                     f"the first {nb} batches ({done} inserts) of the stream")
 
 
 def config5(args):
@@ -202,16 +263,32 @@ def config5(args):
     g = build_csr(gen_uniform_pairs(lg, 4 * n, seed=1), keep_host=False)
     off, tgt = host_csr(g)
     ref, comps = oracle.components(n, off, tgt)
-    for text in ["bfs+async+halve", "kout+async+halve", "none+async+halve"]:
+    tag5 = f"5: spanning forest uniform 2^{lg} deg 8"
+    for text in want(["bfs+async+halve", "kout+async+halve", "none+async+halve"]):
         spec = parse_spec(text)
         df, st = spanning_forest_device(g, spec)
         rep = oracle.check_forest(n, off, tgt, df.fu.cpu().numpy(), df.fv.cpu().numpy(), ref)
         med, _ = ev_time(lambda: spanning_forest_device(g, spec), args.reps)
-        emit(args.out, {"config": f"5: spanning forest uniform 2^{lg} deg 8", "spec": text, "n": n,
-                        "m_directed": g.m, "seconds": med, "edges_per_s": (g.m / 2) / med,
-                        "forest_clauses": rep["clauses"], "forest_ok": rep["passed"],
-                        "components": comps, "forest_edges": n - st.component_count,
-                        "phase_ms": {k: v * 1e3 for k, v in st.phase_times.items()}})
+        rec = {"config": tag5, "spec": text, "n": n,
+               "m_directed": g.m, "seconds": med, "edges_per_s": (g.m / 2) / med,
+               "forest_clauses": rep["clauses"], "forest_ok": rep["passed"],
+               "components": comps, "forest_edges": n - st.component_count,
+               "insp_sample": st.edge_inspections.get("sample", 0),
+               "insp_finish": st.edge_inspections.get("finish", 0),
+               "phase_ms": {k: v * 1e3 for k, v in st.phase_times.items()}}
+        rec.update(roofline_fields(alg_bytes_static(n, rec["insp_sample"], rec["insp_finish"],
+                                                    spec.sample.value != "none", 0, n - st.component_count), med))
+        emit(args.out, rec)
+    if args.cpu:
+        from paper_2008_11839_b200.api import bfs_source
+        threads = oracle.max_threads()
+        spec = parse_spec("bfs+async+halve")
+        src = bfs_source(g, spec.bfs_probes, spec.seed)
+        for text in ["bfs+async+halve", "none+async+halve"]:
+            lab, st, tm, (fu, fv) = oracle.pipeline(n, off, tgt, text, threads, forest=True, bfs_source=src)
+            ok = oracle.check_forest(n, off, tgt, fu, fv, ref)["passed"]
+            cpu_line(args.out, tag5, text, sum(tm), g.m / 2, "edges_per_s", threads, "the whole workload",
+                     {"forest_ok": ok, "labels_bit_exact": bool(np.array_equal(lab.astype(np.int64), ref))})
 
 
 def main():
@@ -224,7 +301,13 @@ def main():
     ap.add_argument("--batch", type=int, default=10_000_000)
     ap.add_argument("--uniform-log2n", type=int, default=27)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--specs", default=None, help="comma list: only these specs")
+    ap.add_argument("--no-permuted", action="store_true")
+    ap.add_argument("--cpu", type=int, default=1, help="1: time the C/OpenMP port beside each config")
     args = ap.parse_args()
+    global SPECS
+    if args.specs:
+        SPECS = set(args.specs.split(","))
     import torch
     torch.cuda.set_device(0)
     for c in args.configs.split(","):

@@ -200,7 +200,8 @@ int gc_union_edges_list(int32_t* parent, int64_t n, const int32_t* us,
  *     appends its (u, v) to out_u/out_v (capacity n) and bumps *out_count
  *     (device).  stats->insp_sample = this block's sample inspections.
  *   -- exchange: all-gather the merging edges, union the foreign ones --
- *   gc_shard_finish: compress, most-frequent label, active gather (identical
+ *   gc_shard_finish (also after the distributed BFS sampler, gc_dbfs_*):
+ *     compress, most-frequent label, active gather (identical
  *     on every rank once the sampled partitions are merged), then the
  *     union-find finish over the block's active rows, recording merging edges
  *     the same way.  stats: insp_finish (block), l_max, lmax_count, n_active.
@@ -249,6 +250,47 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits,
                   const int64_t* giant_labels, int32_t nranks,
                   const int32_t* us, const int32_t* vs, int64_t k,
                   const gc_spec* spec, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- distributed BFS sampling (csrc/dbfs.cu, BASELINE config 5)
+ * The reference BFS (sampling.py:120-172) as a level-synchronous traversal
+ * over row-sharded CSR.  Each rank owns rows [row_lo, row_hi); frontier,
+ * visited, marks and next are n-bit bitmaps ((n+31)/32 words); the frontier
+ * and visited bitmaps are replicated (identical on every rank).  parent is a
+ * u32[n] (only the owned entries are meaningful).  A level is
+ *   top-down: gc_dbfs_marks (unvisited neighbours of the block's frontier
+ *     rows: marks bitmap + ascending id list out_ids, capacity n, count in
+ *     *out_count, device) -> all-gather the id lists -> gc_dbfs_merge_marks
+ *     for each foreign list -> gc_dbfs_claim(marks);
+ *   bottom-up: gc_dbfs_claim(marks = NULL).
+ * gc_dbfs_claim: every unvisited (marked) vertex of the block takes the
+ *   first frontier vertex of its ascending row as parent (the reference's
+ *   smallest-discoverer rule) and sets its bit in next (zeroed first);
+ *   *count (device) = vertices claimed.  The ranks' next bitmaps are
+ *   disjoint, so their all-reduce SUM is their union; then
+ * gc_dbfs_advance: visited |= next, frontier := next, *count = |next|.
+ * gc_dbfs_finish: labels[v] = min reached id for reached v, else v (every
+ *   vertex); the block's tree edges (parent[v], v) for reached v != source
+ *   into out_u/out_v (capacity n, *out_count device); *insp (device) = degree
+ *   sum of the block's reached rows (the reference's sample inspections,
+ *   summed over ranks).  ws >= 16 bytes.  Malformed merged ids set *bad. */
+int gc_dbfs_init(int64_t n, int64_t source, uint32_t* frontier, uint32_t* visited,
+                 uint32_t* parent, void* stream);
+int gc_dbfs_marks(const gc_csr* g, int64_t row_lo, int64_t row_hi,
+                  const uint32_t* frontier, const uint32_t* visited,
+                  uint32_t* marks, int32_t* out_ids,
+                  unsigned long long* out_count, void* stream);
+int gc_dbfs_merge_marks(int64_t n, const int32_t* ids, int64_t k, uint32_t* marks,
+                        unsigned int* bad, void* stream);
+int gc_dbfs_claim(const gc_csr* g, int64_t row_lo, int64_t row_hi,
+                  const uint32_t* frontier, const uint32_t* visited,
+                  const uint32_t* marks, uint32_t* parent, uint32_t* next,
+                  unsigned long long* count, void* stream);
+int gc_dbfs_advance(int64_t n, uint32_t* visited, uint32_t* frontier,
+                    const uint32_t* next, unsigned long long* count, void* stream);
+int gc_dbfs_finish(const gc_csr* g, int64_t row_lo, int64_t row_hi,
+                   const uint32_t* visited, const uint32_t* parent, int32_t* labels,
+                   int32_t* out_u, int32_t* out_v, unsigned long long* out_count,
+                   unsigned long long* insp, void* ws, size_t ws_bytes, void* stream);
 
 /* Graph contract check (graphs.py:43-51) on device arrays: offsets start at
  * 0, never decrease and end at m; every target in [0, n) -> else

@@ -98,6 +98,13 @@ _SIGNATURES = {
     "gc_shard_summary": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "gc_shard_absorb": (C.c_int, [_VP, _I64, _VP, _VP, C.c_int32, _VP, _VP, _SZ, _VP]),
     "gc_shard_join": (C.c_int, [_VP, _I64, _VP, _VP, C.c_int32, _VP, _VP, _I64, C.POINTER(Spec), _VP, _SZ, _VP]),
+    "gc_dbfs_init": (C.c_int, [_I64, _I64, _VP, _VP, _VP, _VP]),
+    "gc_dbfs_marks": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gc_dbfs_merge_marks": (C.c_int, [_I64, _VP, _I64, _VP, _VP, _VP]),
+    "gc_dbfs_claim": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gc_dbfs_advance": (C.c_int, [_I64, _VP, _VP, _VP, _VP, _VP]),
+    "gc_dbfs_finish": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ,
+                                 _VP]),
     "gc_check_csr": (C.c_int, [C.POINTER(Csr), _VP]),
     "gc_find_batch": (C.c_int, [_VP, _I64, _VP, _I64, C.c_int32, _VP, _VP]),
     "gc_canonical_labels": (C.c_int, [_VP, _I64, _VP, _SZ, _VP]),

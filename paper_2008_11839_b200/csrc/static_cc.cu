@@ -635,10 +635,14 @@ int gc_label_finalization(int32_t* labels, int64_t n, void* ws, size_t ws_bytes,
 // ---- sharded two-phase building blocks ------------------------
 namespace {
 
-void check_shard_spec(const gc_spec* spec) {
+// finish = true: the labels come from any sharded sampler, including the
+// distributed BFS (gc_dbfs_*), which has no gc_shard_sample form
+void check_shard_spec(const gc_spec* spec, bool finish = false) {
   require(is_union_finish(spec->finish), GC_ERR_CONFIG, "sharded pipeline needs a union-find finish");
-  require(spec->sample == GC_SAMPLE_NONE || spec->sample == GC_SAMPLE_KOUT || spec->sample == GC_SAMPLE_HB,
-          GC_ERR_CONFIG, "sharded sampling supports none / k-out / hb");
+  require(spec->sample == GC_SAMPLE_NONE || spec->sample == GC_SAMPLE_KOUT || spec->sample == GC_SAMPLE_HB ||
+              (finish && spec->sample == GC_SAMPLE_BFS),
+          GC_ERR_CONFIG, finish ? "sharded sampling supports none / k-out / hb / bfs"
+                                : "sharded sampling supports none / k-out / hb (bfs: gc_dbfs_*)");
   require(spec->sample != GC_SAMPLE_KOUT || spec->kout_mode == GC_KOUT_FIRST_K, GC_ERR_CONFIG,
           "sharded k-out needs FIRST_K (random offsets are drawn over the whole graph)");
 }
@@ -694,7 +698,7 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_
                     size_t ws_bytes, void* stream) {
   return guarded([&] {
     check_static_args(g, spec, parent);
-    check_shard_spec(spec);
+    check_shard_spec(spec, true);
     require(out_u && out_v && out_count, GC_ERR_ARG, "null merging-edge output");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     GC_CUDA(cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st));

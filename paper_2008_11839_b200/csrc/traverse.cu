@@ -14,12 +14,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "pipeline.cuh"
 #include "samplers.h"
 
 namespace gc {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -631,6 +634,154 @@ __global__ void k_ldd_label(const uint32_t* cluster, const int32_t* mins, int32_
     P[v] = mins[cluster[v]];
 }
 
+// All LDD rounds in one persistent cooperative launch (one CTA group per
+// SM, grid-wide barrier between rounds).  Round r expands the frontier of
+// round r-1 and starts bucket r's centres; the claim word is the packed
+// (round << 32 | cluster) key resolved by one 64-bit atomicMin: the earliest
+// round wins, the smallest cluster within it.  The frontier is expanded
+// edge-parallel inside each warp (32 frontier vertices, their rows
+// concatenated, one edge per lane per step: a lane's source is found by a
+// binary search over the warp's degree prefix), so a round costs one chain of
+// claim latencies instead of a lane walking its whole row; fresh claims go to
+// a block queue flushed once per round.  Per-round frontier counters form a
+// ring of three; the first-round start and the end of the rounds are read on
+// the device, so the sampler needs no host round trip.  After the rounds,
+// the same launch takes the minimum member of each cluster and writes the
+// labels.
+constexpr unsigned long long kFreeKey = ~0ull;
+// reads of words other CTAs wrote earlier in the same launch go to L2
+__device__ __forceinline__ unsigned long long ld_rlx_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool claim_key(unsigned long long* key, int32_t x, unsigned long long mine) {
+  const unsigned long long k = ld_rlx_u64(key + x);
+  if (k <= mine) return false;  // an earlier round, or a smaller claimant of this one
+  return atomicMin(key + x, mine) == kFreeKey;
+}
+
+__global__ void __launch_bounds__(kTB)
+k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n,
+              unsigned long long* key, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
+              const int32_t* dmax_bits, int32_t max_rounds, int32_t* q0, int32_t* q1, unsigned long long* ring,
+              unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ BlockQueue<kQCap> bq;
+  bq.init();
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (int64_t(blockIdx.x) * kTB + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * kTB) >> 5;
+  const int64_t gtid = int64_t(blockIdx.x) * kTB + threadIdx.x;
+  const int64_t gthreads = int64_t(gridDim.x) * kTB;
+  int32_t last_start = int32_t(floorf(__int_as_float(*dmax_bits)));
+  last_start = last_start < 0 ? 0 : (last_start > max_rounds ? max_rounds : last_start);
+  unsigned long long my_insp = 0;
+  int32_t r = 0;
+  for (;; ++r) {
+    int32_t* qin = (r & 1) ? q0 : q1;  // round r reads the queue round r-1 wrote
+    int32_t* qout = (r & 1) ? q1 : q0;
+    unsigned long long* cout = ring + (r + 1) % 3;
+    if (gtid == 0) ring[(r + 2) % 3] = 0;  // read by nobody this round; written next round
+    const int64_t count = r > 0 ? int64_t(*reinterpret_cast<volatile unsigned long long*>(ring + r % 3)) : 0;
+    for (int64_t wb = gwarp * 32; wb < count; wb += nwarps * 32) {
+      const int64_t i = wb + lane;
+      unsigned long long c = 0;
+      int64_t b = 0;
+      int32_t d = 0;
+      if (i < count) {
+        const int32_t f = ld_acq(qin + i);
+        c = ld_rlx_u64(key + f) & 0xffffffffull;  // final since round r-1
+        b = off[f];
+        d = int32_t(off[f + 1] - b);
+        my_insp += d;
+      }
+      int32_t incl = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const unsigned long long mine_round = (unsigned long long)r << 32;
+      for (int32_t e0 = 0; e0 < total; e0 += 32) {
+        const int32_t e = e0 + lane;
+        // source lane: the first lane whose inclusive prefix exceeds e
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+          if (v <= e) lo += step;
+        }
+        const int src = lo > 31 ? 31 : lo;
+        const int32_t se = __shfl_sync(0xffffffffu, incl, src);
+        const int32_t sd = __shfl_sync(0xffffffffu, d, src);
+        const int64_t sb = __shfl_sync(0xffffffffu, b, src);
+        const unsigned long long sc = __shfl_sync(0xffffffffu, c, src);
+        bool fresh = false;
+        int32_t x = 0;
+        if (e < total) {
+          x = tgt[sb + (e - (se - sd))];
+          fresh = claim_key(key, x, mine_round | sc);
+        }
+        bq.push(fresh, x, qout, cout);
+      }
+    }
+    if (r <= last_start) {  // centres of bucket r
+      const int64_t lo = boff[r], hi = boff[r + 1];
+      for (int64_t b0 = lo + int64_t(blockIdx.x) * kTB; b0 < hi; b0 += gthreads) {
+        const int64_t i = b0 + threadIdx.x;
+        int32_t v = 0;
+        bool fresh = false;
+        if (i < hi) {
+          v = order[i];
+          fresh = claim_key(key, v, ((unsigned long long)r << 32) | uint32_t(v));
+        }
+        bq.push(fresh, v, qout, cout);
+      }
+    }
+    bq.flush(qout, cout);
+    grid.sync();
+    const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(cout);
+    if (next == 0 && r >= last_start) break;
+  }
+  block_add<kTB>(insp, my_insp);
+  if (gtid == 0 && rounds_out) *rounds_out = (unsigned long long)(r + 1);
+  // labels: minimum member id per cluster (warp-elected atomicMin over the
+  // lanes holding the same cluster), then P[v] = mins[cluster(v)]
+  for (int64_t v = gtid; v < n; v += gthreads) mins[v] = INT_MAX;
+  grid.sync();
+  for (int64_t base = gtid - lane; base < n; base += gthreads) {
+    const int64_t v = base + lane;
+    const uint32_t c = v < n ? uint32_t(ld_rlx_u64(key + v)) : kFreeCluster;
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    if (v < n && lane == __ffs(int(peers)) - 1) atomicMin(mins + c, int32_t(v));
+  }
+  grid.sync();
+  for (int64_t v = gtid; v < n; v += gthreads) P[v] = ld_acq(mins + uint32_t(ld_rlx_u64(key + v)));
+}
+
+// every vertex unclaimed, start round per vertex + bucket histogram
+__global__ void __launch_bounds__(kEwBlock)
+k_ldd_start_key(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
+                unsigned long long* key, unsigned int* bcount) {
+  __shared__ unsigned int hist[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const float dmax = __int_as_float(*dmax_bits);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+    float r = floorf(dmax - ldd_delta(seed, v, beta));
+    r = r < 0.f ? 0.f : (r > float(kLddMaxRounds) ? float(kLddMaxRounds) : r);
+    start[v] = uint16_t(r);
+    key[v] = kFreeKey;
+    atomicAdd(hist + int(r), 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+    if (hist[i]) atomicAdd(bcount + i, hist[i]);
+}
+
 #define TL(kernel, grid, block, ...) ((kernel<<<grid, block, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
 
 }  // namespace
@@ -803,6 +954,16 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   GC_CHECK_LAUNCH();
 }
 
+// GC_LDD_PERSIST=0 selects the launch-per-round form (k_ldd_round +
+// k_bits_to_queue, host termination check every 16 rounds)
+bool ldd_persistent() {
+  static const bool p = [] {
+    const char* e = getenv("GC_LDD_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  return p;
+}
+
 void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
              cudaStream_t st) {
   const int32_t n = int32_t(g.n);
@@ -815,6 +976,42 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   GC_CUDA(cudaMemsetAsync(bcount, 0, (kBuckets + 1) * sizeof(unsigned int), st));
   const int ge = grid_for(n, kEwBlock, 8);
   TL(k_ldd_delta_max, ge, kEwBlock, n, s.seed, beta, dmax);
+  if (ldd_persistent()) {
+    // one cooperative launch runs every round and the labelling (no host
+    // round trip); the start-round buckets come from the three passes below
+    TL(k_ldd_start_key, ge, kEwBlock, n, s.seed, beta, dmax, w.start, w.key, bcount);
+    TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
+    TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
+       cursor, w.order);
+    GC_CUDA(cudaMemsetAsync(w.stat, 0, 3 * sizeof(unsigned long long), st));
+    static int per_sm = 0;
+    if (!per_sm) {
+      GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ldd_persist, kTB, 0));
+      if (per_sm < 1) throw Error(GC_ERR_CUDA, "LDD persistent kernel does not fit on an SM");
+    }
+    const int64_t* off = g.offsets;
+    const int32_t* tgt = g.targets;
+    unsigned long long* key = w.key;
+    const int32_t* order = w.order;
+    const unsigned int* boff = w.boff;
+    const int32_t* dmb = dmax;
+    int32_t maxr = kLddMaxRounds;
+    int32_t* q0 = w.q0;
+    int32_t* q1 = w.q1;
+    unsigned long long* ring = w.stat;
+    unsigned long long* insp = ctr + C_INSP_SAMPLE;
+    int32_t* mins = w.q0;  // the queues are dead once the rounds end
+    int32_t* Pp = P;
+    unsigned long long* rounds_out = w.stat + 3;
+    int32_t nn = n;
+    void* args[] = {&off, &tgt, &nn, &key, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
+                    &rounds_out};
+    GC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ldd_persist), dim3(num_sms() * per_sm),
+                                        dim3(kTB), args, 0, st));
+    ::gc::count_launch();
+    GC_CHECK_LAUNCH();
+    return;
+  }
   // the claim buffer (8n bytes) holds the u32 clusters and the u16 claim rounds
   uint32_t* cluster = reinterpret_cast<uint32_t*>(w.key);
   uint16_t* croud = reinterpret_cast<uint16_t*>(cluster + n);

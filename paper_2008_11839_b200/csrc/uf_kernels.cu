@@ -138,6 +138,153 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
   }
 }
 
+// Async union (dset.py:222-234) over a COO batch with K unions per thread
+// walked in lock step.  One union is a chain of dependent parent reads (the
+// endpoint slots are random DRAM reads once the parent array outgrows L2;
+// config 4's is 268 MB), so a thread that owns one union keeps one read in
+// flight and the batch is latency-bound (ncu, k_union_coo at RMAT s26: DRAM
+// 8.6%, IPC 0.58).  Here each step issues the next read of all 2K find chains
+// of the thread together, then consumes them.
+//
+// A find chain is the hop sequence x -> P[x] -> ...; the compression writes
+// of split / halve (dset.py:126-147) fall out of the hop sequence: split
+// swings P[prev] from x to P[x] at every hop, halving at every other hop.
+// Their CAS results are never consumed (a failed compression CAS is dropped,
+// as in the reference) and the walk continues from the value it read — an
+// ancestor either way, so the root found is the same.  A link is
+// CAS(P[hi], hi, lo) on the two roots; a failed link resumes the hi chain
+// from the value the CAS saw (hi's new parent) and the lo chain from lo.
+template <class R, int K, bool WEAK>
+__global__ void __launch_bounds__(256)
+k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
+                      const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad) {
+  static_assert(R::kUnion == GC_FINISH_ASYNC, "lock-step form of the async rule");
+  constexpr int F = R::kFind;
+  int32_t* P = s.P;
+  // L1-cacheable reads (static batches) only for the first hops: after that
+  // every read goes to L2, so a stale line cannot stall a retry loop
+  int it = 0;
+  auto ld = [&](const int32_t* p) { return (WEAK && it < 8) ? ld_weak(p) : ld_acq(p); };
+  const int64_t span = int64_t(blockDim.x) * K;
+  for (int64_t base = int64_t(blockIdx.x) * span; base < k; base += int64_t(gridDim.x) * span) {
+    int32_t eu[K], ev[K];     // endpoints (forest records)
+    int32_t x[K][2];          // chain position
+    int32_t px[K][2];         // P[x] once read (valid when have bit set)
+    int32_t pv[K][2];         // previous node (split / halve writes), -1 = none
+    unsigned have = 0;        // bit 2j+c: px[j][c] holds P[x[j][c]]
+    unsigned live = 0;        // bit 2j+c: chain still walking
+    unsigned slot = 0;        // bit j: union j unfinished
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int64_t i = base + int64_t(j) * blockDim.x + threadIdx.x;
+      eu[j] = ev[j] = 0;
+      if (i < k && !(skip && skip[i])) {
+        eu[j] = ldg32(us + i);
+        ev[j] = ldg32(vs + i);
+        if (bad && (uint32_t(eu[j]) >= uint32_t(s.n) || uint32_t(ev[j]) >= uint32_t(s.n))) {
+          atomicOr(bad, 1u);  // malformed pair: never touches the parent array
+        } else {
+          slot |= 1u << j;
+        }
+      }
+      x[j][0] = eu[j];
+      x[j][1] = ev[j];
+      pv[j][0] = pv[j][1] = -1;
+      px[j][0] = px[j][1] = 0;
+    }
+    // endpoint reads, all issued together; lazy init (driver.py:620-625)
+    // of the slots still holding the sentinel
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (slot >> j & 1u) {
+        px[j][0] = ld(P + x[j][0]);
+        px[j][1] = ld(P + x[j][1]);
+      }
+    if (sentinel >= 0) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if ((slot >> j & 1u) && px[j][c] == sentinel) {
+            const int32_t o = atomicCAS(P + x[j][c], sentinel, x[j][c]);
+            px[j][c] = o == sentinel ? x[j][c] : o;
+          }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (slot >> j & 1u) {
+        have |= 3u << (2 * j);
+        live |= 3u << (2 * j);
+      }
+    for (it = 0; slot; ++it) {
+      // 1. issue every missing parent read of a walking chain
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const unsigned b = 1u << (2 * j + c);
+          if ((live & b) && !(have & b)) px[j][c] = ld(P + x[j][c]);
+        }
+      have |= live;
+      // 2. advance the chains one hop (compression writes fire and forget)
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const unsigned b = 1u << (2 * j + c);
+          if (!(live & b)) continue;
+          const int32_t nx = px[j][c];
+          if (nx == x[j][c]) {
+            live &= ~b;  // x is a root
+            continue;
+          }
+          if constexpr (F == GC_FIND_SPLIT || F == GC_FIND_HALVE) {
+            if (pv[j][c] >= 0) atomicCAS(P + pv[j][c], x[j][c], nx);
+            pv[j][c] = (F == GC_FIND_HALVE && pv[j][c] >= 0) ? -1 : x[j][c];
+          }
+          x[j][c] = nx;
+          have &= ~b;
+        }
+      // 3. link the unions whose two roots are known (all CASes issued first)
+      int32_t old[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        old[j] = -1;
+        if ((slot >> j & 1u) && !(live >> (2 * j) & 3u)) {
+          const int32_t ru = x[j][0], rv = x[j][1];
+          if (ru == rv) {
+            slot &= ~(1u << j);
+          } else {
+            const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
+            old[j] = atomicCAS(P + hi, hi, lo);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (old[j] < 0) continue;
+        const int32_t ru = x[j][0], rv = x[j][1];
+        const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
+        if (old[j] == hi) {
+          record<R::kForest>(s, hi, eu[j], ev[j]);
+          slot &= ~(1u << j);
+        } else {
+          // hi was linked meanwhile: resume both finds from the roots
+          // (register selects, no dynamic index into the chain arrays)
+          const bool h0 = ru > rv;
+          x[j][0] = h0 ? hi : lo;
+          x[j][1] = h0 ? lo : hi;
+          px[j][0] = old[j];
+          px[j][1] = old[j];
+          pv[j][0] = pv[j][1] = -1;
+          have = (have & ~(3u << (2 * j))) | (1u << (2 * j + (h0 ? 0 : 1)));
+          live |= 3u << (2 * j);
+        }
+      }
+    }
+  }
+}
+
 // read-only root chase; an uninitialised slot is its own root (driver.py:556-564)
 __device__ __forceinline__ int32_t chase(const int32_t* P, int32_t x, int32_t sentinel) {
   int32_t px = ld_acq(P + x);
@@ -238,6 +385,30 @@ struct RowsLaunch {
   }
 };
 
+// unions per thread of the lock-step async kernel (GC_COO_MLP; 0 selects
+// the one-union-per-thread k_union_coo)
+int coo_mlp() {
+  static const int k = [] {
+    const char* e = getenv("GC_COO_MLP");
+    return e ? atoi(e) : 4;
+  }();
+  return k;
+}
+
+template <class R, int K>
+void launch_mlp(const UFState& s, const CooUnionArgs& a, cudaStream_t st) {
+  int64_t blocks = (a.k + 256 * K - 1) / (256 * K);
+  const int64_t cap = int64_t(num_sms()) * 8 * 16;
+  if (blocks > cap) blocks = cap;
+  if (s.weak)
+    (k_union_coo_async_mlp<R, K, true><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel,
+                                                                     a.bad), ::gc::count_launch());
+  else
+    (k_union_coo_async_mlp<R, K, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
+                                                                      a.init_sentinel, a.bad), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 struct CooLaunch {
   const CooUnionArgs& a;
   cudaStream_t st;
@@ -246,6 +417,14 @@ struct CooLaunch {
     if (a.k <= 0) return;
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     s.weak = a.init_sentinel < 0;
+    if constexpr (R::kUnion == GC_FINISH_ASYNC && R::kFind != GC_FIND_COMPRESS) {
+      switch (coo_mlp()) {
+        case 2: return launch_mlp<R, 2>(s, a, st);
+        case 4: return launch_mlp<R, 4>(s, a, st);
+        case 8: return launch_mlp<R, 8>(s, a, st);
+        default: break;
+      }
+    }
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;

@@ -240,6 +240,90 @@ class GpuEngine:
                                       vs.data_ptr() if k else None, k, C.byref(low.s), ws.data_ptr(), ws.numel(),
                                       _stream()))
 
+    # distributed BFS (gc_dbfs_*): state = dict of device buffers
+    def dbfs_init(self, n, source):
+        from . import _native as N
+        from .api import _stream
+        torch = _torch()
+        words = max((n + 31) // 32, 1)
+        st = {"n": n,
+              "F": torch.zeros(words, dtype=torch.int32, device="cuda"),
+              "V": torch.zeros(words, dtype=torch.int32, device="cuda"),
+              "M": torch.zeros(words, dtype=torch.int32, device="cuda"),
+              "N": torch.zeros(words, dtype=torch.int32, device="cuda"),
+              "par": torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
+              "ids": torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
+              "cnt": torch.zeros(1, dtype=torch.int64, device="cuda"),
+              "bad": torch.zeros(1, dtype=torch.int32, device="cuda")}
+        N.check(N.lib().gc_dbfs_init(n, source, st["F"].data_ptr(), st["V"].data_ptr(), st["par"].data_ptr(),
+                                     _stream()))
+        return st
+
+    def dbfs_marks(self, shard, st):
+        import ctypes as C
+        from . import _native as N
+        from .api import _csr, _stream
+        csr, _keep = _csr(shard)
+        lo, hi = getattr(shard, "row_block", (0, shard.n))
+        N.check(N.lib().gc_dbfs_marks(C.byref(csr), lo, hi, st["F"].data_ptr(), st["V"].data_ptr(),
+                                      st["M"].data_ptr(), st["ids"].data_ptr(), st["cnt"].data_ptr(), _stream()))
+        return st["ids"][:int(st["cnt"].item())]
+
+    def dbfs_merge_marks(self, st, ids):
+        from . import _native as N
+        from .api import _stream
+        ids = ids.to("cuda", dtype=__import__("torch").int32).contiguous()
+        if ids.numel():
+            N.check(N.lib().gc_dbfs_merge_marks(st["n"], ids.data_ptr(), ids.numel(), st["M"].data_ptr(),
+                                                st["bad"].data_ptr(), _stream()))
+
+    def dbfs_claim(self, shard, st, marks):
+        import ctypes as C
+        from . import _native as N
+        from .api import _csr, _stream
+        csr, _keep = _csr(shard)
+        lo, hi = getattr(shard, "row_block", (0, shard.n))
+        N.check(N.lib().gc_dbfs_claim(C.byref(csr), lo, hi, st["F"].data_ptr(), st["V"].data_ptr(),
+                                      st["M"].data_ptr() if marks else None, st["par"].data_ptr(),
+                                      st["N"].data_ptr(), st["cnt"].data_ptr(), _stream()))
+        return st["N"]
+
+    def dbfs_advance(self, st):
+        from . import _native as N
+        from .api import _stream
+        N.check(N.lib().gc_dbfs_advance(st["n"], st["V"].data_ptr(), st["F"].data_ptr(), st["N"].data_ptr(),
+                                        st["cnt"].data_ptr(), _stream()))
+        if int(st["bad"].item()):
+            from .errors import MalformedInputError
+            raise MalformedInputError("a merged frontier mark lies outside [0, n)")
+        return int(st["cnt"].item())
+
+    def dbfs_finish(self, shard, st):
+        import ctypes as C
+        from . import _native as N
+        from .api import _csr, _stream, _workspace
+        torch = _torch()
+        n = st["n"]
+        csr, _keep = _csr(shard)
+        lo, hi = getattr(shard, "row_block", (0, n))
+        labels = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        fu = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        fv = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        insp = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws = _workspace(64)
+        N.check(N.lib().gc_dbfs_finish(C.byref(csr), lo, hi, st["V"].data_ptr(), st["par"].data_ptr(),
+                                       labels.data_ptr(), fu.data_ptr(), fv.data_ptr(), st["cnt"].data_ptr(),
+                                       insp.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+        k = int(st["cnt"].item())
+        return labels[:n], fu[:k], fv[:k], int(insp.item())
+
+    def row_degrees(self, shard, ids):
+        """Degrees of the given vertices in this rank's rows (0 elsewhere)."""
+        torch = _torch()
+        off, _tgt = shard.device_arrays()
+        ids = torch.as_tensor(ids, dtype=torch.int64, device=off.device)
+        return (off[ids + 1] - off[ids]).to(torch.int64)
+
     def finalize(self, parent):
         import ctypes as C
         from . import _native as N
@@ -319,6 +403,27 @@ def all_gather_pairs(us, vs, group=None):
     return [(b[0, :c], b[1, :c]) for b, c in zip(bufs, counts)]
 
 
+def all_gather_ids(ids, group=None):
+    """All-gather variable-length int32 id lists (counts, then padded data)."""
+    torch = _torch()
+    dist = _dist()
+    dev = _comm_device(group)
+    world = dist.get_world_size(group)
+    k = torch.tensor([ids.numel()], dtype=torch.int64, device=dev)
+    ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(ks, k, group=group)
+    counts = [int(x.item()) for x in ks]
+    kmax = max(counts) if counts else 0
+    if kmax == 0:
+        return [ids[:0] for _ in range(world)]
+    mine = torch.full((kmax,), -1, dtype=torch.int32, device=dev)
+    if ids.numel():
+        mine[:ids.numel()] = ids.to(dev, torch.int32)
+    bufs = [torch.empty(kmax, dtype=torch.int32, device=dev) for _ in range(world)]
+    dist.all_gather(bufs, mine, group=group)
+    return [b[:c] for b, c in zip(bufs, counts)]
+
+
 # -------------------------------------------------------- sharded static / forest
 
 @dataclass
@@ -385,11 +490,100 @@ def sharded_spanning_forest(g_shard, spec: AlgorithmSpec, group=None, engine=Non
 def _check_two_phase_spec(spec: AlgorithmSpec):
     if not spec.is_union_finish():
         raise ConfigError(f"sharded connectivity needs a union-find finish; '{format_spec(spec)}' is not")
-    if spec.sample not in (SampleKind.NONE, SampleKind.KOUT, SampleKind.HB):
-        raise ConfigError(f"sharded sampling supports none / kout / hb, not '{spec.sample.value}' "
-                          "(BFS / LDD need a distributed traversal)")
+    if spec.sample not in (SampleKind.NONE, SampleKind.KOUT, SampleKind.HB, SampleKind.BFS):
+        raise ConfigError(f"sharded sampling supports none / kout / hb / bfs, not '{spec.sample.value}' "
+                          "(LDD has no distributed form)")
     if spec.sample is SampleKind.KOUT and spec.kout_mode is not KOutMode.FIRST_K:
         raise ConfigError("sharded k-out needs FIRST_K: random offsets are drawn over the whole graph")
+
+
+# ------------------------------------------------------- distributed BFS
+
+# Beamer's switch (as the single-GPU sampler, traverse.cu): bottom-up once
+# the frontier is more than 1/alpha of the unreached vertices, back to
+# top-down below n/beta frontier vertices
+DBFS_ALPHA = 14
+DBFS_BETA = 24
+
+
+def global_bfs_source(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> int:
+    """sampling.py:130-132 over a row-sharded graph: the highest-degree vertex
+    of the seeded probe set (ties: the smaller id), degrees summed over the
+    ranks that own the probes' rows."""
+    torch = _torch()
+    dist = _dist()
+    engine = engine or GpuEngine()
+    n = g_shard.n
+    probes = np.unique(np.random.default_rng(spec.seed).integers(0, n, size=spec.bfs_probes))
+    deg = engine.row_degrees(g_shard, probes).to(_comm_device(group), torch.int64)
+    dist.all_reduce(deg, group=group)
+    d = deg.cpu().numpy()
+    return int(probes[int(np.argmax(d))])
+
+
+@dataclass
+class DistributedBfs:
+    labels: object      # reached set -> its minimum id, others identity (every rank)
+    tree_u: object      # the whole BFS tree (every rank): (parent, v) per reached v != source
+    tree_v: object
+    insp_sample: int    # sum of the reached vertices' degrees (sampling.py:141-144)
+    levels: int
+    reached: int
+    exchanged_ids: int  # top-down mark ids all-gathered over all levels
+
+
+def distributed_bfs(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> DistributedBfs:
+    """BFS sampling (sampling.py:120-172) as a level-synchronous traversal over
+    row-sharded CSR.  The frontier and visited bitmaps are
+    replicated; the owner of a vertex decides its parent (the first frontier
+    vertex of its ascending row, the reference's smallest-discoverer rule),
+    so only bits cross the interconnect: per level, the top-down marks as id
+    lists (narrow frontiers) and the next-frontier bitmap as an all-reduce
+    SUM (the ranks' claimed bits are disjoint, so the sum is the union)."""
+    torch = _torch()
+    dist = _dist()
+    engine = engine or GpuEngine()
+    n = g_shard.n
+    if n == 0:
+        z = torch.zeros(0, dtype=torch.int32)
+        return DistributedBfs(z, z, z, 0, 0, 0, 0)
+    m_tot = torch.tensor([g_shard.m], dtype=torch.int64, device=_comm_device(group))
+    dist.all_reduce(m_tot, group=group)
+    if int(m_tot.item()) == 0:  # sampling.py:128-129: nothing to traverse
+        lab = torch.arange(n, dtype=torch.int32, device=engine.device)
+        z = torch.zeros(0, dtype=torch.int32, device=engine.device)
+        return DistributedBfs(lab, z, z, 0, 0, 0, 0)
+    src = global_bfs_source(g_shard, spec, group, engine)
+    st = engine.dbfs_init(n, src)
+    dev = _comm_device(group)
+    nf, reached, levels, bottom_up, sent = 1, 1, 0, False, 0
+    while nf:
+        want_bu = nf * DBFS_ALPHA > n - reached if not bottom_up else nf >= n // DBFS_BETA
+        bottom_up = want_bu
+        if bottom_up:
+            nxt = engine.dbfs_claim(g_shard, st, marks=False)
+        else:
+            ids = engine.dbfs_marks(g_shard, st)
+            rank = dist.get_rank(group)
+            for r, ou in enumerate(all_gather_ids(ids, group)):
+                sent += int(ou.numel())
+                if r != rank:
+                    engine.dbfs_merge_marks(st, ou)
+            nxt = engine.dbfs_claim(g_shard, st, marks=True)
+        buf = nxt.to(dev)
+        dist.all_reduce(buf, group=group)  # disjoint bits: SUM == OR
+        if buf is not nxt:
+            nxt.copy_(buf.to(nxt.device))
+        nf = engine.dbfs_advance(st)
+        reached += nf
+        levels += 1
+    labels, fu, fv, insp = engine.dbfs_finish(g_shard, st)
+    tot = torch.tensor([insp], dtype=torch.int64, device=dev)
+    dist.all_reduce(tot, group=group)
+    tree = all_gather_pairs(fu, fv, group)
+    tu = torch.cat([t[0].to(labels.device) for t in tree])
+    tv = torch.cat([t[1].to(labels.device) for t in tree])
+    return DistributedBfs(labels, tu, tv, int(tot.item()), levels, reached, sent)
 
 
 @dataclass
@@ -487,12 +681,20 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     dist = _dist()
     engine = engine or GpuEngine()
     rank = dist.get_rank(group)
-    summary = not forest and spec.sample is not SampleKind.NONE
-    parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec, record=not summary)
+    summary = not forest and spec.sample not in (SampleKind.NONE, SampleKind.BFS)
     torch = _torch()
-    if not summary:
+    if spec.sample is SampleKind.BFS:
+        # the distributed traversal leaves the same global labels on every
+        # rank (no partition exchange); its tree is the sampled forest
+        bfs = distributed_bfs(g_shard, spec, group, engine)
+        parent, insp_s = bfs.labels.contiguous(), bfs.insp_sample
+        # the tree edges were exchanged once: count them like merging edges
+        f1u, f1v, x1 = bfs.tree_u, bfs.tree_v, int(bfs.tree_u.numel())
+    elif not summary:
+        parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec, record=True)
         f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
     else:
+        parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec, record=False)
         x1 = _exchange_summary(parent, spec, engine, group)
         f1u = f1v = torch.empty(0, dtype=torch.int32, device=parent.device)
     mu, mv, info = engine.shard_finish(g_shard, spec, parent)
@@ -501,8 +703,11 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     labels = engine.finalize(parent)
     n = g_shard.n
     dev = _comm_device(group)
-    tot = torch.tensor([insp_s, info["insp_finish"]], dtype=torch.int64, device=dev)
+    tot = torch.tensor([0 if spec.sample is SampleKind.BFS else insp_s, info["insp_finish"]], dtype=torch.int64,
+                       device=dev)
     dist.all_reduce(tot, group=group)
+    if spec.sample is SampleKind.BFS:
+        tot[0] = insp_s  # already the sum over ranks
     labels = labels[:n]
     comps = int((labels == torch.arange(n, device=labels.device, dtype=labels.dtype)).sum().item())
     keep = forest and spec.is_root_based()

@@ -234,3 +234,88 @@ class CpuEngine:
         lab = np.array([_find(p, v) if inited[v] else v for v in range(cap)], dtype=np.int32)
         comps = int(sum(1 for v in range(cap) if inited[v] and lab[v] == v))
         return torch.from_numpy(lab), comps
+
+    # distributed BFS (gc_dbfs_* semantics): int32 bitmap words, as the GPU
+    # engine, so the driver's SUM all-reduce of next-frontier words is tested
+    @staticmethod
+    def _words(n):
+        return torch.zeros(max((n + 31) // 32, 1), dtype=torch.int32)
+
+    @staticmethod
+    def _test(words, x):
+        return bool((int(words[x >> 5]) >> (x & 31)) & 1)
+
+    @staticmethod
+    def _set(words, x):
+        w = np.array([int(words[x >> 5])], dtype=np.int32).view(np.uint32)
+        w |= np.uint32(1 << (x & 31))
+        words[x >> 5] = int(w.view(np.int32)[0])
+
+    def dbfs_init(self, n, source):
+        st = {"n": n, "F": self._words(n), "V": self._words(n), "M": self._words(n), "N": self._words(n),
+              "par": np.full(max(n, 1), -1, dtype=np.int64)}
+        self._set(st["F"], source)
+        self._set(st["V"], source)
+        st["par"][source] = -2
+        return st
+
+    def dbfs_marks(self, shard, st):
+        lo, hi = getattr(shard, "row_block", (0, shard.n))
+        off, tgt = shard.offsets, shard.targets
+        st["M"].zero_()
+        for f in range(lo, hi):
+            if self._test(st["F"], f):
+                for j in range(off[f], off[f + 1]):
+                    x = int(tgt[j])
+                    if not self._test(st["V"], x):
+                        self._set(st["M"], x)
+        ids = [x for x in range(st["n"]) if self._test(st["M"], x)]
+        return torch.tensor(ids, dtype=torch.int32)
+
+    def dbfs_merge_marks(self, st, ids):
+        for x in ids.tolist():
+            self._set(st["M"], x)
+
+    def dbfs_claim(self, shard, st, marks):
+        lo, hi = getattr(shard, "row_block", (0, shard.n))
+        off, tgt = shard.offsets, shard.targets
+        st["N"].zero_()
+        for x in range(lo, hi):
+            if self._test(st["V"], x) or (marks and not self._test(st["M"], x)):
+                continue
+            for j in range(off[x], off[x + 1]):
+                t = int(tgt[j])
+                if self._test(st["F"], t):
+                    st["par"][x] = t
+                    self._set(st["N"], x)
+                    break
+        return st["N"]
+
+    def dbfs_advance(self, st):
+        nw = st["N"].numpy().view(np.uint32)
+        st["F"].copy_(st["N"])
+        v = st["V"].numpy().view(np.uint32)
+        v |= nw
+        return int(sum(bin(int(w)).count("1") for w in nw))
+
+    def dbfs_finish(self, shard, st):
+        n = st["n"]
+        lo, hi = getattr(shard, "row_block", (0, n))
+        off = shard.offsets
+        reached = [self._test(st["V"], v) for v in range(n)]
+        mn = min(v for v in range(n) if reached[v])
+        lab = np.array([mn if reached[v] else v for v in range(n)], dtype=np.int32)
+        fu, fv, insp = [], [], 0
+        for v in range(lo, hi):
+            if reached[v]:
+                insp += int(off[v + 1] - off[v])
+                if st["par"][v] >= 0:
+                    fu.append(int(st["par"][v]))
+                    fv.append(v)
+        return (torch.from_numpy(lab), torch.tensor(fu, dtype=torch.int32), torch.tensor(fv, dtype=torch.int32),
+                insp)
+
+    def row_degrees(self, shard, ids):
+        off = shard.offsets
+        ids = np.asarray(ids, dtype=np.int64)
+        return torch.from_numpy((off[ids + 1] - off[ids]).astype(np.int64))

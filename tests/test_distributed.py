@@ -198,7 +198,9 @@ def test_sharded_two_phase_matches_reference_stats(world):
     names = ["rmat_s10_ef8", "comps_30", "star_150", "grid_12x12", "edgeless4", "ba_120_a3"]
     # "~spec": labels only, compact giant-bitmap summary exchange
     specs = ["kout+async+halve", "hb+async+halve", "none+async+halve", "kout+rem_cas+halve+splice",
-             "~kout+rem_cas+halve+splice", "~hb+async+halve"]
+             "~kout+rem_cas+halve+splice", "~hb+async+halve",
+             # distributed level-synchronous BFS sampling (config 5's spec)
+             "bfs+async+halve", "~bfs+rem_cas+halve+splice"]
     res = _run(_two_phase_worker, world, names, specs)
     for name in names:
         n, off, tgt, orc = gold.graphs[name]

@@ -142,7 +142,9 @@ def test_two_phase_sampled_ranks_share_one_gpu(world):
     from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec, static_connectivity_device
     # "~spec": labels only through the compact giant-bitmap summary exchange
     specs = ["kout+rem_cas+halve+splice", "kout+async+halve", "hb+rem_cas+split+halve", "none+hooks+compress",
-             "~kout+rem_cas+halve+splice", "~hb+jtb+twotry", "~kout+hooks+compress"]
+             "~kout+rem_cas+halve+splice", "~hb+jtb+twotry", "~kout+hooks+compress",
+             # distributed level-synchronous BFS sampling (gc_dbfs_*)
+             "bfs+async+halve", "~bfs+rem_cas+halve+splice"]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -216,3 +218,54 @@ def test_summary_exchange_disjoint_giants(world):
         assert np.array_equal(labels.astype(np.int64), orc), r
         assert i_s == st.edge_inspections.get("sample", 0) and i_f == st.edge_inspections.get("finish", 0), r
         assert lcnt / g.n == st.cov and nact == st.active, r
+
+
+def _dbfs_uniform_worker(rank, world, port, log2n, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2008_11839_b200 import build_csr, gen_uniform_pairs, parse_spec
+        from paper_2008_11839_b200.distributed import shard_bounds, shard_graph, sharded_two_phase
+        n = 1 << log2n
+        g = build_csr(gen_uniform_pairs(log2n, 4 * n, seed=1), keep_host=False)
+        lo, hi = shard_bounds(g._d_off, world)[rank]
+        r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec("bfs+async+halve"), forest=True)
+        q.put((rank, (r.labels.cpu().numpy(), r.forest_u.cpu().numpy(), r.forest_v.cpu().numpy(), r.insp_sample,
+                      r.insp_finish, r.lmax_count, r.n_active)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_bfs_forest_config5_shape(world):
+    """Config 5 scaled (uniform 2^20, 4n pairs, bfs+async+halve spanning
+    forest): the distributed BFS sampler + sharded finish give the oracle
+    labels, a forest passing the four clauses on every rank, and the
+    single-GPU pipeline's inspection counts / cov / active set."""
+    import torch.multiprocessing as mp
+    from paper_2008_11839_b200 import build_csr, gen_uniform_pairs, parse_spec, spanning_forest_device
+    log2n = 20
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dbfs_uniform_worker, args=(r, world, port, log2n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    n = 1 << log2n
+    g = build_csr(gen_uniform_pairs(log2n, 4 * n, seed=1))
+    orc, comps = oracle.components(n, g.offsets, g.targets)
+    _, st = spanning_forest_device(g, parse_spec("bfs+async+halve"))
+    for r in range(world):
+        labels, fu, fv, i_s, i_f, lcnt, nact = res[r]
+        assert np.array_equal(labels.astype(np.int64), orc), r
+        assert i_s == st.edge_inspections.get("sample", 0) and i_f == st.edge_inspections.get("finish", 0), r
+        assert lcnt / n == st.cov and nact == st.active, r
+        assert len(fu) == n - comps
+        su = np.full(n, -1, np.int32); sv = np.full(n, -1, np.int32)
+        su[:len(fu)] = fu; sv[:len(fv)] = fv
+        assert oracle.check_forest(n, g.offsets, g.targets, su, sv, orc)["passed"], r
