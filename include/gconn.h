@@ -292,6 +292,37 @@ int gc_dbfs_finish(const gc_csr* g, int64_t row_lo, int64_t row_hi,
                    int32_t* out_u, int32_t* out_v, unsigned long long* out_count,
                    unsigned long long* insp, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- single-process multi-device communicator (csrc/comm.cu)
+ * gc_comm_init: one rank per listed device, NCCL over NVLink / NVSwitch
+ *   (ncclCommInitAll) when the devices are distinct; a list that repeats one
+ *   device gives a loopback communicator (ranks share it, collectives are
+ *   device copies) for one-GPU hosts.  Mixed lists -> GC_ERR_ARG.
+ * gc_comm_static_cc / gc_comm_spanning_forest: the two-phase sharded
+ *   pipeline (gc_shard_sample -> all-gather merging edges -> gc_shard_finish
+ *   -> all-gather -> gc_label_finalization), BFS sampling as the distributed
+ *   traversal (gc_dbfs_*; spec->bfs_source must hold the probe source,
+ *   sampling.py:130-132).  shards[r]: rank r's CSR row block [row_lo[r],
+ *   row_hi[r]) resident on devs[r] (rows outside it empty, same n
+ *   everywhere).  labels[r] (device, n int32, 16-byte aligned): the canonical
+ *   labels, identical on every rank.  Forest: fu[r] / fv[r] (device, capacity
+ *   n) receive a spanning forest of the whole graph on every rank,
+ *   forest_count[r] (host) its edge count.  stats: sample / finish
+ *   inspections summed over ranks, l_max / lmax_count / n_active.  Union-find
+ *   finishes except JTB; samplers none / kout / hb / bfs. */
+typedef struct gc_comm gc_comm;
+int gc_comm_init(int ndev, const int* devs, gc_comm** out);
+void gc_comm_destroy(gc_comm* comm);
+int gc_comm_size(const gc_comm* comm);
+int gc_comm_is_loopback(const gc_comm* comm);
+int gc_comm_static_cc(gc_comm* comm, const gc_csr* shards, const int64_t* row_lo,
+                      const int64_t* row_hi, const gc_spec* spec,
+                      int32_t* const* labels, gc_stats* stats);
+int gc_comm_spanning_forest(gc_comm* comm, const gc_csr* shards,
+                            const int64_t* row_lo, const int64_t* row_hi,
+                            const gc_spec* spec, int32_t* const* labels,
+                            int32_t* const* fu, int32_t* const* fv,
+                            int64_t* forest_count, gc_stats* stats);
+
 /* Graph contract check (graphs.py:43-51) on device arrays: offsets start at
  * 0, never decrease and end at m; every target in [0, n) -> else
  * GC_ERR_MALFORMED.  One streaming pass; the Python layer runs it once per

@@ -63,7 +63,7 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
         list(ex.map(run, jobs))
     if jobs or not LIB.exists() or force:
         tmp = LIB.with_suffix(".so.tmp")
-        run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static"])
+        run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static", "-ldl"])
         os.replace(tmp, LIB)
     return LIB
 

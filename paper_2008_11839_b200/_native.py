@@ -105,6 +105,15 @@ _SIGNATURES = {
     "gc_dbfs_advance": (C.c_int, [_I64, _VP, _VP, _VP, _VP, _VP]),
     "gc_dbfs_finish": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ,
                                  _VP]),
+    "gc_comm_init": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(_VP)]),
+    "gc_comm_destroy": (None, [_VP]),
+    "gc_comm_size": (C.c_int, [_VP]),
+    "gc_comm_is_loopback": (C.c_int, [_VP]),
+    "gc_comm_static_cc": (C.c_int, [_VP, C.POINTER(Csr), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(Spec),
+                                    C.POINTER(_VP), C.POINTER(Stats)]),
+    "gc_comm_spanning_forest": (C.c_int, [_VP, C.POINTER(Csr), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(Spec),
+                                          C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_I64),
+                                          C.POINTER(Stats)]),
     "gc_check_csr": (C.c_int, [C.POINTER(Csr), _VP]),
     "gc_find_batch": (C.c_int, [_VP, _I64, _VP, _I64, C.c_int32, _VP, _VP]),
     "gc_canonical_labels": (C.c_int, [_VP, _I64, _VP, _SZ, _VP]),

@@ -143,8 +143,12 @@ k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned
 
 constexpr int kProbe = 1024;
 
+// walk = 1: P is a parent forest and each sample is resolved to its root
+// (the probe runs before compression); walk = 0: P is a plain label array
+// (the census of arbitrary labels, which need not be a forest — a label
+// cycle would never end the walk)
 __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t n,
-                                                       unsigned long long* ctr) {
+                                                       unsigned long long* ctr, int walk) {
   // sample labels counted in a shared-memory hash table (open addressing,
   // warp-aggregated adds: the dominant label is one add per warp)
   constexpr int kSlots = 2 * kProbe;
@@ -163,7 +167,8 @@ __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t
     // walk to the root so the probe can run before compression
     x = ld_weak(P + (int64_t(i) * n) / s);
     int32_t y;
-    while ((y = ld_weak(P + x)) != x) x = y;
+    if (walk)
+      while ((y = ld_weak(P + x)) != x) x = y;
   }
   __syncthreads();
   int slot = -1;
@@ -702,7 +707,7 @@ void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st) {
 void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cudaStream_t st) {
   if (n > 0) {
     const int g = grid_for(n, kEwBlock, 8);
-    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr), ::gc::count_launch());
+    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 0), ::gc::count_launch());
     (k_count_eq<<<g, kEwBlock, 0, st>>>(P, n, ctr), ::gc::count_launch());
     (k_hist_zero<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
     (k_hist_add<<<g, kEwBlock, 0, st>>>(P, hist, n, ctr), ::gc::count_launch());
@@ -720,7 +725,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
     // the fallback kernels usually exit at once: one resident wave keeps
     // their early exit cheap and still streams when they do run
     const int g = grid_for(n, kEwBlock, 1);
-    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr), ::gc::count_launch());
+    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1), ::gc::count_launch());
     if (compress) (k_post_sample<true><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
     else (k_post_sample<false><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
     // exact-mode fallback: every kernel below exits at once on a strict majority

@@ -21,7 +21,7 @@ __global__ void k_compress(int32_t* P, int32_t n);
 // Most-frequent label (sampling.py:29-35): probe a strided sample for the
 // candidate, count it exactly; a strict majority is provably the argmax,
 // otherwise an exact histogram decides (ties -> smaller label).
-__global__ void k_mode_probe(const int32_t* P, int32_t n, unsigned long long* ctr);
+__global__ void k_mode_probe(const int32_t* P, int32_t n, unsigned long long* ctr, int walk);
 __global__ void k_count_eq(const int32_t* P, int32_t n, unsigned long long* ctr);
 __global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr);
 __global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr);

@@ -474,7 +474,7 @@ int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint, uint
       return;
     }
     (k_compress<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
-    if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr), count_launch());
+    if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr, 1), count_launch());
     (k_pick_class<<<1, 1, 0, st>>>(parent, giant_hint, ctr, giant_label), count_launch());
     // a null pair output summarises the bitmap class only (round A)
     (k_summary<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,

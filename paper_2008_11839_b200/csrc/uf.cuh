@@ -38,6 +38,9 @@ struct UFState {
   // L1 line could still hold the uninitialised sentinel, which is not an
   // ancestor of anything.
   bool weak = true;
+  // parent reads carry an L2 evict_last policy (the parent array stays
+  // resident while the target stream passes through L2); GC_P_EVICT_LAST
+  bool evict_last = false;
 };
 
 template <bool FOREST>
@@ -78,13 +81,17 @@ constexpr int kWeakReads = 48;
 
 struct Reader {
   int budget;
+  uint64_t pol = 0;  // L2 policy of every read (0: none)
   __device__ __forceinline__ explicit Reader(bool weak = true) : budget(weak ? kWeakReads : 0) {}
+  __device__ __forceinline__ explicit Reader(const UFState& s) : budget(s.weak ? kWeakReads : 0) {
+    if (s.evict_last) pol = evict_last_policy();
+  }
   __device__ __forceinline__ int32_t operator()(const int32_t* p) {
     if (budget > 0) {
       --budget;
-      return ld_weak(p);
+      return pol ? ld_weak_pol(p, pol) : ld_weak(p);
     }
-    return ld_acq(p);
+    return pol ? ld_acq_pol(p, pol) : ld_acq(p);
   }
 };
 
@@ -199,7 +206,7 @@ __device__ __forceinline__ bool union_async(const UFState& s, int32_t u, int32_t
   // read; for the one-step finds the grandparent reads of both endpoints are
   // then issued together before either walk starts.
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   int32_t pu, pv;
   if (FIND == GC_FIND_HALVE || FIND == GC_FIND_SPLIT) {
     if (ku >= 0 && kv >= 0) {
@@ -231,7 +238,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_hooks(const UFState& s, int32_t u, int32_t v) {
   // dset.py:237-252: claim the hook slot, then an uncontended parent write.
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   const int32_t unhooked = s.n;
   int32_t pu = find<FIND>(u, P, rd);
   int32_t pv = find<FIND>(v, P, rd);
@@ -254,7 +261,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_early(const UFState& s, int32_t u, int32_t v) {
   // dset.py:255-274
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   int32_t pu = u, pv = v;
   bool merged = false;
   while (pu != pv) {
@@ -281,7 +288,7 @@ __device__ __forceinline__ bool union_rem_lock(const UFState& s, int32_t u, int3
   // dset.py:277-300.  A failed re-validation re-derives and loops, as the
   // reference does (the paper's pseudocode returns instead).
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   int32_t ru = u, rv = v;
   while (true) {
     int32_t pru = rd(P + ru);
@@ -322,7 +329,7 @@ __device__ __forceinline__ bool union_rem_cas(const UFState& s, int32_t u, int32
                                               int32_t kv = -1) {
   // dset.py:303-316 (ku / kv: held values of P[u] / P[v] for the first step)
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   int32_t ru = u, rv = v;
   bool first = ku >= 0 && kv >= 0;
   while (true) {
@@ -356,7 +363,7 @@ template <int FIND, bool FOREST>
 __device__ __forceinline__ bool union_jtb(const UFState& s, int32_t u, int32_t v) {
   // dset.py:319-331: link the lower (rank, id) root under the higher one
   int32_t* P = s.P;
-  Reader rd(s.weak);
+  Reader rd(s);
   while (true) {
     int32_t ru = find<FIND>(u, P, rd);
     int32_t rv = find<FIND>(v, P, rd);

@@ -354,6 +354,14 @@ int num_sms() {
 namespace {
 
 // Functor-style launchers so one dispatch switch serves both kernels.
+bool p_evict_last() {
+  static const bool on = [] {
+    const char* e = getenv("GC_P_EVICT_LAST");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 struct RowsLaunch {
   const RowUnionArgs& a;
   cudaStream_t st;
@@ -361,6 +369,7 @@ struct RowsLaunch {
   void go() const {
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     s.fpair = a.fpair;
+    s.evict_last = p_evict_last();
     if (a.all_edges >= 0 && !a.list && a.lower_only && a.count_host == a.n &&
         a.count_host < int64_t(num_sms()) * 2048) {
       if (a.all_edges == 0) return;

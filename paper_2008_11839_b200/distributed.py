@@ -776,3 +776,108 @@ class ShardedIncremental:
 
     def labels(self):
         return self.engine.incr_labels(self.h)
+
+
+# ------------------------------------------- single-process communicator
+
+class DeviceComm:
+    """The C-ABI communicator (``gc_comm_init``): one process drives one rank
+    per listed device — NCCL over NVLink / NVSwitch when the devices are
+    distinct, a loopback communicator (ranks share the device, collectives
+    are device copies) when the list repeats one device.  The same two-phase
+    pipeline as ``sharded_two_phase``, orchestrated natively, for callers
+    that cannot run one process per GPU."""
+
+    def __init__(self, devices):
+        import ctypes as C
+        from . import _native as N
+        devs = list(int(d) for d in devices)
+        if not devs:
+            raise ValueError("a communicator needs at least one device")
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        N.check(N.lib().gc_comm_init(len(devs), arr, C.byref(h)))
+        self._h, self.devices = h, devs
+
+    @property
+    def size(self) -> int:
+        from . import _native as N
+        return int(N.lib().gc_comm_size(self._h))
+
+    @property
+    def loopback(self) -> bool:
+        from . import _native as N
+        return bool(N.lib().gc_comm_is_loopback(self._h))
+
+    def close(self):
+        from . import _native as N
+        if self._h:
+            N.lib().gc_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _shards(self, g, spec, balance=None):
+        """Row blocks of a device graph, one per rank (each copied to the
+        rank's device), with the lowered spec (its BFS source computed on the
+        whole graph, sampling.py:130-132)."""
+        import ctypes as C
+        from . import _native as N
+        from .api import LoweredSpec, _csr
+        torch = _torch()
+        if not g.on_device:
+            g = g.cuda()
+        low = LoweredSpec(spec, g, g.n)
+        bounds = shard_bounds(g.offsets if g._h_off is not None else g._d_off, self.size,
+                              balance or shard_balance(spec))
+        csrs = (N.Csr * self.size)()
+        keep = []
+        for r, (lo, hi) in enumerate(bounds):
+            with torch.cuda.device(self.devices[r]):
+                sh = shard_graph(g, lo, hi)
+                off, tgt = sh.device_arrays()
+                off = off.to(f"cuda:{self.devices[r]}")
+                tgt = tgt.to(f"cuda:{self.devices[r]}")
+                keep += [off, tgt]
+                csrs[r].n, csrs[r].m = g.n, int(tgt.numel())
+                csrs[r].offsets = off.data_ptr()
+                csrs[r].targets = tgt.data_ptr() if tgt.numel() else None
+        lo = (C.c_int64 * self.size)(*[b[0] for b in bounds])
+        hi = (C.c_int64 * self.size)(*[b[1] for b in bounds])
+        return csrs, lo, hi, low, keep
+
+    def static_connectivity(self, g, spec):
+        """Canonical labels on every rank (list of device tensors) + stats."""
+        import ctypes as C
+        from . import _native as N
+        torch = _torch()
+        csrs, lo, hi, low, keep = self._shards(g, spec)
+        labels = [torch.empty(max(g.n, 4), dtype=torch.int32, device=f"cuda:{d}") for d in self.devices]
+        ptrs = (C.c_void_p * self.size)(*[t.data_ptr() for t in labels])
+        st = N.Stats()
+        N.check(N.lib().gc_comm_static_cc(self._h, csrs, lo, hi, C.byref(low.s), ptrs, C.byref(st)))
+        return [t[:g.n] for t in labels], st
+
+    def spanning_forest(self, g, spec):
+        """(labels per rank, [(fu, fv)] per rank: a spanning forest of the
+        whole graph on every rank, stats)."""
+        import ctypes as C
+        from . import _native as N
+        torch = _torch()
+        csrs, lo, hi, low, keep = self._shards(g, spec)
+        n = g.n
+        mk = (lambda d: torch.empty(max(n, 4), dtype=torch.int32, device=f"cuda:{d}"))
+        labels = [mk(d) for d in self.devices]
+        fu = [mk(d) for d in self.devices]
+        fv = [mk(d) for d in self.devices]
+        P = C.c_void_p * self.size
+        cnt = (C.c_int64 * self.size)()
+        st = N.Stats()
+        N.check(N.lib().gc_comm_spanning_forest(self._h, csrs, lo, hi, C.byref(low.s),
+                                                P(*[t.data_ptr() for t in labels]), P(*[t.data_ptr() for t in fu]),
+                                                P(*[t.data_ptr() for t in fv]), cnt, C.byref(st)))
+        return ([t[:n] for t in labels], [(fu[r][:cnt[r]], fv[r][:cnt[r]]) for r in range(self.size)], st)
