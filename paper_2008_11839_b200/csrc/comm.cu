@@ -226,6 +226,7 @@ void exchange(Call& k, const gc_spec& s, int64_t n, std::vector<int32_t*>& paren
       const int32_t* us = x.recv + size_t(q) * 2 * kmax;
       const int32_t* vs = us + kmax;
       if (forest) {
+        GC_CUDA(cudaMemsetAsync(x.cnt, 0, 8, c->st[r]));  // the list call accumulates into its count
         check(gc_union_edges_list(parent[r], n, us, vs, cnt[q], &s, x.aux, x.fu + x.fcount, x.fv + x.fcount,
                                   x.cnt, c->st[r]));
         x.fcount += int64_t(read_u64(x.cnt, c->st[r]));

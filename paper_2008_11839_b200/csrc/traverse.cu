@@ -636,34 +636,43 @@ __global__ void k_ldd_label(const uint32_t* cluster, const int32_t* mins, int32_
 
 // All LDD rounds in one persistent cooperative launch (one CTA group per
 // SM, grid-wide barrier between rounds).  Round r expands the frontier of
-// round r-1 and starts bucket r's centres; the claim word is the packed
-// (round << 32 | cluster) key resolved by one 64-bit atomicMin: the earliest
-// round wins, the smallest cluster within it.  The frontier is expanded
-// edge-parallel inside each warp (32 frontier vertices, their rows
-// concatenated, one edge per lane per step: a lane's source is found by a
-// binary search over the warp's degree prefix), so a round costs one chain of
-// claim latencies instead of a lane walking its whole row; fresh claims go to
-// a block queue flushed once per round.  Per-round frontier counters form a
-// ring of three; the first-round start and the end of the rounds are read on
-// the device, so the sampler needs no host round trip.  After the rounds,
-// the same launch takes the minimum member of each cluster and writes the
-// labels.
-constexpr unsigned long long kFreeKey = ~0ull;
-// reads of words other CTAs wrote earlier in the same launch go to L2
-__device__ __forceinline__ unsigned long long ld_rlx_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+// round r-1 and starts bucket r's centres.  Claim state is the 6-byte form
+// of the launch-per-round kernel: cluster[x] (u32, atomicMin) and croud[x]
+// (u16, claim round + 1, written by the first claimant).  The croud filter
+// rejects vertices claimed in an earlier round with a 2-byte read of a
+// 2n-byte array that stays in L2 (ncu of an 8-byte packed (round, cluster)
+// key: 10.3 GB of DRAM reads for one LDD on the permuted 256^3 grid, L2 hit
+// 25%); only vertices unclaimed or claimed in this round reach the
+// cluster atomicMin, so the result is the deterministic MPX clustering.
+// The frontier is expanded edge-parallel inside each warp (32 frontier
+// vertices, their rows concatenated, one edge per lane per step: a lane's
+// source is found by a binary search over the warp's degree prefix); fresh
+// claims go to a block queue flushed once per round.  Per-round frontier
+// counters form a ring of three; the first start round and the end of the
+// rounds are read on the device, so the sampler needs no host round trip.
+// After the rounds the same launch takes the minimum member of each cluster
+// and writes the labels.
+__device__ __forceinline__ uint32_t ld_rlx_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ bool claim_key(unsigned long long* key, int32_t x, unsigned long long mine) {
-  const unsigned long long k = ld_rlx_u64(key + x);
-  if (k <= mine) return false;  // an earlier round, or a smaller claimant of this one
-  return atomicMin(key + x, mine) == kFreeKey;
+__device__ __forceinline__ uint16_t ld_rlx_u16(const uint16_t* p) {
+  uint16_t v;
+  asm volatile("ld.relaxed.gpu.global.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool claim_rel(uint32_t* cluster, uint16_t* croud, int32_t x, int32_t round, uint32_t c) {
+  const uint16_t cr = ld_rlx_u16(croud + x);
+  if (cr != 0 && int32_t(cr) - 1 != round) return false;  // reached in an earlier round
+  if (atomicMin(cluster + x, c) != kFreeCluster) return false;
+  croud[x] = uint16_t(round + 1);
+  return true;
 }
 
 __global__ void __launch_bounds__(kTB)
-k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n,
-              unsigned long long* key, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
+k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, uint32_t* cluster,
+              uint16_t* croud, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
               const int32_t* dmax_bits, int32_t max_rounds, int32_t* q0, int32_t* q1, unsigned long long* ring,
               unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out) {
   cg::grid_group grid = cg::this_grid();
@@ -686,12 +695,12 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     const int64_t count = r > 0 ? int64_t(*reinterpret_cast<volatile unsigned long long*>(ring + r % 3)) : 0;
     for (int64_t wb = gwarp * 32; wb < count; wb += nwarps * 32) {
       const int64_t i = wb + lane;
-      unsigned long long c = 0;
+      uint32_t c = 0;
       int64_t b = 0;
       int32_t d = 0;
       if (i < count) {
         const int32_t f = ld_acq(qin + i);
-        c = ld_rlx_u64(key + f) & 0xffffffffull;  // final since round r-1
+        c = ld_rlx_u32(cluster + f);  // final since round r-1
         b = off[f];
         d = int32_t(off[f + 1] - b);
         my_insp += d;
@@ -703,7 +712,6 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         if (lane >= o) incl += t;
       }
       const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const unsigned long long mine_round = (unsigned long long)r << 32;
       for (int32_t e0 = 0; e0 < total; e0 += 32) {
         const int32_t e = e0 + lane;
         // source lane: the first lane whose inclusive prefix exceeds e
@@ -717,12 +725,12 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         const int32_t se = __shfl_sync(0xffffffffu, incl, src);
         const int32_t sd = __shfl_sync(0xffffffffu, d, src);
         const int64_t sb = __shfl_sync(0xffffffffu, b, src);
-        const unsigned long long sc = __shfl_sync(0xffffffffu, c, src);
+        const uint32_t sc = __shfl_sync(0xffffffffu, c, src);
         bool fresh = false;
         int32_t x = 0;
         if (e < total) {
           x = tgt[sb + (e - (se - sd))];
-          fresh = claim_key(key, x, mine_round | sc);
+          fresh = claim_rel(cluster, croud, x, r, sc);
         }
         bq.push(fresh, x, qout, cout);
       }
@@ -735,7 +743,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         bool fresh = false;
         if (i < hi) {
           v = order[i];
-          fresh = claim_key(key, v, ((unsigned long long)r << 32) | uint32_t(v));
+          fresh = claim_rel(cluster, croud, v, r, uint32_t(v));
         }
         bq.push(fresh, v, qout, cout);
       }
@@ -753,33 +761,12 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
   grid.sync();
   for (int64_t base = gtid - lane; base < n; base += gthreads) {
     const int64_t v = base + lane;
-    const uint32_t c = v < n ? uint32_t(ld_rlx_u64(key + v)) : kFreeCluster;
+    const uint32_t c = v < n ? ld_rlx_u32(cluster + v) : kFreeCluster;
     const unsigned peers = __match_any_sync(0xffffffffu, c);
     if (v < n && lane == __ffs(int(peers)) - 1) atomicMin(mins + c, int32_t(v));
   }
   grid.sync();
-  for (int64_t v = gtid; v < n; v += gthreads) P[v] = ld_acq(mins + uint32_t(ld_rlx_u64(key + v)));
-}
-
-// every vertex unclaimed, start round per vertex + bucket histogram
-__global__ void __launch_bounds__(kEwBlock)
-k_ldd_start_key(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
-                unsigned long long* key, unsigned int* bcount) {
-  __shared__ unsigned int hist[kBuckets];
-  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  const float dmax = __int_as_float(*dmax_bits);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-    float r = floorf(dmax - ldd_delta(seed, v, beta));
-    r = r < 0.f ? 0.f : (r > float(kLddMaxRounds) ? float(kLddMaxRounds) : r);
-    start[v] = uint16_t(r);
-    key[v] = kFreeKey;
-    atomicAdd(hist + int(r), 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
-    if (hist[i]) atomicAdd(bcount + i, hist[i]);
+  for (int64_t v = gtid; v < n; v += gthreads) P[v] = ld_acq(mins + ld_rlx_u32(cluster + v));
 }
 
 #define TL(kernel, grid, block, ...) ((kernel<<<grid, block, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
@@ -979,7 +966,9 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   if (ldd_persistent()) {
     // one cooperative launch runs every round and the labelling (no host
     // round trip); the start-round buckets come from the three passes below
-    TL(k_ldd_start_key, ge, kEwBlock, n, s.seed, beta, dmax, w.start, w.key, bcount);
+    uint32_t* cl = reinterpret_cast<uint32_t*>(w.key);
+    uint16_t* cr = reinterpret_cast<uint16_t*>(cl + n);
+    TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount);
     TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
     TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
        cursor, w.order);
@@ -991,7 +980,8 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     }
     const int64_t* off = g.offsets;
     const int32_t* tgt = g.targets;
-    unsigned long long* key = w.key;
+    uint32_t* clp = cl;
+    uint16_t* crp = cr;
     const int32_t* order = w.order;
     const unsigned int* boff = w.boff;
     const int32_t* dmb = dmax;
@@ -1004,7 +994,7 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     int32_t* Pp = P;
     unsigned long long* rounds_out = w.stat + 3;
     int32_t nn = n;
-    void* args[] = {&off, &tgt, &nn, &key, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
+    void* args[] = {&off, &tgt, &nn, &clp, &crp, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
                     &rounds_out};
     GC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ldd_persist), dim3(num_sms() * per_sm),
                                         dim3(kTB), args, 0, st));

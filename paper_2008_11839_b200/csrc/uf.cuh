@@ -38,9 +38,6 @@ struct UFState {
   // L1 line could still hold the uninitialised sentinel, which is not an
   // ancestor of anything.
   bool weak = true;
-  // parent reads carry an L2 evict_last policy (the parent array stays
-  // resident while the target stream passes through L2); GC_P_EVICT_LAST
-  bool evict_last = false;
 };
 
 template <bool FOREST>
@@ -81,17 +78,14 @@ constexpr int kWeakReads = 48;
 
 struct Reader {
   int budget;
-  uint64_t pol = 0;  // L2 policy of every read (0: none)
   __device__ __forceinline__ explicit Reader(bool weak = true) : budget(weak ? kWeakReads : 0) {}
-  __device__ __forceinline__ explicit Reader(const UFState& s) : budget(s.weak ? kWeakReads : 0) {
-    if (s.evict_last) pol = evict_last_policy();
-  }
+  __device__ __forceinline__ explicit Reader(const UFState& s) : budget(s.weak ? kWeakReads : 0) {}
   __device__ __forceinline__ int32_t operator()(const int32_t* p) {
     if (budget > 0) {
       --budget;
-      return pol ? ld_weak_pol(p, pol) : ld_weak(p);
+      return ld_weak(p);
     }
-    return pol ? ld_acq_pol(p, pol) : ld_acq(p);
+    return ld_acq(p);
   }
 };
 

@@ -354,14 +354,6 @@ int num_sms() {
 namespace {
 
 // Functor-style launchers so one dispatch switch serves both kernels.
-bool p_evict_last() {
-  static const bool on = [] {
-    const char* e = getenv("GC_P_EVICT_LAST");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 struct RowsLaunch {
   const RowUnionArgs& a;
   cudaStream_t st;
@@ -369,7 +361,6 @@ struct RowsLaunch {
   void go() const {
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     s.fpair = a.fpair;
-    s.evict_last = p_evict_last();
     if (a.all_edges >= 0 && !a.list && a.lower_only && a.count_host == a.n &&
         a.count_host < int64_t(num_sms()) * 2048) {
       if (a.all_edges == 0) return;
@@ -395,11 +386,15 @@ struct RowsLaunch {
 };
 
 // unions per thread of the lock-step async kernel (GC_COO_MLP; 0 selects
-// the one-union-per-thread k_union_coo)
+// the one-union-per-thread k_union_coo).  Config 4 (54 x 10M inserts into
+// RMAT s26), measured: K = 0 / 2 / 4 / 8 -> 17.5 / 16.3 / 18.2 / 24.6 ms —
+// the batch is bound by random 32-byte-sector DRAM reads of the 268 MB
+// parent array (ncu: 1.5 GB read per 10M batch), not by per-thread latency,
+// so more unions per thread only cost occupancy
 int coo_mlp() {
   static const int k = [] {
     const char* e = getenv("GC_COO_MLP");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 2;
   }();
   return k;
 }
