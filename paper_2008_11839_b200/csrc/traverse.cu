@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -670,11 +671,12 @@ __device__ __forceinline__ bool claim_rel(uint32_t* cluster, uint16_t* croud, in
   return true;
 }
 
-__global__ void __launch_bounds__(kTB)
+__global__ void __launch_bounds__(kTB, 6)
 k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, uint32_t* cluster,
               uint16_t* croud, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
               const int32_t* dmax_bits, int32_t max_rounds, int32_t* q0, int32_t* q1, unsigned long long* ring,
-              unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out) {
+              unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out,
+              unsigned int* trace) {
   cg::grid_group grid = cg::this_grid();
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
@@ -686,6 +688,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
   int32_t last_start = int32_t(floorf(__int_as_float(*dmax_bits)));
   last_start = last_start < 0 ? 0 : (last_start > max_rounds ? max_rounds : last_start);
   unsigned long long my_insp = 0;
+  const uint64_t pol = evict_first_policy();
   int32_t r = 0;
   for (;; ++r) {
     int32_t* qin = (r & 1) ? q0 : q1;  // round r reads the queue round r-1 wrote
@@ -701,8 +704,9 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
       if (i < count) {
         const int32_t f = ld_acq(qin + i);
         c = ld_rlx_u32(cluster + f);  // final since round r-1
-        b = off[f];
-        d = int32_t(off[f + 1] - b);
+        // graph data is read once: L2 evict-first keeps the claim state resident
+        b = ld_stream64(off + f, pol);
+        d = int32_t(ld_stream64(off + f + 1, pol) - b);
         my_insp += d;
       }
       int32_t incl = d;
@@ -712,27 +716,35 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         if (lane >= o) incl += t;
       }
       const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      for (int32_t e0 = 0; e0 < total; e0 += 32) {
-        const int32_t e = e0 + lane;
-        // source lane: the first lane whose inclusive prefix exceeds e
-        int lo = 0;
+      // two edges per lane per step (e and e + 32): two independent claim
+      // chains in flight per lane
+      for (int32_t e0 = 0; e0 < total; e0 += 64) {
+        int32_t x[2];
+        uint32_t sc[2];
+        bool ok[2];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-          if (v <= e) lo += step;
+        for (int h = 0; h < 2; ++h) {
+          const int32_t e = e0 + 32 * h + lane;
+          // source lane: the first lane whose inclusive prefix exceeds e
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+            if (v <= e) lo += step;
+          }
+          const int src = lo > 31 ? 31 : lo;
+          const int32_t se = __shfl_sync(0xffffffffu, incl, src);
+          const int32_t sd = __shfl_sync(0xffffffffu, d, src);
+          const int64_t sb = __shfl_sync(0xffffffffu, b, src);
+          sc[h] = __shfl_sync(0xffffffffu, c, src);
+          ok[h] = e < total;
+          x[h] = ok[h] ? ld_stream(tgt + sb + (e - (se - sd)), pol) : 0;
         }
-        const int src = lo > 31 ? 31 : lo;
-        const int32_t se = __shfl_sync(0xffffffffu, incl, src);
-        const int32_t sd = __shfl_sync(0xffffffffu, d, src);
-        const int64_t sb = __shfl_sync(0xffffffffu, b, src);
-        const uint32_t sc = __shfl_sync(0xffffffffu, c, src);
-        bool fresh = false;
-        int32_t x = 0;
-        if (e < total) {
-          x = tgt[sb + (e - (se - sd))];
-          fresh = claim_rel(cluster, croud, x, r, sc);
-        }
-        bq.push(fresh, x, qout, cout);
+        bool fresh[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) fresh[h] = ok[h] && claim_rel(cluster, croud, x[h], r, sc[h]);
+        bq.push(fresh[0], x[0], qout, cout);
+        bq.push(fresh[1], x[1], qout, cout);
       }
     }
     if (r <= last_start) {  // centres of bucket r
@@ -751,6 +763,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     bq.flush(qout, cout);
     grid.sync();
     const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(cout);
+    if (trace && gtid == 0 && r < max_rounds) trace[r] = unsigned(next);
     if (next == 0 && r >= last_start) break;
   }
   block_add<kTB>(insp, my_insp);
@@ -994,12 +1007,28 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     int32_t* Pp = P;
     unsigned long long* rounds_out = w.stat + 3;
     int32_t nn = n;
+    // GC_LDD_TRACE: per-round frontier sizes on stderr
+    static const bool trace_on = getenv("GC_LDD_TRACE") != nullptr;
+    unsigned int* trace = nullptr;
+    if (trace_on) GC_CUDA(cudaMallocAsync(&trace, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
+    if (trace) GC_CUDA(cudaMemsetAsync(trace, 0, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
     void* args[] = {&off, &tgt, &nn, &clp, &crp, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
-                    &rounds_out};
+                    &rounds_out, &trace};
     GC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ldd_persist), dim3(num_sms() * per_sm),
                                         dim3(kTB), args, 0, st));
     ::gc::count_launch();
     GC_CHECK_LAUNCH();
+    if (trace) {
+      std::vector<unsigned int> h(kLddMaxRounds + 1);
+      unsigned long long nr = 0;
+      GC_CUDA(cudaMemcpyAsync(h.data(), trace, sizeof(unsigned int) * h.size(), cudaMemcpyDeviceToHost, st));
+      GC_CUDA(cudaMemcpyAsync(&nr, rounds_out, 8, cudaMemcpyDeviceToHost, st));
+      GC_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "ldd rounds %llu:", nr);
+      for (unsigned long long i = 0; i < nr && i < h.size(); ++i) fprintf(stderr, " %u", h[i]);
+      fprintf(stderr, "\n");
+      GC_CUDA(cudaFreeAsync(trace, st));
+    }
     return;
   }
   // the claim buffer (8n bytes) holds the u32 clusters and the u16 claim rounds

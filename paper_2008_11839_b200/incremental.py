@@ -87,7 +87,9 @@ class LiveState:
 
     @property
     def __cuda_array_interface__(self):
-        return {"shape": (self._slots,), "typestr": "<i4", "data": (self._ptr, True), "version": 3,
+        # writable, as the reference hands the live (mutable) state; torch
+        # rejects read-only device arrays
+        return {"shape": (self._slots,), "typestr": "<i4", "data": (self._ptr, False), "version": 3,
                 "strides": None}
 
     def tensor(self):
