@@ -3,6 +3,7 @@
 // active gather, finalisation and canonical relabelling.
 #include <atomic>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <cstdlib>
@@ -10,6 +11,8 @@
 #include "pipeline.cuh"
 
 namespace gc {
+
+namespace cg = cooperative_groups;
 
 __global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -74,53 +77,72 @@ __global__ void k_compress(int32_t* P, int32_t n) {
 // atomic per block.  If the candidate turns out not to be the mode, the
 // histogram fallback re-gathers (k_gather_active).
 template <bool COMPRESS>
-__global__ void __launch_bounds__(kEwBlock)
+__global__ void __launch_bounds__(kEwBlock, 6)
 k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr) {
+  // two 4-vertex quads per thread per step (eight first hops in flight; the
+  // step's barriers are paid once per eight vertices)
+  constexpr int kQ = 2;
   using Scan = cub::BlockScan<int, kEwBlock>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
   const int32_t cand = int32_t(ctr[C_CAND]);
   unsigned long long ccount = 0, degsum = 0;
   const int64_t nq = (int64_t(n) + 3) / 4;
-  for (int64_t q0 = int64_t(blockIdx.x) * kEwBlock; q0 < nq; q0 += int64_t(gridDim.x) * kEwBlock) {
-    const int64_t q = q0 + threadIdx.x;
-    int32_t lab[4] = {cand, cand, cand, cand};
-    const int64_t v0 = q * 4;
-    if (q < nq) {
-      if (v0 + 3 < n) {
-        const int4 p4 = *reinterpret_cast<const int4*>(P + v0);
-        lab[0] = p4.x; lab[1] = p4.y; lab[2] = p4.z; lab[3] = p4.w;
-      } else {
-        for (int j = 0; j < 4; ++j) if (v0 + j < n) lab[j] = P[v0 + j];
-      }
-      if (COMPRESS) {
-        bool dirty = false;
-        // first hop of all four walks issued together (most labels are
-        // already roots after the union kernel's halving); only labels that
-        // moved continue walking
-        int32_t hop[4];
+  for (int64_t q0 = int64_t(blockIdx.x) * kEwBlock * kQ; q0 < nq; q0 += int64_t(gridDim.x) * kEwBlock * kQ) {
+    int32_t lab[kQ][4];
+    int64_t v0[kQ];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) hop[j] = v0 + j < n ? ld_free(P + lab[j]) : lab[j];
+    for (int h = 0; h < kQ; ++h) {
+      const int64_t q = q0 + int64_t(h) * kEwBlock + threadIdx.x;
+      v0[h] = q * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lab[h][j] = cand;
+      if (q < nq) {
+        if (v0[h] + 3 < n) {
+          const int4 p4 = *reinterpret_cast<const int4*>(P + v0[h]);
+          lab[h][0] = p4.x; lab[h][1] = p4.y; lab[h][2] = p4.z; lab[h][3] = p4.w;
+        } else {
+          for (int j = 0; j < 4; ++j) if (v0[h] + j < n) lab[h][j] = P[v0[h] + j];
+        }
+      }
+    }
+    if (COMPRESS) {
+      // first hop of all eight walks issued together (most labels are
+      // already roots after the union kernel's halving); only labels that
+      // moved continue walking
+      int32_t hop[kQ][4];
+#pragma unroll
+      for (int h = 0; h < kQ; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hop[h][j] = v0[h] + j < n ? ld_free(P + lab[h][j]) : lab[h][j];
+#pragma unroll
+      for (int h = 0; h < kQ; ++h) {
+        if (v0[h] >= n) continue;
+        bool dirty = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          if (v0 + j >= n) continue;
-          const int32_t r = hop[j] == lab[j] ? lab[j] : root_weak(P, hop[j]);
-          dirty |= r != lab[j];
-          lab[j] = r;
+          if (v0[h] + j >= n) continue;
+          const int32_t r = hop[h][j] == lab[h][j] ? lab[h][j] : root_weak(P, hop[h][j]);
+          dirty |= r != lab[h][j];
+          lab[h][j] = r;
         }
         if (dirty) {
-          if (v0 + 3 < n) *reinterpret_cast<int4*>(P + v0) = make_int4(lab[0], lab[1], lab[2], lab[3]);
-          else for (int j = 0; j < 4; ++j) if (v0 + j < n) P[v0 + j] = lab[j];
+          if (v0[h] + 3 < n)
+            *reinterpret_cast<int4*>(P + v0[h]) = make_int4(lab[h][0], lab[h][1], lab[h][2], lab[h][3]);
+          else
+            for (int j = 0; j < 4; ++j) if (v0[h] + j < n) P[v0[h] + j] = lab[h][j];
         }
       }
     }
     int act = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (v0 + j >= n || q >= nq) continue;
-      ccount += lab[j] == cand;
-      act += lab[j] != cand;
-    }
+    for (int h = 0; h < kQ; ++h)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (v0[h] + j >= n) continue;
+        ccount += lab[h][j] == cand;
+        act += lab[h][j] != cand;
+      }
     int rank, total;
     Scan(tmp).ExclusiveSum(act, rank, total);
     if (threadIdx.x == 0) base = total ? atomicAdd(ctr + C_N_ACTIVE, static_cast<unsigned long long>(total)) : 0ull;
@@ -128,12 +150,14 @@ k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned
     if (act) {
       unsigned long long pos = base + rank;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (v0 + j < n && lab[j] != cand) {
-          list[pos++] = int32_t(v0 + j);
-          degsum += static_cast<unsigned long long>(off[v0 + j + 1] - off[v0 + j]);
+      for (int h = 0; h < kQ; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (v0[h] + j < n && lab[h][j] != cand) {
+            list[pos++] = int32_t(v0[h] + j);
+            degsum += static_cast<unsigned long long>(off[v0[h] + j + 1] - off[v0[h] + j]);
+          }
         }
-      }
     }
     __syncthreads();
   }
@@ -210,8 +234,7 @@ __device__ __forceinline__ bool majority(const unsigned long long* ctr, int32_t 
   return 2ull * ctr[C_CAND_COUNT] > static_cast<unsigned long long>(n);
 }
 
-__global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr) {
-  if (majority(ctr, n)) return;
+__device__ __forceinline__ void hist_zero_body(int32_t* hist, int32_t n, unsigned long long* ctr) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) hist[v] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -221,8 +244,12 @@ __global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr) {
   }
 }
 
-__global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr) {
+__global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr) {
   if (majority(ctr, n)) return;
+  hist_zero_body(hist, n, ctr);
+}
+
+__device__ __forceinline__ void hist_add_body(const int32_t* P, int32_t* hist, int32_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
     const int64_t v = base + threadIdx.x;
@@ -237,8 +264,12 @@ __global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned 
   }
 }
 
-__global__ void k_hist_argmax(const int32_t* hist, int32_t n, unsigned long long* ctr) {
+__global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr) {
   if (majority(ctr, n)) return;
+  hist_add_body(P, hist, n);
+}
+
+__device__ __forceinline__ void hist_argmax_body(const int32_t* hist, int32_t n, unsigned long long* ctr) {
   __shared__ unsigned long long best;
   if (threadIdx.x == 0) best = 0ull;
   __syncthreads();
@@ -254,7 +285,12 @@ __global__ void k_hist_argmax(const int32_t* hist, int32_t n, unsigned long long
   if (threadIdx.x == 0) atomicMax(ctr + C_SCRATCH0, best);
 }
 
-__global__ void k_mode_finish(int32_t n, unsigned long long* ctr) {
+__global__ void k_hist_argmax(const int32_t* hist, int32_t n, unsigned long long* ctr) {
+  if (majority(ctr, n)) return;
+  hist_argmax_body(hist, n, ctr);
+}
+
+__device__ __forceinline__ void mode_finish_body(int32_t n, unsigned long long* ctr) {
   if (n == 0) {
     ctr[C_LMAX] = 0;
     ctr[C_LMAX_COUNT] = 0;
@@ -268,10 +304,10 @@ __global__ void k_mode_finish(int32_t n, unsigned long long* ctr) {
   }
 }
 
-__global__ void __launch_bounds__(kEwBlock)
-k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
-                unsigned long long* ctr, int only_fallback) {
-  if (only_fallback && majority(ctr, n)) return;
+__global__ void k_mode_finish(int32_t n, unsigned long long* ctr) { mode_finish_body(n, ctr); }
+
+__device__ __forceinline__ void gather_active_body(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
+                                                   unsigned long long* ctr) {
   // four vertices per thread (one 16-byte label load), one scan and one
   // global atomic per 1024 vertices
   using Scan = cub::BlockScan<int, kEwBlock>;
@@ -313,6 +349,37 @@ k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
     __syncthreads();
   }
   block_add<kEwBlock>(ctr + C_INSP_FINISH, degsum);
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_gather_active(const int32_t* P, int32_t n, const int64_t* off, int32_t* list,
+                unsigned long long* ctr, int only_fallback) {
+  if (only_fallback && majority(ctr, n)) return;
+  gather_active_body(P, n, off, list, ctr);
+}
+
+// The exact-mode fallback of the post-sampling pass as ONE cooperative
+// launch (histogram zero -> add -> arg-max -> L_max -> active re-gather,
+// grid barriers between): on a strict majority of the probe's candidate —
+// the usual case — it only publishes L_max and exits, one launch instead of
+// five early-exit launches per pipeline.
+__global__ void __launch_bounds__(kEwBlock)
+k_mode_fallback(const int32_t* P, int32_t* hist, int32_t n, const int64_t* off, int32_t* list,
+                unsigned long long* ctr) {
+  if (majority(ctr, n)) {  // the same decision in every block (C_CAND_COUNT is final)
+    if (blockIdx.x == 0 && threadIdx.x == 0) mode_finish_body(n, ctr);
+    return;
+  }
+  cg::grid_group grid = cg::this_grid();
+  hist_zero_body(hist, n, ctr);
+  grid.sync();
+  hist_add_body(P, hist, n);
+  grid.sync();
+  hist_argmax_body(hist, n, ctr);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) mode_finish_body(n, ctr);
+  grid.sync();
+  gather_active_body(P, n, off, list, ctr);
 }
 
 __global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
@@ -717,6 +784,14 @@ void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cud
   GC_CHECK_LAUNCH();
 }
 
+bool mode_coop() {
+  static const bool on = [] {
+    const char* e = getenv("GC_MODE_COOP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, int32_t* hist,
                      unsigned long long* ctr, bool compress, cudaStream_t st) {
   if (n > 0) {
@@ -726,9 +801,31 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
     // their early exit cheap and still streams when they do run
     const int g = grid_for(n, kEwBlock, 1);
     (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1), ::gc::count_launch());
-    if (compress) (k_post_sample<true><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
-    else (k_post_sample<false><<<gq, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
-    // exact-mode fallback: every kernel below exits at once on a strict majority
+    // one resident wave: six 256-thread blocks per SM, two quads per thread
+    const int gps = grid_for((nq + 1) / 2, kEwBlock, 1) < num_sms() * 6 ? grid_for((nq + 1) / 2, kEwBlock, 1)
+                                                                          : num_sms() * 6;
+    if (compress) (k_post_sample<true><<<gps, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
+    else (k_post_sample<false><<<gps, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
+    // exact-mode fallback: one cooperative launch that exits at once on a
+    // strict majority (GC_MODE_COOP=0: the five separate early-exit kernels)
+    if (mode_coop()) {
+      static int per_sm = 0;
+      if (!per_sm) GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mode_fallback, kEwBlock, 0));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(num_sms() * (per_sm > 0 ? per_sm : 1));
+      cfg.blockDim = dim3(kEwBlock);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const int32_t* Pc = P;
+      GC_CUDA(cudaLaunchKernelEx(&cfg, k_mode_fallback, Pc, hist, n, off, list, ctr));
+      ::gc::count_launch();
+      GC_CHECK_LAUNCH();
+      return;
+    }
     (k_hist_zero<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
     (k_hist_add<<<g, kEwBlock, 0, st>>>(P, hist, n, ctr), ::gc::count_launch());
     (k_hist_argmax<<<g, kEwBlock, 0, st>>>(hist, n, ctr), ::gc::count_launch());
