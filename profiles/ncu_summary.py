@@ -25,13 +25,14 @@ def details(rep):
 def raw(rep, names):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
         d = {}
         for n in names:
             if n in h:
-                d[n] = r[h.index(n)]
+                i = h.index(n)
+                d[n] = f"{r[i]} {units[i]}".strip()  # ncu picks the unit per value (byte, Kbyte, Mbyte, Gbyte)
         res.append(d)
     return res
 
