@@ -218,6 +218,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Phase timestamps taken at the entry of the next kernel: thread 0 of block
+// 0 writes %globaltimer into every slot of `mask` (ctr[stamp_base + i]).  A
+// separate one-thread stamp node between two kernels costs ~1.5 us of a plan
+// replay; the next kernel's first block starts within ~1 us of the previous
+// kernel's end, which is the same phase boundary.
+__device__ __forceinline__ void entry_stamp(unsigned long long* slots, unsigned mask) {
+  if (mask == 0u || blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  for (int i = 0; i < 10; ++i)
+    if (mask & (1u << i)) slots[i] = t;
+}
+
 // Grid size for an elementwise kernel: enough CTAs to cover `work` items
 // but capped at a whole number of waves over the 148 SMs.
 inline int grid_for(int64_t work, int block, int max_waves = 32) {

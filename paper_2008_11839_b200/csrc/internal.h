@@ -131,8 +131,12 @@ struct RowUnionArgs {
   int2* fpair = nullptr;   // forest slots as pairs (see UFState::fpair)
   int64_t all_edges = -1;  // >= 0: the rows are the whole graph with this many entries
                            // (all-active lower-only finish; small graphs go edge-parallel)
+  unsigned long long* stamps = nullptr;  // non-null: the kernel takes the pending phase stamps
+                                         // (take_stamps) at entry into these slots
 };
 void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, cudaStream_t st);
+// pending deferred phase stamps (pipeline.cu), cleared by the call
+unsigned take_stamps();
 
 // Union over COO pairs (union_edge_list, incremental inserts).
 struct CooUnionArgs {

@@ -14,7 +14,9 @@ namespace gc {
 
 namespace cg = cooperative_groups;
 
-__global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n) {
+__global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n, unsigned long long* stamps,
+                            unsigned stamp_mask) {
+  entry_stamp(stamps, stamp_mask);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if (!H && !L && (reinterpret_cast<uintptr_t>(P) & 15) == 0) {
     // 16-byte stores, four vertices per thread
@@ -172,7 +174,8 @@ constexpr int kProbe = 1024;
 // (the census of arbitrary labels, which need not be a forest — a label
 // cycle would never end the walk)
 __global__ void __launch_bounds__(kProbe) k_mode_probe(const int32_t* P, int32_t n,
-                                                       unsigned long long* ctr, int walk) {
+                                                       unsigned long long* ctr, int walk, unsigned stamp_mask) {
+  entry_stamp(ctr + C_STAMP0, stamp_mask);
   // sample labels counted in a shared-memory hash table (open addressing,
   // warp-aggregated adds: the dominant label is one add per warp)
   constexpr int kSlots = 2 * kProbe;
@@ -382,7 +385,8 @@ k_mode_fallback(const int32_t* P, int32_t* hist, int32_t n, const int64_t* off, 
   gather_active_body(P, n, off, list, ctr);
 }
 
-__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr) {
+__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask) {
+  entry_stamp(ctr + C_STAMP0, stamp_mask);
   unsigned long long roots = 0;
   bool noncanon = false, cyc = false;
   const int64_t nq = (int64_t(n) + 3) / 4;
@@ -449,7 +453,8 @@ constexpr int kFinTile = 4096;
 constexpr int kFinStages = 2;
 
 __global__ void __launch_bounds__(kEwBlock)
-k_finalize_tma(int32_t* P, int32_t n, unsigned long long* ctr) {
+k_finalize_tma(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask) {
+  entry_stamp(ctr + C_STAMP0, stamp_mask);
   __shared__ alignas(128) int32_t buf[kFinStages][kFinTile];
   __shared__ alignas(8) uint64_t bar[kFinStages];
   const int64_t n4 = (int64_t(n) / 4) * 4;  // bulk-copied part (16-byte multiple)
@@ -753,6 +758,12 @@ thread_local unsigned t_pending_stamps = 0;
 
 void stamp_defer(int i) { t_pending_stamps |= 1u << i; }
 
+unsigned take_stamps() {
+  const unsigned m = t_pending_stamps;
+  t_pending_stamps = 0;
+  return m;
+}
+
 void stamp_flush(unsigned long long* ctr, cudaStream_t st) {
   if (!t_pending_stamps) return;
   (k_stamp_mask<<<1, 1, 0, st>>>(ctr, t_pending_stamps), ::gc::count_launch());
@@ -800,7 +811,7 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
     // the fallback kernels usually exit at once: one resident wave keeps
     // their early exit cheap and still streams when they do run
     const int g = grid_for(n, kEwBlock, 1);
-    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1), ::gc::count_launch());
+    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1, take_stamps()), ::gc::count_launch());
     // one resident wave: six 256-thread blocks per SM, two quads per thread
     const int gps = grid_for((nq + 1) / 2, kEwBlock, 1) < num_sms() * 6 ? grid_for((nq + 1) / 2, kEwBlock, 1)
                                                                           : num_sms() * 6;
@@ -855,10 +866,11 @@ void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr,
   if (tma && reinterpret_cast<uintptr_t>(P) % 16 == 0) {
     const int64_t tiles = ((int64_t(n) / 4) * 4 + kFinTile - 1) / kFinTile;
     const int64_t cap = int64_t(num_sms()) * 6;  // 6 blocks x 33 KB of stages per SM
-    (k_finalize_tma<<<int(tiles < cap ? (tiles > 0 ? tiles : 1) : cap), kEwBlock, 0, st>>>(P, n, ctr),
+    (k_finalize_tma<<<int(tiles < cap ? (tiles > 0 ? tiles : 1) : cap), kEwBlock, 0, st>>>(P, n, ctr,
+                                                                                          take_stamps()),
      ::gc::count_launch());
   } else
-  (k_finalize<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, ctr),
+  (k_finalize<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, ctr, take_stamps()),
    ::gc::count_launch());
   if (!maybe_noncanon) {
     GC_CHECK_LAUNCH();

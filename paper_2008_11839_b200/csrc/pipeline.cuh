@@ -13,7 +13,8 @@ namespace gc {
 constexpr int kEwBlock = 256;
 
 // P[v] = v; optional hook / lock arrays (DisjointSets.__init__, dset.py:353-379)
-__global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n);
+__global__ void k_init_sets(int32_t* P, int32_t* H, int32_t* L, int32_t n, unsigned long long* stamps = nullptr,
+                            unsigned stamp_mask = 0u);
 
 // Full compression to the fixpoint (sampling.py:38-47 compress_all).
 __global__ void k_compress(int32_t* P, int32_t n);
@@ -21,7 +22,7 @@ __global__ void k_compress(int32_t* P, int32_t n);
 // Most-frequent label (sampling.py:29-35): probe a strided sample for the
 // candidate, count it exactly; a strict majority is provably the argmax,
 // otherwise an exact histogram decides (ties -> smaller label).
-__global__ void k_mode_probe(const int32_t* P, int32_t n, unsigned long long* ctr, int walk);
+__global__ void k_mode_probe(const int32_t* P, int32_t n, unsigned long long* ctr, int walk, unsigned stamp_mask = 0u);
 __global__ void k_count_eq(const int32_t* P, int32_t n, unsigned long long* ctr);
 __global__ void k_hist_zero(int32_t* hist, int32_t n, unsigned long long* ctr);
 __global__ void k_hist_add(const int32_t* P, int32_t* hist, int32_t n, unsigned long long* ctr);
@@ -34,7 +35,7 @@ __global__ void k_gather_active(const int32_t* P, int32_t n, const int64_t* off,
 
 // Pointer jump to the root in place; counts roots and flags labels that are
 // not their class minimum (label_finalization, driver.py:420-429).
-__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr);
+__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask = 0u);
 // canonical_labels (validate.py:251-259), skipped on device when the
 // finalize pass proved labels already canonical.
 __global__ void k_canon_init(int32_t* mins, int32_t n, const unsigned long long* ctr);
@@ -71,6 +72,9 @@ void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st);
 void stamp(unsigned long long* ctr, int i, cudaStream_t st);
 void stamp_defer(int i);
 void stamp_flush(unsigned long long* ctr, cudaStream_t st);
+// the pending (deferred) stamps, handed to the next kernel launch that takes
+// them at entry (entry_stamp); clears them
+unsigned take_stamps();
 void set_ctr_add(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 
 }  // namespace gc

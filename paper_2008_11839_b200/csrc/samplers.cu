@@ -56,6 +56,7 @@ void run_kout(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs
   }
   require(s.kout_k == 1 || s.kout_rand_offsets != nullptr, GC_ERR_ARG,
           "FIRST_PLUS_RANDOM needs host-drawn row offsets");
+  stamp_flush(ctr, st);  // deferred phase stamps: this path starts with a pair kernel
   (k_kout_random_pairs<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(
       g.offsets, g.targets, n, s.kout_k, s.kout_rand_offsets, w.coo_u, w.coo_v, ctr), ::gc::count_launch());
   GC_CHECK_LAUNCH();
@@ -115,6 +116,7 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
             SamplerWs& w, unsigned long long* ctr, cudaStream_t st) {
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:95-96
+  stamp_flush(ctr, st);  // deferred phase stamps: phase 1 runs first
   GC_CUDA(cudaMemsetAsync(ctr + C_SCRATCH0, 0, 8, st));
   int64_t lo = 0, hi = n;
   if (a.count_host > 0 && a.count_host <= n) {  // sharded caller: its row block

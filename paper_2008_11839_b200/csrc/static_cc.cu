@@ -216,7 +216,8 @@ struct Pipeline {
     if (n == 0) return;
     int32_t* H = c.unite == GC_FINISH_HOOKS ? ws.H : nullptr;
     int32_t* L = c.unite == GC_FINISH_REM_LOCK ? ws.L : nullptr;
-    (k_init_sets<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, H, L, n), ::gc::count_launch());
+    (k_init_sets<<<grid_for(n, kEwBlock, 8), kEwBlock, 0, st>>>(P, H, L, n, ws.ctr + C_STAMP0, take_stamps()),
+     ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 
@@ -229,13 +230,17 @@ struct Pipeline {
     }
     if (s.sample == GC_SAMPLE_KOUT || s.sample == GC_SAMPLE_HB) {
       init_sets(sc);
-      if (kev) stamp(ws.ctr, 5, st);
+      // the sampler kernel's span: taken at the entry of the union kernel
+      // and of the mode probe that follows it (no stamp nodes)
+      if (kev) stamp_defer(5);
+      RowUnionArgs ra = rows(sc);
+      ra.stamps = ws.ctr + C_STAMP0;
       if (s.sample == GC_SAMPLE_KOUT) {
-        run_kout(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
+        run_kout(g, s, sc, ra, fu != nullptr, ws.samp, ws.ctr, st);
       } else {
-        run_hb(g, s, sc, rows(sc), fu != nullptr, ws.samp, ws.ctr, st);
+        run_hb(g, s, sc, ra, fu != nullptr, ws.samp, ws.ctr, st);
       }
-      if (kev) stamp(ws.ctr, 6, st);
+      if (kev) stamp_defer(6);
       timed_sample = true;
       run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, true, st);
     } else if (s.sample == GC_SAMPLE_BFS) {
@@ -294,7 +299,7 @@ struct Pipeline {
         a.insp = nullptr;  // counted by the gather
       }
       if (kev) stamp_defer(7);
-      stamp_flush(ws.ctr, st);
+      a.stamps = ws.ctr + C_STAMP0;  // the pending stamps are taken at the union kernel's entry
       launch_union_rows(finish_cfg(s), fu != nullptr, a, st);
       if (kev) stamp_defer(8);
       return 0;
@@ -354,7 +359,12 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   pl.kev = ev + 5;
   const int32_t n = pl.n;
 
-  stamp(pl.ws.ctr, 0, st);
+  // union-find samplers start with the set init, which takes stamp 0 at its
+  // entry; the traversal samplers stamp with a node
+  if (spec->sample == GC_SAMPLE_NONE || spec->sample == GC_SAMPLE_KOUT || spec->sample == GC_SAMPLE_HB)
+    stamp_defer(0);
+  else
+    stamp(pl.ws.ctr, 0, st);
   pl.sample();
   stamp_defer(1);  // shares a node with the finish-phase stamps when nothing runs between
   if (spec->sample == GC_SAMPLE_NONE) pl.set_lmax_sentinel();
@@ -374,7 +384,8 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   stamp_defer(2);
   rs.rounds = pl.finish();
   stamp_defer(3);
-  stamp_flush(pl.ws.ctr, st);
+  // finalize takes the pending stamps at its entry
+  if (forest || n == 0) stamp_flush(pl.ws.ctr, st);
   if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
   if (forest && n) {
     // spanning_forest: component_count = n - |forest| (driver.py:535); the

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(kRowBlock)
 k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restrict__ tgt,
              const int32_t* __restrict__ list, const unsigned long long* count_dev,
              int64_t count_host, int32_t take_max, int32_t lower_only,
-             unsigned long long* insp, int64_t row_base) {
+             unsigned long long* insp, int64_t row_base, unsigned long long* stamps, unsigned stamp_mask) {
+  entry_stamp(stamps, stamp_mask);
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (int64_t(blockIdx.x) * kRowBlock + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * kRowBlock) >> 5;
@@ -88,7 +89,8 @@ k_union_rows(UFState s, const int64_t* __restrict__ off, const int32_t* __restri
 template <class R>
 __global__ void __launch_bounds__(256)
 k_union_csr_edges(UFState s, const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n,
-                  int64_t m) {
+                  int64_t m, unsigned long long* stamps, unsigned stamp_mask) {
+  entry_stamp(stamps, stamp_mask);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += stride) {
     const int32_t t = ldg32(tgt + j);
@@ -367,7 +369,8 @@ struct RowsLaunch {
       int64_t blocks = (a.all_edges + 255) / 256;
       const int64_t cap = int64_t(num_sms()) * 8 * 16;
       if (blocks > cap) blocks = cap;
-      (k_union_csr_edges<R><<<int(blocks), 256, 0, st>>>(s, a.off, a.tgt, a.n, a.all_edges),
+      const unsigned sm = a.stamps ? take_stamps() : 0u;
+      (k_union_csr_edges<R><<<int(blocks), 256, 0, st>>>(s, a.off, a.tgt, a.n, a.all_edges, a.stamps, sm),
        ::gc::count_launch());
       GC_CHECK_LAUNCH();
       return;
@@ -378,9 +381,10 @@ struct RowsLaunch {
     const int64_t cap = int64_t(num_sms()) * (2048 / kRowBlock);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    const unsigned sm = a.stamps ? take_stamps() : 0u;
     (k_union_rows<R><<<int(blocks), kRowBlock, 0, st>>>(s, a.off, a.tgt, a.list, a.count_dev,
                                                         a.count_host, a.take_max, a.lower_only,
-                                                        a.insp, a.row_base), ::gc::count_launch());
+                                                        a.insp, a.row_base, a.stamps, sm), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
