@@ -82,17 +82,17 @@ __device__ __forceinline__ bool test_bit(const uint32_t* bits, int32_t x) {
   return (__ldg(bits + (x >> 5)) >> (x & 31)) & 1u;
 }
 
-__device__ __forceinline__ bool claim_par(uint32_t* par, const uint32_t* vis, int32_t x, int32_t f) {
-  // both filters load in parallel: reached in an earlier level (the frozen
-  // bitmap; required — a 32-bit parent carries no level), or a claim of
-  // this level at or below f already landed (a stale L1 value only costs
-  // one atomic)
-  const uint32_t vw = __ldg(vis + (x >> 5));
-  const uint32_t seen = uint32_t(ld_weak(reinterpret_cast<const int32_t*>(par + x)));
-  if ((vw >> (x & 31)) & 1u) return false;
-  if (seen <= uint32_t(f)) return false;
-  return atomicMin(par + x, uint32_t(f)) == kUnreached;
-}
+
+// One top-down level over the frontier queue q (count in qstat[0]); claims
+// go to qn through the caller's block queue.  `frozen`: the visited bitmap
+// is read through the non-coherent path (a separate launch froze it); the
+// persistent form reads it coherently (other CTAs marked it in this launch).
+template <bool COHERENT>
+__device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_t* __restrict__ off,
+                                             const int32_t* __restrict__ tgt, const int32_t* q, int64_t count,
+                                             uint32_t* par, const uint32_t* vis, int32_t* qn,
+                                             unsigned long long* nstat, uint32_t* nbits, int32_t* minv,
+                                             unsigned long long* insp);
 
 __global__ void __launch_bounds__(kTB)
 k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
@@ -103,8 +103,30 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
   bq.init();
   // batched levels: clear the stat slot the level after next will fill
   if (zero_next && blockIdx.x == 0 && threadIdx.x == 0) zero_next[0] = zero_next[1] = 0;
+  bfs_td_level<false>(bq, off, tgt, q, int64_t(qstat[0]), par, vis, qn, nstat, nbits, minv, insp);
+}
+
+__device__ __forceinline__ uint32_t ld_vis(const uint32_t* p, bool coherent) {
+  if (!coherent) return __ldg(p);
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool COHERENT>
+__device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_t* __restrict__ off,
+                                             const int32_t* __restrict__ tgt, const int32_t* q, int64_t count,
+                                             uint32_t* par, const uint32_t* vis, int32_t* qn,
+                                             unsigned long long* nstat, uint32_t* nbits, int32_t* minv,
+                                             unsigned long long* insp) {
   const int lane = threadIdx.x & 31;
-  const int64_t count = int64_t(qstat[0]);
+  auto claim_p = [&](int32_t x, int32_t f) {
+    const uint32_t vw = ld_vis(vis + (x >> 5), COHERENT);
+    const uint32_t seen = uint32_t(ld_weak(reinterpret_cast<const int32_t*>(par + x)));
+    if ((vw >> (x & 31)) & 1u) return false;
+    if (seen <= uint32_t(f)) return false;
+    return atomicMin(par + x, uint32_t(f)) == kUnreached;
+  };
   unsigned long long degs = 0;
   int32_t my_min = INT_MAX;
   auto take = [&](bool fresh, int32_t x) {
@@ -119,7 +141,7 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
     int32_t f = -1;
     int64_t b = 0, d = 0;
     if (i < count) {
-      f = q[i];
+      f = COHERENT ? ld_acq(q + i) : q[i];
       b = off[f];
       d = off[f + 1] - b;
       degs += static_cast<unsigned long long>(d);  // frontier degree (counted at expansion)
@@ -135,7 +157,7 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
       bool fresh = false;
       if (!big && j < d) {
         x = tgt[b + j];
-        fresh = claim_par(par, vis, x, f);
+        fresh = claim_p(x, f);
       }
       take(fresh, x);
     }
@@ -152,7 +174,7 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
         bool fresh = false;
         if (j < dd) {
           x = tgt[bb + j];
-          fresh = claim_par(par, vis, x, ff);
+          fresh = claim_p(x, ff);
         }
         take(fresh, x);
       }
@@ -163,6 +185,53 @@ k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const
   if (insp) block_add<kTB>(insp, degs);
   my_min = warp_min(my_min);
   if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+}
+
+// Narrow top-down levels in ONE persistent cooperative launch (SURVEY hard
+// part 6: a 256^3 grid has 765 levels, and a launch pair per level cost
+// ~21 us).  Per level: the claims of bfs_td_level, a grid barrier, the new
+// queue's vertices marked visited (the bitmap stays frozen while a level
+// claims, so same-level claimants all reach the atomicMin and the smallest
+// frontier id wins, as in the reference), a grid barrier.  The launch stops
+// after max_levels levels, on an empty frontier, or once the frontier
+// reaches nf_stop (the host then re-evaluates the direction switch).
+// Frontier stats [count, degree sum] use the ring of three slots of the
+// launch-per-level form; out[0] = levels run.
+__global__ void __launch_bounds__(kTB)
+k_bfs_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t* q0, int32_t* q1,
+              unsigned long long* stat, int64_t level0, int32_t max_levels, unsigned long long nf_stop,
+              uint32_t* par, uint32_t* vis, int32_t* minv, unsigned long long* reached,
+              unsigned long long* out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ BlockQueue<kQCap> bq;
+  bq.init();
+  const int64_t gtid = int64_t(blockIdx.x) * kTB + threadIdx.x;
+  const int64_t gthreads = int64_t(gridDim.x) * kTB;
+  int32_t k = 0;
+  while (k < max_levels) {
+    const int64_t L = level0 + k;
+    int32_t* q = (L & 1) ? q1 : q0;
+    int32_t* qn = (L & 1) ? q0 : q1;
+    unsigned long long* cur = stat + 2 * (L % 3);
+    unsigned long long* nxt = stat + 2 * ((L + 1) % 3);
+    if (gtid == 0) {
+      unsigned long long* z = stat + 2 * ((L + 2) % 3);
+      z[0] = z[1] = 0;
+    }
+    const int64_t count = int64_t(*reinterpret_cast<volatile unsigned long long*>(cur));
+    bfs_td_level<true>(bq, off, tgt, q, count, par, vis, qn, nxt, nullptr, minv, nullptr);
+    grid.sync();
+    const unsigned long long nn = *reinterpret_cast<volatile unsigned long long*>(nxt);
+    for (int64_t i = gtid; i < int64_t(nn); i += gthreads) {
+      const int32_t x = ld_acq(qn + i);
+      atomicOr(vis + (x >> 5), 1u << (x & 31));
+    }
+    if (gtid == 0 && nn) atomicAdd(reached, nn);
+    ++k;
+    grid.sync();
+    if (nn == 0 || nn >= nf_stop) break;
+  }
+  if (gtid == 0) out[0] = static_cast<unsigned long long>(k);
 }
 
 // Wide top-down levels (the frontier is no longer narrow) run in two
@@ -817,6 +886,16 @@ unsigned long long bfs_wide_min(int64_t n) {
   return static_cast<unsigned long long>(t > 256 ? t : 256);
 }
 
+// GC_BFS_PERSIST=0: narrow levels as a launch pair per level (batched 64 per
+// host round trip) instead of one persistent cooperative launch
+bool bfs_persistent() {
+  static const bool p = [] {
+    const char* e = getenv("GC_BFS_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  return p;
+}
+
 bool bfs_trace() {
   static const bool t = getenv("GC_BFS_TRACE") != nullptr;
   return t;
@@ -876,14 +955,43 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
     if (batch >= 2) {
       const unsigned long long nf0 = nf;
       GC_CUDA(cudaMemsetAsync(slot(level + 1), 0, 16, st));
-      for (int k = 0; k < batch; ++k) {
-        const int64_t L = level + k;
-        TL(k_bfs_td, narrow_grid, kTB, g.offsets, g.targets, q[L & 1], slot(L), par, w.vis, q[(L + 1) & 1],
-           slot(L + 1), static_cast<uint32_t*>(nullptr), minv, static_cast<unsigned long long*>(nullptr),
-           slot(L + 2));
-        TL(k_mark_queue, narrow_grid, kEwBlock, q[(L + 1) & 1], slot(L + 1), w.vis, reached);
+      if (bfs_persistent()) {
+        // every narrow level in one cooperative launch, until the frontier
+        // reaches the narrow bound (the direction switch is re-evaluated
+        // on the host) or empties
+        static int per_sm = 0;
+        if (!per_sm) {
+          GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_persist, kTB, 0));
+          if (per_sm < 1) throw Error(GC_ERR_CUDA, "BFS persistent kernel does not fit on an SM");
+        }
+        const int64_t* off = g.offsets;
+        const int32_t* tgt = g.targets;
+        int32_t* q0 = q[0];
+        int32_t* q1 = q[1];
+        unsigned long long* stat = w.stat;
+        int64_t lv0 = level;
+        int32_t maxl = 1 << 20;
+        unsigned long long nfs = static_cast<unsigned long long>(limit > 1.0 ? limit : 1.0);
+        uint32_t* vis = w.vis;
+        unsigned long long* outp = w.stat + 7;
+        void* args[] = {&off, &tgt, &q0, &q1, &stat, &lv0, &maxl, &nfs, &par, &vis, &minv, &reached, &outp};
+        GC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_bfs_persist),
+                                            dim3(num_sms() * per_sm), dim3(kTB), args, 0, st));
+        ::gc::count_launch();
+        GC_CHECK_LAUNCH();
+        GC_CUDA(cudaMemcpyAsync(h + 3, outp, 8, cudaMemcpyDeviceToHost, st));
+        GC_CUDA(cudaStreamSynchronize(st));
+        batch = int(h[3]);
+      } else {
+        for (int k = 0; k < batch; ++k) {
+          const int64_t L = level + k;
+          TL(k_bfs_td, narrow_grid, kTB, g.offsets, g.targets, q[L & 1], slot(L), par, w.vis, q[(L + 1) & 1],
+             slot(L + 1), static_cast<uint32_t*>(nullptr), minv, static_cast<unsigned long long*>(nullptr),
+             slot(L + 2));
+          TL(k_mark_queue, narrow_grid, kEwBlock, q[(L + 1) & 1], slot(L + 1), w.vis, reached);
+        }
+        GC_CHECK_LAUNCH();
       }
-      GC_CHECK_LAUNCH();
       level += batch;
       GC_CUDA(cudaMemcpyAsync(h, slot(level), 16, cudaMemcpyDeviceToHost, st));
       GC_CUDA(cudaMemcpyAsync(h + 2, reached, 8, cudaMemcpyDeviceToHost, st));
