@@ -147,17 +147,36 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
       degs += static_cast<unsigned long long>(d);  // frontier degree (counted at expansion)
     }
     const bool big = d > 32;
-    int64_t dm = big ? 0 : d;
-    for (int o = 16; o > 0; o >>= 1) {
-      const int64_t t = __shfl_xor_sync(0xffffffffu, dm, o);
-      dm = t > dm ? t : dm;
+    // rows of at most 32 entries: the warp concatenates them and every lane
+    // claims one entry per step (its row found by a binary search over the
+    // warp's degree prefix), so a level costs one claim latency per 32 row
+    // entries of the warp instead of one per entry of the longest row
+    int32_t incl = big ? 0 : int32_t(d);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    for (int64_t j = 0; j < dm; ++j) {
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t dsm = big ? 0 : int32_t(d);
+    for (int32_t e0 = 0; e0 < total; e0 += 32) {
+      const int32_t e = e0 + lane;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (v <= e) lo += step;
+      }
+      const int src = lo > 31 ? 31 : lo;
+      const int32_t se = __shfl_sync(0xffffffffu, incl, src);
+      const int32_t sd = __shfl_sync(0xffffffffu, dsm, src);
+      const int64_t sb = __shfl_sync(0xffffffffu, b, src);
+      const int32_t sf = __shfl_sync(0xffffffffu, f, src);
       int32_t x = 0;
       bool fresh = false;
-      if (!big && j < d) {
-        x = tgt[b + j];
-        fresh = claim_p(x, f);
+      if (e < total) {
+        x = tgt[sb + (e - (se - sd))];
+        fresh = claim_p(x, sf);
       }
       take(fresh, x);
     }
