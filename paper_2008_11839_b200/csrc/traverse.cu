@@ -136,11 +136,20 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
     }
     bq.push(fresh, x, qn, nstat);
   };
-  for (int64_t base = int64_t(blockIdx.x) * kTB; base < count; base += int64_t(gridDim.x) * kTB) {
-    const int64_t i = base + threadIdx.x;
+  // a warp takes vpw frontier vertices per step: 32 while the frontier
+  // fills every warp, fewer on narrow levels so that every warp of the grid
+  // holds part of the level (a high-diameter level is a few thousand rows:
+  // 32 rows per warp left most warps idle and the rest walking ~6 claim
+  // steps each)
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int64_t vpw64 = (count + nwarps - 1) / nwarps;
+  const int vpw = int(vpw64 < 1 ? 1 : (vpw64 > 32 ? 32 : vpw64));
+  for (int64_t base = gw * vpw; base < count; base += nwarps * vpw) {
+    const int64_t i = base + lane;
     int32_t f = -1;
     int64_t b = 0, d = 0;
-    if (i < count) {
+    if (lane < vpw && i < count) {
       f = COHERENT ? ld_acq(q + i) : q[i];
       b = off[f];
       d = off[f + 1] - b;
@@ -198,7 +207,8 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
         take(fresh, x);
       }
     }
-    bq.maybe_flush(qn, nstat, kQCap / 2);
+    // (warps run different trip counts: no block-wide flush inside the loop;
+    // a full staging area spills straight to the queue)
   }
   bq.flush(qn, nstat);
   if (insp) block_add<kTB>(insp, degs);
@@ -784,12 +794,16 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     unsigned long long* cout = ring + (r + 1) % 3;
     if (gtid == 0) ring[(r + 2) % 3] = 0;  // read by nobody this round; written next round
     const int64_t count = r > 0 ? int64_t(*reinterpret_cast<volatile unsigned long long*>(ring + r % 3)) : 0;
-    for (int64_t wb = gwarp * 32; wb < count; wb += nwarps * 32) {
+    // vpw frontier vertices per warp step: fewer than 32 on narrow rounds so
+    // every warp of the grid takes part (see bfs_td_level)
+    const int64_t vpw64 = (count + nwarps - 1) / nwarps;
+    const int vpw = int(vpw64 < 1 ? 1 : (vpw64 > 32 ? 32 : vpw64));
+    for (int64_t wb = gwarp * vpw; wb < count; wb += nwarps * vpw) {
       const int64_t i = wb + lane;
       uint32_t c = 0;
       int64_t b = 0;
       int32_t d = 0;
-      if (i < count) {
+      if (lane < vpw && i < count) {
         const int32_t f = ld_acq(qin + i);
         c = ld_rlx_u32(cluster + f);  // final since round r-1
         // graph data is read once: L2 evict-first keeps the claim state resident
