@@ -46,6 +46,18 @@ __device__ __forceinline__ bool cas(int32_t* p, int32_t expect, int32_t desired)
   return atomicCAS(p, expect, desired) == expect;
 }
 
+// bitmap words that other threads set concurrently (plain L1-cacheable
+// load: a stale word only misses bits, which every user tolerates)
+__device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_or_bits(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ bool gbit(uint32_t w, int32_t x) { return (w >> (x & 31)) & 1u; }
+
 // fire-and-forget min (RED.MIN): the result is not needed by the caller
 __device__ __forceinline__ void red_min(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -23,6 +23,19 @@ struct gc_incr {
   int32_t* aux = nullptr;     // hooks / locks
   unsigned long long* ctr = nullptr;
   unsigned int* bad = nullptr;  // sticky device flag: an op had an endpoint outside [0, cap)
+  // giant filter (union-find rules): bit x set => x is connected to the
+  // anchor; gstate[0] = the anchor component's root (-1: none yet),
+  // gstate[1] = the anchor moved to another component (clear the bits)
+  uint32_t* gbits = nullptr;
+  // 32 bytes: [0] anchor, [1] moved flag, [2..3] u64 count of compacted
+  // inserts (~0: passed through), [4] compact the next batch (1) or pass it
+  // through (0)
+  int32_t* gstate = nullptr;
+  int32_t* hmode = nullptr;      // mapped pinned copy of gstate[4] (grid choice only)
+  int32_t* hmode_dev = nullptr;
+  int32_t* cu = nullptr;       // the compacted inserts of the current batch
+  int32_t* cv = nullptr;
+  int64_t ccap = 0;
   // rounds scratch
   gc::RoundsWs rw;
   int64_t coo_cap = 0;
@@ -41,7 +54,7 @@ constexpr int kIB = 256;
 // == 0) read as 0.
 __global__ void k_incr_query(const int32_t* P, const int32_t* us, const int32_t* vs,
                              const uint8_t* isq, int64_t len, int32_t sentinel, uint32_t* bits,
-                             unsigned int* bad) {
+                             unsigned int* bad, const uint32_t* gbits) {
   const int lane = threadIdx.x & 31;
   const int64_t words = (len + 31) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -52,6 +65,8 @@ __global__ void k_incr_query(const int32_t* P, const int32_t* us, const int32_t*
       int32_t x = us[i], y = vs[i];
       if (uint32_t(x) >= uint32_t(sentinel) || uint32_t(y) >= uint32_t(sentinel)) {
         atomicOr(bad, 1u);
+      } else if (gbits && gbit(gbits[x >> 5], x) && gbit(gbits[y >> 5], y)) {
+        hit = true;  // both connected to the giant filter's anchor
       } else {
         int32_t px = P[x];
         if (px != sentinel)
@@ -136,6 +151,286 @@ __global__ void k_incr_count(const int32_t* S, const int32_t* fin, int64_t cap, 
 
 int g1(int64_t work) { return grid_for(work, kIB, 8); }
 
+// Giant filter upkeep, after every union-find insert sub-phase.  One block
+// samples 1024 evenly spaced slots, chases their roots and takes the most
+// frequent one (warp-aggregated shared-memory hash, as k_mode_probe).  The
+// anchor is re-resolved to its component's current root; it moves to the
+// sampled mode only when that component clearly dominates (then the bits,
+// which mean "connected to the old anchor", are cleared by k_giant_clear).
+// Roots of the min-linking rules are component minima, so once the giant
+// has formed its root — the anchor — stays put.
+__global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t cap, int32_t sentinel,
+                                                      int32_t* gstate, const uint32_t* gbits, const int32_t* us,
+                                                      const int32_t* vs, const uint8_t* isq, int64_t len,
+                                                      volatile int32_t* hmode) {
+  __shared__ unsigned both, seen;
+  constexpr int kS = 1024, kSlots = 2 * kS;
+  __shared__ int32_t key_[kSlots];
+  __shared__ unsigned cnt_[kSlots];
+  __shared__ unsigned long long best;
+  const int i = threadIdx.x;
+  for (int k = i; k < kSlots; k += kS) {
+    key_[k] = -1;
+    cnt_[k] = 0;
+  }
+  if (i == 0) {
+    best = 0ull;
+    both = seen = 0u;
+  }
+  const int s = cap < kS ? int(cap) : kS;
+  int32_t x = -1;
+  if (i < s) {
+    x = int32_t((int64_t(i) * cap) / s);
+    int32_t p = ld_acq(P + x);
+    if (p == sentinel) {
+      x = -1;
+    } else {
+      while (p != x) {
+        x = p;
+        p = ld_acq(P + x);
+      }
+    }
+  }
+  __syncthreads();
+  auto slot_of = [](int32_t v) { return int((uint32_t(v) * 2654435761u) >> (32 - 11)); };
+  int slot = -1;
+  if (x >= 0) {
+    const unsigned same = __match_any_sync(__activemask(), x);
+    slot = slot_of(x);
+    while (true) {
+      const int32_t k = atomicCAS(&key_[slot], -1, x);
+      if (k == -1 || k == x) break;
+      slot = (slot + 1) % kSlots;
+    }
+    if ((i & 31) == __ffs(int(same)) - 1) atomicAdd(&cnt_[slot], __popc(same));
+  }
+  __syncthreads();
+  if (x >= 0)
+    atomicMax(&best, (static_cast<unsigned long long>(cnt_[slot]) << 32) | (0xffffffffull - uint32_t(x)));
+  // the filter rate the next batch can expect: the share of this batch's
+  // inserts (1024 evenly spaced samples) whose endpoints are both marked now
+  const int ns = len < kS ? int(len) : kS;
+  if (i < ns) {
+    const int64_t j = (int64_t(i) * len) / ns;
+    if (!(isq && isq[j])) {
+      const int32_t a = us[j], b = vs[j];
+      if (uint32_t(a) < uint32_t(cap) && uint32_t(b) < uint32_t(cap)) {
+        atomicAdd(&seen, 1u);
+        if (gbit(ld_bits(gbits + (a >> 5)), a) && gbit(ld_bits(gbits + (b >> 5)), b)) atomicAdd(&both, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (i != 0) return;
+  int32_t cur = gstate[0];
+  if (cur >= 0) {
+    int32_t p = ld_acq(P + cur);
+    while (p != cur) {
+      cur = p;
+      p = ld_acq(P + cur);
+    }
+  }
+  const unsigned cm = unsigned(best >> 32);
+  const int32_t m = int32_t(0xffffffffull - (best & 0xffffffffull));
+  unsigned cc = 0;
+  if (cur >= 0)
+    for (int k = slot_of(cur), t = 0; t < kSlots && key_[k] != -1; k = (k + 1) % kSlots, ++t)
+      if (key_[k] == cur) {
+        cc = cnt_[k];
+        break;
+      }
+  const bool move = cm > 0 && m != cur && (cur < 0 || cm >= 2 * cc + 8);
+  gstate[0] = move ? m : cur;
+  gstate[1] = move && cur >= 0;
+  *reinterpret_cast<unsigned long long*>(gstate + 2) = 0ull;  // the next batch's compaction count
+  // compacting costs one pass over the batch plus two bit tests per insert;
+  // it pays once about half of the inserts can be dropped (config 4: from
+  // the ~12th of 54 batches on)
+  gstate[4] = !move && seen > 0 && 2 * both >= seen;
+  if (hmode) *hmode = gstate[4];
+}
+
+// Giant filter, first step of a union-find insert sub-phase: inserts whose
+// two endpoints are both marked as connected to the anchor cannot change
+// the partition and are dropped (two bit tests against a cap/8-byte bitmap
+// that stays in L2, instead of two random parent reads in a cap*4-byte
+// array that does not); the rest — and every insert while no anchor is set
+// — are compacted for the union kernel.  A block owns a contiguous chunk
+// of the batch, each thread four consecutive inserts per step (16-byte
+// loads), survivors are staged in a shared-memory queue that is flushed
+// with one counter atomic once half full.  Queries of a mixed batch are
+// dropped here too; malformed endpoints set the sticky flag.
+constexpr int kGcQ = 2048;
+__global__ void __launch_bounds__(kIB)
+k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const uint8_t* __restrict__ isq,
+                int64_t len, int32_t cap, const uint32_t* __restrict__ gbits, int32_t* gstate, int32_t* ou,
+                int32_t* ov, unsigned int* bad) {
+  constexpr int kStep = kIB * 4;
+  __shared__ int2 q[kGcQ];
+  __shared__ int qn;
+  __shared__ unsigned long long qbase;
+  unsigned long long* ocount = reinterpret_cast<unsigned long long*>(gstate + 2);
+  const int32_t anc = gstate[0];
+  const bool on = anc >= 0;
+  if (!on || !gstate[4]) {  // pass the batch through: the union reads the caller's arrays
+    if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<unsigned long long*>(gstate + 2) = ~0ull;
+    return;
+  }
+  const bool vec = ((reinterpret_cast<uintptr_t>(us) | reinterpret_cast<uintptr_t>(vs)) & 15) == 0;
+  if (threadIdx.x == 0) qn = 0;
+  // the anchor is connected to itself: its bit seeds the marking (the other
+  // blocks may test it before it lands, which only keeps an insert)
+  if (on && blockIdx.x == 0 && threadIdx.x == 0) red_or_bits(const_cast<uint32_t*>(gbits) + (anc >> 5), 1u << (anc & 31));
+  const int64_t per = ((len + gridDim.x - 1) / gridDim.x + kStep - 1) / kStep * kStep;
+  const int64_t lo = int64_t(blockIdx.x) * per;
+  const int64_t hi = lo + per < len ? lo + per : len;
+  const int lane = threadIdx.x & 31;
+  auto flush = [&]() {
+    __syncthreads();
+    const int c = qn;
+    if (threadIdx.x == 0) qbase = c ? atomicAdd(ocount, static_cast<unsigned long long>(c)) : 0ull;
+    __syncthreads();
+    for (int k = threadIdx.x; k < c; k += kIB) {
+      ou[qbase + k] = q[k].x;
+      ov[qbase + k] = q[k].y;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+  };
+  __syncthreads();
+  for (int64_t b = lo; b < hi; b += kStep) {
+    const int64_t i0 = b + 4 * int64_t(threadIdx.x);
+    int32_t u[4] = {0, 0, 0, 0}, v[4] = {0, 0, 0, 0};
+    bool keep[4] = {false, false, false, false};
+    if (vec && i0 + 3 < hi) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(us + i0));
+      const int4 c = __ldg(reinterpret_cast<const int4*>(vs + i0));
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+      v[0] = c.x; v[1] = c.y; v[2] = c.z; v[3] = c.w;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) keep[j] = true;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j < hi) {
+          u[j] = __ldg(us + i0 + j);
+          v[j] = __ldg(vs + i0 + j);
+          keep[j] = true;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!keep[j]) continue;
+      if (isq && isq[i0 + j]) keep[j] = false;
+      else if (uint32_t(u[j]) >= uint32_t(cap) || uint32_t(v[j]) >= uint32_t(cap)) {
+        atomicOr(bad, 1u);
+        keep[j] = false;
+      }
+    }
+    if (on) {
+      uint32_t wu[4], wv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        wu[j] = keep[j] ? __ldg(gbits + (u[j] >> 5)) : 0u;
+        wv[j] = keep[j] ? __ldg(gbits + (v[j] >> 5)) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool bu = gbit(wu[j], u[j]), bv = gbit(wv[j], v[j]);
+        if (bu && bv) keep[j] = false;
+        // survivors carry "bit already set" in bit 31 (the union marks
+        // only the endpoints that lack it)
+        u[j] |= bu ? int32_t(0x80000000u) : 0;
+        v[j] |= bv ? int32_t(0x80000000u) : 0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, keep[j]);
+      if (!bal) continue;
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(&qn, __popc(bal));
+      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(bal & ((1u << lane) - 1u));
+      if (keep[j]) q[pos] = make_int2(u[j], v[j]);
+    }
+    __syncthreads();
+    if (qn >= kGcQ / 2) flush();  // a step adds at most kStep = kGcQ / 2
+  }
+  flush();
+}
+
+__global__ void k_giant_clear(uint32_t* bits, int64_t words, const int32_t* gstate) {
+  if (!gstate[1]) return;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) bits[w] = 0u;
+}
+
+// GC_INCR_GIANT=0 turns the filter off (every insert runs its union)
+bool giant_filter_on() {
+  static const bool on = [] {
+    const char* e = getenv("GC_INCR_GIANT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// compacts the batch into h->cu / h->cv and points the union at it (count
+// on the device); the caller runs giant_after once the union is enqueued
+void giant_reserve(gc_incr* h, int64_t len) {
+  if (!h->gbits || len <= h->ccap) return;
+  cudaFree(h->cu);
+  cudaFree(h->cv);
+  h->cu = h->cv = nullptr;
+  h->ccap = 0;
+  GC_CUDA(cudaMalloc(&h->cu, len * 4));
+  GC_CUDA(cudaMalloc(&h->cv, len * 4));
+  h->ccap = len;
+}
+
+void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
+  if (!h->gbits || a.k <= 0) return;
+  if (a.k > h->ccap) {
+    cudaFree(h->cu);
+    cudaFree(h->cv);
+    h->cu = h->cv = nullptr;
+    h->ccap = 0;
+    GC_CUDA(cudaMalloc(&h->cu, a.k * 4));
+    GC_CUDA(cudaMalloc(&h->cv, a.k * 4));
+    h->ccap = a.k;
+  }
+  static const int per_sm = [] {
+    int b = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_giant_compact, kIB, 0));
+    return b > 0 ? b : 1;
+  }();
+  int64_t blocks = (a.k + 4 * kIB - 1) / (4 * kIB);
+  if (blocks > int64_t(num_sms()) * per_sm) blocks = int64_t(num_sms()) * per_sm;
+  (k_giant_compact<<<int(blocks), kIB, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap),
+                                                                      h->gbits, h->gstate, h->cu, h->cv, h->bad),
+   ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+  a.alt.us = a.us;
+  a.alt.vs = a.vs;
+  a.alt.skip = a.skip;
+  a.alt.k = a.k;
+  a.us = h->cu;
+  a.vs = h->cv;
+  a.skip = nullptr;
+  a.kdev = reinterpret_cast<const unsigned long long*>(h->gstate + 2);
+  a.kdev_wave = h->hmode && *reinterpret_cast<volatile int32_t*>(h->hmode) != 0;
+}
+
+void giant_after(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len) {
+  if (!h->gbits) return;
+  (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->gbits, us, vs, isq, len,
+                                                h->hmode_dev),
+   ::gc::count_launch());
+  const int64_t words = (h->cap + 31) / 32;
+  (k_giant_clear<<<grid_for(words, kIB, 2), kIB, 0, h->st>>>(h->gbits, words, h->gstate), ::gc::count_launch());
+  GC_CHECK_LAUNCH();
+}
+
 __global__ void k_count_bytes(const uint8_t* a, int64_t n, unsigned long long* out) {
   unsigned long long c = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -183,6 +478,8 @@ CooUnionArgs uf_args(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t l
   a.k = len;
   a.skip = skip;
   a.bad = h->bad;
+  a.gbits = h->gbits;
+  a.ganchor = h->gstate;
   return a;
 }
 
@@ -213,7 +510,9 @@ void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     // lazy init fused into the union launch (measured +44% inserts/s at
     // RMAT s26 over a separate init pass)
     a.init_sentinel = sentinel;
+    giant_compact(h, a, isq);
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
+    giant_after(h, us, vs, isq, len);
     if (stats) stats->insp_finish += n_ins;
     return;
   }
@@ -291,6 +590,19 @@ int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream, gc_incr*
         GC_CUDA(cudaMalloc(&h->aux, (capacity > 0 ? capacity : 1) * 4));
         fill(h->aux, capacity, spec->finish == GC_FINISH_HOOKS ? int32_t(capacity) : 0, h->st);
       }
+      // the giant filter rides on the lock-step async kernel (GC_COO_MLP > 0)
+      if (spec->finish == GC_FINISH_ASYNC && spec->find != GC_FIND_COMPRESS && coo_mlp() > 0 && capacity > 0 &&
+          giant_filter_on()) {
+        const int64_t words = (capacity + 31) / 32;
+        GC_CUDA(cudaMalloc(&h->gbits, words * 4));
+        GC_CUDA(cudaMalloc(&h->gstate, 32));
+        GC_CUDA(cudaMemsetAsync(h->gbits, 0, words * 4, h->st));
+        GC_CUDA(cudaMemsetAsync(h->gstate, 0xff, 4, h->st));  // no anchor yet
+        GC_CUDA(cudaMemsetAsync(h->gstate + 1, 0, 28, h->st));
+        GC_CUDA(cudaHostAlloc(&h->hmode, 4, cudaHostAllocMapped));
+        *h->hmode = 0;
+        GC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->hmode_dev), h->hmode, 0));
+      }
       if (!uf) {
         GC_CUDA(cudaMalloc(&h->rw.a, (capacity + 1) * 4));
         GC_CUDA(cudaMalloc(&h->rw.b, (capacity + 1) * 4));
@@ -311,6 +623,11 @@ void gc_incr_destroy(gc_incr* h) {
   cudaFree(h->aux);
   cudaFree(h->ctr);
   cudaFree(h->bad);
+  cudaFree(h->gbits);
+  cudaFree(h->gstate);
+  cudaFree(h->cu);
+  cudaFree(h->cv);
+  if (h->hmode) cudaFreeHost(h->hmode);
   cudaFree(h->rw.a);
   cudaFree(h->rw.b);
   for (Coo* c : {&h->rw.work, &h->rw.spare}) {
@@ -344,6 +661,7 @@ int gc_incr_reserve(gc_incr* h, int64_t batch_len) {
   return guarded([&] {
     require(h != nullptr && batch_len >= 0, GC_ERR_ARG, "bad reserve");
     if (!h->uf && batch_len > 0) ensure_coo(h, batch_len);
+    if (h->uf && batch_len > 0) giant_reserve(h, batch_len);
   });
 }
 
@@ -377,8 +695,8 @@ int gc_incr_batch(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     GC_CUDA(cudaEventRecord(h->ev[0], st));
     if (n_ins) insert_phase(h, us, vs, is_query, len, n_ins, stats);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
-    (k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out, h->bad),
-     ::gc::count_launch());
+    (k_incr_query<<<g1(len), kIB, 0, st>>>(h->state, us, vs, is_query, len, sentinel, bits_out, h->bad,
+                                          h->gbits), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[2], st));
     fetch_bad(h);
@@ -443,7 +761,9 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
     a.lu = out_u;
     a.lv = out_v;
     a.lcount = out_count;
+    giant_compact(h, a, nullptr);
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
+    giant_after(h, us, vs, nullptr, len);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
     fetch_bad(h);
     GC_CUDA(cudaStreamSynchronize(st));
@@ -463,7 +783,7 @@ int gc_incr_query(gc_incr* h, const int32_t* us, const int32_t* vs, int64_t len,
     require(us && vs && bits_out, GC_ERR_ARG, "null batch arrays");
     GC_CUDA(cudaEventRecord(h->ev[0], h->st));
     (k_incr_query<<<g1(len), kIB, 0, h->st>>>(h->state, us, vs, nullptr, len, int32_t(h->cap), bits_out,
-                                             h->bad), ::gc::count_launch());
+                                             h->bad, h->gbits), ::gc::count_launch());
     GC_CHECK_LAUNCH();
     GC_CUDA(cudaEventRecord(h->ev[1], h->st));
     fetch_bad(h);

@@ -138,6 +138,15 @@ void launch_union_rows(const UFConfig& cfg, bool forest, const RowUnionArgs& a, 
 // pending deferred phase stamps (pipeline.cu), cleared by the call
 unsigned take_stamps();
 
+// The caller's batch arrays for a giant-filter compaction that passed the
+// batch through (see k_union_coo_async_mlp).
+struct GiantPass {
+  const int32_t* us = nullptr;
+  const int32_t* vs = nullptr;
+  const uint8_t* skip = nullptr;
+  int64_t k = 0;
+};
+
 // Union over COO pairs (union_edge_list, incremental inserts).
 struct CooUnionArgs {
   int32_t* P;
@@ -157,6 +166,12 @@ struct CooUnionArgs {
   int32_t init_sentinel = -1;  // >= 0: lazily initialise both endpoints first (incremental)
   unsigned int* bad = nullptr;  // non-null: pairs with an endpoint outside [0, n) are skipped
                                 // and set *bad (the incremental handle's sticky input flag)
+  uint32_t* gbits = nullptr;         // incremental giant filter (see UFState::gbits)
+  const int32_t* ganchor = nullptr;
+  const unsigned long long* kdev = nullptr;  // non-null (async giant filter): the compaction's
+                                             // survivor count, ~0 = use `alt`
+  GiantPass alt;
+  bool kdev_wave = false;  // the batch is expected to be compacted: one-wave grid
 };
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st);
 
@@ -168,6 +183,8 @@ void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t*
                       int32_t sentinel, uint32_t* bits, cudaStream_t st);
 
 int num_sms();
+// unions per thread of the lock-step async COO kernel (GC_COO_MLP, 0 = one per thread)
+int coo_mlp();
 
 // Kernel launches issued by libgconn (process-wide, exported through
 // gc_launch_count for the bench's gpu_launches claim).

@@ -38,7 +38,14 @@ struct UFState {
   // L1 line could still hold the uninitialised sentinel, which is not an
   // ancestor of anything.
   bool weak = true;
+  // incremental giant filter (nullable): bit x of gbits set => x is
+  // connected to the anchor vertex; *ganchor = the anchor component's root
+  // as of the batch start (-1: none yet).  Membership only grows, so a set
+  // bit never goes stale.
+  uint32_t* gbits = nullptr;
+  const int32_t* ganchor = nullptr;
 };
+
 
 template <bool FOREST>
 __device__ __forceinline__ void record(const UFState& s, int32_t slot, int32_t u, int32_t v) {

@@ -159,14 +159,32 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
 template <class R, int K, bool WEAK>
 __global__ void __launch_bounds__(256)
 k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
-                      const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad) {
+                      const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad,
+                      const unsigned long long* kdev, GiantPass alt) {
   static_assert(R::kUnion == GC_FINISH_ASYNC, "lock-step form of the async rule");
+  // giant filter: *kdev = survivors of the compaction (their endpoints
+  // carry bit 31 = "giant bit already set"), or ~0 when the compaction
+  // passed the batch through (the caller's arrays, no flags)
+  bool flags = false;
+  if (kdev) {
+    const unsigned long long c = *kdev;
+    if (c == ~0ull) {
+      us = alt.us;
+      vs = alt.vs;
+      skip = alt.skip;
+      k = alt.k;
+    } else {
+      k = min(k, int64_t(c));
+      flags = true;
+    }
+  }
   constexpr int F = R::kFind;
   int32_t* P = s.P;
   // L1-cacheable reads (static batches) only for the first hops: after that
   // every read goes to L2, so a stale line cannot stall a retry loop
   int it = 0;
   auto ld = [&](const int32_t* p) { return (WEAK && it < 8) ? ld_weak(p) : ld_acq(p); };
+  const int32_t anc = s.gbits ? ld_acq(s.ganchor) : -1;
   const int64_t span = int64_t(blockDim.x) * K;
   for (int64_t base = int64_t(blockIdx.x) * span; base < k; base += int64_t(gridDim.x) * span) {
     int32_t eu[K], ev[K];     // endpoints (forest records)
@@ -176,6 +194,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
     unsigned have = 0;        // bit 2j+c: px[j][c] holds P[x[j][c]]
     unsigned live = 0;        // bit 2j+c: chain still walking
     unsigned slot = 0;        // bit j: union j unfinished
+    unsigned gneed = 0;       // giant filter: bit 2j+c = endpoint c of union j lacks its bit
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const int64_t i = base + int64_t(j) * blockDim.x + threadIdx.x;
@@ -183,6 +202,12 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
       if (i < k && !(skip && skip[i])) {
         eu[j] = ldg32(us + i);
         ev[j] = ldg32(vs + i);
+        if (flags) {
+          // compacted batch: bit 31 = the endpoint's giant bit is already set
+          gneed |= (eu[j] < 0 ? 0u : 1u) << (2 * j) | (ev[j] < 0 ? 0u : 2u) << (2 * j);
+          eu[j] &= 0x7fffffff;
+          ev[j] &= 0x7fffffff;
+        }
         if (bad && (uint32_t(eu[j]) >= uint32_t(s.n) || uint32_t(ev[j]) >= uint32_t(s.n))) {
           atomicOr(bad, 1u);  // malformed pair: never touches the parent array
         } else {
@@ -194,14 +219,41 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
       pv[j][0] = pv[j][1] = -1;
       px[j][0] = px[j][1] = 0;
     }
+    // giant filter (the batch was compacted by k_giant_compact): a union
+    // that ends at the anchor root marks both endpoints as connected to it
+    auto mark = [&](int j, int32_t root) {
+      // connected to the anchor once the union is done: its root is the
+      // anchor, or one endpoint already carried its bit
+      if (root != anc && (gneed >> (2 * j) & 3u) == 3u) return;
+      if (gneed >> (2 * j) & 1u) red_or_bits(s.gbits + (eu[j] >> 5), 1u << (eu[j] & 31));
+      if (gneed >> (2 * j) & 2u) red_or_bits(s.gbits + (ev[j] >> 5), 1u << (ev[j] & 31));
+    };
     // endpoint reads, all issued together; lazy init (driver.py:620-625)
     // of the slots still holding the sentinel
+    uint32_t wb[K][2];
+    const bool probe_bits = anc >= 0 && !flags;
 #pragma unroll
     for (int j = 0; j < K; ++j)
       if (slot >> j & 1u) {
         px[j][0] = ld(P + x[j][0]);
         px[j][1] = ld(P + x[j][1]);
+        if (probe_bits) {
+          // passed-through batch: the endpoints' giant bits, read beside
+          // the parent reads (no added latency), so only missing bits are
+          // set and doubly marked inserts stop here
+          wb[j][0] = ld_bits(s.gbits + (eu[j] >> 5));
+          wb[j][1] = ld_bits(s.gbits + (ev[j] >> 5));
+        }
       }
+    if (probe_bits) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (slot >> j & 1u) {
+          const bool bu = gbit(wb[j][0], eu[j]), bv = gbit(wb[j][1], ev[j]);
+          gneed |= (bu ? 0u : 1u) << (2 * j) | (bv ? 0u : 2u) << (2 * j);
+          if (bu && bv) slot &= ~(1u << j);
+        }
+    }
     if (sentinel >= 0) {
 #pragma unroll
       for (int j = 0; j < K; ++j)
@@ -256,6 +308,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           const int32_t ru = x[j][0], rv = x[j][1];
           if (ru == rv) {
             slot &= ~(1u << j);
+            if (anc >= 0) mark(j, ru);
           } else {
             const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
             old[j] = atomicCAS(P + hi, hi, lo);
@@ -270,6 +323,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
         if (old[j] == hi) {
           record<R::kForest>(s, hi, eu[j], ev[j]);
           slot &= ~(1u << j);
+          if (anc >= 0) mark(j, lo);
         } else {
           // hi was linked meanwhile: resume both finds from the roots
           // (register selects, no dynamic index into the chain arrays)
@@ -353,6 +407,20 @@ int num_sms() {
   return cached;
 }
 
+// unions per thread of the lock-step async kernel (GC_COO_MLP; 0 selects
+// the one-union-per-thread k_union_coo).  Config 4 (54 x 10M inserts into
+// RMAT s26), measured: K = 0 / 2 / 4 / 8 -> 17.5 / 16.3 / 18.2 / 24.6 ms —
+// the batch is bound by random 32-byte-sector DRAM reads of the 268 MB
+// parent array (ncu: 1.5 GB read per 10M batch), not by per-thread latency,
+// so more unions per thread only cost occupancy
+int coo_mlp() {
+  static const int k = [] {
+    const char* e = getenv("GC_COO_MLP");
+    return e ? atoi(e) : 2;
+  }();
+  return k;
+}
+
 namespace {
 
 // Functor-style launchers so one dispatch switch serves both kernels.
@@ -389,31 +457,28 @@ struct RowsLaunch {
   }
 };
 
-// unions per thread of the lock-step async kernel (GC_COO_MLP; 0 selects
-// the one-union-per-thread k_union_coo).  Config 4 (54 x 10M inserts into
-// RMAT s26), measured: K = 0 / 2 / 4 / 8 -> 17.5 / 16.3 / 18.2 / 24.6 ms —
-// the batch is bound by random 32-byte-sector DRAM reads of the 268 MB
-// parent array (ncu: 1.5 GB read per 10M batch), not by per-thread latency,
-// so more unions per thread only cost occupancy
-int coo_mlp() {
-  static const int k = [] {
-    const char* e = getenv("GC_COO_MLP");
-    return e ? atoi(e) : 2;
-  }();
-  return k;
-}
-
 template <class R, int K>
 void launch_mlp(const UFState& s, const CooUnionArgs& a, cudaStream_t st) {
   int64_t blocks = (a.k + 256 * K - 1) / (256 * K);
-  const int64_t cap = int64_t(num_sms()) * 8 * 16;
+  // a compacted batch (giant filter, survivors counted on the device) is
+  // walked grid-stride by one resident wave; a full batch takes the wide
+  // grid (one wave over a full 10M batch measured 40% slower).  kdev_wave
+  // is the host's view of the device's mode (a batch or two stale at worst:
+  // either grid is correct for either mode)
+  static const int per_sm = [] {
+    int b = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_coo_async_mlp<R, K, false>, 256, 0));
+    return b > 0 ? b : 1;
+  }();
+  const int64_t cap = int64_t(num_sms()) * (a.kdev && a.kdev_wave ? per_sm : 8 * 16);
   if (blocks > cap) blocks = cap;
   if (s.weak)
     (k_union_coo_async_mlp<R, K, true><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel,
-                                                                     a.bad), ::gc::count_launch());
+                                                                     a.bad, a.kdev, a.alt), ::gc::count_launch());
   else
     (k_union_coo_async_mlp<R, K, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
-                                                                      a.init_sentinel, a.bad), ::gc::count_launch());
+                                                                      a.init_sentinel, a.bad, a.kdev, a.alt),
+     ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
@@ -425,6 +490,12 @@ struct CooLaunch {
     if (a.k <= 0) return;
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     s.weak = a.init_sentinel < 0;
+    // the giant filter: the lock-step async kernel (roots are component
+    // minima and known when a union ends)
+    if (a.gbits && R::kUnion == GC_FINISH_ASYNC) {
+      s.gbits = a.gbits;
+      s.ganchor = a.ganchor;
+    }
     if constexpr (R::kUnion == GC_FINISH_ASYNC && R::kFind != GC_FIND_COMPRESS) {
       switch (coo_mlp()) {
         case 2: return launch_mlp<R, 2>(s, a, st);

@@ -172,7 +172,8 @@ class IncrementalConnectivity:
             self._h = None
 
     def reserve(self, batch_len: int) -> None:
-        """Pre-size the round finishes' per-batch buffers (gc_incr_reserve)."""
+        """Pre-size the per-batch buffers (gc_incr_reserve): the round finishes' COO, the
+        giant filter's compacted batch."""
         N.check(N.lib().gc_incr_reserve(self._h, int(batch_len)))
 
     def insert(self, us, vs, sync: bool = True) -> None:
