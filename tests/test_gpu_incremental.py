@@ -106,3 +106,50 @@ def test_async_insert_stream(text):
     lab = labels.cpu().numpy().astype(np.int64)
     touched = np.diff(g.offsets) > 0
     assert np.array_equal(lab[touched], ref[touched])
+
+
+@pytest.mark.parametrize("text", ["none+async+halve", "none+async+split"])
+def test_giant_filter_stream(text):
+    """The giant filter (async rules): an RMAT stream inserted twice, so the
+    second pass runs in the filter's compact mode (every insert's endpoints
+    are marked), with queries answered from the marks and by root chases;
+    labels, query bits and merging-edge lists checked against the oracle."""
+    import torch
+    from paper_2008_11839_b200 import IncrementalConnectivity, build_csr, gen_rmat
+    g = build_csr(gen_rmat(14, 8, seed=5, device=True))
+    ref, comps = oracle.components(g.n, g.offsets, g.targets)
+    ue = g.undirected_edges()
+    rng = np.random.default_rng(6)
+    ue = ue[rng.permutation(len(ue))]
+    us = torch.from_numpy(ue[:, 0].astype(np.int32)).cuda()
+    vs = torch.from_numpy(ue[:, 1].astype(np.int32)).cuda()
+    inc = IncrementalConnectivity(parse_spec(text), g.n)
+    inc.reserve(8192)
+    touched = np.diff(g.offsets) > 0
+    for rep in range(2):
+        merged = 0
+        for b0 in range(0, us.numel(), 8192):
+            mu, mv = inc.insert_list(us[b0:b0 + 8192], vs[b0:b0 + 8192])
+            merged += int(mu.numel())
+            # merging edges join distinct reference components only once
+            assert np.array_equal(ref[mu.cpu().numpy()], ref[mv.cpu().numpy()])
+        # first pass: a spanning forest of the touched vertices; second: nothing merges
+        assert merged == (int(touched.sum()) - (comps - int((~touched).sum())) if rep == 0 else 0)
+    # queries: every edge (connected) and random pairs
+    qu = np.concatenate([ue[:5000, 0], rng.integers(0, g.n, 5000)]).astype(np.int32)
+    qv = np.concatenate([ue[:5000, 1], rng.integers(0, g.n, 5000)]).astype(np.int32)
+    bits = inc.query(torch.from_numpy(qu).cuda(), torch.from_numpy(qv).cuda()).numpy()
+    exp = (ref[qu] == ref[qv]) & touched[qu] & touched[qv]
+    exp |= qu == qv
+    assert np.array_equal(bits, exp)
+    labels, _ = inc.labels()
+    lab = labels.cpu().numpy().astype(np.int64)
+    assert np.array_equal(lab[touched], ref[touched])
+    # a mixed batch in compact mode: re-inserted edges (all filtered) + queries
+    mix_u = np.concatenate([ue[:3000, 0], qu[:3000]]).astype(np.int32)
+    mix_v = np.concatenate([ue[:3000, 1], qv[:3000]]).astype(np.int32)
+    isq = np.concatenate([np.zeros(3000, bool), np.ones(3000, bool)])
+    order = rng.permutation(6000)
+    bits = inc.batch(torch.from_numpy(mix_u[order]).cuda(), torch.from_numpy(mix_v[order]).cuda(),
+                     isq[order]).numpy()
+    assert np.array_equal(bits, isq[order] & np.concatenate([np.zeros(3000, bool), exp[:3000]])[order])
