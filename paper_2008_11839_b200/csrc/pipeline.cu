@@ -385,8 +385,53 @@ k_mode_fallback(const int32_t* P, int32_t* hist, int32_t n, const int64_t* off, 
   gather_active_body(P, n, off, list, ctr);
 }
 
-__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask) {
+// Finalize over the active list alone (union-find finishes after a
+// sampler, driver.py:483-490): the finish links only trees outside L_max,
+// so while L_max is still a root every vertex labelled L_max is final and
+// only the active vertices can have moved.  Components = the list's roots
+// + L_max.  When the finish linked L_max itself (under a smaller root),
+// this kernel does nothing and the whole-array kernel after it runs.
+__global__ void __launch_bounds__(kEwBlock)
+k_finalize_list(int32_t* P, int32_t n, const int32_t* __restrict__ list, unsigned long long* ctr,
+                unsigned stamp_mask) {
   entry_stamp(ctr + C_STAMP0, stamp_mask);
+  const int32_t lmax = int32_t(ctr[C_LMAX]);
+  if (ld_acq(P + lmax) != lmax) return;
+  const int64_t cnt = int64_t(ctr[C_N_ACTIVE]);
+  unsigned long long roots = (blockIdx.x == 0 && threadIdx.x == 0) ? 1ull : 0ull;  // L_max
+  bool noncanon = false, cyc = false;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+    const int32_t v = __ldg(list + i);
+    const int32_t lab = ld_weak(P + v);
+    if (lab == v) {
+      ++roots;
+      continue;
+    }
+    int32_t r = lab, y;
+    int64_t steps = 0;
+    while ((y = ld_weak(P + r)) != r) {
+      r = y;
+      if (++steps > n) { cyc = true; break; }
+    }
+    if (r != lab) P[v] = r;
+    noncanon |= r > v;
+  }
+  block_add<kEwBlock>(ctr + C_COMPONENTS, roots);
+  if (__syncthreads_or(noncanon) && threadIdx.x == 0) ctr[C_NONCANON] = 1;
+  if (cyc) ctr[C_CYCLE] = 1;
+}
+
+// list_mode: k_finalize_list ran first; skip when L_max stayed a root
+__device__ __forceinline__ bool list_done(const int32_t* P, const unsigned long long* ctr, int list_mode) {
+  if (!list_mode) return false;
+  const int32_t lmax = int32_t(ctr[C_LMAX]);
+  return ld_acq(P + lmax) == lmax;
+}
+
+__global__ void k_finalize(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask, int list_mode) {
+  entry_stamp(ctr + C_STAMP0, stamp_mask);
+  if (list_done(P, ctr, list_mode)) return;
   unsigned long long roots = 0;
   bool noncanon = false, cyc = false;
   const int64_t nq = (int64_t(n) + 3) / 4;
@@ -453,8 +498,9 @@ constexpr int kFinTile = 4096;
 constexpr int kFinStages = 2;
 
 __global__ void __launch_bounds__(kEwBlock)
-k_finalize_tma(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask) {
+k_finalize_tma(int32_t* P, int32_t n, unsigned long long* ctr, unsigned stamp_mask, int list_mode) {
   entry_stamp(ctr + C_STAMP0, stamp_mask);
+  if (list_done(P, ctr, list_mode)) return;
   __shared__ alignas(128) int32_t buf[kFinStages][kFinTile];
   __shared__ alignas(8) uint64_t bar[kFinStages];
   const int64_t n4 = (int64_t(n) / 4) * 4;  // bulk-copied part (16-byte multiple)
@@ -857,20 +903,26 @@ void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsign
 }
 
 void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st,
-                  bool maybe_noncanon) {
+                  bool maybe_noncanon, const int32_t* list) {
   if (n <= 0) return;
   const int g = grid_for(n, kEwBlock, 8);
+  unsigned sm = 0;
+  if (list) {
+    (k_finalize_list<<<num_sms() * 8, kEwBlock, 0, st>>>(P, n, list, ctr, take_stamps()), ::gc::count_launch());
+  } else {
+    sm = take_stamps();
+  }
+  const int lm = list != nullptr;
   // TMA-staged form by default (ncu, s24: 23.5 vs 25.1 us per launch);
   // GC_FIN_TMA=0 selects the register-staged kernel
   static const bool tma = !(getenv("GC_FIN_TMA") && atoi(getenv("GC_FIN_TMA")) == 0);
   if (tma && reinterpret_cast<uintptr_t>(P) % 16 == 0) {
     const int64_t tiles = ((int64_t(n) / 4) * 4 + kFinTile - 1) / kFinTile;
     const int64_t cap = int64_t(num_sms()) * 6;  // 6 blocks x 33 KB of stages per SM
-    (k_finalize_tma<<<int(tiles < cap ? (tiles > 0 ? tiles : 1) : cap), kEwBlock, 0, st>>>(P, n, ctr,
-                                                                                          take_stamps()),
+    (k_finalize_tma<<<int(tiles < cap ? (tiles > 0 ? tiles : 1) : cap), kEwBlock, 0, st>>>(P, n, ctr, sm, lm),
      ::gc::count_launch());
   } else
-  (k_finalize<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, ctr, take_stamps()),
+  (k_finalize<<<grid_for((int64_t(n) + 3) / 4, kEwBlock, 4), kEwBlock, 0, st>>>(P, n, ctr, sm, lm),
    ::gc::count_launch());
   if (!maybe_noncanon) {
     GC_CHECK_LAUNCH();

@@ -65,7 +65,7 @@ void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsign
                 cudaStream_t st);
 // Pointer jump (+ canonical relabel when labels may not be class minima).
 void run_finalize(int32_t* P, int32_t n, int32_t* mins, unsigned long long* ctr, cudaStream_t st,
-                  bool maybe_noncanon = true);
+                  bool maybe_noncanon = true, const int32_t* list = nullptr);
 void fill(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
 void set_ctr(unsigned long long* ctr, int idx, unsigned long long v, cudaStream_t st);
 void zero_ctr(unsigned long long* ctr, int words, cudaStream_t st);

@@ -329,6 +329,15 @@ struct RunState {
   ~RunState() { cudaFreeHost(host_ctr); }
 };
 
+// GC_FIN_LIST=0: always finalize the whole label array
+bool finalize_list_on() {
+  static const bool on = [] {
+    const char* e = getenv("GC_FIN_LIST");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void check_static_args(const gc_csr* g, const gc_spec* spec, int32_t* labels) {
   validate_csr(g);
   require(spec != nullptr, GC_ERR_ARG, "null spec");
@@ -386,7 +395,15 @@ void enqueue_static(const gc_csr* g, const gc_spec* spec, int32_t* labels, int32
   stamp_defer(3);
   // finalize takes the pending stamps at its entry
   if (forest || n == 0) stamp_flush(pl.ws.ctr, st);
-  if (!forest) run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB);
+  if (!forest) {
+    // after a sampler and a union-find finish only the active list can
+    // have moved (k_finalize_list; the whole-array pass stays as the
+    // fallback when the finish linked L_max itself)
+    const bool uf_finish = spec->finish >= GC_FINISH_ASYNC && spec->finish <= GC_FINISH_REM_CAS;
+    const bool list_ok = uf_finish && spec->sample != GC_SAMPLE_NONE && finalize_list_on();
+    run_finalize(labels, n, pl.ws.hist, pl.ws.ctr, st, spec->finish == GC_FINISH_JTB,
+                 list_ok ? pl.ws.list : nullptr);
+  }
   if (forest && n) {
     // spanning_forest: component_count = n - |forest| (driver.py:535); the
     // pair form is split into fu / fv and counted in the same pass

@@ -8,6 +8,7 @@ import torch  # noqa: E402
 from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec, IncrementalConnectivity  # noqa: E402
 
 spec = sys.argv[1] if len(sys.argv) > 1 else "none+async+halve"
+as_list = "--list" in sys.argv  # insert_list (records merging edges, as the sharded driver)
 g = build_csr(gen_rmat(26, 8, seed=1, device=True), keep_host=False)
 off, tgt = g._d_off, g._d_tgt
 src = torch.repeat_interleave(torch.arange(g.n, device="cuda", dtype=torch.int32), off[1:] - off[:-1])
@@ -25,10 +26,13 @@ for rep in range(2):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        inc.insert(us[b0:b0 + 10_000_000], vs[b0:b0 + 10_000_000], sync=False)
+        if as_list:
+            inc.insert_list(us[b0:b0 + 10_000_000], vs[b0:b0 + 10_000_000])
+        else:
+            inc.insert(us[b0:b0 + 10_000_000], vs[b0:b0 + 10_000_000], sync=False)
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     if rep:
-        print(json.dumps({"spec": spec, "total_ms": sum(ts), "batch_ms": [round(t, 4) for t in ts]}))
+        print(json.dumps({"spec": spec, "list": as_list, "total_ms": sum(ts), "batch_ms": [round(t, 4) for t in ts]}))
     del inc
