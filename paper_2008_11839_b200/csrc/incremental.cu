@@ -33,6 +33,8 @@ struct gc_incr {
   int32_t* gstate = nullptr;
   int32_t* hmode = nullptr;      // mapped pinned copy of gstate[4] (grid choice only)
   int32_t* hmode_dev = nullptr;
+  uint8_t* mflag = nullptr;    // insert_list: per-insert "merged two trees" flags
+  int64_t mcap = 0;
   int32_t* cu = nullptr;       // the compacted inserts of the current batch
   int32_t* cv = nullptr;
   int64_t ccap = 0;
@@ -360,6 +362,58 @@ k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, 
   flush();
 }
 
+// insert_list with the lock-step async kernel: the kernel flags merging
+// inserts by index; this pass gathers their (u, v) from the array the
+// kernel walked (the giant compaction's survivors, or the caller's batch
+// when it was passed through / the filter is off), one counter atomic per
+// block flush
+__global__ void __launch_bounds__(kIB)
+k_merge_compact(const int32_t* __restrict__ cu, const int32_t* __restrict__ cv, const int32_t* __restrict__ us,
+                const int32_t* __restrict__ vs, int64_t len, const unsigned long long* kdev,
+                const uint8_t* __restrict__ flags, int32_t* ou, int32_t* ov, unsigned long long* ocount) {
+  __shared__ int2 q[kGcQ];
+  __shared__ int qn;
+  __shared__ unsigned long long qbase;
+  const unsigned long long c = kdev ? *kdev : ~0ull;
+  const bool compacted = c != ~0ull;
+  const int64_t k = compacted ? int64_t(c) : len;
+  const int32_t* a = compacted ? cu : us;
+  const int32_t* b = compacted ? cv : vs;
+  if (threadIdx.x == 0) qn = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t per = ((k + gridDim.x - 1) / gridDim.x + kIB - 1) / kIB * kIB;
+  const int64_t lo = int64_t(blockIdx.x) * per;
+  const int64_t hi = lo + per < k ? lo + per : k;
+  auto flush = [&]() {
+    __syncthreads();
+    const int n = qn;
+    if (threadIdx.x == 0) qbase = n ? atomicAdd(ocount, static_cast<unsigned long long>(n)) : 0ull;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kIB) {
+      ou[qbase + i] = q[i].x;
+      ov[qbase + i] = q[i].y;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+  };
+  __syncthreads();
+  for (int64_t i0 = lo; i0 < hi; i0 += kIB) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool m = i < hi && flags[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (bal) {
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(&qn, __popc(bal));
+      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(bal & ((1u << lane) - 1u));
+      if (m) q[pos] = make_int2(a[i] & 0x7fffffff, b[i] & 0x7fffffff);
+    }
+    __syncthreads();
+    if (qn > kGcQ - kIB) flush();
+  }
+  flush();
+}
+
 __global__ void k_giant_clear(uint32_t* bits, int64_t words, const int32_t* gstate) {
   if (!gstate[1]) return;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -628,6 +682,7 @@ void gc_incr_destroy(gc_incr* h) {
   cudaFree(h->cu);
   cudaFree(h->cv);
   if (h->hmode) cudaFreeHost(h->hmode);
+  cudaFree(h->mflag);
   cudaFree(h->rw.a);
   cudaFree(h->rw.b);
   for (Coo* c : {&h->rw.work, &h->rw.spare}) {
@@ -761,8 +816,31 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
     a.lu = out_u;
     a.lv = out_v;
     a.lcount = out_count;
+    // the lock-step async kernel flags merging inserts by index (a shared
+    // append counter serialised the early batches, where ~every insert
+    // merges: RMAT s26 batch 1, 1.73 ms vs 0.60 for a plain insert)
+    const bool flagged = h->spec.finish == GC_FINISH_ASYNC && h->spec.find != GC_FIND_COMPRESS && coo_mlp() > 0;
+    if (flagged) {
+      if (len > h->mcap) {
+        cudaFree(h->mflag);
+        h->mflag = nullptr;
+        h->mcap = 0;
+        GC_CUDA(cudaMalloc(&h->mflag, len));
+        h->mcap = len;
+      }
+      GC_CUDA(cudaMemsetAsync(h->mflag, 0, len, st));
+      a.lu = a.lv = nullptr;
+      a.lcount = nullptr;
+      a.lflag = h->mflag;
+    }
     giant_compact(h, a, nullptr);
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
+    if (flagged) {
+      GC_CUDA(cudaMemsetAsync(out_count, 0, 8, st));
+      (k_merge_compact<<<num_sms() * 4, kIB, 0, st>>>(h->cu, h->cv, us, vs, len, a.kdev, h->mflag, out_u, out_v,
+                                                      out_count), ::gc::count_launch());
+      GC_CHECK_LAUNCH();
+    }
     giant_after(h, us, vs, nullptr, len);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
     fetch_bad(h);

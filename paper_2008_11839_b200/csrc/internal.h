@@ -172,6 +172,7 @@ struct CooUnionArgs {
                                              // survivor count, ~0 = use `alt`
   GiantPass alt;
   bool kdev_wave = false;  // the batch is expected to be compacted: one-wave grid
+  uint8_t* lflag = nullptr;  // lock-step async kernel: lflag[i] = 1 when pair i merged two trees
 };
 void launch_union_coo(const UFConfig& cfg, bool forest, const CooUnionArgs& a, cudaStream_t st);
 

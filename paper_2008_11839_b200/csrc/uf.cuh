@@ -44,6 +44,9 @@ struct UFState {
   // bit never goes stale.
   uint32_t* gbits = nullptr;
   const int32_t* ganchor = nullptr;
+  // lock-step async COO kernel: mark merging inserts by index (lflag[i] = 1)
+  // instead of appending (u, v) to lu / lv through one shared counter
+  uint8_t* lflag = nullptr;
 };
 
 

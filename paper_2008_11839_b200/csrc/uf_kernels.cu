@@ -321,7 +321,8 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
         const int32_t ru = x[j][0], rv = x[j][1];
         const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
         if (old[j] == hi) {
-          record<R::kForest>(s, hi, eu[j], ev[j]);
+          if (s.lflag) s.lflag[base + int64_t(j) * blockDim.x + threadIdx.x] = 1;
+          else record<R::kForest>(s, hi, eu[j], ev[j]);
           slot &= ~(1u << j);
           if (anc >= 0) mark(j, lo);
         } else {
@@ -496,6 +497,7 @@ struct CooLaunch {
       s.gbits = a.gbits;
       s.ganchor = a.ganchor;
     }
+    s.lflag = a.lflag;
     if constexpr (R::kUnion == GC_FINISH_ASYNC && R::kFind != GC_FIND_COMPRESS) {
       switch (coo_mlp()) {
         case 2: return launch_mlp<R, 2>(s, a, st);

