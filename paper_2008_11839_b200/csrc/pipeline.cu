@@ -677,6 +677,52 @@ __global__ void __launch_bounds__(kEwBlock) k_root_bitmap(const int32_t* __restr
   }
 }
 
+// The same snapshot / transitions over the active list alone (a sampled
+// sharded finish, driver.py:473): the finish can hook only roots of active
+// trees or L_max itself — every other vertex carries label L_max and is no
+// root — so one flag per list entry (slot `count` for L_max) stands in for
+// the n-bit bitmap and both passes are O(active) instead of O(n).
+__global__ void __launch_bounds__(kEwBlock)
+k_root_flags_list(const int32_t* __restrict__ P, const int32_t* __restrict__ list, const unsigned long long* ctr,
+                  uint8_t* flags) {
+  const int64_t count = int64_t(ctr[C_N_ACTIVE]);
+  const int32_t lmax = int32_t(ctr[C_LMAX]);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= count; i += stride) {
+    const int32_t v = i < count ? __ldg(list + i) : lmax;
+    flags[i] = P[v] == v;
+  }
+}
+
+__global__ void __launch_bounds__(kEwBlock)
+k_root_transitions_list(const int32_t* __restrict__ P, const int32_t* __restrict__ list,
+                        const unsigned long long* ctr, const uint8_t* __restrict__ flags, int32_t* out_u,
+                        int32_t* out_v, unsigned long long* out_count) {
+  const int64_t count = int64_t(ctr[C_N_ACTIVE]);
+  const int32_t lmax = int32_t(ctr[C_LMAX]);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x; b <= count; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    int32_t v = 0, p = 0;
+    bool moved = false;
+    if (i <= count && flags[i]) {
+      v = i < count ? __ldg(list + i) : lmax;
+      p = P[v];
+      moved = p != v;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, moved);
+    if (!bal) continue;
+    unsigned long long pos = 0;
+    if (lane == __ffs(int(bal)) - 1) pos = atomicAdd(out_count, static_cast<unsigned long long>(__popc(bal)));
+    pos = __shfl_sync(0xffffffffu, pos, __ffs(int(bal)) - 1) + __popc(bal & ((1u << lane) - 1u));
+    if (moved) {
+      out_u[pos] = v;
+      out_v[pos] = p;
+    }
+  }
+}
+
 // Root transitions of one phase: every v that was a root before it
 // (before == nullptr: every vertex was) and is not one now emits (v, P[v]) —
 // one pair per merge, all inside one component, so unioning them elsewhere

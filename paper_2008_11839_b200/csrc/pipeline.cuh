@@ -49,6 +49,11 @@ __global__ void k_ic_census(const int32_t* P, int32_t n, const int64_t* off, con
 
 __global__ void k_fill(int32_t* a, int64_t n, int32_t v);
 __global__ void k_root_bitmap(const int32_t* P, int32_t n, uint32_t* bits);
+__global__ void k_root_flags_list(const int32_t* P, const int32_t* list, const unsigned long long* ctr,
+                                  uint8_t* flags);
+__global__ void k_root_transitions_list(const int32_t* P, const int32_t* list, const unsigned long long* ctr,
+                                        const uint8_t* flags, int32_t* out_u, int32_t* out_v,
+                                        unsigned long long* out_count);
 __global__ void k_root_transitions(const int32_t* P, const uint32_t* before, int32_t n, int32_t* out_u,
                                    int32_t* out_v, unsigned long long* count);
 __global__ void k_count_ne(const int32_t* a, int64_t n, int32_t v, unsigned long long* out);

@@ -755,10 +755,25 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo, int64_
     // after the finish
     uint32_t* roots = reinterpret_cast<uint32_t*>(pl.ws.hist);
     const int gq = grid_for((int64_t(pl.n) + 3) / 4, kEwBlock, 8);
-    if (!edges && pl.n) (k_root_bitmap<<<gq, kEwBlock, 0, st>>>(parent, pl.n, roots), count_launch());
+    // after a sampler only active roots and L_max can be hooked: snapshot
+    // and compare over the active list (one flag per entry in the same
+    // buffer) instead of the whole parent array
+    const bool by_list = spec->sample != GC_SAMPLE_NONE;
+    uint8_t* flags = reinterpret_cast<uint8_t*>(pl.ws.hist);
+    if (!edges && pl.n) {
+      if (by_list)
+        (k_root_flags_list<<<grid_for(pl.n, kEwBlock, 2), kEwBlock, 0, st>>>(parent, pl.ws.list, pl.ws.ctr, flags),
+         count_launch());
+      else
+        (k_root_bitmap<<<gq, kEwBlock, 0, st>>>(parent, pl.n, roots), count_launch());
+    }
     pl.finish();
     if (!edges && pl.n) {
-      (k_root_transitions<<<gq, kEwBlock, 0, st>>>(parent, roots, pl.n, out_u, out_v, out_count), count_launch());
+      if (by_list)
+        (k_root_transitions_list<<<grid_for(pl.n, kEwBlock, 2), kEwBlock, 0, st>>>(
+             parent, pl.ws.list, pl.ws.ctr, flags, out_u, out_v, out_count), count_launch());
+      else
+        (k_root_transitions<<<gq, kEwBlock, 0, st>>>(parent, roots, pl.n, out_u, out_v, out_count), count_launch());
       GC_CHECK_LAUNCH();
     }
     unsigned long long c[C_COUNT_];

@@ -324,11 +324,13 @@ class GpuEngine:
         ids = torch.as_tensor(ids, dtype=torch.int64, device=off.device)
         return (off[ids + 1] - off[ids]).to(torch.int64)
 
-    def finalize(self, parent):
+    def finalize(self, parent, inplace=False):
+        """Canonical labels (gc_label_finalization); inplace=True reuses the
+        parent buffer (the sharded drivers no longer need it afterwards)."""
         import ctypes as C
         from . import _native as N
         from .api import _stream, _workspace
-        lab = parent.clone()
+        lab = parent if inplace else parent.clone()
         n = lab.numel()
         if n:
             ws = _workspace(4 * n + 8192)
@@ -700,7 +702,7 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     mu, mv, info = engine.shard_finish(g_shard, spec, parent)
     f2u, f2v, x2 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
     torch = _torch()
-    labels = engine.finalize(parent)
+    labels = engine.finalize(parent, inplace=True)
     n = g_shard.n
     dev = _comm_device(group)
     tot = torch.tensor([0 if spec.sample is SampleKind.BFS else insp_s, info["insp_finish"]], dtype=torch.int64,

@@ -91,7 +91,7 @@ def run(P, scale, g, shards, check):
         for q in range(P):
             if q != r and fin[q][0].numel():
                 T("merge2", lambda: eng.union_pairs(parent, fin[q][0], fin[q][1], spec))
-        lab = T("finalize", lambda: eng.finalize(parent))
+        lab = T("finalize", lambda: eng.finalize(parent, inplace=True))
         if r == 0:
             labels = lab
     ok = None

@@ -196,7 +196,7 @@ class CpuEngine:
     def union_pairs(self, parent, us, vs, spec):
         self.union_list(parent, us, vs, spec)
 
-    def finalize(self, parent):
+    def finalize(self, parent, inplace=False):
         p = parent.numpy().astype(np.int64)
         return torch.from_numpy(np.array([_find(p, v) for v in range(len(p))], dtype=np.int32))
 
