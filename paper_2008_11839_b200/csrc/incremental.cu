@@ -162,10 +162,7 @@ int g1(int64_t work) { return grid_for(work, kIB, 8); }
 // Roots of the min-linking rules are component minima, so once the giant
 // has formed its root — the anchor — stays put.
 __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t cap, int32_t sentinel,
-                                                      int32_t* gstate, const uint32_t* gbits, const int32_t* us,
-                                                      const int32_t* vs, const uint8_t* isq, int64_t len,
-                                                      volatile int32_t* hmode) {
-  __shared__ unsigned both, seen;
+                                                      int32_t* gstate, volatile int32_t* hmode) {
   constexpr int kS = 1024, kSlots = 2 * kS;
   __shared__ int32_t key_[kSlots];
   __shared__ unsigned cnt_[kSlots];
@@ -175,10 +172,7 @@ __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t 
     key_[k] = -1;
     cnt_[k] = 0;
   }
-  if (i == 0) {
-    best = 0ull;
-    both = seen = 0u;
-  }
+  if (i == 0) best = 0ull;
   const int s = cap < kS ? int(cap) : kS;
   int32_t x = -1;
   if (i < s) {
@@ -209,19 +203,6 @@ __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t 
   __syncthreads();
   if (x >= 0)
     atomicMax(&best, (static_cast<unsigned long long>(cnt_[slot]) << 32) | (0xffffffffull - uint32_t(x)));
-  // the filter rate the next batch can expect: the share of this batch's
-  // inserts (1024 evenly spaced samples) whose endpoints are both marked now
-  const int ns = len < kS ? int(len) : kS;
-  if (i < ns) {
-    const int64_t j = (int64_t(i) * len) / ns;
-    if (!(isq && isq[j])) {
-      const int32_t a = us[j], b = vs[j];
-      if (uint32_t(a) < uint32_t(cap) && uint32_t(b) < uint32_t(cap)) {
-        atomicAdd(&seen, 1u);
-        if (gbit(ld_bits(gbits + (a >> 5)), a) && gbit(ld_bits(gbits + (b >> 5)), b)) atomicAdd(&both, 1u);
-      }
-    }
-  }
   __syncthreads();
   if (i != 0) return;
   int32_t cur = gstate[0];
@@ -248,8 +229,35 @@ __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t 
   // compacting costs one pass over the batch plus two bit tests per insert;
   // it pays once about half of the inserts can be dropped (config 4: from
   // the ~12th of 54 batches on)
-  gstate[4] = !move && seen > 0 && 2 * both >= seen;
+  if (move) gstate[4] = 0;  // the bits were cleared: pass the next batch through
   if (hmode) *hmode = gstate[4];
+}
+
+// Whether this batch is worth compacting: one block tests the giant bits of
+// 1024 evenly spaced inserts of the batch itself.  Compacting costs a pass
+// over the batch plus two bit tests per insert (~0.1 ms per 10M) and pays
+// once about two thirds of the inserts can be dropped (RMAT s26, 10M
+// batches: from about the 12th batch on).
+__global__ void __launch_bounds__(1024)
+k_giant_decide(const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len, int32_t cap,
+               const uint32_t* gbits, int32_t* gstate) {
+  __shared__ unsigned both, seen;
+  if (threadIdx.x == 0) both = seen = 0u;
+  __syncthreads();
+  const int32_t anc = gstate[0];
+  const int ns = len < 1024 ? int(len) : 1024;
+  if (anc >= 0 && int(threadIdx.x) < ns) {
+    const int64_t j = (int64_t(threadIdx.x) * len) / ns;
+    if (!(isq && isq[j])) {
+      const int32_t a = us[j], b = vs[j];
+      if (uint32_t(a) < uint32_t(cap) && uint32_t(b) < uint32_t(cap)) {
+        atomicAdd(&seen, 1u);
+        if (gbit(ld_bits(gbits + (a >> 5)), a) && gbit(ld_bits(gbits + (b >> 5)), b)) atomicAdd(&both, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) gstate[4] = anc >= 0 && seen > 0 && 3 * both >= 2 * seen;
 }
 
 // Giant filter, first step of a union-find insert sub-phase: inserts whose
@@ -431,10 +439,20 @@ bool giant_filter_on() {
 
 // compacts the batch into h->cu / h->cv and points the union at it (count
 // on the device); the caller runs giant_after once the union is enqueued
+// per-insert merge flags of insert_list (lock-step async kernel)
+void flags_reserve(gc_incr* h, int64_t len) {
+  if (len <= h->mcap) return;
+  if (h->mflag) cudaFree(h->mflag);
+  h->mflag = nullptr;
+  h->mcap = 0;
+  GC_CUDA(cudaMalloc(&h->mflag, len));
+  h->mcap = len;
+}
+
 void giant_reserve(gc_incr* h, int64_t len) {
   if (!h->gbits || len <= h->ccap) return;
-  cudaFree(h->cu);
-  cudaFree(h->cv);
+  if (h->cu) cudaFree(h->cu);
+  if (h->cv) cudaFree(h->cv);
   h->cu = h->cv = nullptr;
   h->ccap = 0;
   GC_CUDA(cudaMalloc(&h->cu, len * 4));
@@ -444,15 +462,7 @@ void giant_reserve(gc_incr* h, int64_t len) {
 
 void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
   if (!h->gbits || a.k <= 0) return;
-  if (a.k > h->ccap) {
-    cudaFree(h->cu);
-    cudaFree(h->cv);
-    h->cu = h->cv = nullptr;
-    h->ccap = 0;
-    GC_CUDA(cudaMalloc(&h->cu, a.k * 4));
-    GC_CUDA(cudaMalloc(&h->cv, a.k * 4));
-    h->ccap = a.k;
-  }
+  giant_reserve(h, a.k);
   static const int per_sm = [] {
     int b = 0;
     GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_giant_compact, kIB, 0));
@@ -460,6 +470,8 @@ void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
   }();
   int64_t blocks = (a.k + 4 * kIB - 1) / (4 * kIB);
   if (blocks > int64_t(num_sms()) * per_sm) blocks = int64_t(num_sms()) * per_sm;
+  (k_giant_decide<<<1, 1024, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap), h->gbits, h->gstate),
+   ::gc::count_launch());
   (k_giant_compact<<<int(blocks), kIB, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap),
                                                                       h->gbits, h->gstate, h->cu, h->cv, h->bad),
    ::gc::count_launch());
@@ -477,8 +489,7 @@ void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
 
 void giant_after(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len) {
   if (!h->gbits) return;
-  (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->gbits, us, vs, isq, len,
-                                                h->hmode_dev),
+  (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->hmode_dev),
    ::gc::count_launch());
   const int64_t words = (h->cap + 31) / 32;
   (k_giant_clear<<<grid_for(words, kIB, 2), kIB, 0, h->st>>>(h->gbits, words, h->gstate), ::gc::count_launch());
@@ -716,7 +727,11 @@ int gc_incr_reserve(gc_incr* h, int64_t batch_len) {
   return guarded([&] {
     require(h != nullptr && batch_len >= 0, GC_ERR_ARG, "bad reserve");
     if (!h->uf && batch_len > 0) ensure_coo(h, batch_len);
-    if (h->uf && batch_len > 0) giant_reserve(h, batch_len);
+    if (h->uf && batch_len > 0) {
+      giant_reserve(h, batch_len);
+      if (h->spec.finish == GC_FINISH_ASYNC && h->spec.find != GC_FIND_COMPRESS && coo_mlp() > 0)
+        flags_reserve(h, batch_len);
+    }
   });
 }
 
@@ -821,13 +836,7 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
     // merges: RMAT s26 batch 1, 1.73 ms vs 0.60 for a plain insert)
     const bool flagged = h->spec.finish == GC_FINISH_ASYNC && h->spec.find != GC_FIND_COMPRESS && coo_mlp() > 0;
     if (flagged) {
-      if (len > h->mcap) {
-        cudaFree(h->mflag);
-        h->mflag = nullptr;
-        h->mcap = 0;
-        GC_CUDA(cudaMalloc(&h->mflag, len));
-        h->mcap = len;
-      }
+      flags_reserve(h, len);
       GC_CUDA(cudaMemsetAsync(h->mflag, 0, len, st));
       a.lu = a.lv = nullptr;
       a.lcount = nullptr;

@@ -157,7 +157,7 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
 // CAS(P[hi], hi, lo) on the two roots; a failed link resumes the hi chain
 // from the value the CAS saw (hi's new parent) and the lo chain from lo.
 template <class R, int K, bool WEAK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
 k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
                       const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad,
                       const unsigned long long* kdev, GiantPass alt) {
