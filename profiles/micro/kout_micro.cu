@@ -205,6 +205,127 @@ __global__ void __launch_bounds__(kAW * 32) k_rows_async(int32_t* P, const int64
   cp_wait<0>();
 }
 
+// ---- per-warp bulk-copy (TMA engine) staging -------------------------------
+// Each warp stages its own tiles: lane 0 bulk-copies the offsets of tile
+// k + 2 and, once tile k + 1's offsets have landed, the contiguous window of
+// targets its 32 rows start in (capped at kWin bytes; rows past the window
+// read their heads from global).  The copies run on the TMA engine, off the
+// LSU / L1 path the union chains use; lanes copy their heads into registers
+// and release the stage before their unions.
+constexpr int kBW = 16;
+constexpr int kWin = 1024;  // bytes per window stage
+
+struct BulkSmem {
+  alignas(16) int64_t off[kBW][2][34];
+  alignas(16) int32_t win[kBW][2][kWin / 4];
+  alignas(8) uint64_t boff[kBW][2];
+  alignas(8) uint64_t bwin[kBW][2];
+};
+
+__device__ __forceinline__ void win_bounds(const int64_t* o, int64_t r0, int32_t n, int64_t m, int64_t& ws,
+                                           int64_t& we) {
+  const int64_t last = r0 + 32 <= n ? r0 + 32 : n;
+  const int64_t lo = o[0], hi = o[last - r0];
+  ws = lo & ~int64_t(3);
+  int64_t e = (hi + 3) & ~int64_t(3);
+  if (e > ws + kWin / 4) e = ws + kWin / 4;
+  const int64_t mfloor = m & ~int64_t(3);
+  if (e > mfloor) e = mfloor > ws ? mfloor : ws;
+  we = e;
+}
+
+__global__ void __launch_bounds__(kBW * 32) k_rows_bulk(int32_t* P, const int64_t* __restrict__ off,
+                                                      const int32_t* __restrict__ tgt, int32_t n, int64_t m) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BulkSmem& sm = *reinterpret_cast<BulkSmem*>(smem_raw);
+  UFState s{P, nullptr, nullptr, nullptr, nullptr, nullptr, n};
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t(blockIdx.x) * kBW * 32 + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * kBW * 32) >> 5;
+  auto tile_r0 = [&](int64_t k) { return (gw + k * nw) * 32; };
+  // offsets of tile k into stage st: entries r0 .. min(r0 + 33, n + 1) (16-byte multiple)
+  auto issue_off = [&](int64_t k, int st) {
+    const int64_t r0 = tile_r0(k);
+    if (r0 >= n) return;
+    int64_t cnt = (n + 1) - r0;
+    if (cnt > 34) cnt = 34;
+    cnt &= ~int64_t(1);  // 16-byte multiple; the odd last entry is read from global
+    mbar_expect_tx(&sm.boff[w][st], uint32_t(cnt * 8));
+    bulk_g2s(sm.off[w][st], off + r0, uint32_t(cnt * 8), &sm.boff[w][st]);
+  };
+  auto off_at = [&](int st, int64_t r0, int i) -> int64_t {
+    // entry r0 + i of the offsets: from the stage unless it is the odd tail
+    const int64_t avail = ((n + 1) - r0) < 34 ? (((n + 1) - r0) & ~int64_t(1)) : 34;
+    return i < avail ? sm.off[w][st][i] : __ldg(off + r0 + i);
+  };
+  auto issue_win = [&](int64_t k, int st) {
+    const int64_t r0 = tile_r0(k);
+    if (r0 >= n) return;
+    int64_t o[33];
+    (void)o;
+    const int64_t last = r0 + 32 <= n ? r0 + 32 : n;
+    const int64_t lo = off_at(st, r0, 0), hi = off_at(st, r0, int(last - r0));
+    int64_t ws = lo & ~int64_t(3);
+    int64_t e = (hi + 3) & ~int64_t(3);
+    if (e > ws + kWin / 4) e = ws + kWin / 4;
+    const int64_t mfloor = m & ~int64_t(3);
+    if (e > mfloor) e = mfloor > ws ? mfloor : ws;
+    const uint32_t bytes = uint32_t((e - ws) * 4);
+    mbar_expect_tx(&sm.bwin[w][st], bytes);
+    if (bytes) bulk_g2s(sm.win[w][st], tgt + ws, bytes, &sm.bwin[w][st]);
+  };
+  if (lane == 0) {
+    for (int st = 0; st < 2; ++st) {
+      mbar_init(&sm.boff[w][st], 1);
+      mbar_init(&sm.bwin[w][st], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    issue_off(0, 0);
+    issue_off(1, 1);
+    if (tile_r0(0) < n) {
+      mbar_wait(&sm.boff[w][0], 0);
+      issue_win(0, 0);
+    }
+  }
+  __syncwarp();
+  for (int64_t k = 0; tile_r0(k) < n; ++k) {
+    const int st = int(k & 1);
+    const uint32_t ph = uint32_t((k >> 1) & 1);
+    const int64_t r0 = tile_r0(k);
+    // the next tile's window, as soon as its offsets are in
+    if (lane == 0 && tile_r0(k + 1) < n) {
+      mbar_wait(&sm.boff[w][st ^ 1], uint32_t(((k + 1) >> 1) & 1));
+      issue_win(k + 1, st ^ 1);
+    }
+    mbar_wait(&sm.boff[w][st], ph);
+    mbar_wait(&sm.bwin[w][st], ph);
+    const int64_t u = r0 + lane;
+    int32_t take = 0, f0 = 0, f1 = 0;
+    if (u < n) {
+      const int64_t b = off_at(st, r0, lane), e = off_at(st, r0, lane + 1);
+      const int64_t d = e - b;
+      take = int32_t(d < 2 ? d : 2);
+      const int64_t last = r0 + 32 <= n ? r0 + 32 : n;
+      const int64_t lo = off_at(st, r0, 0), hi = off_at(st, r0, int(last - r0));
+      int64_t ws = lo & ~int64_t(3);
+      int64_t we = (hi + 3) & ~int64_t(3);
+      if (we > ws + kWin / 4) we = ws + kWin / 4;
+      const int64_t mfloor = m & ~int64_t(3);
+      if (we > mfloor) we = mfloor > ws ? mfloor : ws;
+      if (take > 0) f0 = b < we ? sm.win[w][st][b - ws] : ldg32(tgt + b);
+      if (take > 1) f1 = b + 1 < we ? sm.win[w][st][b + 1 - ws] : ldg32(tgt + b + 1);
+    }
+    __syncwarp();  // stage st fully read
+    if (lane == 0) issue_off(k + 2, st);
+    if (take > 0) R::unite(s, int32_t(u), f0);
+    if (take > 1) R::unite(s, int32_t(u), f1);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -242,4 +363,12 @@ int km_rows_async(int32_t* P, const int64_t* off, const int32_t* tgt, int32_t n,
   return int(cudaGetLastError());
 }
 int km_async_smem() { return int(sizeof(AsyncSmem)); }
+int km_rows_bulk(int32_t* P, const int64_t* off, const int32_t* tgt, int32_t n, int64_t m, int blocks_per_sm,
+                 cudaStream_t st) {
+  const int bytes = int(sizeof(BulkSmem));
+  cudaFuncSetAttribute(k_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  k_rows_bulk<<<148 * blocks_per_sm, kBW * 32, bytes, st>>>(P, off, tgt, n, m);
+  return int(cudaGetLastError());
+}
+int km_bulk_smem() { return int(sizeof(BulkSmem)); }
 }

@@ -64,9 +64,11 @@ def main():
         "rows_async_b4": (True, lambda: lib.km_rows_async(Pp, O, T, n, ctypes.c_int64(m), 4, 0, st)),
         "rows_async_b4_ef": (True, lambda: lib.km_rows_async(Pp, O, T, n, ctypes.c_int64(m), 4, 1, st)),
         "rows_async_b3_ef": (True, lambda: lib.km_rows_async(Pp, O, T, n, ctypes.c_int64(m), 3, 1, st)),
+        "rows_bulk_b4": (True, lambda: lib.km_rows_bulk(Pp, O, T, n, ctypes.c_int64(m), 4, st)),
+        "rows_bulk_b3": (True, lambda: lib.km_rows_bulk(Pp, O, T, n, ctypes.c_int64(m), 3, st)),
     }
     ref = None
-    out = {"n": n, "m": m, "async_smem_per_block": lib.km_async_smem()}
+    out = {"n": n, "m": m, "async_smem_per_block": lib.km_async_smem(), "bulk_smem_per_block": lib.km_bulk_smem()}
     for name, (uses_p, fn) in variants.items():
         ts = []
         for r in range(a.reps + 1):
