@@ -38,6 +38,17 @@ for text, racy in [("none+async+halve", False), ("none+rem_cas+halve+split", Tru
     isq[::7] = 1
     inc.batch(us, vs, isq)
     inc.labels()
+# the incremental giant filter: a second pass over the same edges runs in
+# compact mode; insert_list flags merges by index
+inc = IncrementalConnectivity(parse_spec("none+async+halve"), g.n)
+inc.reserve(2048)
+for rep in range(2):
+    for b0 in range(0, us.numel(), 2048):
+        inc.insert_list(us[b0:b0 + 2048], vs[b0:b0 + 2048])
+for b0 in range(0, us.numel(), 2048):
+    inc.insert(us[b0:b0 + 2048], vs[b0:b0 + 2048], sync=False)
+inc.query(us[:1000], vs[:1000])
+inc.labels()
 ds = DisjointSets(g.n, UnionConfig(UnionOp.REM_CAS, FindOp.HALVE, SpliceOp.SPLIT_ONE))
 ds.union_batch(us, vs)
 ds.labels_array()
