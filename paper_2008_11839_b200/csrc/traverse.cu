@@ -586,7 +586,7 @@ k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint
     r = r < 0.f ? 0.f : (r > float(kLddMaxRounds) ? float(kLddMaxRounds) : r);
     start[v] = uint16_t(r);
     cluster[v] = kFreeCluster;
-    croud[v] = 0;
+    if (croud) croud[v] = 0;
     atomicAdd(hist + int(r), 1u);
   }
   __syncthreads();
@@ -769,6 +769,20 @@ __device__ __forceinline__ bool claim_rel(uint32_t* cluster, uint16_t* croud, in
   return true;
 }
 
+// Packed claim state (n <= 2^24 and every round < 255): one u32 per vertex,
+// key = round << 24 | cluster.  atomicMin on the key keeps the earliest
+// round and, within it, the smallest cluster — the MPX rule itself — so the
+// separate claim-round array (and its write) goes away: 4 bytes of claim
+// state per vertex instead of 6 (67 MB at 2^24, which the L2 can hold).  The
+// filter read rejects keys of earlier rounds before the atomic.
+constexpr uint32_t kPackMask = 0xffffffu;
+__device__ __forceinline__ bool claim_packed(uint32_t* key, int32_t x, int32_t round, uint32_t c) {
+  const uint32_t k = ld_rlx_u32(key + x);
+  if ((k >> 24) < uint32_t(round)) return false;  // reached in an earlier round (free = round 255)
+  return atomicMin(key + x, (uint32_t(round) << 24) | c) == kFreeCluster;
+}
+
+template <bool PACKED>
 __global__ void __launch_bounds__(kTB, 6)
 k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t n, uint32_t* cluster,
               uint16_t* croud, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
@@ -806,6 +820,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
       if (lane < vpw && i < count) {
         const int32_t f = ld_acq(qin + i);
         c = ld_rlx_u32(cluster + f);  // final since round r-1
+        if constexpr (PACKED) c &= kPackMask;
         // graph data is read once: L2 evict-first keeps the claim state resident
         b = ld_stream64(off + f, pol);
         d = int32_t(ld_stream64(off + f + 1, pol) - b);
@@ -844,7 +859,10 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         }
         bool fresh[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) fresh[h] = ok[h] && claim_rel(cluster, croud, x[h], r, sc[h]);
+        for (int h = 0; h < 2; ++h) {
+          if constexpr (PACKED) fresh[h] = ok[h] && claim_packed(cluster, x[h], r, sc[h]);
+          else fresh[h] = ok[h] && claim_rel(cluster, croud, x[h], r, sc[h]);
+        }
         bq.push(fresh[0], x[0], qout, cout);
         bq.push(fresh[1], x[1], qout, cout);
       }
@@ -857,7 +875,8 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         bool fresh = false;
         if (i < hi) {
           v = order[i];
-          fresh = claim_rel(cluster, croud, v, r, uint32_t(v));
+          if constexpr (PACKED) fresh = claim_packed(cluster, v, r, uint32_t(v));
+          else fresh = claim_rel(cluster, croud, v, r, uint32_t(v));
         }
         bq.push(fresh, v, qout, cout);
       }
@@ -876,12 +895,17 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
   grid.sync();
   for (int64_t base = gtid - lane; base < n; base += gthreads) {
     const int64_t v = base + lane;
-    const uint32_t c = v < n ? ld_rlx_u32(cluster + v) : kFreeCluster;
+    uint32_t c = v < n ? ld_rlx_u32(cluster + v) : kFreeCluster;
+    if constexpr (PACKED) c = v < n ? c & kPackMask : c;
     const unsigned peers = __match_any_sync(0xffffffffu, c);
     if (v < n && lane == __ffs(int(peers)) - 1) atomicMin(mins + c, int32_t(v));
   }
   grid.sync();
-  for (int64_t v = gtid; v < n; v += gthreads) P[v] = ld_acq(mins + ld_rlx_u32(cluster + v));
+  for (int64_t v = gtid; v < n; v += gthreads) {
+    uint32_t c = ld_rlx_u32(cluster + v);
+    if constexpr (PACKED) c &= kPackMask;
+    P[v] = ld_acq(mins + c);
+  }
 }
 
 #define TL(kernel, grid, block, ...) ((kernel<<<grid, block, 0, st>>>(__VA_ARGS__)), ::gc::count_launch())
@@ -1095,6 +1119,16 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   GC_CHECK_LAUNCH();
 }
 
+// GC_LDD_PACKED=0 keeps the 6-byte (u32 cluster + u16 round) claim state
+// in the persistent kernel even when the packed key fits
+bool ldd_packed() {
+  static const bool p = [] {
+    const char* e = getenv("GC_LDD_PACKED");
+    return !(e && e[0] == '0');
+  }();
+  return p;
+}
+
 // GC_LDD_PERSIST=0 selects the launch-per-round form (k_ldd_round +
 // k_bits_to_queue, host termination check every 16 rounds)
 bool ldd_persistent() {
@@ -1121,7 +1155,11 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     // one cooperative launch runs every round and the labelling (no host
     // round trip); the start-round buckets come from the three passes below
     uint32_t* cl = reinterpret_cast<uint32_t*>(w.key);
-    uint16_t* cr = reinterpret_cast<uint16_t*>(cl + n);
+    // packed 4-byte claim keys when ids fit 24 bits and every round fits 8:
+    // the start rounds are <= delta_max <= -ln(2^-53) / beta (the
+    // exponential draw's largest value), so beta > 0.145 keeps them < 254
+    const bool packed = ldd_packed() && n <= (1 << 24) && 36.8f / beta < 253.f;
+    uint16_t* cr = packed ? nullptr : reinterpret_cast<uint16_t*>(cl + n);
     TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount);
     TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
     TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
@@ -1129,7 +1167,10 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     GC_CUDA(cudaMemsetAsync(w.stat, 0, 3 * sizeof(unsigned long long), st));
     static int per_sm = 0;
     if (!per_sm) {
-      GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ldd_persist, kTB, 0));
+      int a = 0, b = 0;
+      GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_ldd_persist<false>, kTB, 0));
+      GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_ldd_persist<true>, kTB, 0));
+      per_sm = a < b ? a : b;
       if (per_sm < 1) throw Error(GC_ERR_CUDA, "LDD persistent kernel does not fit on an SM");
     }
     const int64_t* off = g.offsets;
@@ -1155,8 +1196,9 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     if (trace) GC_CUDA(cudaMemsetAsync(trace, 0, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
     void* args[] = {&off, &tgt, &nn, &clp, &crp, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
                     &rounds_out, &trace};
-    GC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_ldd_persist), dim3(num_sms() * per_sm),
-                                        dim3(kTB), args, 0, st));
+    const void* kfn = packed ? reinterpret_cast<const void*>(k_ldd_persist<true>)
+                             : reinterpret_cast<const void*>(k_ldd_persist<false>);
+    GC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(num_sms() * per_sm), dim3(kTB), args, 0, st));
     ::gc::count_launch();
     GC_CHECK_LAUNCH();
     if (trace) {
