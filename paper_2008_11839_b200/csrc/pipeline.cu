@@ -233,8 +233,10 @@ __global__ void k_count_eq(const int32_t* P, int32_t n, unsigned long long* ctr)
   block_add<kEwBlock>(ctr + C_CAND_COUNT, c);
 }
 
+// the candidate is the mode: a strict majority, or a sampler that counted
+// its classes exactly (C_MODE_EXACT)
 __device__ __forceinline__ bool majority(const unsigned long long* ctr, int32_t n) {
-  return 2ull * ctr[C_CAND_COUNT] > static_cast<unsigned long long>(n);
+  return ctr[C_MODE_EXACT] != 0 || 2ull * ctr[C_CAND_COUNT] > static_cast<unsigned long long>(n);
 }
 
 __device__ __forceinline__ void hist_zero_body(int32_t* hist, int32_t n, unsigned long long* ctr) {
@@ -896,14 +898,16 @@ bool mode_coop() {
 }
 
 void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, int32_t* hist,
-                     unsigned long long* ctr, bool compress, cudaStream_t st) {
+                     unsigned long long* ctr, bool compress, cudaStream_t st, bool exact_mode) {
   if (n > 0) {
     const int64_t nq = (int64_t(n) + 3) / 4;
     const int gq = grid_for(nq, kEwBlock, 1);
     // the fallback kernels usually exit at once: one resident wave keeps
     // their early exit cheap and still streams when they do run
     const int g = grid_for(n, kEwBlock, 1);
-    (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1, take_stamps()), ::gc::count_launch());
+    // the sampler may have set the exact mode (C_CAND + C_MODE_EXACT)
+    if (exact_mode) stamp_flush(ctr, st);
+    else (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1, take_stamps()), ::gc::count_launch());
     // one resident wave: six 256-thread blocks per SM, two quads per thread
     const int gps = grid_for((nq + 1) / 2, kEwBlock, 1) < num_sms() * 6 ? grid_for((nq + 1) / 2, kEwBlock, 1)
                                                                           : num_sms() * 6;

@@ -64,7 +64,7 @@ void run_mode(int32_t* P, int32_t n, int32_t* hist, unsigned long long* ctr, cud
 // active gather in one pass, exact-mode fallback.  Leaves L_max, the active
 // list, its size and degree sum in the counters.
 void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, int32_t* hist,
-                     unsigned long long* ctr, bool compress, cudaStream_t st);
+                     unsigned long long* ctr, bool compress, cudaStream_t st, bool exact_mode = false);
 // Active gather for a known L_max (finish_phase).
 void run_gather(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr,
                 cudaStream_t st);

@@ -58,7 +58,9 @@ void run_hb(const gc_csr& g, const gc_spec& s, const UFConfig& c, RowUnionArgs a
             SamplerWs& w, unsigned long long* ctr, cudaStream_t st);
 void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t* fv, SamplerWs& w,
              unsigned long long* ctr, cudaStream_t st);
-void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
+// true when the persistent packed form also left the exact mode in
+// ctr[C_CAND] (+ C_MODE_EXACT): the pipeline then skips its probe / histogram
+bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
              cudaStream_t st);
 
 }  // namespace gc

@@ -255,10 +255,10 @@ struct Pipeline {
     } else {
       init_sets(sc);
       if (kev) stamp(ws.ctr, 5, st);
-      run_ldd(g, s, P, ws.samp, ws.ctr, st);
+      const bool exact = run_ldd(g, s, P, ws.samp, ws.ctr, st);
       if (kev) stamp(ws.ctr, 6, st);
       timed_sample = true;
-      run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st);
+      run_post_sample(P, n, g.offsets, ws.list, ws.hist, ws.ctr, false, st, exact);
     }
   }
 

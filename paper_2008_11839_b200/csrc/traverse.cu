@@ -575,7 +575,7 @@ constexpr int kBuckets = kLddMaxRounds + 1;
 // start round per vertex + block-aggregated bucket histogram
 __global__ void __launch_bounds__(kEwBlock)
 k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
-            uint32_t* cluster, uint16_t* croud, unsigned int* bcount) {
+            uint32_t* cluster, uint16_t* croud, unsigned int* bcount, uint32_t* csize = nullptr) {
   __shared__ unsigned int hist[kBuckets];
   for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -587,6 +587,7 @@ k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint
     start[v] = uint16_t(r);
     cluster[v] = kFreeCluster;
     if (croud) croud[v] = 0;
+    if (csize) csize[v] = 0;
     atomicAdd(hist + int(r), 1u);
   }
   __syncthreads();
@@ -788,7 +789,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
               uint16_t* croud, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
               const int32_t* dmax_bits, int32_t max_rounds, int32_t* q0, int32_t* q1, unsigned long long* ring,
               unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out,
-              unsigned int* trace) {
+              unsigned int* trace, uint32_t* csize, unsigned long long* ctr) {
   cg::grid_group grid = cg::this_grid();
   __shared__ BlockQueue<kQCap> bq;
   bq.init();
@@ -825,6 +826,16 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         b = ld_stream64(off + f, pol);
         d = int32_t(ld_stream64(off + f + 1, pol) - b);
         my_insp += d;
+      }
+      if constexpr (PACKED) {
+        // every claimed vertex is expanded exactly once, in the round after
+        // its (final) claim: count it for its cluster here — the exact
+        // cluster sizes, so the pipeline needs no label histogram for the
+        // mode (lanes holding the same cluster add once)
+        const bool has = lane < vpw && i < count;
+        const unsigned act = __ballot_sync(0xffffffffu, has);
+        const unsigned peers = __match_any_sync(0xffffffffu, has ? c : kFreeCluster);
+        if (has && lane == __ffs(int(peers & act)) - 1) atomicAdd(csize + c, unsigned(__popc(peers & act)));
       }
       int32_t incl = d;
 #pragma unroll
@@ -905,6 +916,32 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     uint32_t c = ld_rlx_u32(cluster + v);
     if constexpr (PACKED) c &= kPackMask;
     P[v] = ld_acq(mins + c);
+  }
+  if constexpr (PACKED) {
+    // the mode: the largest cluster, ties to the smaller label (its minimum
+    // member), as np.bincount(...).argmax() (sampling.py:29-35)
+    unsigned long long best = 0;
+    for (int64_t c = gtid; c < n; c += gthreads) {
+      const uint32_t sz = csize[c];
+      if (sz) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(sz) << 32) | (0xffffffffull - uint32_t(ld_acq(mins + c)));
+        best = key > best ? key : best;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+      best = t > best ? t : best;
+    }
+    if (lane == 0 && best) atomicMax(ctr + C_SCRATCH0, best);
+    grid.sync();
+    if (gtid == 0) {
+      const unsigned long long k = ctr[C_SCRATCH0];
+      ctr[C_CAND] = 0xffffffffull - (k & 0xffffffffull);
+      ctr[C_SCRATCH0] = 0;
+      ctr[C_MODE_EXACT] = 1;
+    }
   }
 }
 
@@ -1139,10 +1176,10 @@ bool ldd_persistent() {
   return p;
 }
 
-void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
+bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
              cudaStream_t st) {
   const int32_t n = int32_t(g.n);
-  if (n == 0) return;
+  if (n == 0) return false;
   const float beta = s.ldd_beta > 0 ? float(s.ldd_beta) : 0.2f;
   int32_t* dmax = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
   unsigned int* bcount = w.boff;
@@ -1160,7 +1197,9 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     // exponential draw's largest value), so beta > 0.145 keeps them < 254
     const bool packed = ldd_packed() && n <= (1 << 24) && 36.8f / beta < 253.f;
     uint16_t* cr = packed ? nullptr : reinterpret_cast<uint16_t*>(cl + n);
-    TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount);
+    // packed: the second half of the 8n-byte claim buffer counts cluster sizes
+    uint32_t* csz = packed ? cl + n : nullptr;
+    TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount, csz);
     TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
     TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
        cursor, w.order);
@@ -1194,8 +1233,10 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     unsigned int* trace = nullptr;
     if (trace_on) GC_CUDA(cudaMallocAsync(&trace, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
     if (trace) GC_CUDA(cudaMemsetAsync(trace, 0, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
+    uint32_t* cszp = csz;
+    unsigned long long* ctrp = ctr;
     void* args[] = {&off, &tgt, &nn, &clp, &crp, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
-                    &rounds_out, &trace};
+                    &rounds_out, &trace, &cszp, &ctrp};
     const void* kfn = packed ? reinterpret_cast<const void*>(k_ldd_persist<true>)
                              : reinterpret_cast<const void*>(k_ldd_persist<false>);
     GC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(num_sms() * per_sm), dim3(kTB), args, 0, st));
@@ -1212,7 +1253,7 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
       fprintf(stderr, "\n");
       GC_CUDA(cudaFreeAsync(trace, st));
     }
-    return;
+    return packed;
   }
   // the claim buffer (8n bytes) holds the u32 clusters and the u16 claim rounds
   uint32_t* cluster = reinterpret_cast<uint32_t*>(w.key);
@@ -1268,6 +1309,7 @@ void run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
   TL(k_ldd_mins, ge, kEwBlock, cluster, mins, n);
   TL(k_ldd_label, ge, kEwBlock, cluster, mins, P, n);
   GC_CHECK_LAUNCH();
+  return false;
 }
 
 }  // namespace gc
