@@ -556,9 +556,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 }
 
 __device__ __forceinline__ float ldd_delta(uint64_t seed, int64_t v, float beta) {
+  // a 24-bit uniform in (0, 1] and the fast hardware log: delta <= 24 ln 2 /
+  // beta (the double-precision form cost 0.19 ms of two passes at 2^24)
   const uint64_t h = mix64(seed * 0xd1b54a32d192ed03ull + uint64_t(v));
-  const double u = (double((h >> 11) + 1)) * (1.0 / 9007199254740992.0);  // (0, 1]
-  return float(-log(u) / double(beta));
+  const float u = float(uint32_t(h >> 40) + 1u) * (1.0f / 16777216.0f);
+  return -__logf(u) / beta;
 }
 
 __global__ void k_ldd_delta_max(int32_t n, uint64_t seed, float beta, int32_t* dmax_bits) {
@@ -1193,9 +1195,9 @@ bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     // round trip); the start-round buckets come from the three passes below
     uint32_t* cl = reinterpret_cast<uint32_t*>(w.key);
     // packed 4-byte claim keys when ids fit 24 bits and every round fits 8:
-    // the start rounds are <= delta_max <= -ln(2^-53) / beta (the
-    // exponential draw's largest value), so beta > 0.145 keeps them < 254
-    const bool packed = ldd_packed() && n <= (1 << 24) && 36.8f / beta < 253.f;
+    // the start rounds are <= delta_max <= 24 ln 2 / beta (the exponential
+    // draw's largest value), so beta > 0.066 keeps them < 254
+    const bool packed = ldd_packed() && n <= (1 << 24) && 16.7f / beta < 253.f;
     uint16_t* cr = packed ? nullptr : reinterpret_cast<uint16_t*>(cl + n);
     // packed: the second half of the 8n-byte claim buffer counts cluster sizes
     uint32_t* csz = packed ? cl + n : nullptr;
