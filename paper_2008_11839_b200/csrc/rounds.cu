@@ -110,15 +110,20 @@ k_coo_gather(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, c
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long base;
   const int64_t stride = int64_t(gridDim.x) * kRB;
+  const uint64_t pol = evict_first_policy();
   for (int64_t i0 = int64_t(blockIdx.x) * kRB; i0 < count; i0 += stride) {
     const int64_t i = i0 + threadIdx.x;
     int32_t u = 0;
     int64_t b = 0, e = 0;
     int c = 0;
+    // the first 32 entries' keep / twin decisions, so the write pass does
+    // not repeat their random label reads (longer rows re-evaluate the rest)
+    uint32_t keepm = 0, twinm = 0;
     if (i < count) {
       u = list ? list[i] : int32_t(i);
-      b = off[u];
-      e = off[u + 1];
+      // graph data streams through L2 evict-first: the labels stay resident
+      b = ld_stream64(off + u, pol);
+      e = ld_stream64(off + u + 1, pol);
       if (all_active) {
         int64_t lo = b, hi = e;  // rows are sorted: the kept entries t > u are a suffix
         while (lo < hi) {
@@ -129,7 +134,14 @@ k_coo_gather(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, c
         c = int(e - lo);
       } else {
         bool twin;
-        for (int64_t j = b; j < e; ++j) c += keep_entry(u, tgt[j], false, P, lmax, twin);
+        for (int64_t j = b; j < e; ++j) {
+          const bool k = keep_entry(u, tgt[j], false, P, lmax, twin);
+          c += k;
+          if (j - b < 32) {
+            keepm |= uint32_t(k) << (j - b);
+            twinm |= uint32_t(twin) << (j - b);
+          }
+        }
       }
     }
     int rank, total;
@@ -140,9 +152,13 @@ k_coo_gather(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, c
       const int32_t lu = map_labels ? P[u] : u;
       unsigned long long p = base + rank;
       for (int64_t j = b; j < e; ++j) {
-        const int32_t t = tgt[j];
         bool twin = true;
-        if (!all_active && !keep_entry(u, t, false, P, lmax, twin)) continue;
+        if (!all_active && j - b < 32) {
+          if (!(keepm >> (j - b) & 1u)) continue;
+          twin = twinm >> (j - b) & 1u;
+        }
+        const int32_t t = tgt[j];
+        if (!all_active && j - b >= 32 && !keep_entry(u, t, false, P, lmax, twin)) continue;
         out.u[p] = lu;
         out.v[p] = map_labels ? P[t] : t;
         out.w[p] = twin ? 2 : 1;
