@@ -577,7 +577,8 @@ constexpr int kBuckets = kLddMaxRounds + 1;
 // start round per vertex + block-aggregated bucket histogram
 __global__ void __launch_bounds__(kEwBlock)
 k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint16_t* start,
-            uint32_t* cluster, uint16_t* croud, unsigned int* bcount, uint32_t* csize = nullptr) {
+            uint32_t* cluster, uint16_t* croud, unsigned int* bcount, uint32_t* csize = nullptr,
+            int32_t* pmin = nullptr) {
   __shared__ unsigned int hist[kBuckets];
   for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -590,6 +591,7 @@ k_ldd_start(int32_t n, uint64_t seed, float beta, const int32_t* dmax_bits, uint
     cluster[v] = kFreeCluster;
     if (croud) croud[v] = 0;
     if (csize) csize[v] = 0;
+    if (pmin) pmin[v] = INT_MAX;
     atomicAdd(hist + int(r), 1u);
   }
   __syncthreads();
@@ -820,8 +822,9 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
       uint32_t c = 0;
       int64_t b = 0;
       int32_t d = 0;
+      int32_t f = INT_MAX;
       if (lane < vpw && i < count) {
-        const int32_t f = ld_acq(qin + i);
+        f = ld_acq(qin + i);
         c = ld_rlx_u32(cluster + f);  // final since round r-1
         if constexpr (PACKED) c &= kPackMask;
         // graph data is read once: L2 evict-first keeps the claim state resident
@@ -835,9 +838,15 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
         // cluster sizes, so the pipeline needs no label histogram for the
         // mode (lanes holding the same cluster add once)
         const bool has = lane < vpw && i < count;
-        const unsigned act = __ballot_sync(0xffffffffu, has);
         const unsigned peers = __match_any_sync(0xffffffffu, has ? c : kFreeCluster);
-        if (has && lane == __ffs(int(peers & act)) - 1) atomicAdd(csize + c, unsigned(__popc(peers & act)));
+        // and its minimum member, straight into P[c] (P[v] = INT_MAX until
+        // the labelling; a non-empty cluster's centre c is its own member,
+        // so P[c] ends as its own label and can serve as the cluster slot)
+        const unsigned fmin = __reduce_min_sync(peers, unsigned(f));
+        if (has && lane == __ffs(int(peers)) - 1) {
+          atomicAdd(csize + c, unsigned(__popc(peers)));
+          atomicMin(P + c, int32_t(fmin));
+        }
       }
       int32_t incl = d;
 #pragma unroll
@@ -902,6 +911,15 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
   }
   block_add<kTB>(insp, my_insp);
   if (gtid == 0 && rounds_out) *rounds_out = (unsigned long long)(r + 1);
+  if constexpr (PACKED) {
+    // the cluster minima are in P[centre] already (taken while expanding):
+    // every other vertex reads its centre's slot, which never changes
+    for (int64_t v = gtid; v < n; v += gthreads) {
+      const int32_t c = int32_t(ld_rlx_u32(cluster + v) & kPackMask);
+      if (c != v) P[v] = ld_acq(P + c);
+    }
+    mins = P;  // the mode pass below reads the minima from the centres' slots
+  } else {
   // labels: minimum member id per cluster (warp-elected atomicMin over the
   // lanes holding the same cluster), then P[v] = mins[cluster(v)]
   for (int64_t v = gtid; v < n; v += gthreads) mins[v] = INT_MAX;
@@ -918,6 +936,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     uint32_t c = ld_rlx_u32(cluster + v);
     if constexpr (PACKED) c &= kPackMask;
     P[v] = ld_acq(mins + c);
+  }
   }
   if constexpr (PACKED) {
     // the mode: the largest cluster, ties to the smaller label (its minimum
@@ -1201,7 +1220,7 @@ bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     uint16_t* cr = packed ? nullptr : reinterpret_cast<uint16_t*>(cl + n);
     // packed: the second half of the 8n-byte claim buffer counts cluster sizes
     uint32_t* csz = packed ? cl + n : nullptr;
-    TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount, csz);
+    TL(k_ldd_start, ge, kEwBlock, n, s.seed, beta, dmax, w.start, cl, cr, bcount, csz, packed ? P : nullptr);
     TL(k_ldd_bucket_scan, 1, 1024, bcount, cursor);
     TL(k_ldd_scatter, grid_for(((int64_t(n) + 4095) / 4096) * kEwBlock, kEwBlock, 64), kEwBlock, n, w.start,
        cursor, w.order);
