@@ -548,18 +548,19 @@ __global__ void k_bfs_reroot(const uint32_t* par, const int32_t* minv, int32_t* 
 // Vertices are bucketed by start round once, so each round touches only its
 // own centres.  Labels are cluster minima: P[v] <= v and every class is
 // connected, so the partition refines the true one (validate.py:290-297).
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ull;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
-}
 
 __device__ __forceinline__ float ldd_delta(uint64_t seed, int64_t v, float beta) {
-  // a 24-bit uniform in (0, 1] and the fast hardware log: delta <= 24 ln 2 /
-  // beta (the double-precision form cost 0.19 ms of two passes at 2^24)
-  const uint64_t h = mix64(seed * 0xd1b54a32d192ed03ull + uint64_t(v));
-  const float u = float(uint32_t(h >> 40) + 1u) * (1.0f / 16777216.0f);
+  // a 24-bit uniform in (0, 1] from a 32-bit finaliser (murmur3 fmix32; the
+  // 64-bit mix is emulated 64-bit multiplies) and the hardware log: delta <=
+  // 24 ln 2 / beta (the double-precision form cost 0.19 ms of two passes at
+  // 2^24)
+  uint32_t h = uint32_t(v) * 0x9e3779b1u ^ uint32_t(seed) ^ uint32_t(seed >> 32) * 0x85ebca77u;
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  const float u = float((h >> 8) + 1u) * (1.0f / 16777216.0f);
   return -__logf(u) / beta;
 }
 
