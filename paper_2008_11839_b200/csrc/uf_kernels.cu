@@ -156,17 +156,19 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
 // ancestor either way, so the root found is the same.  A link is
 // CAS(P[hi], hi, lo) on the two roots; a failed link resumes the hi chain
 // from the value the CAS saw (hi's new parent) and the lo chain from lo.
-template <class R, int K, bool WEAK>
-__global__ void __launch_bounds__(256, 5)
+// GIANT = false compiles the giant-filter machinery out (batches without a
+// filter: static union_edge_list, sharded merges, GC_INCR_GIANT=0)
+template <class R, int K, bool WEAK, bool GIANT>
+__global__ void __launch_bounds__(256, K <= 2 ? 5 : 1)
 k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
                       const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad,
-                      const unsigned long long* kdev, GiantPass alt) {
+                      const unsigned long long* kdev, GiantPass alt, bool lazy_self) {
   static_assert(R::kUnion == GC_FINISH_ASYNC, "lock-step form of the async rule");
   // giant filter: *kdev = survivors of the compaction (their endpoints
   // carry bit 31 = "giant bit already set"), or ~0 when the compaction
   // passed the batch through (the caller's arrays, no flags)
   bool flags = false;
-  if (kdev) {
+  if (GIANT && kdev) {
     const unsigned long long c = *kdev;
     if (c == ~0ull) {
       us = alt.us;
@@ -184,7 +186,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
   // every read goes to L2, so a stale line cannot stall a retry loop
   int it = 0;
   auto ld = [&](const int32_t* p) { return (WEAK && it < 8) ? ld_weak(p) : ld_acq(p); };
-  const int32_t anc = s.gbits ? ld_acq(s.ganchor) : -1;
+  const int32_t anc = GIANT && s.gbits ? ld_acq(s.ganchor) : -1;
   const int64_t span = int64_t(blockDim.x) * K;
   for (int64_t base = int64_t(blockIdx.x) * span; base < k; base += int64_t(gridDim.x) * span) {
     int32_t eu[K], ev[K];     // endpoints (forest records)
@@ -254,7 +256,16 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           if (bu && bv) slot &= ~(1u << j);
         }
     }
-    if (sentinel >= 0) {
+    // lazy init (driver.py:620-625) without a returning CAS per endpoint: an
+    // uninitialised slot (the sentinel) reads as its own root; the link CAS
+    // expects the value actually stored (sentinel or the id), and whoever
+    // links under an uninitialised root initialises it with a
+    // fire-and-forget CAS — every touched vertex ends initialised, as the
+    // reference's ensure_init leaves it, without two dependent atomics per
+    // insert (early batches: every endpoint is fresh)
+    unsigned sent = 0;  // bit 2j+c: x[j][c]'s slot read as the sentinel
+    if (sentinel >= 0 && !lazy_self) {
+      // A/B form: claim every fresh endpoint with a returning CAS first
 #pragma unroll
       for (int j = 0; j < K; ++j)
 #pragma unroll
@@ -262,6 +273,15 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           if ((slot >> j & 1u) && px[j][c] == sentinel) {
             const int32_t o = atomicCAS(P + x[j][c], sentinel, x[j][c]);
             px[j][c] = o == sentinel ? x[j][c] : o;
+          }
+    } else if (sentinel >= 0) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if ((slot >> j & 1u) && px[j][c] == sentinel) {
+            px[j][c] = x[j][c];
+            sent |= 1u << (2 * j + c);
           }
     }
 #pragma unroll
@@ -277,7 +297,15 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const unsigned b = 1u << (2 * j + c);
-          if ((live & b) && !(have & b)) px[j][c] = ld(P + x[j][c]);
+          if ((live & b) && !(have & b)) {
+            px[j][c] = ld(P + x[j][c]);
+            if (sentinel >= 0 && px[j][c] == sentinel) {
+              px[j][c] = x[j][c];
+              sent |= b;
+            } else {
+              sent &= ~b;
+            }
+          }
         }
       have |= live;
       // 2. advance the chains one hop (compression writes fire and forget)
@@ -298,6 +326,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           }
           x[j][c] = nx;
           have &= ~b;
+          sent &= ~b;
         }
       // 3. link the unions whose two roots are known (all CASes issued first)
       int32_t old[K];
@@ -308,10 +337,13 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           const int32_t ru = x[j][0], rv = x[j][1];
           if (ru == rv) {
             slot &= ~(1u << j);
+            // an insert (u, u) of a fresh vertex initialises it
+            if (sent >> (2 * j) & 3u) atomicCAS(P + ru, sentinel, ru);
             if (anc >= 0) mark(j, ru);
           } else {
             const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
-            old[j] = atomicCAS(P + hi, hi, lo);
+            const bool hs = (sent >> (2 * j + (ru > rv ? 0 : 1))) & 1u;
+            old[j] = atomicCAS(P + hi, hs ? sentinel : hi, lo);
           }
         }
       }
@@ -320,11 +352,19 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
         if (old[j] < 0) continue;
         const int32_t ru = x[j][0], rv = x[j][1];
         const int32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
-        if (old[j] == hi) {
+        const unsigned bh = 1u << (2 * j + (ru > rv ? 0 : 1)), bl = 1u << (2 * j + (ru > rv ? 1 : 0));
+        const bool hs = sent & bh;
+        if (old[j] == (hs ? sentinel : hi)) {
           if (s.lflag) s.lflag[base + int64_t(j) * blockDim.x + threadIdx.x] = 1;
           else record<R::kForest>(s, hi, eu[j], ev[j]);
+          // lo may still be uninitialised: it is a root with children now
+          if (sent & bl) atomicCAS(P + lo, sentinel, lo);
           slot &= ~(1u << j);
           if (anc >= 0) mark(j, lo);
+        } else if (sentinel >= 0 && (old[j] == hi || old[j] == sentinel)) {
+          // hi is still a root: only its slot was initialised meanwhile;
+          // link again next step with the value now stored
+          sent = old[j] == sentinel ? (sent | bh) : (sent & ~bh);
         } else {
           // hi was linked meanwhile: resume both finds from the roots
           // (register selects, no dynamic index into the chain arrays)
@@ -336,6 +376,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
           pv[j][0] = pv[j][1] = -1;
           have = (have & ~(3u << (2 * j))) | (1u << (2 * j + (h0 ? 0 : 1)));
           live |= 3u << (2 * j);
+          sent &= ~(3u << (2 * j));  // old is a real parent; lo is read again
         }
       }
     }
@@ -458,6 +499,17 @@ struct RowsLaunch {
   }
 };
 
+// GC_INCR_LAZY=0: incremental inserts claim every fresh endpoint with a
+// returning CAS before the union (instead of reading the sentinel as "its
+// own root" and initialising linked-under roots fire-and-forget)
+bool lazy_self() {
+  static const bool on = [] {
+    const char* e = getenv("GC_INCR_LAZY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class R, int K>
 void launch_mlp(const UFState& s, const CooUnionArgs& a, cudaStream_t st) {
   int64_t blocks = (a.k + 256 * K - 1) / (256 * K);
@@ -468,17 +520,25 @@ void launch_mlp(const UFState& s, const CooUnionArgs& a, cudaStream_t st) {
   // either grid is correct for either mode)
   static const int per_sm = [] {
     int b = 0;
-    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_coo_async_mlp<R, K, false>, 256, 0));
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_coo_async_mlp<R, K, false, true>, 256, 0));
     return b > 0 ? b : 1;
   }();
   const int64_t cap = int64_t(num_sms()) * (a.kdev && a.kdev_wave ? per_sm : 8 * 16);
   if (blocks > cap) blocks = cap;
   if (s.weak)
-    (k_union_coo_async_mlp<R, K, true><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel,
-                                                                     a.bad, a.kdev, a.alt), ::gc::count_launch());
+    (k_union_coo_async_mlp<R, K, true, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
+                                                                            a.init_sentinel, a.bad, nullptr,
+                                                                            a.alt, lazy_self()),
+     ::gc::count_launch());
+  else if (s.gbits)
+    (k_union_coo_async_mlp<R, K, false, true><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
+                                                                            a.init_sentinel, a.bad, a.kdev, a.alt,
+                                                                            lazy_self()),
+     ::gc::count_launch());
   else
-    (k_union_coo_async_mlp<R, K, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
-                                                                      a.init_sentinel, a.bad, a.kdev, a.alt),
+    (k_union_coo_async_mlp<R, K, false, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip,
+                                                                             a.init_sentinel, a.bad, nullptr,
+                                                                             a.alt, lazy_self()),
      ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }

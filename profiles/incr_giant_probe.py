@@ -3,7 +3,8 @@ union-find spec; run once with GC_INCR_GIANT=1 and once with =0.
   python profiles/incr_giant_probe.py [spec]"""
 import json
 import sys
-sys.path.insert(0, "/root/repo")
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 from paper_2008_11839_b200 import build_csr, gen_rmat, parse_spec, IncrementalConnectivity  # noqa: E402
 
