@@ -487,7 +487,7 @@ void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
   a.kdev_wave = h->hmode && *reinterpret_cast<volatile int32_t*>(h->hmode) != 0;
 }
 
-void giant_after(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len) {
+void giant_after(gc_incr* h) {
   if (!h->gbits) return;
   (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->hmode_dev),
    ::gc::count_launch());
@@ -577,7 +577,7 @@ void insert_phase(gc_incr* h, const int32_t* us, const int32_t* vs, const uint8_
     a.init_sentinel = sentinel;
     giant_compact(h, a, isq);
     launch_union_coo(UFConfig{h->spec.finish, h->spec.find, h->spec.splice}, false, a, st);
-    giant_after(h, us, vs, isq, len);
+    giant_after(h);
     if (stats) stats->insp_finish += n_ins;
     return;
   }
@@ -850,7 +850,7 @@ int gc_incr_insert_list(gc_incr* h, const int32_t* us, const int32_t* vs, int64_
                                                       out_count), ::gc::count_launch());
       GC_CHECK_LAUNCH();
     }
-    giant_after(h, us, vs, nullptr, len);
+    giant_after(h);
     GC_CUDA(cudaEventRecord(h->ev[1], st));
     fetch_bad(h);
     GC_CUDA(cudaStreamSynchronize(st));
