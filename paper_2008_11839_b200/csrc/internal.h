@@ -91,6 +91,7 @@ enum Counter : int {
   C_WWT0,          // round loops: working weight, parity 0 / 1
   C_WWT1,
   C_MODE_EXACT,    // the sampler computed the exact mode itself (C_CAND is L_max)
+  C_CUT,           // LDD: cut edges emitted into the rounds finish's COO
   C_STAMP0,        // 10 %globaltimer stamps of the static pipeline's phases
   C_COUNT_ = C_STAMP0 + 10
 };

@@ -170,6 +170,36 @@ k_coo_gather(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, c
   }
 }
 
+// The gather's entries from a list of label-crossing pairs (LDD cut edges,
+// each unordered pair once): a pair touching L_max becomes (active end,
+// L_max end) with weight 1, any other (smaller id, larger id) with weight 2
+// — the same entries k_coo_gather keeps (keep_entry), in place.
+__global__ void __launch_bounds__(kRB)
+k_cut_orient(const int32_t* __restrict__ P, int64_t count, int32_t lmax, int map_labels, Coo out) {
+  const int64_t stride = int64_t(gridDim.x) * kRB;
+  for (int64_t i = int64_t(blockIdx.x) * kRB + threadIdx.x; i < count; i += stride) {
+    int32_t a = out.u[i], b = out.v[i];
+    const int32_t la = P[a], lb = P[b];
+    uint8_t w = 2;
+    int32_t pa = la, pb = lb;
+    if (la == lmax) {
+      const int32_t t = a; a = b; b = t;
+      pa = lb;
+      pb = la;
+      w = 1;
+    } else if (lb == lmax) {
+      w = 1;
+    } else if (a > b) {
+      const int32_t t = a; a = b; b = t;
+      pa = lb;
+      pb = la;
+    }
+    out.u[i] = map_labels ? pa : a;
+    out.v[i] = map_labels ? pb : b;
+    out.w[i] = w;
+  }
+}
+
 // ----------------------------------------------------------------- forest ---
 // Winner commit: root r records the original pair of its smallest winning
 // edge index (minbased.py:95-116); the source row of CSR position j is found
@@ -766,7 +796,7 @@ void loop_rounds(const gc_spec& s, int32_t* P, int64_t nl, Coo& work, RoundsWs& 
 
 int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const int32_t* list,
                           unsigned long long* ctr, int32_t* fu, int32_t* fv, RoundsWs& w,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool cut_ready) {
   const int32_t n = int32_t(g.n);
   if (n == 0) return 0;
   // active count / gather degree sum / l_max from the device counters
@@ -788,14 +818,24 @@ int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const i
   Coo& work = w.work;
   Coo out = work;
   if (!fu) out.idx = nullptr;
-  unsigned long long* cursor = reinterpret_cast<unsigned long long*>(w.cnt);
-  GC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
-  (k_coo_gather<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
-                                              map_labels, out, cursor), ::gc::count_launch());
-  GC_CHECK_LAUNCH();
-  GC_CUDA(cudaMemcpyAsync(h, cursor, 8, cudaMemcpyDeviceToHost, st));
-  GC_CUDA(cudaStreamSynchronize(st));
-  work.len = int64_t(h[0]);
+  if (cut_ready && !fu && !all_active) {
+    // the sampler's cut edges, exactly the entries the gather keeps: orient
+    // and weight them in place
+    const int64_t cuts = int64_t(h[C_CUT]);
+    if (cuts)
+      (k_cut_orient<<<grid_e(cuts), kRB, 0, st>>>(P, cuts, lmax, map_labels, out), ::gc::count_launch());
+    GC_CHECK_LAUNCH();
+    work.len = cuts;
+  } else {
+    unsigned long long* cursor = reinterpret_cast<unsigned long long*>(w.cnt);
+    GC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+    (k_coo_gather<<<grid_e(count), kRB, 0, st>>>(g.offsets, g.targets, P, list, count, lmax, all_active,
+                                                map_labels, out, cursor), ::gc::count_launch());
+    GC_CHECK_LAUNCH();
+    GC_CUDA(cudaMemcpyAsync(h, cursor, 8, cudaMemcpyDeviceToHost, st));
+    GC_CUDA(cudaStreamSynchronize(st));
+    work.len = int64_t(h[0]);
+  }
   work.weight = degsum;
   work.idx = out.idx;
   ForestOut fo;

@@ -62,9 +62,12 @@ void rounds_carve(A& a, RoundsWs& w, int64_t n, int64_t m, const gc_spec& s, boo
 // Static / finish-phase driver: gathers the working COO of the active rows
 // (all rows when list == nullptr) and runs the configured rounds on P.
 // Returns the round count.
+// cut_ready: work.u / work.v already hold every edge between two different
+// labels once (LDD's cut edges, count in ctr[C_CUT]); they are oriented and
+// weighted in place instead of gathered from the active rows.
 int64_t run_rounds_finish(const gc_csr& g, const gc_spec& s, int32_t* P, const int32_t* list,
                           unsigned long long* ctr, int32_t* fu, int32_t* fv, RoundsWs& w,
-                          cudaStream_t st);
+                          cudaStream_t st, bool cut_ready = false);
 
 // Incremental driver: rounds over an explicit batch COO on labels[nl]
 // (nl = capacity + 1, minbased.py:124 / :163 with phase="insert").

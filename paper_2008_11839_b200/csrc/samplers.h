@@ -20,6 +20,13 @@ struct SamplerWs {
   int32_t* order = nullptr;   // LDD vertices bucketed by start round
   unsigned int* boff = nullptr;    // LDD bucket offsets [kLddMaxRounds + 2]
   unsigned int* cursor = nullptr;  // LDD scatter cursors
+  // LDD cut-edge emission (set by a labels-only rounds finish; the
+  // finish's working COO arrays): every pair of adjacent vertices in
+  // different clusters, once; cut_done when the sampler produced it
+  int32_t* cut_u = nullptr;
+  int32_t* cut_v = nullptr;
+  unsigned long long* cut_count = nullptr;
+  bool cut_done = false;
 };
 
 constexpr int kLddMaxRounds = 4094;

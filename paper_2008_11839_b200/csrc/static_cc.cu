@@ -136,6 +136,16 @@ __global__ void k_split_pairs(const int2* __restrict__ pr, int32_t n, int32_t* f
 }
 
 // Workspace layout shared by every static entry point.
+// GC_LDD_CUT=0: rounds finishes after LDD gather their working COO from the
+// active rows instead of taking the sampler's cut edges
+bool ldd_cut_on() {
+  static const bool on = [] {
+    const char* e = getenv("GC_LDD_CUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class A>
 struct Layout {
   unsigned long long* ctr = nullptr;
@@ -255,6 +265,13 @@ struct Pipeline {
     } else {
       init_sets(sc);
       if (kev) stamp(ws.ctr, 5, st);
+      // a labels-only rounds finish takes its working COO from the sampler
+      // (the cut edges; GC_LDD_CUT=0 keeps the gather)
+      if (!fu && !is_union_finish(s.finish) && ldd_cut_on()) {
+        ws.samp.cut_u = ws.rounds.work.u;
+        ws.samp.cut_v = ws.rounds.work.v;
+        ws.samp.cut_count = ws.ctr + C_CUT;
+      }
       const bool exact = run_ldd(g, s, P, ws.samp, ws.ctr, st);
       if (kev) stamp(ws.ctr, 6, st);
       timed_sample = true;
@@ -306,8 +323,8 @@ struct Pipeline {
     }
     if (kev) stamp_defer(7);
     stamp_flush(ws.ctr, st);
-    const int64_t r =
-        run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st);
+    const int64_t r = run_rounds_finish(g, s, P, all_active ? nullptr : ws.list, ws.ctr, fu, fv, ws.rounds, st,
+                                        ws.samp.cut_done);
     if (kev) stamp_defer(8);
     return r;
   }

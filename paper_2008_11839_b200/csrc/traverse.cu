@@ -782,6 +782,53 @@ __device__ __forceinline__ bool claim_rel(uint32_t* cluster, uint16_t* croud, in
 // state per vertex instead of 6 (67 MB at 2^24, which the L2 can hold).  The
 // filter read rejects keys of earlier rounds before the atomic.
 constexpr uint32_t kPackMask = 0xffffffu;
+
+// Block-aggregated append of (u, v) pairs (the cut edges LDD emits): warps
+// stage into shared memory, the block reserves its range with one counter
+// atomic per flush; a full stage overflows per warp to the global list.
+template <int CAP>
+struct PairQueue {
+  int2 items[CAP];
+  int count;
+  unsigned long long base;
+  __device__ __forceinline__ void init() {
+    if (threadIdx.x == 0) count = 0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void push(bool p, int32_t a, int32_t b, int32_t* gu, int32_t* gv,
+                                       unsigned long long* gc) {
+    const unsigned bal = __ballot_sync(0xffffffffu, p);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(&count, __popc(bal));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const int mine = pos + __popc(bal & ((1u << lane) - 1u));
+    if (p && mine < CAP) items[mine] = make_int2(a, b);
+    const unsigned over = __ballot_sync(0xffffffffu, p && mine >= CAP);
+    if (!over) return;
+    unsigned long long g = 0;
+    if (lane == __ffs(int(over)) - 1) g = atomicAdd(gc, static_cast<unsigned long long>(__popc(over)));
+    g = __shfl_sync(0xffffffffu, g, __ffs(int(over)) - 1) + __popc(over & ((1u << lane) - 1u));
+    if (p && mine >= CAP) {
+      gu[g] = a;
+      gv[g] = b;
+    }
+  }
+  __device__ __forceinline__ void flush(int32_t* gu, int32_t* gv, unsigned long long* gc) {
+    __syncthreads();
+    const int c = count < CAP ? count : CAP;
+    if (threadIdx.x == 0) base = c ? atomicAdd(gc, static_cast<unsigned long long>(c)) : 0ull;
+    __syncthreads();
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+      gu[base + i] = items[i].x;
+      gv[base + i] = items[i].y;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) count = 0;
+    __syncthreads();
+  }
+};
 __device__ __forceinline__ bool claim_packed(uint32_t* key, int32_t x, int32_t round, uint32_t c) {
   const uint32_t k = ld_rlx_u32(key + x);
   if ((k >> 24) < uint32_t(round)) return false;  // reached in an earlier round (free = round 255)
@@ -794,10 +841,24 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
               uint16_t* croud, const int32_t* __restrict__ order, const unsigned int* __restrict__ boff,
               const int32_t* dmax_bits, int32_t max_rounds, int32_t* q0, int32_t* q1, unsigned long long* ring,
               unsigned long long* insp, int32_t* mins, int32_t* P, unsigned long long* rounds_out,
-              unsigned int* trace, uint32_t* csize, unsigned long long* ctr) {
+              unsigned int* trace, uint32_t* csize, unsigned long long* ctr, int32_t* cut_u, int32_t* cut_v,
+              unsigned long long* cut_count) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ BlockQueue<kQCap> bq;
+  // 12 KB of frontier staging + 8 KB of cut-pair staging: the same shared
+  // memory as the 16 KB frontier stage plus a 4 KB pair stage (a larger
+  // total costs the cooperative grid resident blocks: 2048 pairs measured
+  // the sampler 2.6 -> 4.6 ms)
+  __shared__ BlockQueue<kTB * 12> bq;
+  __shared__ PairQueue<1024> pq;
   bq.init();
+  pq.init();
+  // cut-edge emission (packed form, labels-only rounds finishes): expanding
+  // a vertex of cluster c claimed in round r - 1, a neighbour x whose claim
+  // is final (claimed in an earlier round) and in another cluster is a cut
+  // edge; of two vertices claimed in the same round only the smaller id
+  // emits — every edge between two clusters exactly once, so the finish
+  // needs no gather over the active rows
+  const bool emit = PACKED && cut_u != nullptr;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t(blockIdx.x) * kTB + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * kTB) >> 5;
@@ -859,7 +920,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
       // two edges per lane per step (e and e + 32): two independent claim
       // chains in flight per lane
       for (int32_t e0 = 0; e0 < total; e0 += 64) {
-        int32_t x[2];
+        int32_t x[2], sf[2];
         uint32_t sc[2];
         bool ok[2];
 #pragma unroll
@@ -877,17 +938,35 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
           const int32_t sd = __shfl_sync(0xffffffffu, d, src);
           const int64_t sb = __shfl_sync(0xffffffffu, b, src);
           sc[h] = __shfl_sync(0xffffffffu, c, src);
+          sf[h] = __shfl_sync(0xffffffffu, f, src);
           ok[h] = e < total;
           x[h] = ok[h] ? ld_stream(tgt + sb + (e - (se - sd)), pol) : 0;
         }
-        bool fresh[2];
+        bool fresh[2], cut[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if constexpr (PACKED) fresh[h] = ok[h] && claim_packed(cluster, x[h], r, sc[h]);
-          else fresh[h] = ok[h] && claim_rel(cluster, croud, x[h], r, sc[h]);
+          cut[h] = false;
+          if constexpr (PACKED) {
+            fresh[h] = false;
+            if (ok[h]) {
+              const uint32_t kx = ld_rlx_u32(cluster + x[h]);
+              const uint32_t kr = kx >> 24;
+              if (kr < uint32_t(r)) {  // claimed in an earlier round: final
+                cut[h] = emit && (kx & kPackMask) != sc[h] && (kr != uint32_t(r - 1) || sf[h] < x[h]);
+              } else {
+                fresh[h] = atomicMin(cluster + x[h], (uint32_t(r) << 24) | sc[h]) == kFreeCluster;
+              }
+            }
+          } else {
+            fresh[h] = ok[h] && claim_rel(cluster, croud, x[h], r, sc[h]);
+          }
         }
         bq.push(fresh[0], x[0], qout, cout);
         bq.push(fresh[1], x[1], qout, cout);
+        if (emit) {
+          pq.push(cut[0], sf[0], x[0], cut_u, cut_v, cut_count);
+          pq.push(cut[1], sf[1], x[1], cut_u, cut_v, cut_count);
+        }
       }
     }
     if (r <= last_start) {  // centres of bucket r
@@ -905,6 +984,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
       }
     }
     bq.flush(qout, cout);
+    if (emit) pq.flush(cut_u, cut_v, cut_count);
     grid.sync();
     const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(cout);
     if (trace && gtid == 0 && r < max_rounds) trace[r] = unsigned(next);
@@ -1201,6 +1281,7 @@ bool ldd_persistent() {
 bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsigned long long* ctr,
              cudaStream_t st) {
   const int32_t n = int32_t(g.n);
+  w.cut_done = false;
   if (n == 0) return false;
   const float beta = s.ldd_beta > 0 ? float(s.ldd_beta) : 0.2f;
   int32_t* dmax = reinterpret_cast<int32_t*>(ctr + C_SCRATCH1);
@@ -1257,8 +1338,16 @@ bool run_ldd(const gc_csr& g, const gc_spec& s, int32_t* P, SamplerWs& w, unsign
     if (trace) GC_CUDA(cudaMemsetAsync(trace, 0, sizeof(unsigned int) * (kLddMaxRounds + 1), st));
     uint32_t* cszp = csz;
     unsigned long long* ctrp = ctr;
+    // emitting costs per cut edge, the gather it replaces is a fixed pass
+    // over the active rows: emit while the cut share is small (ic ~ beta /
+    // 2 on the 3-D grid: 0.05 / 0.10 / 0.24 at beta 0.1 / 0.2 / 0.5; the
+    // gather won at 0.5)
+    w.cut_done = packed && w.cut_u != nullptr && beta <= 0.3f;
+    int32_t* cutu = w.cut_done ? w.cut_u : nullptr;
+    int32_t* cutv = w.cut_done ? w.cut_v : nullptr;
+    unsigned long long* cutc = w.cut_done ? w.cut_count : nullptr;
     void* args[] = {&off, &tgt, &nn, &clp, &crp, &order, &boff, &dmb, &maxr, &q0, &q1, &ring, &insp, &mins, &Pp,
-                    &rounds_out, &trace, &cszp, &ctrp};
+                    &rounds_out, &trace, &cszp, &ctrp, &cutu, &cutv, &cutc};
     const void* kfn = packed ? reinterpret_cast<const void*>(k_ldd_persist<true>)
                              : reinterpret_cast<const void*>(k_ldd_persist<false>);
     GC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(num_sms() * per_sm), dim3(kTB), args, 0, st));

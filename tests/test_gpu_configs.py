@@ -227,3 +227,43 @@ def test_finish_phase_rejects_out_of_range_labels():
     from paper_2008_11839_b200 import MalformedInputError, finish_phase, path_graph
     with pytest.raises(MalformedInputError):
         finish_phase(path_graph(4), [0, 0, 9, 3], l_max=0, spec=parse_spec("none+async+halve"))
+
+
+_CUT_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+from test_gpu_configs import _grid
+from paper_2008_11839_b200 import Graph, parse_spec, static_connectivity_device
+out = {}
+for side, permuted in [(64, False), (64, True)]:
+    n, off, tgt, ref, comps = _grid(side, permuted)
+    g = Graph(n, off, tgt)
+    for text in ["ldd+sv", "ldd+lt_prs", "ldd+lt_crfa", "ldd(0.1)+stergiou"]:
+        labels, st = static_connectivity_device(g, parse_spec(text))
+        out[f"{side}{permuted}{text}"] = [st.rounds, st.edge_inspections.get("finish", 0),
+                                          st.component_count, int(labels.sum().item())]
+print(json.dumps(out))
+"""
+
+
+def test_config3_ldd_cut_edges_match_gather():
+    """The labels-only rounds finish after LDD takes its working COO from the
+    sampler's cut edges (GC_LDD_CUT); the rounds, counted finish inspections,
+    components and labels must equal the gather path's (GC_LDD_CUT=0), run in
+    a second process because the knob is read once."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = []
+    for cut in ("1", "0"):
+        env = dict(os.environ, GC_LDD_CUT=cut)
+        r = subprocess.run([sys.executable, "-c", _CUT_SCRIPT, root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
