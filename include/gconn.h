@@ -226,7 +226,9 @@ int gc_shard_finish(const gc_csr* g, const gc_spec* spec, int64_t row_lo,
  *   gc_shard_summary: compress parent in place and describe one class as an
  *     n-bit bitmap giant_bits[(n+31)/32] with its label (*giant_label,
  *     device): the class of *giant_hint (device vertex id) or, with a NULL
- *     hint, the probe's most frequent label.  With out_u/out_v (capacity n)
+ *     hint, the probe's most frequent label.  With a hint (round B) parent
+ *     must already be compressed, as gc_shard_absorb leaves it: the compress
+ *     pass is skipped.  With out_u/out_v (capacity n)
  *     every other non-singleton vertex v also emits (v, root(v)), counted in
  *     *out_count (device); NULL pair outputs give the bitmap alone.
  *   gc_shard_absorb (round A): union every vertex of every rank's bitmap

@@ -473,7 +473,11 @@ int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint, uint
       GC_CUDA(cudaMemsetAsync(giant_label, 0, sizeof(int64_t), st));
       return;
     }
-    (k_compress<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
+    // round B (a hint) follows gc_shard_absorb, which leaves every vertex
+    // pointing at its root: the compress pass would read 4n bytes plus one
+    // hop per vertex for nothing (P = 8 model at s27: 0.2 ms per rank)
+    if (!giant_hint)
+      (k_compress<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
     if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr, 1), count_launch());
     (k_pick_class<<<1, 1, 0, st>>>(parent, giant_hint, ctr, giant_label), count_launch());
     // a null pair output summarises the bitmap class only (round A)

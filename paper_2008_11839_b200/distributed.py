@@ -608,19 +608,26 @@ def _exchange_and_merge(parent, mu, mv, spec, engine, group, rank):
     Root-based rules exchange real merging edges (a forest); the others
     (Rem with the atomic splice) exchange root transitions (v, P[v]), which
     carry the partition but are not graph edges."""
+    torch = _torch()
     fu, fv = [mu], [mv]
     total = 0
     record = spec.is_root_based()
+    # the foreign lists are unioned as one batch (one launch and one range
+    # check instead of one per rank)
+    gu, gv = [], []
     for r, (ou, ov) in enumerate(all_gather_pairs(mu, mv, group)):
         total += int(ou.numel())
         if r != rank and ou.numel():
-            if record:
-                au, av = engine.union_list(parent, ou.to(parent.device), ov.to(parent.device), spec)
-                fu.append(au)
-                fv.append(av)
-            else:
-                engine.union_pairs(parent, ou.to(parent.device), ov.to(parent.device), spec)
-    torch = _torch()
+            gu.append(ou.to(parent.device))
+            gv.append(ov.to(parent.device))
+    if gu:
+        ou, ov = torch.cat(gu), torch.cat(gv)
+        if record:
+            au, av = engine.union_list(parent, ou, ov, spec)
+            fu.append(au)
+            fv.append(av)
+        else:
+            engine.union_pairs(parent, ou, ov, spec)
     return torch.cat(fu), torch.cat(fv), total
 
 

@@ -88,9 +88,10 @@ def run(P, scale, g, shards, check):
     for r in range(P):
         T = timers[r]
         parent = states[r][0]
-        for q in range(P):
-            if q != r and fin[q][0].numel():
-                T("merge2", lambda: eng.union_pairs(parent, fin[q][0], fin[q][1], spec))
+        fq = [fin[q] for q in range(P) if q != r and fin[q][0].numel()]
+        if fq:  # the foreign lists as one batch, as _exchange_and_merge does
+            ou, ov = torch.cat([f[0] for f in fq]), torch.cat([f[1] for f in fq])
+            T("merge2", lambda: eng.union_pairs(parent, ou, ov, spec))
         lab = T("finalize", lambda: eng.finalize(parent, inplace=True))
         if r == 0:
             labels = lab
