@@ -78,7 +78,11 @@ class LiveState:
     ``__cuda_array_interface__`` (``torch.as_tensor(state, device="cuda")``
     aliases it) and converts to a host int64 array only when read as numpy
     (``np.asarray(state)``, indexing).  Valid during the callback; later
-    batches mutate it."""
+    batches mutate it.  Writes through the view change the live parent
+    array, as in the reference; a write that splits a component (rather
+    than merging) would leave the async rules' giant-filter bitmap marking
+    vertices as connected that no longer are — run such a stream with
+    ``GC_INCR_GIANT=0``."""
 
     def __init__(self, ptr: int, slots: int, owner):
         self._ptr = int(ptr or 0)
