@@ -42,8 +42,12 @@ __global__ void k_pick_class(const int32_t* P, const int32_t* hint, unsigned lon
 // bitmap words + block-aggregated remainder pairs (P compressed).  Four
 // vertices per thread (one 16-byte load): a warp covers 128 vertices = four
 // bitmap words, each OR-reduced over the eight lanes that hold it.
+// COMPRESS: the labels are first resolved to their roots and written back
+// (the compress pass fused in: round A's parents come straight from the
+// sampler; the class was picked by the probe, which walks to roots itself)
+template <bool COMPRESS>
 __global__ void __launch_bounds__(kEwBlock)
-k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ctr, uint32_t* bits,
+k_summary(int32_t* __restrict__ P, int32_t n, const unsigned long long* ctr, uint32_t* bits,
           int32_t* out_u, int32_t* out_v, unsigned long long* out_count) {
   constexpr int kWarps = kEwBlock / 32;
   __shared__ unsigned warp_n[kWarps];
@@ -64,6 +68,27 @@ k_summary(const int32_t* __restrict__ P, int32_t n, const unsigned long long* ct
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) lab[k] = v0 + k < n ? P[v0 + k] : g;
+    }
+    if constexpr (COMPRESS) {
+      // first hops of the four walks together; only labels that moved walk on
+      int32_t hop[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) hop[k] = (v0 + k < n && lab[k] != int32_t(v0 + k)) ? ld_weak(P + lab[k]) : lab[k];
+      bool dirty = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (v0 + k >= n || hop[k] == lab[k]) continue;
+        int32_t r = hop[k], y;
+        while ((y = ld_weak(P + r)) != r) r = y;
+        lab[k] = r;
+        dirty = true;
+      }
+      if (dirty) {
+        if (v0 + 3 < n) reinterpret_cast<int4*>(P)[q] = make_int4(lab[0], lab[1], lab[2], lab[3]);
+        else
+          for (int k = 0; k < 4; ++k)
+            if (v0 + k < n) P[v0 + k] = lab[k];
+      }
     }
     unsigned nib = 0, pairs = 0;
 #pragma unroll
@@ -476,13 +501,19 @@ int gc_shard_summary(int32_t* parent, int64_t n, const int32_t* giant_hint, uint
     // round B (a hint) follows gc_shard_absorb, which leaves every vertex
     // pointing at its root: the compress pass would read 4n bytes plus one
     // hop per vertex for nothing (P = 8 model at s27: 0.2 ms per rank)
-    if (!giant_hint)
-      (k_compress<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn), count_launch());
+    // the probe walks to roots itself, so it runs before the compress, which
+    // is fused into the summary pass (round A); round B's parents are
+    // compressed already
     if (!giant_hint) (k_mode_probe<<<1, 1024, 0, st>>>(parent, nn, ctr, 1), count_launch());
     (k_pick_class<<<1, 1, 0, st>>>(parent, giant_hint, ctr, giant_label), count_launch());
     // a null pair output summarises the bitmap class only (round A)
-    (k_summary<<<grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8), kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v,
-                                                              out_count), count_launch());
+    const int gs = grid_for((int64_t(nn) + 3) / 4, kEwBlock, 8);
+    if (giant_hint)
+      (k_summary<false><<<gs, kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v, out_count),
+       count_launch());
+    else
+      (k_summary<true><<<gs, kEwBlock, 0, st>>>(parent, nn, ctr, giant_bits, out_u, out_v, out_count),
+       count_launch());
     GC_CHECK_LAUNCH();
   });
 }
