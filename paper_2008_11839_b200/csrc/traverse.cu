@@ -868,18 +868,20 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
   last_start = last_start < 0 ? 0 : (last_start > max_rounds ? max_rounds : last_start);
   unsigned long long my_insp = 0;
   const uint64_t pol = evict_first_policy();
-  int32_t r = 0;
-  for (;; ++r) {
+  // One round (frontier expansion + the round's centres) over the warps /
+  // threads [w0, w0 + nw) / [t0, t0 + nt); ends with the block queues
+  // flushed.  The caller synchronises the participants.
+  auto round = [&](int32_t r, int64_t w0, int64_t nw, int64_t t0, int64_t nt) -> unsigned long long* {
     int32_t* qin = (r & 1) ? q0 : q1;  // round r reads the queue round r-1 wrote
     int32_t* qout = (r & 1) ? q1 : q0;
     unsigned long long* cout = ring + (r + 1) % 3;
-    if (gtid == 0) ring[(r + 2) % 3] = 0;  // read by nobody this round; written next round
+    if (t0 == 0) ring[(r + 2) % 3] = 0;  // read by nobody this round; written next round
     const int64_t count = r > 0 ? int64_t(*reinterpret_cast<volatile unsigned long long*>(ring + r % 3)) : 0;
     // vpw frontier vertices per warp step: fewer than 32 on narrow rounds so
     // every warp of the grid takes part (see bfs_td_level)
-    const int64_t vpw64 = (count + nwarps - 1) / nwarps;
+    const int64_t vpw64 = (count + nw - 1) / nw;
     const int vpw = int(vpw64 < 1 ? 1 : (vpw64 > 32 ? 32 : vpw64));
-    for (int64_t wb = gwarp * vpw; wb < count; wb += nwarps * vpw) {
+    for (int64_t wb = w0 * vpw; wb < count; wb += nw * vpw) {
       const int64_t i = wb + lane;
       uint32_t c = 0;
       int64_t b = 0;
@@ -971,7 +973,7 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     }
     if (r <= last_start) {  // centres of bucket r
       const int64_t lo = boff[r], hi = boff[r + 1];
-      for (int64_t b0 = lo + int64_t(blockIdx.x) * kTB; b0 < hi; b0 += gthreads) {
+      for (int64_t b0 = lo + (t0 - int64_t(threadIdx.x)); b0 < hi; b0 += nt) {
         const int64_t i = b0 + threadIdx.x;
         int32_t v = 0;
         bool fresh = false;
@@ -985,10 +987,21 @@ k_ldd_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, 
     }
     bq.flush(qout, cout);
     if (emit) pq.flush(cut_u, cut_v, cut_count);
+    return cout;
+  };
+  int32_t r = 0;
+  // every claim is a fresh vertex: once all n are claimed the remaining
+  // start buckets hold only claimed vertices and their rounds would claim
+  // nothing (the trace of the permuted 256^3 grid shows ~18 such trailing
+  // rounds, each a grid barrier)
+  unsigned long long claimed = 0;
+  for (;; ++r) {
+    unsigned long long* cout = round(r, gwarp, nwarps, gtid, gthreads);
     grid.sync();
     const unsigned long long next = *reinterpret_cast<volatile unsigned long long*>(cout);
+    claimed += next;
     if (trace && gtid == 0 && r < max_rounds) trace[r] = unsigned(next);
-    if (next == 0 && r >= last_start) break;
+    if ((next == 0 && r >= last_start) || (next == 0 && claimed >= static_cast<unsigned long long>(n))) break;
   }
   block_add<kTB>(insp, my_insp);
   if (gtid == 0 && rounds_out) *rounds_out = (unsigned long long)(r + 1);
