@@ -570,7 +570,16 @@ __global__ void k_ldd_delta_max(int32_t n, uint64_t seed, float beta, int32_t* d
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
     mx = fmaxf(mx, ldd_delta(seed, v, beta));
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(dmax_bits, __float_as_int(mx));  // positive floats order as ints
+  // one atomic per block (one per warp serialised ~75K atomics on the one
+  // word: 53 us at 2^24)
+  __shared__ float wmax[32];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 0.f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) b = fmaxf(b, wmax[w]);
+    atomicMax(dmax_bits, __float_as_int(b));  // positive floats order as ints
+  }
 }
 
 constexpr int kBuckets = kLddMaxRounds + 1;
