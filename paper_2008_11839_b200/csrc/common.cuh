@@ -58,6 +58,14 @@ __device__ __forceinline__ void red_or_bits(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ bool gbit(uint32_t w, int32_t x) { return (w >> (x & 31)) & 1u; }
 
+// atomicMin on a word many warps update (a running minimum): skip the atomic
+// when a plain read already shows a value <= v (the word only decreases, so
+// a stale read is never below the true value) — tens of thousands of
+// per-warp atomics on one word serialise at its L2 slice
+__device__ __forceinline__ void atomic_min_if_lower(int32_t* p, int32_t v) {
+  if (v < ld_weak(p)) atomicMin(p, v);
+}
+
 // fire-and-forget min (RED.MIN): the result is not needed by the caller
 __device__ __forceinline__ void red_min(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

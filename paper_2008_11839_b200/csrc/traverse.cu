@@ -213,7 +213,7 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
   bq.flush(qn, nstat);
   if (insp) block_add<kTB>(insp, degs);
   my_min = warp_min(my_min);
-  if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+  if (lane == 0 && my_min != INT_MAX) atomic_min_if_lower(minv, my_min);
 }
 
 // Narrow top-down levels in ONE persistent cooperative launch (SURVEY hard
@@ -380,7 +380,7 @@ k_bfs_bu(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32
   block_add<kTB>(nstat, cnt);
   block_add<kTB>(nstat + 1, degs);
   my_min = warp_min(my_min);
-  if (lane == 0 && my_min != INT_MAX) atomicMin(minv, my_min);
+  if (lane == 0 && my_min != INT_MAX) atomic_min_if_lower(minv, my_min);
 }
 
 // narrow levels: the visited bitmap takes the claimed queue's vertices
@@ -439,7 +439,7 @@ k_bits_to_queue(uint32_t* bits, int32_t n, int32_t* q, unsigned long long* qc, i
     if (minv) {  // the smallest vertex reached (first set bit of the block's words)
       int32_t lo = word ? int32_t(wi * 32 + __ffs(word) - 1) : INT_MAX;
       lo = warp_min(lo);
-      if ((threadIdx.x & 31) == 0 && lo != INT_MAX) atomicMin(minv, lo);
+      if ((threadIdx.x & 31) == 0 && lo != INT_MAX) atomic_min_if_lower(minv, lo);
     }
     while (word) {
       const int bit = __ffs(word) - 1;
