@@ -45,36 +45,56 @@ __global__ void k_dbfs_init(uint32_t* F, uint32_t* V, uint32_t* par, int64_t s) 
 }
 
 // marks: unvisited neighbours of the block's frontier rows (red.or, no
-// result needed); a warp walks a row with more than 32 entries together
+// result needed).  A warp scans 32 frontier words per step and walks only
+// the words with set bits (narrow top-down levels touch a sliver of the
+// rows: scanning every row's bit cost ~0.3 ms per level at 2^27); a row
+// with more than 32 entries is walked by the whole warp.
+__device__ __forceinline__ uint32_t range_mask(int64_t w, int64_t lo, int64_t hi) {
+  uint32_t m = ~0u;
+  if (w == (lo >> 5)) m &= ~0u << (lo & 31);
+  if (w == ((hi - 1) >> 5) && (hi & 31)) m &= (1u << (hi & 31)) - 1u;
+  return m;
+}
+
 __global__ void __launch_bounds__(kDB)
 k_dbfs_marks(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int64_t lo, int64_t hi,
              const uint32_t* __restrict__ F, const uint32_t* __restrict__ V, uint32_t* M) {
   const int lane = threadIdx.x & 31;
-  const int64_t stride = int64_t(gridDim.x) * kDB;
-  for (int64_t x0 = lo + int64_t(blockIdx.x) * kDB; x0 < hi; x0 += stride) {
-    const int64_t f = x0 + threadIdx.x;
-    int64_t b = 0, d = 0;
-    if (f < hi && bit(F, f)) {
-      b = off[f];
-      d = off[f + 1] - b;
-    }
-    const bool big = d > 32;
-    if (!big)
-      for (int64_t j = 0; j < d; ++j) {
-        const int32_t x = tgt[b + j];
-        if (!bit(V, x))
-          asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(M + (x >> 5)), "r"(1u << (x & 31)) : "memory");
+  const int64_t w_lo = lo >> 5, w_hi = (hi + 31) >> 5;
+  const int64_t gw = (int64_t(blockIdx.x) * kDB + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * kDB) >> 5;
+  for (int64_t w0 = w_lo + gw * 32; w0 < w_hi; w0 += nw * 32) {
+    const int64_t wl = w0 + lane;
+    const uint32_t fw = wl < w_hi ? __ldg(F + wl) & range_mask(wl, lo, hi) : 0u;
+    unsigned todo = __ballot_sync(0xffffffffu, fw != 0u);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, fw, src);
+      const int64_t f = (w0 + src) * 32 + lane;
+      int64_t b = 0, d = 0;
+      if ((word >> lane) & 1u) {
+        b = off[f];
+        d = off[f + 1] - b;
       }
-    unsigned mask = __ballot_sync(0xffffffffu, big);
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const int64_t bb = __shfl_sync(0xffffffffu, b, src);
-      const int64_t dd = __shfl_sync(0xffffffffu, d, src);
-      for (int64_t j = lane; j < dd; j += 32) {
-        const int32_t x = tgt[bb + j];
-        if (!bit(V, x))
-          asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(M + (x >> 5)), "r"(1u << (x & 31)) : "memory");
+      const bool big = d > 32;
+      if (!big)
+        for (int64_t j = 0; j < d; ++j) {
+          const int32_t x = tgt[b + j];
+          if (!bit(V, x))
+            asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(M + (x >> 5)), "r"(1u << (x & 31)) : "memory");
+        }
+      unsigned mask = __ballot_sync(0xffffffffu, big);
+      while (mask) {
+        const int s2 = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int64_t bb = __shfl_sync(0xffffffffu, b, s2);
+        const int64_t dd = __shfl_sync(0xffffffffu, d, s2);
+        for (int64_t j = lane; j < dd; j += 32) {
+          const int32_t x = tgt[bb + j];
+          if (!bit(V, x))
+            asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(M + (x >> 5)), "r"(1u << (x & 31)) : "memory");
+        }
       }
     }
   }
@@ -115,37 +135,46 @@ __global__ void k_dbfs_merge(const int32_t* ids, int64_t k, int64_t n, uint32_t*
   }
 }
 
-// claim: a warp owns one 32-vertex word of the block's rows; an unvisited
-// vertex that is marked (top-down) or any unvisited vertex (bottom-up) takes
-// the first frontier vertex of its row
+// claim: a warp scans 32 words of the block's rows per step and walks the
+// words holding candidates — unvisited vertices that are marked (top-down)
+// or any unvisited vertex (bottom-up); a candidate takes the first frontier
+// vertex of its row (the reference's smallest-discoverer rule)
 __global__ void __launch_bounds__(kDB)
 k_dbfs_claim(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int64_t lo, int64_t hi,
              const uint32_t* __restrict__ F, const uint32_t* __restrict__ V, const uint32_t* __restrict__ M,
              uint32_t* par, uint32_t* N, unsigned long long* cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t w_lo = lo >> 5, w_hi = (hi + 31) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * kDB) >> 5;
+  const int64_t gw = (int64_t(blockIdx.x) * kDB + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * kDB) >> 5;
   unsigned long long c = 0;
-  for (int64_t w = w_lo + ((int64_t(blockIdx.x) * kDB + threadIdx.x) >> 5); w < w_hi; w += nwarps) {
-    const uint32_t vw = __ldg(V + w);
-    const uint32_t mw = M ? __ldg(M + w) : ~0u;
-    const int64_t x = w * 32 + lane;
-    bool found = false;
-    if (x >= lo && x < hi && !((vw >> lane) & 1u) && ((mw >> lane) & 1u)) {
-      const int64_t b = off[x], e = off[x + 1];
-      for (int64_t j = b; j < e; ++j) {
-        const int32_t t = tgt[j];
-        if (bit(F, t)) {
-          par[x] = uint32_t(t);
-          found = true;
-          break;
+  for (int64_t w0 = w_lo + gw * 32; w0 < w_hi; w0 += nw * 32) {
+    const int64_t wl = w0 + lane;
+    uint32_t cand = 0u;
+    if (wl < w_hi) cand = ~__ldg(V + wl) & (M ? __ldg(M + wl) : ~0u) & range_mask(wl, lo, hi);
+    unsigned todo = __ballot_sync(0xffffffffu, cand != 0u);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, cand, src);
+      const int64_t x = (w0 + src) * 32 + lane;
+      bool found = false;
+      if ((word >> lane) & 1u) {
+        const int64_t b = off[x], e = off[x + 1];
+        for (int64_t j = b; j < e; ++j) {
+          const int32_t t = tgt[j];
+          if (bit(F, t)) {
+            par[x] = uint32_t(t);
+            found = true;
+            break;
+          }
         }
       }
-    }
-    const uint32_t word = __ballot_sync(0xffffffffu, found);
-    if (lane == 0 && word) {
-      N[w] = word;
-      c += __popc(word);
+      const uint32_t got = __ballot_sync(0xffffffffu, found);
+      if (lane == 0 && got) {
+        N[w0 + src] = got;
+        c += __popc(got);
+      }
     }
   }
   block_add<kDB>(cnt, c);
@@ -189,35 +218,45 @@ __global__ void __launch_bounds__(kDB)
 k_dbfs_finish(const int64_t* __restrict__ off, int64_t n, int64_t lo, int64_t hi, const uint32_t* __restrict__ V,
               const uint32_t* __restrict__ par, const int32_t* mn_p, int32_t* P, int32_t* fu, int32_t* fv,
               unsigned long long* fcnt, unsigned long long* insp) {
+  // eight vertices per thread per step and one cursor atomic per block step
+  // (a per-warp atomic on the one cursor serialised ~4M appends at 2^27)
+  constexpr int kJ = 8;
+  using Scan = cub::BlockScan<int, kDB>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long base;
   const int32_t mn = *mn_p;
-  const int lane = threadIdx.x & 31;
   unsigned long long degs = 0;
-  const int64_t stride = int64_t(gridDim.x) * kDB;
-  for (int64_t b0 = int64_t(blockIdx.x) * kDB; b0 < n; b0 += stride) {
-    const int64_t v = b0 + threadIdx.x;
-    bool edge = false;
-    uint32_t p = kNoParent;
-    if (v < n) {
-      const bool r = bit(V, v);
-      P[v] = r ? mn : int32_t(v);
-      if (r && v >= lo && v < hi) {
-        degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
-        p = par[v];
-        edge = p < kNoParent - 1;
+  const int64_t step = int64_t(kDB) * kJ;
+  for (int64_t b0 = int64_t(blockIdx.x) * step; b0 < n; b0 += int64_t(gridDim.x) * step) {
+    uint32_t p[kJ];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int64_t v = b0 + int64_t(j) * kDB + threadIdx.x;
+      p[j] = kNoParent;
+      if (v < n) {
+        const bool r = bit(V, v);
+        P[v] = r ? mn : int32_t(v);
+        if (r && v >= lo && v < hi) {
+          degs += static_cast<unsigned long long>(off[v + 1] - off[v]);
+          p[j] = par[v];
+          c += p[j] < kNoParent - 1;
+        }
       }
     }
-    // warp-aggregated append of the tree edges
-    const unsigned m = __ballot_sync(0xffffffffu, edge);
-    if (m) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(fcnt, static_cast<unsigned long long>(__popc(m)));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (edge) {
-        const unsigned long long i = base + __popc(m & ((1u << lane) - 1u));
-        fu[i] = int32_t(p);
-        fv[i] = int32_t(v);
+    int rank, total;
+    Scan(tmp).ExclusiveSum(c, rank, total);
+    if (threadIdx.x == 0) base = total ? atomicAdd(fcnt, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    unsigned long long i = base + rank;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+      if (p[j] < kNoParent - 1) {
+        fu[i] = int32_t(p[j]);
+        fv[i] = int32_t(b0 + int64_t(j) * kDB + threadIdx.x);
+        ++i;
       }
-    }
+    __syncthreads();
   }
   block_add<kDB>(insp, degs);
 }

@@ -201,6 +201,141 @@ def run_incremental(P, scale, batch, check):
             "exchanged_bytes": comm_bytes, "batch_ms_merges": per_batch}
 
 
+def run_bfs_forest(P, log2n, check):
+    """Config 5 sharded (sharded_two_phase with BFS sampling, spanning
+    forest, bfs+async+halve on uniform 2^log2n, strong scaling: the same
+    graph split over P row blocks), replayed on one GPU.  Per BFS level: each
+    rank's marks / merge / claim / advance timed with CUDA events, the mark
+    lists all-gathered and the next-frontier bitmaps all-reduced (costed at
+    NVLink rate); then each rank's tree edges all-gathered, its finish over
+    its active rows, the merging edges exchanged and unioned, finalise.
+    Step = sum over levels of (max over ranks + collectives) + the same for
+    the later phases."""
+    from paper_2008_11839_b200 import gen_uniform_pairs
+    from paper_2008_11839_b200.distributed import DBFS_ALPHA, DBFS_BETA
+    spec = parse_spec("bfs+async+halve")
+    g = build_csr(gen_uniform_pairs(log2n, 4 << log2n, seed=1, device=True), keep_host=False)
+    n, m = g.n, g.m
+    shards = [shard_graph(g, lo, hi) for lo, hi in shard_bounds(g._d_off, P, "edges")]
+    eng = GpuEngine()
+    words_bytes = ((n + 31) // 32) * 4
+
+    def ev(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        e1.synchronize()
+        return out, e0.elapsed_time(e1)
+
+    # BFS source: highest-degree probe (sampling.py:130-132), global degrees
+    probes = np.unique(np.random.default_rng(spec.seed).integers(0, n, size=spec.bfs_probes))
+    deg = (g._d_off[torch.as_tensor(probes + 1, device="cuda")] - g._d_off[torch.as_tensor(probes, device="cuda")])
+    src = int(probes[int(torch.argmax(deg).item())])
+    sts = [eng.dbfs_init(n, src) for _ in range(P)]
+    torch.cuda.synchronize()
+    total_ms, comm_ms = 0.0, 0.0
+    nf, reached, bottom_up, levels = 1, 1, False, 0
+    while nf:
+        bottom_up = nf * DBFS_ALPHA > n - reached if not bottom_up else nf >= n // DBFS_BETA
+        t = [0.0] * P
+        nxt = []
+        if bottom_up:
+            for r in range(P):
+                out, dt = ev(lambda: eng.dbfs_claim(shards[r], sts[r], marks=False))
+                t[r] += dt
+                nxt.append(out)
+        else:
+            ids = []
+            for r in range(P):
+                out, dt = ev(lambda: eng.dbfs_marks(shards[r], sts[r]).clone())
+                t[r] += dt
+                ids.append(out)
+            sent = sum(int(x.numel()) for x in ids)
+            comm_ms += sent * 4 / NVLINK * 1e3 if P > 1 else 0.0
+            for r in range(P):
+                for q in range(P):
+                    if q != r and ids[q].numel():
+                        _, dt = ev(lambda: eng.dbfs_merge_marks(sts[r], ids[q]))
+                        t[r] += dt
+                out, dt = ev(lambda: eng.dbfs_claim(shards[r], sts[r], marks=True))
+                t[r] += dt
+                nxt.append(out)
+        # all-reduce of the disjoint next-frontier bitmaps (SUM == OR)
+        acc = nxt[0].clone()
+        for q in range(1, P):
+            acc += nxt[q]
+        for r in range(P):
+            nxt[r].copy_(acc)
+        if P > 1:
+            comm_ms += 2 * (P - 1) / P * words_bytes / NVLINK * 1e3
+        nfs = []
+        for r in range(P):
+            out, dt = ev(lambda: eng.dbfs_advance(sts[r]))
+            t[r] += dt
+            nfs.append(out)
+        nf = nfs[0]
+        reached += nf
+        levels += 1
+        total_ms += max(t)
+    fin = []
+    t = [0.0] * P
+    for r in range(P):
+        out, dt = ev(lambda: eng.dbfs_finish(shards[r], sts[r]))
+        t[r] += dt
+        fin.append(out)
+    total_ms += max(t)
+    tree_pairs = sum(int(f[1].numel()) for f in fin)
+    if P > 1:
+        comm_ms += tree_pairs * 8 * (P - 1) / P / NVLINK * 1e3
+    parents = [f[0].contiguous() for f in fin]
+    del sts
+    # finish over each rank's active rows, merge exchange, finalise
+    t = [0.0] * P
+    merges = []
+    for r in range(P):
+        out, dt = ev(lambda: eng.shard_finish(shards[r], spec, parents[r]))
+        t[r] += dt
+        merges.append(out)
+    mbytes = sum(int(x[0].numel()) for x in merges) * 8
+    if P > 1:
+        comm_ms += mbytes / NVLINK * 1e3
+    labels = None
+    for r in range(P):
+        fq = [merges[q] for q in range(P) if q != r and merges[q][0].numel()]
+        if fq:
+            ou, ov = torch.cat([f[0] for f in fq]), torch.cat([f[1] for f in fq])
+            _, dt = ev(lambda: eng.union_list(parents[r], ou, ov, spec))
+            t[r] += dt
+        lab, dt = ev(lambda: eng.finalize(parents[r], inplace=True))
+        t[r] += dt
+        if r == 0:
+            labels = lab
+    total_ms += max(t)
+    ok = None
+    if check:
+        import oracle
+        ref, _ = oracle.components(n, g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy())
+        ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref))
+    step = total_ms + comm_ms
+    return {"mode": "bfs_forest", "ranks": P, "log2n": log2n, "n": n, "m_directed": m, "labels_ok": ok,
+            "levels": levels, "device_ms": total_ms, "comm_ms_model": comm_ms, "step_ms_model": step,
+            "edges_per_s_model": (m / 2) / (step / 1e3), "tree_pairs": tree_pairs}
+
+
+def main_bfs():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bfs", action="store_true")
+    ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--log2n", type=int, default=27)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    for P in (int(x) for x in a.ranks.split(",")):
+        run_bfs_forest(P, a.log2n, False)  # warm-up
+        print(json.dumps(run_bfs_forest(P, a.log2n, a.check)), flush=True)
+        torch.cuda.empty_cache()
+
+
 def main_incremental():
     ap = argparse.ArgumentParser()
     ap.add_argument("--incremental", action="store_true")
@@ -218,5 +353,7 @@ def main_incremental():
 if __name__ == "__main__":
     if "--incremental" in sys.argv:
         main_incremental()
+    elif "--bfs" in sys.argv:
+        main_bfs()
     else:
         main()
