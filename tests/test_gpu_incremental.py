@@ -153,3 +153,12 @@ def test_giant_filter_stream(text):
     bits = inc.batch(torch.from_numpy(mix_u[order]).cuda(), torch.from_numpy(mix_v[order]).cuda(),
                      isq[order]).numpy()
     assert np.array_equal(bits, isq[order] & np.concatenate([np.zeros(3000, bool), exp[:3000]])[order])
+    # compact mode with a malformed endpoint: the compaction drops it and
+    # raises the sticky flag; the batch's good inserts still apply
+    from paper_2008_11839_b200 import MalformedInputError
+    bad_u = torch.from_numpy(np.concatenate([ue[:9000, 0], [g.n + 5]]).astype(np.int32)).cuda()
+    bad_v = torch.from_numpy(np.concatenate([ue[:9000, 1], [0]]).astype(np.int32)).cuda()
+    with pytest.raises(MalformedInputError):
+        inc.insert(bad_u, bad_v)
+    q = inc.query(bad_u[:100], bad_v[:100]).numpy()
+    assert q.all()
