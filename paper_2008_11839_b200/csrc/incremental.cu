@@ -282,15 +282,16 @@ k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, 
   unsigned long long* ocount = reinterpret_cast<unsigned long long*>(gstate + 2);
   const int32_t anc = gstate[0];
   const bool on = anc >= 0;
+  // the anchor is connected to itself: its bit seeds the marking (the other
+  // blocks may test it before it lands, which only keeps an insert)
+  if (on && blockIdx.x == 0 && threadIdx.x == 0)
+    red_or_bits(const_cast<uint32_t*>(gbits) + (anc >> 5), 1u << (anc & 31));
   if (!on || !gstate[4]) {  // pass the batch through: the union reads the caller's arrays
     if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<unsigned long long*>(gstate + 2) = ~0ull;
     return;
   }
   const bool vec = ((reinterpret_cast<uintptr_t>(us) | reinterpret_cast<uintptr_t>(vs)) & 15) == 0;
   if (threadIdx.x == 0) qn = 0;
-  // the anchor is connected to itself: its bit seeds the marking (the other
-  // blocks may test it before it lands, which only keeps an insert)
-  if (on && blockIdx.x == 0 && threadIdx.x == 0) red_or_bits(const_cast<uint32_t*>(gbits) + (anc >> 5), 1u << (anc & 31));
   const int64_t per = ((len + gridDim.x - 1) / gridDim.x + kStep - 1) / kStep * kStep;
   const int64_t lo = int64_t(blockIdx.x) * per;
   const int64_t hi = lo + per < len ? lo + per : len;
@@ -655,9 +656,8 @@ int gc_incr_create(int64_t capacity, const gc_spec* spec, void* stream, gc_incr*
         GC_CUDA(cudaMalloc(&h->aux, (capacity > 0 ? capacity : 1) * 4));
         fill(h->aux, capacity, spec->finish == GC_FINISH_HOOKS ? int32_t(capacity) : 0, h->st);
       }
-      // the giant filter rides on the lock-step async kernel (GC_COO_MLP > 0)
-      if (spec->finish == GC_FINISH_ASYNC && spec->find != GC_FIND_COMPRESS && coo_mlp() > 0 && capacity > 0 &&
-          giant_filter_on()) {
+      // the giant filter: union-find rules whose roots are component minima
+      if (uf && spec->finish != GC_FINISH_JTB && capacity > 0 && giant_filter_on()) {
         const int64_t words = (capacity + 31) / 32;
         GC_CUDA(cudaMalloc(&h->gbits, words * 4));
         GC_CUDA(cudaMalloc(&h->gstate, 32));

@@ -104,17 +104,49 @@ k_union_csr_edges(UFState s, const int64_t* __restrict__ off, const int32_t* __r
   }
 }
 
-template <class R>
+template <class R, bool GIANT>
 __global__ void __launch_bounds__(256)
 k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
-            const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad) {
+            const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad,
+            const unsigned long long* kdev, GiantPass alt) {
+  // giant filter (GIANT, incremental handles of the non-async rules): as in
+  // the lock-step async kernel, *kdev is the compaction's survivor count
+  // (endpoints carry bit 31 = "giant bit set") or ~0 (the caller's batch);
+  // these rules do not expose the union's root, so an endpoint is marked
+  // only when the other one already carried its bit (the marks spread from
+  // the anchor along the inserted edges)
+  bool flags = false;
+  if (GIANT && kdev) {
+    const unsigned long long c = *kdev;
+    if (c == ~0ull) {
+      us = alt.us;
+      vs = alt.vs;
+      skip = alt.skip;
+      k = alt.k;
+    } else {
+      k = min(k, int64_t(c));
+      flags = true;
+    }
+  }
+  const int32_t anc = GIANT && s.gbits ? ld_acq(s.ganchor) : -1;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k; i += stride) {
     if (skip && skip[i]) continue;
-    const int32_t u = ldg32(us + i), v = ldg32(vs + i);
+    int32_t u = ldg32(us + i), v = ldg32(vs + i);
+    unsigned need = 0;  // bit 0 / 1: u / v lacks its giant bit
+    if (GIANT && flags) {
+      need = (u < 0 ? 0u : 1u) | (v < 0 ? 0u : 2u);
+      u &= 0x7fffffff;
+      v &= 0x7fffffff;
+    }
     if (bad && (uint32_t(u) >= uint32_t(s.n) || uint32_t(v) >= uint32_t(s.n))) {
       atomicOr(bad, 1u);  // malformed pair: never touches the parent array
       continue;
+    }
+    if (GIANT && anc >= 0 && !flags) {
+      const bool bu = gbit(ld_bits(s.gbits + (u >> 5)), u), bv = gbit(ld_bits(s.gbits + (v >> 5)), v);
+      if (bu && bv) continue;  // both connected to the anchor already
+      need = (bu ? 0u : 1u) | (bv ? 0u : 2u);
     }
     if (sentinel >= 0) {
       // ensure_init (driver.py:620-625) fused into the insert: every parent
@@ -134,6 +166,10 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
         pv = o == sentinel ? v : o;
       }
       R::unite_known(s, u, v, pu, pv);
+      if (GIANT && anc >= 0) {
+        if (need == 1u) red_or_bits(s.gbits + (u >> 5), 1u << (u & 31));
+        else if (need == 2u) red_or_bits(s.gbits + (v >> 5), 1u << (v & 31));
+      }
       continue;
     }
     R::unite(s, u, v);
@@ -551,9 +587,9 @@ struct CooLaunch {
     if (a.k <= 0) return;
     UFState s{a.P, a.H, a.L, a.R, a.fu, a.fv, a.n, a.lu, a.lv, a.lcount};
     s.weak = a.init_sentinel < 0;
-    // the giant filter: the lock-step async kernel (roots are component
-    // minima and known when a union ends)
-    if (a.gbits && R::kUnion == GC_FINISH_ASYNC) {
+    // the giant filter (incremental handles of the non-JTB rules: roots
+    // are component minima)
+    if (a.gbits && R::kUnion != GC_FINISH_JTB) {
       s.gbits = a.gbits;
       s.ganchor = a.ganchor;
     }
@@ -569,8 +605,12 @@ struct CooLaunch {
     int64_t blocks = (a.k + 255) / 256;
     const int64_t cap = int64_t(num_sms()) * 8 * 16;
     if (blocks > cap) blocks = cap;
-    (k_union_coo<R><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel, a.bad),
-     ::gc::count_launch());
+    if (s.gbits)
+      (k_union_coo<R, true><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel, a.bad,
+                                                         a.kdev, a.alt), ::gc::count_launch());
+    else
+      (k_union_coo<R, false><<<int(blocks), 256, 0, st>>>(s, a.us, a.vs, a.k, a.skip, a.init_sentinel, a.bad,
+                                                          nullptr, a.alt), ::gc::count_launch());
     GC_CHECK_LAUNCH();
   }
 };
