@@ -80,7 +80,7 @@ class LiveState:
     (``np.asarray(state)``, indexing).  Valid during the callback; later
     batches mutate it.  Writes through the view change the live parent
     array, as in the reference; a write that splits a component (rather
-    than merging) would leave the async rules' giant-filter bitmap marking
+    than merging) would leave the union-find rules' giant-filter bitmap marking
     vertices as connected that no longer are — run such a stream with
     ``GC_INCR_GIANT=0``."""
 
