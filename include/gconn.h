@@ -262,7 +262,8 @@ int gc_shard_join(int32_t* parent, int64_t n, const uint32_t* bits,
  *   top-down: gc_dbfs_marks (unvisited neighbours of the block's frontier
  *     rows: marks bitmap + ascending id list out_ids, capacity n, count in
  *     *out_count, device) -> all-gather the id lists -> gc_dbfs_merge_marks
- *     for each foreign list -> gc_dbfs_claim(marks);
+ *     for each foreign list -> gc_dbfs_claim(marks) (gc_dbfs_merge_claim:
+ *     both in one call, the foreign lists concatenated);
  *   bottom-up: gc_dbfs_claim(marks = NULL).
  * gc_dbfs_claim: every unvisited (marked) vertex of the block takes the
  *   first frontier vertex of its ascending row as parent (the reference's
@@ -287,6 +288,11 @@ int gc_dbfs_claim(const gc_csr* g, int64_t row_lo, int64_t row_hi,
                   const uint32_t* frontier, const uint32_t* visited,
                   const uint32_t* marks, uint32_t* parent, uint32_t* next,
                   unsigned long long* count, void* stream);
+int gc_dbfs_merge_claim(const gc_csr* g, int64_t row_lo, int64_t row_hi,
+                        const uint32_t* frontier, const uint32_t* visited, uint32_t* marks,
+                        const int32_t* ids, int64_t k, unsigned int* bad,
+                        uint32_t* parent, uint32_t* next, unsigned long long* count,
+                        void* stream);
 int gc_dbfs_advance(int64_t n, uint32_t* visited, uint32_t* frontier,
                     const uint32_t* next, unsigned long long* count, void* stream);
 int gc_dbfs_finish(const gc_csr* g, int64_t row_lo, int64_t row_hi,

@@ -102,6 +102,8 @@ _SIGNATURES = {
     "gc_dbfs_marks": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "gc_dbfs_merge_marks": (C.c_int, [_I64, _VP, _I64, _VP, _VP, _VP]),
     "gc_dbfs_claim": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "gc_dbfs_merge_claim": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
+                                      _VP]),
     "gc_dbfs_advance": (C.c_int, [_I64, _VP, _VP, _VP, _VP, _VP]),
     "gc_dbfs_finish": (C.c_int, [C.POINTER(Csr), _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ,
                                  _VP]),

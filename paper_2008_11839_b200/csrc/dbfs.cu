@@ -339,6 +339,14 @@ int gc_dbfs_claim(const gc_csr* g, int64_t row_lo, int64_t row_hi, const uint32_
   });
 }
 
+int gc_dbfs_merge_claim(const gc_csr* g, int64_t row_lo, int64_t row_hi, const uint32_t* frontier,
+                        const uint32_t* visited, uint32_t* marks, const int32_t* ids, int64_t k, unsigned int* bad,
+                        uint32_t* parent, uint32_t* next, unsigned long long* count, void* stream) {
+  const int rc = gc_dbfs_merge_marks(g ? g->n : 0, ids, k, marks, bad, stream);
+  if (rc != GC_OK) return rc;
+  return gc_dbfs_claim(g, row_lo, row_hi, frontier, visited, marks, parent, next, count, stream);
+}
+
 int gc_dbfs_advance(int64_t n, uint32_t* visited, uint32_t* frontier, const uint32_t* next,
                     unsigned long long* count, void* stream) {
   return guarded([&] {

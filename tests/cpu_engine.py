@@ -276,7 +276,9 @@ class CpuEngine:
         for x in ids.tolist():
             self._set(st["M"], x)
 
-    def dbfs_claim(self, shard, st, marks):
+    def dbfs_claim(self, shard, st, marks, foreign=None):
+        if foreign is not None:
+            self.dbfs_merge_marks(st, foreign)
         lo, hi = getattr(shard, "row_block", (0, shard.n))
         off, tgt = shard.offsets, shard.targets
         st["N"].zero_()

@@ -178,8 +178,8 @@ def _two_phase_worker(rank, world, port, names, specs, q):
             lo, hi = shard_bounds(off, world)[rank]
             for text in specs:
                 forest = not text.startswith("~")
-                r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec(text.lstrip("~")), engine=CpuEngine(),
-                                      forest=forest)
+                r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec(text.lstrip("~/")), engine=CpuEngine(),
+                                      forest=forest, forest_slices=text.startswith("/"))
                 out[(name, text)] = (r.labels.numpy().astype(np.int64),
                                      r.forest_u.numpy() if r.forest_u is not None else None,
                                      r.forest_v.numpy() if r.forest_v is not None else None,
@@ -200,13 +200,24 @@ def test_sharded_two_phase_matches_reference_stats(world):
     specs = ["kout+async+halve", "hb+async+halve", "none+async+halve", "kout+rem_cas+halve+splice",
              "~kout+rem_cas+halve+splice", "~hb+async+halve",
              # distributed level-synchronous BFS sampling (config 5's spec)
-             "bfs+async+halve", "~bfs+rem_cas+halve+splice"]
+             "bfs+async+halve", "~bfs+rem_cas+halve+splice",
+             # "/spec": the forest distributed over the ranks (BFS tree slices)
+             "/bfs+async+halve"]
     res = _run(_two_phase_worker, world, names, specs)
     for name in names:
         n, off, tgt, orc = gold.graphs[name]
         comps = len(np.unique(orc)) if n else 0
         for text in specs:
-            want = gold.spec_stats[name][text.lstrip("~")]
+            want = gold.spec_stats[name][text.lstrip("~/")]
+            if text.startswith("/"):  # the slices' union is one spanning forest
+                fu = np.concatenate([res[r][(name, text)][1] for r in range(world)])
+                fv = np.concatenate([res[r][(name, text)][2] for r in range(world)])
+                su = np.full(max(n, len(fu)), -1, np.int32)
+                sv = np.full(max(n, len(fv)), -1, np.int32)
+                su[:len(fu)] = fu
+                sv[:len(fv)] = fv
+                rep = oracle.check_forest(n, off, tgt, su[:n], sv[:n], orc) if len(fu) <= n else {"passed": False}
+                assert rep["passed"], (name, text, rep)
             for rank in range(world):
                 lab, fu, fv, c, i_s, i_f, lcnt, nact = res[rank][(name, text)]
                 assert np.array_equal(lab, orc), (name, text, rank)
@@ -214,7 +225,7 @@ def test_sharded_two_phase_matches_reference_stats(world):
                 assert i_s == want["insp_sample"] and i_f == want["insp_finish"], (name, text, rank, i_s, i_f)
                 if n:
                     assert lcnt / n == want["cov"], (name, text)
-                if fu is None:  # atomic splice: labels only
+                if fu is None or text.startswith("/"):  # atomic splice: labels only; slices checked above
                     continue
                 su = np.full(n, -1, np.int32)
                 sv = np.full(n, -1, np.int32)
