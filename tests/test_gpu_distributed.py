@@ -232,8 +232,12 @@ def _dbfs_uniform_worker(rank, world, port, log2n, q):
         g = build_csr(gen_uniform_pairs(log2n, 4 * n, seed=1), keep_host=False)
         lo, hi = shard_bounds(g._d_off, world)[rank]
         r = sharded_two_phase(shard_graph(g, lo, hi), parse_spec("bfs+async+halve"), forest=True)
+        # the same run with the forest returned as per-rank slices
+        s = sharded_two_phase(shard_graph(g, lo, hi), parse_spec("bfs+async+halve"), forest=True,
+                              forest_slices=True)
         q.put((rank, (r.labels.cpu().numpy(), r.forest_u.cpu().numpy(), r.forest_v.cpu().numpy(), r.insp_sample,
-                      r.insp_finish, r.lmax_count, r.n_active)))
+                      r.insp_finish, r.lmax_count, r.n_active, s.labels.cpu().numpy(), s.forest_u.cpu().numpy(),
+                      s.forest_v.cpu().numpy())))
     finally:
         dist.destroy_process_group()
 
@@ -260,8 +264,12 @@ def test_distributed_bfs_forest_config5_shape(world):
     g = build_csr(gen_uniform_pairs(log2n, 4 * n, seed=1))
     orc, comps = oracle.components(n, g.offsets, g.targets)
     _, st = spanning_forest_device(g, parse_spec("bfs+async+halve"))
+    slices_u, slices_v = [], []
     for r in range(world):
-        labels, fu, fv, i_s, i_f, lcnt, nact = res[r]
+        labels, fu, fv, i_s, i_f, lcnt, nact, slab, slu, slv = res[r]
+        assert np.array_equal(slab.astype(np.int64), orc), r
+        slices_u.append(slu)
+        slices_v.append(slv)
         assert np.array_equal(labels.astype(np.int64), orc), r
         assert i_s == st.edge_inspections.get("sample", 0) and i_f == st.edge_inspections.get("finish", 0), r
         assert lcnt / n == st.cov and nact == st.active, r
@@ -269,3 +277,9 @@ def test_distributed_bfs_forest_config5_shape(world):
         su = np.full(n, -1, np.int32); sv = np.full(n, -1, np.int32)
         su[:len(fu)] = fu; sv[:len(fv)] = fv
         assert oracle.check_forest(n, g.offsets, g.targets, su, sv, orc)["passed"], r
+    # the slices' union is one spanning forest
+    fu, fv = np.concatenate(slices_u), np.concatenate(slices_v)
+    assert len(fu) == n - comps
+    su = np.full(n, -1, np.int32); sv = np.full(n, -1, np.int32)
+    su[:len(fu)] = fu; sv[:len(fv)] = fv
+    assert oracle.check_forest(n, g.offsets, g.targets, su, sv, orc)["passed"]
