@@ -48,6 +48,13 @@ struct L2Residency {
     // survive the benchmark's L2 flush between steps — not a fair default
     static const bool disabled = getenv("GC_L2_WINDOW") == nullptr;
     if (disabled) return;
+    // not inside a stream capture: the persisting-cache reset at the end is
+    // not a capturable operation (plans run without the window)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return;
+    }
     static int max_persist = -1, max_window = 0;
     if (max_persist < 0) {
       int dev = 0;
