@@ -130,6 +130,7 @@ _KNOBS = [
     {"GC_COO_MLP": "8"},
     {"GC_FIN_LIST": "0", "GC_FIN_TMA": "0", "GC_MODE_COOP": "0"},
     {"GC_NO_GRAPH": "1", "GC_LDD_CUT": "0", "GC_BFS_WIDE_MIN": "1073741824"},
+    {"GC_BFS_TRACE": "1", "GC_LDD_TRACE": "1", "GC_BFS_ALPHA": "4", "GC_BFS_WIDE_MIN": "256"},
     {"GC_L2_WINDOW": "1"},
     {"GC_L2_WINDOW": "1", "GC_NO_GRAPH": "1"},
 ]
