@@ -15,6 +15,10 @@ from pathlib import Path
 from .errors import ConfigError, MalformedInputError, NativeError
 
 LIB_PATH = Path(__file__).resolve().parent / "libgconn.so"
+# A/B experiments only (profiles/ab_*.sh): an in-tree variant of the library
+# built with different compile-time tunings
+if os.environ.get("GC_LIB_VARIANT"):
+    LIB_PATH = Path(__file__).resolve().parent / "_variants" / f"libgconn_{os.environ['GC_LIB_VARIANT']}.so"
 
 GC_OK, GC_ERR_CONFIG, GC_ERR_MALFORMED, GC_ERR_CUDA, GC_ERR_OOM, GC_ERR_ARG = 0, 2, 3, 4, 5, 6
 

@@ -56,6 +56,22 @@ __device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
 __device__ __forceinline__ void red_or_bits(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// giant-filter bitmap accesses with an L2 eviction-priority hint (evict_last
+// keeps the n/8-byte bitmap resident while the batch's random parent reads
+// stream a parent array several times the L2 through the cache)
+__device__ __forceinline__ uint32_t ld_bits(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_bits_nc(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void red_or_bits(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("red.relaxed.gpu.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ bool gbit(uint32_t w, int32_t x) { return (w >> (x & 31)) & 1u; }
 
 // atomicMin on a word many warps update (a running minimum): skip the atomic
@@ -83,6 +99,15 @@ __device__ __forceinline__ uint64_t evict_last_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// policy for the giant-filter bitmap (keep: evict_last, else evict_normal)
+__device__ __forceinline__ uint64_t bits_policy(bool keep) {
+  return keep ? evict_last_policy() : evict_normal_policy();
 }
 __device__ __forceinline__ int32_t ld_weak_pol(const int32_t* p, uint64_t pol) {
   int32_t v;

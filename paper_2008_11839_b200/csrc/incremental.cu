@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t 
 // batches: from about the 12th batch on).
 __global__ void __launch_bounds__(1024)
 k_giant_decide(const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t len, int32_t cap,
-               const uint32_t* gbits, int32_t* gstate) {
+               const uint32_t* gbits, int32_t* gstate, bool gkeep) {
   __shared__ unsigned both, seen;
   if (threadIdx.x == 0) both = seen = 0u;
   __syncthreads();
@@ -252,7 +252,8 @@ k_giant_decide(const int32_t* us, const int32_t* vs, const uint8_t* isq, int64_t
       const int32_t a = us[j], b = vs[j];
       if (uint32_t(a) < uint32_t(cap) && uint32_t(b) < uint32_t(cap)) {
         atomicAdd(&seen, 1u);
-        if (gbit(ld_bits(gbits + (a >> 5)), a) && gbit(ld_bits(gbits + (b >> 5)), b)) atomicAdd(&both, 1u);
+        const uint64_t bpol = bits_policy(gkeep);
+        if (gbit(ld_bits(gbits + (a >> 5), bpol), a) && gbit(ld_bits(gbits + (b >> 5), bpol), b)) atomicAdd(&both, 1u);
       }
     }
   }
@@ -274,7 +275,7 @@ constexpr int kGcQ = 2048;
 __global__ void __launch_bounds__(kIB)
 k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const uint8_t* __restrict__ isq,
                 int64_t len, int32_t cap, const uint32_t* __restrict__ gbits, int32_t* gstate, int32_t* ou,
-                int32_t* ov, unsigned int* bad) {
+                int32_t* ov, unsigned int* bad, bool gkeep) {
   constexpr int kStep = kIB * 4;
   __shared__ int2 q[kGcQ];
   __shared__ int qn;
@@ -285,7 +286,7 @@ k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, 
   // the anchor is connected to itself: its bit seeds the marking (the other
   // blocks may test it before it lands, which only keeps an insert)
   if (on && blockIdx.x == 0 && threadIdx.x == 0)
-    red_or_bits(const_cast<uint32_t*>(gbits) + (anc >> 5), 1u << (anc & 31));
+    red_or_bits(const_cast<uint32_t*>(gbits) + (anc >> 5), 1u << (anc & 31), bits_policy(gkeep));
   if (!on || !gstate[4]) {  // pass the batch through: the union reads the caller's arrays
     if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<unsigned long long*>(gstate + 2) = ~0ull;
     return;
@@ -341,10 +342,11 @@ k_giant_compact(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, 
     }
     if (on) {
       uint32_t wu[4], wv[4];
+      const uint64_t bpol = bits_policy(gkeep);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        wu[j] = keep[j] ? __ldg(gbits + (u[j] >> 5)) : 0u;
-        wv[j] = keep[j] ? __ldg(gbits + (v[j] >> 5)) : 0u;
+        wu[j] = keep[j] ? ld_bits_nc(gbits + (u[j] >> 5), bpol) : 0u;
+        wv[j] = keep[j] ? ld_bits_nc(gbits + (v[j] >> 5), bpol) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -471,10 +473,12 @@ void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
   }();
   int64_t blocks = (a.k + 4 * kIB - 1) / (4 * kIB);
   if (blocks > int64_t(num_sms()) * per_sm) blocks = int64_t(num_sms()) * per_sm;
-  (k_giant_decide<<<1, 1024, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap), h->gbits, h->gstate),
+  (k_giant_decide<<<1, 1024, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap), h->gbits, h->gstate,
+                                              giant_keep()),
    ::gc::count_launch());
   (k_giant_compact<<<int(blocks), kIB, 0, h->st>>>(a.us, a.vs, isq, a.k, int32_t(h->cap),
-                                                                      h->gbits, h->gstate, h->cu, h->cv, h->bad),
+                                                                      h->gbits, h->gstate, h->cu, h->cv, h->bad,
+                                                                      giant_keep()),
    ::gc::count_launch());
   GC_CHECK_LAUNCH();
   a.alt.us = a.us;

@@ -188,6 +188,8 @@ void launch_incr_racy(const UFConfig& cfg, const CooUnionArgs& a, const uint8_t*
 int num_sms();
 // unions per thread of the lock-step async COO kernel (GC_COO_MLP, 0 = one per thread)
 int coo_mlp();
+// giant-filter bitmap accesses with an L2 evict_last hint (GC_GIANT_KEEP=0: off)
+bool giant_keep();
 
 // Kernel launches issued by libgconn (process-wide, exported through
 // gc_launch_count for the bench's gpu_launches claim).

@@ -47,6 +47,9 @@ struct UFState {
   // lock-step async COO kernel: mark merging inserts by index (lflag[i] = 1)
   // instead of appending (u, v) to lu / lv through one shared counter
   uint8_t* lflag = nullptr;
+  // giant-filter bitmap accesses carry an L2 evict_last hint (GC_GIANT_KEEP=0:
+  // evict_normal)
+  bool gkeep = true;
 };
 
 

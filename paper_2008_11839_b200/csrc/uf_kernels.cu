@@ -144,7 +144,8 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
       continue;
     }
     if (GIANT && anc >= 0 && !flags) {
-      const bool bu = gbit(ld_bits(s.gbits + (u >> 5)), u), bv = gbit(ld_bits(s.gbits + (v >> 5)), v);
+      const uint64_t bpol = bits_policy(s.gkeep);
+      const bool bu = gbit(ld_bits(s.gbits + (u >> 5), bpol), u), bv = gbit(ld_bits(s.gbits + (v >> 5), bpol), v);
       if (bu && bv) continue;  // both connected to the anchor already
       need = (bu ? 0u : 1u) | (bv ? 0u : 2u);
     }
@@ -167,8 +168,9 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
       }
       R::unite_known(s, u, v, pu, pv);
       if (GIANT && anc >= 0) {
-        if (need == 1u) red_or_bits(s.gbits + (u >> 5), 1u << (u & 31));
-        else if (need == 2u) red_or_bits(s.gbits + (v >> 5), 1u << (v & 31));
+        const uint64_t bpol = bits_policy(s.gkeep);
+        if (need == 1u) red_or_bits(s.gbits + (u >> 5), 1u << (u & 31), bpol);
+        else if (need == 2u) red_or_bits(s.gbits + (v >> 5), 1u << (v & 31), bpol);
       }
       continue;
     }
@@ -195,7 +197,17 @@ k_union_coo(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict
 // GIANT = false compiles the giant-filter machinery out (batches without a
 // filter: static union_edge_list, sharded merges, GC_INCR_GIANT=0)
 template <class R, int K, bool WEAK, bool GIANT>
-__global__ void __launch_bounds__(256, K <= 2 ? 5 : 1)
+// min resident blocks (registers vs occupancy), measured on config 4's
+// stream: unfiltered 5 (34 registers; 8 -> 32 registers was 2% faster there
+// but spills the filter form); giant-filter form 6 (40 registers, 4 bytes of
+// spill) 13.2 ms vs 13.4 at 5 and 14.0 at 8 (profiles/r3f)
+#ifndef GC_MLP_MINB
+#define GC_MLP_MINB 5
+#endif
+#ifndef GC_MLP_MINB_G
+#define GC_MLP_MINB_G 6
+#endif
+__global__ void __launch_bounds__(256, K <= 2 ? (GIANT ? GC_MLP_MINB_G : GC_MLP_MINB) : 1)
 k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t k,
                       const uint8_t* __restrict__ skip, int32_t sentinel, unsigned int* bad,
                       const unsigned long long* kdev, GiantPass alt, bool lazy_self) {
@@ -223,6 +235,7 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
   int it = 0;
   auto ld = [&](const int32_t* p) { return (WEAK && it < 8) ? ld_weak(p) : ld_acq(p); };
   const int32_t anc = GIANT && s.gbits ? ld_acq(s.ganchor) : -1;
+  const uint64_t bpol = bits_policy(s.gkeep);
   const int64_t span = int64_t(blockDim.x) * K;
   for (int64_t base = int64_t(blockIdx.x) * span; base < k; base += int64_t(gridDim.x) * span) {
     int32_t eu[K], ev[K];     // endpoints (forest records)
@@ -263,35 +276,26 @@ k_union_coo_async_mlp(UFState s, const int32_t* __restrict__ us, const int32_t* 
       // connected to the anchor once the union is done: its root is the
       // anchor, or one endpoint already carried its bit
       if (root != anc && (gneed >> (2 * j) & 3u) == 3u) return;
-      if (gneed >> (2 * j) & 1u) red_or_bits(s.gbits + (eu[j] >> 5), 1u << (eu[j] & 31));
-      if (gneed >> (2 * j) & 2u) red_or_bits(s.gbits + (ev[j] >> 5), 1u << (ev[j] & 31));
+      if (gneed >> (2 * j) & 1u) red_or_bits(s.gbits + (eu[j] >> 5), 1u << (eu[j] & 31), bpol);
+      if (gneed >> (2 * j) & 2u) red_or_bits(s.gbits + (ev[j] >> 5), 1u << (ev[j] & 31), bpol);
     };
+    // passed-through batch: the endpoints' bits are not probed (reading them
+    // beside the first parent reads measured 0.3 ms slower over config 4's
+    // stream than marking blind); a union that ends at the anchor root sets
+    // both (red.or is idempotent)
+    if (anc >= 0 && !flags) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (slot >> j & 1u) gneed |= 3u << (2 * j);
+    }
     // endpoint reads, all issued together; lazy init (driver.py:620-625)
     // of the slots still holding the sentinel
-    uint32_t wb[K][2];
-    const bool probe_bits = anc >= 0 && !flags;
 #pragma unroll
     for (int j = 0; j < K; ++j)
       if (slot >> j & 1u) {
         px[j][0] = ld(P + x[j][0]);
         px[j][1] = ld(P + x[j][1]);
-        if (probe_bits) {
-          // passed-through batch: the endpoints' giant bits, read beside
-          // the parent reads (no added latency), so only missing bits are
-          // set and doubly marked inserts stop here
-          wb[j][0] = ld_bits(s.gbits + (eu[j] >> 5));
-          wb[j][1] = ld_bits(s.gbits + (ev[j] >> 5));
-        }
       }
-    if (probe_bits) {
-#pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (slot >> j & 1u) {
-          const bool bu = gbit(wb[j][0], eu[j]), bv = gbit(wb[j][1], ev[j]);
-          gneed |= (bu ? 0u : 1u) << (2 * j) | (bv ? 0u : 2u) << (2 * j);
-          if (bu && bv) slot &= ~(1u << j);
-        }
-    }
     // lazy init (driver.py:620-625) without a returning CAS per endpoint: an
     // uninitialised slot (the sentinel) reads as its own root; the link CAS
     // expects the value actually stored (sentinel or the id), and whoever
@@ -499,6 +503,14 @@ int coo_mlp() {
   return k;
 }
 
+bool giant_keep() {
+  static const bool on = [] {
+    const char* e = getenv("GC_GIANT_KEEP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 // Functor-style launchers so one dispatch switch serves both kernels.
@@ -592,6 +604,7 @@ struct CooLaunch {
     if (a.gbits && R::kUnion != GC_FINISH_JTB) {
       s.gbits = a.gbits;
       s.ganchor = a.ganchor;
+      s.gkeep = giant_keep();
     }
     s.lflag = a.lflag;
     if constexpr (R::kUnion == GC_FINISH_ASYNC && R::kFind != GC_FIND_COMPRESS) {

@@ -33,6 +33,27 @@ def workload(name):
         g = build_csr(grid3d_edges(256), keep_host=False)
         sp = parse_spec(name.split(":")[1])
         return lambda: static_connectivity_device(g, sp, metrics=False)
+    if name.startswith("incrp"):  # incrp26:spec[:batches] — config 4's randomly permuted stream (incr_giant_probe)
+        parts = name[5:].split(":")
+        scale, spec = parts[0], parts[1]
+        nb = int(parts[2]) if len(parts) > 2 else 12
+        from paper_2008_11839_b200 import IncrementalConnectivity
+        g = build_csr(gen_rmat(int(scale), 8, seed=1, device=True), keep_host=False)
+        off, tgt = g._d_off, g._d_tgt
+        src = torch.repeat_interleave(torch.arange(g.n, device="cuda", dtype=torch.int32), off[1:] - off[:-1])
+        keep = src < tgt
+        us, vs = src[keep].contiguous(), tgt[keep].contiguous()
+        perm = torch.randperm(us.numel(), device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+        us, vs = us[perm].contiguous(), vs[perm].contiguous()
+        del src, keep, perm
+        sp = parse_spec(spec)
+
+        def run():
+            inc = IncrementalConnectivity(sp, g.n)
+            inc.reserve(10_000_000)
+            for b0 in range(0, min(us.numel(), nb * 10_000_000), 10_000_000):
+                inc.insert(us[b0:b0 + 10_000_000], vs[b0:b0 + 10_000_000])
+        return run
     if name.startswith("incr"):  # incr24:none+sv — 10M-insert batches of RMAT s24's undirected edges
         scale, spec = name[4:].split(":")
         from paper_2008_11839_b200 import IncrementalConnectivity
