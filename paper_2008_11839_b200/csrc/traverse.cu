@@ -28,6 +28,9 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kTB = 256;                  // traversal block
+#ifndef GC_TRAV_MINB
+#define GC_TRAV_MINB 1  // min resident blocks of the frontier-expansion kernels
+#endif
 constexpr int kQCap = kTB * 16;           // 16 KB staging per block
 __device__ __forceinline__ void red_or_u32(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -94,7 +97,7 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
                                              unsigned long long* nstat, uint32_t* nbits, int32_t* minv,
                                              unsigned long long* insp);
 
-__global__ void __launch_bounds__(kTB)
+__global__ void __launch_bounds__(kTB, GC_TRAV_MINB)
 k_bfs_td(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, const int32_t* __restrict__ q,
          const unsigned long long* qstat, uint32_t* par, const uint32_t* vis, int32_t* qn,
          unsigned long long* nstat, uint32_t* nbits, int32_t* minv, unsigned long long* insp,
@@ -226,7 +229,7 @@ __device__ __forceinline__ void bfs_td_level(BlockQueue<kQCap>& bq, const int64_
 // reaches nf_stop (the host then re-evaluates the direction switch).
 // Frontier stats [count, degree sum] use the ring of three slots of the
 // launch-per-level form; out[0] = levels run.
-__global__ void __launch_bounds__(kTB)
+__global__ void __launch_bounds__(kTB, GC_TRAV_MINB)
 k_bfs_persist(const int64_t* __restrict__ off, const int32_t* __restrict__ tgt, int32_t* q0, int32_t* q1,
               unsigned long long* stat, int64_t level0, int32_t max_levels, unsigned long long nf_stop,
               uint32_t* par, uint32_t* vis, int32_t* minv, unsigned long long* reached,
