@@ -95,6 +95,12 @@ typedef struct gc_spec {
   double ldd_beta;       /* LDD sampler: exponential shift rate              */
   const uint32_t* jtb_ranks;          /* device, n entries, or NULL (dset.py:372-374) */
   const int32_t* kout_rand_offsets;   /* device, (#deg>0 vertices) x (k-1) row offsets */
+  /* BFS sampler source chosen on the device (sampling.py:130-132): used when
+   * bfs_source < 0 — host array of the sorted, distinct probe vertices; the
+   * source is the first probe of maximum degree (np.argmax order) */
+  const int32_t* bfs_probes;
+  int32_t bfs_nprobes;
+  int32_t reserved1;
 } gc_spec;
 
 /* RunStats (validate.py:20-43) as produced on device.  Times are CUDA-event

@@ -44,7 +44,8 @@ class Spec(C.Structure):
                 ("lt_shortcut", C.c_int32), ("lt_alter", C.c_int32), ("kout_k", C.c_int32),
                 ("kout_mode", C.c_int32), ("hb_edges", C.c_int32), ("reserved0", C.c_int32),
                 ("bfs_source", C.c_int64), ("seed", C.c_uint64), ("ldd_beta", C.c_double),
-                ("jtb_ranks", C.c_void_p), ("kout_rand_offsets", C.c_void_p)]
+                ("jtb_ranks", C.c_void_p), ("kout_rand_offsets", C.c_void_p),
+                ("bfs_probes", C.c_void_p), ("bfs_nprobes", C.c_int32), ("reserved1", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -78,8 +78,11 @@ __global__ void k_compress(int32_t* P, int32_t n) {
 // appends the vertices not carrying it to the active list with one global
 // atomic per block.  If the candidate turns out not to be the mode, the
 // histogram fallback re-gathers (k_gather_active).
+#ifndef GC_PS_BLOCKS
+#define GC_PS_BLOCKS 6  // resident 256-thread blocks per SM of k_post_sample (one wave)
+#endif
 template <bool COMPRESS>
-__global__ void __launch_bounds__(kEwBlock, 6)
+__global__ void __launch_bounds__(kEwBlock, GC_PS_BLOCKS)
 k_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, unsigned long long* ctr) {
   // two 4-vertex quads per thread per step (eight first hops in flight; the
   // step's barriers are paid once per eight vertices)
@@ -909,8 +912,9 @@ void run_post_sample(int32_t* P, int32_t n, const int64_t* off, int32_t* list, i
     if (exact_mode) stamp_flush(ctr, st);
     else (k_mode_probe<<<1, kProbe, 0, st>>>(P, n, ctr, 1, take_stamps()), ::gc::count_launch());
     // one resident wave: six 256-thread blocks per SM, two quads per thread
-    const int gps = grid_for((nq + 1) / 2, kEwBlock, 1) < num_sms() * 6 ? grid_for((nq + 1) / 2, kEwBlock, 1)
-                                                                          : num_sms() * 6;
+    const int gps = grid_for((nq + 1) / 2, kEwBlock, 1) < num_sms() * GC_PS_BLOCKS
+                        ? grid_for((nq + 1) / 2, kEwBlock, 1)
+                        : num_sms() * GC_PS_BLOCKS;
     if (compress) (k_post_sample<true><<<gps, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
     else (k_post_sample<false><<<gps, kEwBlock, 0, st>>>(P, n, off, list, ctr), ::gc::count_launch());
     // exact-mode fallback: one cooperative launch that exits at once on a

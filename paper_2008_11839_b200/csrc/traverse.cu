@@ -464,6 +464,38 @@ __global__ void k_bfs_seed(const int64_t* off, uint32_t* par, int32_t* q, unsign
   *minv = s;
 }
 
+// k_bfs_seed with the source picked on the device (sampling.py:130-132):
+// the first probe (sorted, distinct) of maximum degree, as np.argmax; the
+// key (degree, -position) is reduced over the block
+constexpr int kProbeTB = 256;
+__global__ void __launch_bounds__(kProbeTB)
+k_bfs_seed_probe(const int64_t* off, const int32_t* probes, int32_t np, uint32_t* par, int32_t* q,
+                 unsigned long long* qstat, uint32_t* bits, uint32_t* vis, int32_t* minv) {
+  __shared__ unsigned long long best;
+  if (threadIdx.x == 0) best = 0ull;
+  __syncthreads();
+  unsigned long long mine = 0ull;
+  for (int32_t i = threadIdx.x; i < np; i += kProbeTB) {
+    const int32_t p = probes[i];
+    const int64_t dd = off[p + 1] - off[p];
+    const unsigned long long d = dd < 0xffffffffll ? static_cast<unsigned long long>(dd) : 0xffffffffull;
+    // degree < 2^32 here (ids are int32); position breaks ties toward the first
+    const unsigned long long key = (d << 32) | (0xffffffffull - uint32_t(i));
+    mine = key > mine ? key : mine;
+  }
+  atomicMax(&best, mine);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int32_t s = probes[0xffffffffull - (best & 0xffffffffull)];
+  par[s] = kSourcePar;
+  q[0] = s;
+  qstat[0] = 1;
+  qstat[1] = static_cast<unsigned long long>(off[s + 1] - off[s]);
+  bits[s >> 5] |= 1u << (s & 31);
+  vis[s >> 5] |= 1u << (s & 31);
+  *minv = s;
+}
+
 // label the component with its minimum (sampling.py:158-160), emit forest
 // slots (slot v = (parent, v)), and count the sample inspections: the
 // reference adds every frontier's degree sum (:141-144), i.e. the degree of
@@ -1126,7 +1158,11 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
              unsigned long long* ctr, cudaStream_t st) {
   const int32_t n = int32_t(g.n);
   if (n == 0 || g.m == 0) return;  // sampling.py:128-129
-  require(s.bfs_source >= 0 && s.bfs_source < n, GC_ERR_ARG, "BFS source out of range");
+  const bool probe_src = s.bfs_source < 0 && s.bfs_probes && s.bfs_nprobes > 0;
+  require(probe_src || (s.bfs_source >= 0 && s.bfs_source < n), GC_ERR_ARG, "BFS source out of range");
+  if (probe_src)
+    for (int32_t i = 0; i < s.bfs_nprobes; ++i)
+      require(s.bfs_probes[i] >= 0 && s.bfs_probes[i] < n, GC_ERR_ARG, "BFS probe out of range");
   const int64_t words = (int64_t(n) + 31) / 32;
   uint32_t* par = reinterpret_cast<uint32_t*>(w.key);  // the claim buffer, as u32 parents
   GC_CUDA(cudaMemsetAsync(par, 0xff, size_t(n) * 4, st));  // kUnreached
@@ -1141,7 +1177,14 @@ void run_bfs(const gc_csr& g, const gc_spec& s, int32_t* P, int32_t* fu, int32_t
   int32_t* q[2] = {w.q0, w.q1};
   uint32_t* fb[2] = {w.fb0, w.fb1};
   GC_CUDA(cudaMemsetAsync(w.stat, 0, 8 * sizeof(unsigned long long), st));
-  TL(k_bfs_seed, 1, 1, g.offsets, par, q[0], slot(0), fb[0], w.vis, int32_t(s.bfs_source), minv);
+  if (probe_src) {
+    // the probe list rides in the second frontier queue until the seed
+    // kernel has picked the source from it
+    GC_CUDA(cudaMemcpyAsync(q[1], s.bfs_probes, size_t(s.bfs_nprobes) * 4, cudaMemcpyHostToDevice, st));
+    TL(k_bfs_seed_probe, 1, kProbeTB, g.offsets, q[1], s.bfs_nprobes, par, q[0], slot(0), fb[0], w.vis, minv);
+  } else {
+    TL(k_bfs_seed, 1, 1, g.offsets, par, q[0], slot(0), fb[0], w.vis, int32_t(s.bfs_source), minv);
+  }
   GC_CHECK_LAUNCH();
   unsigned long long* h = pinned_words();
   GC_CUDA(cudaMemcpyAsync(h, slot(0), 16, cudaMemcpyDeviceToHost, st));

@@ -102,3 +102,35 @@ def test_bfs_forest_matches_min_parent_tree(log2n):
     assert np.array_equal(fv[comp], ef_v[comp])
     ref, _ = oracle.components(g.n, g.offsets, g.targets)
     assert check_forest(g, df, ref)["passed"]
+
+
+def test_bfs_source_picked_on_device(golden):
+    """Device-only graphs pick the BFS source in the seed kernel from the probe
+    list (sampling.py:130-132); the forests must equal the host-picked ones
+    (and the reference's hashes where the golden file pins them)."""
+    import dataclasses
+    from paper_2008_11839_b200 import gen_rmat, build_csr
+    # deterministic finishes (SV / LT record the minimum edge index), so the
+    # whole forest is a function of the source
+    specs = [parse_spec(t) for t in ("bfs+sv", "bfs+lt_prs")]
+    specs.append(dataclasses.replace(parse_spec("bfs+sv"), bfs_probes=1000, seed=7))
+    for name in golden.names():
+        n, off, tgt, orc = golden.graphs[name]
+        for spec in specs:
+            g_host = graph_of(golden, name)
+            g_dev = graph_of(golden, name).cuda()
+            g_dev.drop_host()
+            a, _ = spanning_forest_device(g_host, spec)
+            b, _ = spanning_forest_device(g_dev, spec)
+            assert np.array_equal(a.fu.cpu().numpy(), b.fu.cpu().numpy()), (name, format_spec(spec))
+            assert np.array_equal(a.fv.cpu().numpy(), b.fv.cpu().numpy()), (name, format_spec(spec))
+    # a device-generated graph against its host-backed copy
+    g = build_csr(gen_rmat(14, 8, seed=3, device=True), keep_host=False)
+    gh = g.cuda()
+    gh._h_off = g._d_off.cpu().numpy()
+    gh._h_tgt = g._d_tgt.cpu().numpy()
+    spec = parse_spec("bfs+sv")
+    a, _, pa = spanning_forest_device(gh, spec, want_parent=True)
+    b, _, pb = spanning_forest_device(g, spec, want_parent=True)
+    assert np.array_equal(a.fu.cpu().numpy(), b.fu.cpu().numpy())
+    assert np.array_equal(pa.cpu().numpy(), pb.cpu().numpy())
