@@ -158,11 +158,12 @@ int g1(int64_t work) { return grid_for(work, kIB, 8); }
 // frequent one (warp-aggregated shared-memory hash, as k_mode_probe).  The
 // anchor is re-resolved to its component's current root; it moves to the
 // sampled mode only when that component clearly dominates (then the bits,
-// which mean "connected to the old anchor", are cleared by k_giant_clear).
+// which mean "connected to the old anchor", are cleared by the same block).
 // Roots of the min-linking rules are component minima, so once the giant
 // has formed its root — the anchor — stays put.
 __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t cap, int32_t sentinel,
-                                                      int32_t* gstate, volatile int32_t* hmode) {
+                                                      int32_t* gstate, volatile int32_t* hmode,
+                                                      uint32_t* bits, int64_t words) {
   constexpr int kS = 1024, kSlots = 2 * kS;
   __shared__ int32_t key_[kSlots];
   __shared__ unsigned cnt_[kSlots];
@@ -204,33 +205,42 @@ __global__ void __launch_bounds__(1024) k_giant_probe(const int32_t* P, int64_t 
   if (x >= 0)
     atomicMax(&best, (static_cast<unsigned long long>(cnt_[slot]) << 32) | (0xffffffffull - uint32_t(x)));
   __syncthreads();
-  if (i != 0) return;
-  int32_t cur = gstate[0];
-  if (cur >= 0) {
-    int32_t p = ld_acq(P + cur);
-    while (p != cur) {
-      cur = p;
-      p = ld_acq(P + cur);
-    }
-  }
-  const unsigned cm = unsigned(best >> 32);
-  const int32_t m = int32_t(0xffffffffull - (best & 0xffffffffull));
-  unsigned cc = 0;
-  if (cur >= 0)
-    for (int k = slot_of(cur), t = 0; t < kSlots && key_[k] != -1; k = (k + 1) % kSlots, ++t)
-      if (key_[k] == cur) {
-        cc = cnt_[k];
-        break;
+  __shared__ int clear;
+  if (i == 0) {
+    int32_t cur = gstate[0];
+    if (cur >= 0) {
+      int32_t p = ld_acq(P + cur);
+      while (p != cur) {
+        cur = p;
+        p = ld_acq(P + cur);
       }
-  const bool move = cm > 0 && m != cur && (cur < 0 || cm >= 2 * cc + 8);
-  gstate[0] = move ? m : cur;
-  gstate[1] = move && cur >= 0;
-  *reinterpret_cast<unsigned long long*>(gstate + 2) = 0ull;  // the next batch's compaction count
-  // compacting costs one pass over the batch plus two bit tests per insert;
-  // it pays once about half of the inserts can be dropped (config 4: from
-  // the ~12th of 54 batches on)
-  if (move) gstate[4] = 0;  // the bits were cleared: pass the next batch through
-  if (hmode) *hmode = gstate[4];
+    }
+    const unsigned cm = unsigned(best >> 32);
+    const int32_t m = int32_t(0xffffffffull - (best & 0xffffffffull));
+    unsigned cc = 0;
+    if (cur >= 0)
+      for (int k = slot_of(cur), t = 0; t < kSlots && key_[k] != -1; k = (k + 1) % kSlots, ++t)
+        if (key_[k] == cur) {
+          cc = cnt_[k];
+          break;
+        }
+    const bool move = cm > 0 && m != cur && (cur < 0 || cm >= 2 * cc + 8);
+    gstate[0] = move ? m : cur;
+    gstate[1] = move && cur >= 0;
+    *reinterpret_cast<unsigned long long*>(gstate + 2) = 0ull;  // the next batch's compaction count
+    // compacting costs one pass over the batch plus two bit tests per insert;
+    // it pays once about half of the inserts can be dropped (config 4: from
+    // the ~12th of 54 batches on)
+    if (move) gstate[4] = 0;  // the bits were cleared: pass the next batch through
+    if (hmode) *hmode = gstate[4];
+    clear = move && cur >= 0;
+  }
+  __syncthreads();
+  // the anchor moved off an old one (rare: the giant overtakes an earlier
+  // mode): its bits, which meant "connected to the old anchor", are cleared
+  // by this block instead of a separate launch per batch
+  if (clear)
+    for (int64_t w = i; w < words; w += kS) bits[w] = 0u;
 }
 
 // Whether this batch is worth compacting: one block tests the giant bits of
@@ -425,12 +435,6 @@ k_merge_compact(const int32_t* __restrict__ cu, const int32_t* __restrict__ cv, 
   flush();
 }
 
-__global__ void k_giant_clear(uint32_t* bits, int64_t words, const int32_t* gstate) {
-  if (!gstate[1]) return;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words; w += stride) bits[w] = 0u;
-}
-
 // GC_INCR_GIANT=0 turns the filter off (every insert runs its union)
 bool giant_filter_on() {
   static const bool on = [] {
@@ -494,10 +498,10 @@ void giant_compact(gc_incr* h, CooUnionArgs& a, const uint8_t* isq) {
 
 void giant_after(gc_incr* h) {
   if (!h->gbits) return;
-  (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->hmode_dev),
-   ::gc::count_launch());
   const int64_t words = (h->cap + 31) / 32;
-  (k_giant_clear<<<grid_for(words, kIB, 2), kIB, 0, h->st>>>(h->gbits, words, h->gstate), ::gc::count_launch());
+  (k_giant_probe<<<1, 1024, 0, h->st>>>(h->state, h->cap, int32_t(h->cap), h->gstate, h->hmode_dev, h->gbits,
+                                        words),
+   ::gc::count_launch());
   GC_CHECK_LAUNCH();
 }
 
